@@ -1,0 +1,374 @@
+// capi.cu -- C-ABI of the B200 env step (include/tissuesim_b200.h).
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/tissuesim_b200.h"
+#include "step_common.h"
+
+namespace ts {
+int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector<uint8_t> &blob,
+                    ts_layout_info &info, std::string &err);
+}
+
+namespace {
+thread_local std::string g_err;
+std::atomic<int64_t> g_launches{0};
+
+int fail(int code, const std::string &msg) {
+    g_err = msg;
+    return code;
+}
+int cuda_fail(cudaError_t e, const char *what) {
+    g_err = std::string(what) + ": " + cudaGetErrorString(e);
+    return TS_ERR_CUDA;
+}
+}  // namespace
+
+struct ts_handle {
+    int device = 0;
+    int precision = TS_F32;
+    std::vector<uint8_t> host_blob;
+    void *dev_blob = nullptr;
+    TsDevProg prog{};
+    TsParams params{};
+    ts_layout_info info{};
+    int smem = 0;
+    int max_grid = 0;   // 0 = one CTA per environment
+};
+
+extern "C" {
+
+const char *ts_last_error(void) { return g_err.c_str(); }
+int32_t ts_abi_version(void) { return TS_ABI_VERSION; }
+int64_t ts_launch_count(void) { return g_launches.load(); }
+
+static ts_layout_opts default_opts() {
+    ts_layout_opts o;
+    std::memset(&o, 0, sizeof(o));
+    return o;
+}
+
+int32_t ts_compile_program(const ts_scene_desc *desc, const ts_layout_opts *opts, void *buf, int64_t *bytes,
+                           ts_layout_info *info) {
+    if (!desc || !bytes) return fail(TS_ERR_INVALID, "null argument");
+    ts_layout_opts o = opts ? *opts : default_opts();
+    std::vector<uint8_t> blob;
+    ts_layout_info inf;
+    std::string err;
+    int rc = ts::compile_program(*desc, o, blob, inf, err);
+    if (rc != TS_OK) return fail(rc, err);
+    if (info) *info = inf;
+    if (buf) {
+        if (*bytes < (int64_t)blob.size()) return fail(TS_ERR_INVALID, "buffer too small");
+        std::memcpy(buf, blob.data(), blob.size());
+    }
+    *bytes = (int64_t)blob.size();
+    return TS_OK;
+}
+
+static void decode(ts_handle *h) {
+    const TsProgHeader *H = reinterpret_cast<const TsProgHeader *>(h->host_blob.data());
+    const uint8_t *b = reinterpret_cast<const uint8_t *>(h->dev_blob);
+    TsDevProg &P = h->prog;
+    P.V = H->V; P.Vf = H->Vf; P.Vf_pad = H->Vf_pad; P.Vstore = H->Vstore;
+    P.F = H->F; P.B = H->B; P.VPT = H->VPT; P.G = H->G;
+    P.n_chunks = H->n_chunks; P.grasp_chunk = H->grasp_chunk; P.slot_cap = H->slot_capacity;
+    P.cbits_words = (3 * H->F + 31) / 32;
+    P.chunks = reinterpret_cast<const TsChunk *>(b + H->off[TS_SEC_CHUNK]);
+    P.edge_idx = reinterpret_cast<const int4 *>(b + H->off[TS_SEC_EDGE_IDX]);
+    P.edge_par = b + H->off[TS_SEC_EDGE_PAR];
+    P.tet_idx = reinterpret_cast<const int4 *>(b + H->off[TS_SEC_TET_IDX]);
+    P.tet_slot = reinterpret_cast<const int4 *>(b + H->off[TS_SEC_TET_SLOT]);
+    P.tet_rv = b + H->off[TS_SEC_TET_RV];
+    P.att_idx = reinterpret_cast<const int4 *>(b + H->off[TS_SEC_ATT_IDX]);
+    P.att_slot = reinterpret_cast<const int4 *>(b + H->off[TS_SEC_ATT_SLOT]);
+    P.att_par = b + H->off[TS_SEC_ATT_PAR];
+    P.att_anchor = b + H->off[TS_SEC_ATT_ANCHOR];
+    P.region = reinterpret_cast<const int32_t *>(b + H->off[TS_SEC_REGION]);
+    P.valence = reinterpret_cast<const int32_t *>(b + H->off[TS_SEC_VALENCE]);
+    P.static_cnt = reinterpret_cast<const int32_t *>(b + H->off[TS_SEC_STATIC_CNT]);
+    P.s2o = reinterpret_cast<const int32_t *>(b + H->off[TS_SEC_S2O]);
+    P.o2s = reinterpret_cast<const int32_t *>(b + H->off[TS_SEC_O2S]);
+    P.w = b + H->off[TS_SEC_W];
+    P.faces = reinterpret_cast<const int32_t *>(b + H->off[TS_SEC_FACES]);
+    P.faces_orig = reinterpret_cast<const int32_t *>(b + H->off[TS_SEC_FACES_ORIG]);
+    P.rest = b + H->off[TS_SEC_REST];
+}
+
+static void fill_params(const ts_scene_desc &d, TsParams &S) {
+    S.h = d.dt / d.substeps;   // SolverParams.h, solver.py:92-94
+    // damping factor, _kernels.pyx:592
+    if (d.damping == 0.0) S.damp = 1.0;
+    else { double v = 1.0 - d.damping * S.h; S.damp = (v > 0.0) ? v : 0.0; }
+    for (int c = 0; c < 3; ++c) S.g[c] = d.gravity[c];
+    S.ks = d.k_s; S.kv = d.k_v; S.k_contact = d.k_contact;
+    S.substeps = d.substeps; S.contact_iters = d.contact_iterations;
+    for (int c = 0; c < 3; ++c) {
+        S.rcm[c] = d.rcm[c]; S.start_axis[c] = d.start_axis[c]; S.start_jaw[c] = d.start_jaw[c];
+        S.target[c] = d.target[c]; S.lo[c] = d.workspace_low[c]; S.hi[c] = d.workspace_high[c];
+        S.target_obs[c] = d.target_obs[c];
+    }
+    S.shaft_r = d.shaft_radius; S.clamp_r = d.clamp_radius; S.clamp_len = d.clamp_length;
+    S.grasp_r2 = d.grasp_radius2;
+    S.start_reach = d.start_reach; S.start_clamp = d.start_clamp;
+    S.held_angle = d.held_clamp_angle; S.held_cos = d.held_cos; S.held_sin = d.held_sin;
+    S.action_scale = d.action_scale; S.success_thr = d.success_threshold;
+    S.w_l = d.w_distance; S.w_d = d.w_delta; S.w_s = d.w_success; S.reward_scale = d.reward_scale;
+    S.max_steps = d.max_episode_steps; S.start_distance = d.start_distance;
+}
+
+int32_t ts_create(const ts_scene_desc *desc, const ts_layout_opts *opts, int32_t device, ts_handle **out) {
+    if (!desc || !out) return fail(TS_ERR_INVALID, "null argument");
+    if (desc->substeps < 1) return fail(TS_ERR_INVALID, "substeps must be >= 1");
+    if (desc->dt <= 0.0) return fail(TS_ERR_INVALID, "dt must be positive");
+    ts_layout_opts o = opts ? *opts : default_opts();
+    ts_handle *h = new ts_handle();
+    h->device = device;
+    h->precision = o.precision;
+    std::string err;
+    int rc = ts::compile_program(*desc, o, h->host_blob, h->info, err);
+    if (rc != TS_OK) { delete h; return fail(rc, err); }
+    cudaError_t e = cudaSetDevice(device);
+    if (e != cudaSuccess) { delete h; return cuda_fail(e, "cudaSetDevice"); }
+    e = cudaMalloc(&h->dev_blob, h->host_blob.size());
+    if (e != cudaSuccess) { delete h; return cuda_fail(e, "cudaMalloc(program)"); }
+    e = cudaMemcpy(h->dev_blob, h->host_blob.data(), h->host_blob.size(), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) { cudaFree(h->dev_blob); delete h; return cuda_fail(e, "cudaMemcpy(program)"); }
+    decode(h);
+    fill_params(*desc, h->params);
+    const int R = o.precision == TS_F64 ? 8 : 4;
+    h->smem = ts_smem_bytes(h->prog, R);
+    int max_smem = 0;
+    cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+    if (h->smem > max_smem) {
+        char buf[256];
+        std::snprintf(buf, sizeof(buf), "layout needs %d B of shared memory per CTA, device allows %d; "
+                      "lower max_chunk_slots", h->smem, max_smem);
+        cudaFree(h->dev_blob); delete h;
+        return fail(TS_ERR_UNSUPPORTED, buf);
+    }
+    h->info.smem_bytes = h->smem;
+    *out = h;
+    return TS_OK;
+}
+
+int32_t ts_destroy(ts_handle *h) {
+    if (!h) return TS_OK;
+    if (h->dev_blob) cudaFree(h->dev_blob);
+    delete h;
+    return TS_OK;
+}
+
+int32_t ts_query(const ts_handle *h, ts_layout_info *info) {
+    if (!h || !info) return fail(TS_ERR_INVALID, "null argument");
+    *info = h->info;
+    return TS_OK;
+}
+
+static void fill_state(TsLaunch &L, const ts_env_state *st) {
+    L.x = st->x; L.v = st->v;
+    L.axis = st->tool_axis; L.jaw = st->tool_jaw; L.reach = st->tool_reach; L.clamp = st->tool_clamp;
+    L.grasp_vertex = st->grasp_vertex; L.grasped = st->grasped;
+    L.steps = st->steps; L.l_prev = st->l_prev; L.ep_return = st->ep_return;
+}
+
+static int launch(ts_handle *h, const TsLaunch &L, cudaStream_t s) {
+    if (L.n_env <= 0) return TS_OK;
+    int grid = (int)std::min<int64_t>(L.n_env, h->max_grid > 0 ? h->max_grid : (int64_t)1 << 30);
+    if (grid > 2147483647) grid = 2147483647;
+    cudaError_t e = h->precision == TS_F64 ? ts_launch_step<double>(h->prog, h->params, L, grid, h->smem, s)
+                                           : ts_launch_step<float>(h->prog, h->params, L, grid, h->smem, s);
+    if (e != cudaSuccess) return cuda_fail(e, "step kernel launch");
+    g_launches.fetch_add(1);
+    return TS_OK;
+}
+
+int32_t ts_env_step(ts_handle *h, const ts_env_state *st, int64_t num_envs, const void *actions,
+                    int32_t actions_f32, const ts_step_out *out, const ts_tool_override *ovr,
+                    int32_t *bad_action_flag, void *stream) {
+    if (!h || !st || !out) return fail(TS_ERR_INVALID, "null argument");
+    if (!actions && !ovr) return fail(TS_ERR_INVALID, "actions required");
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    TsLaunch L;
+    std::memset(&L, 0, sizeof(L));
+    fill_state(L, st);
+    L.n_env = num_envs;
+    L.mode = TS_M_GRASP | TS_M_SUBSTEPS | TS_M_CONTACTS | TS_M_ENV;
+    if (ovr) {
+        L.mode |= TS_M_CMD_OVERRIDE;
+        L.ovr_axis = ovr->axis; L.ovr_jaw = ovr->jaw; L.ovr_reach = ovr->reach; L.ovr_clamp = ovr->clamp;
+        L.ovr_clipped = ovr->clipped;
+    } else {
+        L.mode |= TS_M_CMD_ACTIONS;
+        L.actions = actions; L.actions_f32 = actions_f32;
+    }
+    if (bad_action_flag) {
+        if (!actions) return fail(TS_ERR_INVALID, "action check needs actions");
+        cudaError_t e = ts_launch_check_actions(actions, actions_f32, num_envs, bad_action_flag, s);
+        if (e != cudaSuccess) return cuda_fail(e, "action check launch");
+        g_launches.fetch_add(1);
+        L.mode |= TS_M_CHECK_ACTIONS;
+        L.bad_flag = bad_action_flag;
+    }
+    L.obs = out->obs; L.final_obs = out->final_obs; L.obs_f64 = out->obs_f64;
+    L.reward = out->reward; L.distance = out->distance; L.ret_out = out->episode_return;
+    L.terminated = out->terminated; L.truncated = out->truncated; L.success = out->success;
+    L.diverged = out->diverged; L.clipped = out->clipped; L.done_mask = out->done_mask;
+    L.contacts = out->contacts; L.len_out = out->episode_length;
+    return launch(h, L, s);
+}
+
+int32_t ts_env_reset(ts_handle *h, const ts_env_state *st, int64_t num_envs, const uint8_t *mask, void *obs,
+                     int32_t obs_f64, void *stream) {
+    if (!h || !st) return fail(TS_ERR_INVALID, "null argument");
+    TsLaunch L;
+    std::memset(&L, 0, sizeof(L));
+    fill_state(L, st);
+    L.n_env = num_envs;
+    L.obs = obs; L.obs_f64 = obs_f64;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    if (num_envs <= 0) return TS_OK;
+    cudaError_t e = h->precision == TS_F64 ? ts_launch_reset<double>(h->prog, h->params, L, mask, 0, s)
+                                           : ts_launch_reset<float>(h->prog, h->params, L, mask, 0, s);
+    if (e != cudaSuccess) return cuda_fail(e, "reset kernel launch");
+    g_launches.fetch_add(1);
+    return TS_OK;
+}
+
+int32_t ts_env_observe(ts_handle *h, const ts_env_state *st, int64_t num_envs, void *obs, int32_t obs_f64,
+                       void *stream) {
+    if (!h || !st || !obs) return fail(TS_ERR_INVALID, "null argument");
+    TsLaunch L;
+    std::memset(&L, 0, sizeof(L));
+    fill_state(L, st);
+    L.n_env = num_envs;
+    L.obs = obs; L.obs_f64 = obs_f64;
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    if (num_envs <= 0) return TS_OK;
+    cudaError_t e = h->precision == TS_F64 ? ts_launch_reset<double>(h->prog, h->params, L, nullptr, 1, s)
+                                           : ts_launch_reset<float>(h->prog, h->params, L, nullptr, 1, s);
+    if (e != cudaSuccess) return cuda_fail(e, "observe kernel launch");
+    g_launches.fetch_add(1);
+    return TS_OK;
+}
+
+int32_t ts_sim_step(ts_handle *h, const ts_env_state *st, int64_t num_envs, const double *targets,
+                    const double *angles, const ts_tool_override *ovr, uint8_t *clipped, uint8_t *rejected,
+                    uint8_t *diverged, int32_t *contacts, void *stream) {
+    if (!h || !st) return fail(TS_ERR_INVALID, "null argument");
+    TsLaunch L;
+    std::memset(&L, 0, sizeof(L));
+    fill_state(L, st);
+    L.n_env = num_envs;
+    L.mode = TS_M_GRASP | TS_M_SUBSTEPS | TS_M_CONTACTS;
+    if (ovr) {
+        L.mode |= TS_M_CMD_OVERRIDE;
+        L.ovr_axis = ovr->axis; L.ovr_jaw = ovr->jaw; L.ovr_reach = ovr->reach; L.ovr_clamp = ovr->clamp;
+        L.ovr_clipped = ovr->clipped;
+    } else if (targets) {
+        L.mode |= TS_M_CMD_TARGETS;
+        L.targets = targets; L.angles = angles;
+    }
+    L.clipped = clipped; L.rejected = rejected; L.diverged = diverged; L.contacts = contacts;
+    return launch(h, L, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int32_t ts_run_substeps(ts_handle *h, void *x, void *v, int64_t num_envs, const int64_t *grasp_vertex,
+                        const double *drag_points, const double *gravity, double hstep, int32_t substeps,
+                        double damping, void *stream) {
+    if (!h || !x || !v || !grasp_vertex || !drag_points || !gravity) return fail(TS_ERR_INVALID, "null argument");
+    if (substeps < 0) return fail(TS_ERR_INVALID, "substeps must be >= 0");
+    TsLaunch L;
+    std::memset(&L, 0, sizeof(L));
+    L.x = x; L.v = v; L.n_env = num_envs;
+    L.mode = TS_M_SUBSTEPS | TS_M_EXT_GRASP;
+    L.ext_gv = grasp_vertex; L.ext_drag = drag_points;
+    // per-call solver parameters, as the plugin protocol passes them (_kernels.pyx:583, 592)
+    const TsParams saved = h->params;
+    TsParams &S = h->params;
+    S.h = hstep; S.substeps = substeps;
+    for (int c = 0; c < 3; ++c) S.g[c] = gravity[c];
+    if (damping == 0.0) S.damp = 1.0;
+    else { double dv = 1.0 - damping * hstep; S.damp = (dv > 0.0) ? dv : 0.0; }
+    int rc = substeps > 0 ? launch(h, L, reinterpret_cast<cudaStream_t>(stream)) : TS_OK;
+    h->params = saved;
+    return rc;
+}
+
+int32_t ts_detect_contacts(ts_handle *h, const void *x, int64_t num_envs, const double *caps, int32_t *count,
+                           int32_t *face, int32_t *cap, double *depth, double *dir, double *bary, void *stream) {
+    if (!h || !x || !caps || !count || !face || !cap || !depth || !dir || !bary)
+        return fail(TS_ERR_INVALID, "null argument");
+    TsLaunch L;
+    std::memset(&L, 0, sizeof(L));
+    L.x = const_cast<void *>(x); L.v = const_cast<void *>(x); L.n_env = num_envs;
+    L.mode = TS_M_DETECT_ONLY;
+    L.ext_caps = caps;
+    L.det_count = count; L.det_face = face; L.det_cap = cap; L.det_depth = depth; L.det_dir = dir; L.det_bary = bary;
+    return launch(h, L, reinterpret_cast<cudaStream_t>(stream));
+}
+
+int32_t ts_uniform_actions(double *actions, int64_t num_envs, uint64_t seed, uint64_t counter, void *stream) {
+    if (!actions) return fail(TS_ERR_INVALID, "null argument");
+    if (num_envs <= 0) return TS_OK;
+    cudaError_t e = ts_launch_uniform(actions, 3 * num_envs, seed, counter, reinterpret_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "uniform kernel launch");
+    g_launches.fetch_add(1);
+    return TS_OK;
+}
+
+int32_t ts_set_max_grid(ts_handle *h, int32_t max_grid) {
+    if (!h) return fail(TS_ERR_INVALID, "null argument");
+    h->max_grid = max_grid;
+    return TS_OK;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// small helper kernels
+// ---------------------------------------------------------------------------
+__global__ void check_actions_kernel(const void *actions, int f32, int64_t n, int32_t *flag) {
+    __shared__ int any;
+    if (threadIdx.x == 0) any = 0;
+    __syncthreads();
+    int bad = 0;
+    for (int64_t i = threadIdx.x; i < 3 * n; i += blockDim.x) {
+        const double a = f32 ? (double)reinterpret_cast<const float *>(actions)[i]
+                             : reinterpret_cast<const double *>(actions)[i];
+        bad |= !isfinite(a);
+    }
+    if (bad) atomicOr(&any, 1);
+    __syncthreads();
+    if (threadIdx.x == 0) *flag = any;
+}
+
+cudaError_t ts_launch_check_actions(const void *actions, int actions_f32, int64_t n, int32_t *flag,
+                                    cudaStream_t stream) {
+    check_actions_kernel<<<1, 1024, 0, stream>>>(actions, actions_f32, n, flag);
+    return cudaGetLastError();
+}
+
+__device__ __forceinline__ uint64_t splitmix64(uint64_t z) {
+    z += 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+__global__ void uniform_kernel(double *out, int64_t n, uint64_t seed, uint64_t counter) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t r = splitmix64(seed ^ splitmix64(counter * 0x100000001B3ull + (uint64_t)i));
+        out[i] = 2.0 * ((double)(r >> 11) * (1.0 / 9007199254740992.0)) - 1.0;
+    }
+}
+
+cudaError_t ts_launch_uniform(double *out, int64_t n, uint64_t seed, uint64_t counter, cudaStream_t stream) {
+    int grid = (int)((n + 255) / 256);
+    if (grid > 4096) grid = 4096;
+    uniform_kernel<<<grid, 256, 0, stream>>>(out, n, seed, counter);
+    return cudaGetLastError();
+}

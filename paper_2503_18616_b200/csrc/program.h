@@ -1,0 +1,63 @@
+// program.h -- compiled scene program shared by the host compiler and the
+// sm_100a kernels.  One flat blob: a header with byte offsets of typed
+// sections.  Uploaded once per handle; every CTA (one environment each)
+// reads the same blob through L1/L2.
+//
+// Vertex "storage positions": free vertices (w > 0) first, sorted by
+// incidence count (descending) so each warp owns vertices of similar
+// valence; then pinned vertices.  The owner thread of free position p is
+// p % B (B = CTA size, a multiple of 32), so its lane is p % 32.  Shared
+// memory arrays indexed by p therefore place p in bank p % 32.
+//
+// Constraint "slots": every (constraint, free endpoint) incidence owns one
+// slot in the chunk's slot buffer.  The slots of free position p in chunk c
+// are region(c, p/32) + k*32 + p%32 for k = 0..valence(c,p)-1, in the
+// reference's per-vertex accumulation order (constraint index, then role),
+// so the owner's sequential sum reproduces _kernels.pyx's accumulation
+// order exactly (edges -> grasp -> attachments -> tets, each by index).
+#pragma once
+#include <stdint.h>
+
+#define TS_PROG_MAGIC 0x54534231  // "TSB1"
+#define TS_PROG_VERSION 1
+
+enum TsChunkKind { TS_CHUNK_EDGE = 0, TS_CHUNK_ATT = 1, TS_CHUNK_TET = 2 };
+
+enum TsSection {
+    TS_SEC_CHUNK = 0,     // TsChunk[n_chunks]
+    TS_SEC_EDGE_IDX,      // int4 {pa, pb, sa, sb}   storage pos, slot (-1: pinned endpoint)
+    TS_SEC_EDGE_PAR,      // Real4 {rest_len, wa, wb, wsum}
+    TS_SEC_TET_IDX,       // int4 {pa, pb, pc, pd}
+    TS_SEC_TET_SLOT,      // int4 {sa, sb, sc, sd}
+    TS_SEC_TET_RV,        // Real rest volume
+    TS_SEC_ATT_IDX,       // int4 {vtx, f0, f1, f2}
+    TS_SEC_ATT_SLOT,      // int4 slots of vtx, f0, f1, f2
+    TS_SEC_ATT_PAR,       // Real4 {rest, k, wv, wc}
+    TS_SEC_ATT_ANCHOR,    // Real4 {ax, ay, az, is_face}
+    TS_SEC_REGION,        // int32 [n_chunks][G] base slot of group g's region
+    TS_SEC_VALENCE,       // int32 [n_chunks][Vf_pad]
+    TS_SEC_STATIC_CNT,    // int32 [Vf_pad] total incidences over all chunks
+    TS_SEC_S2O,           // int32 [Vstore] storage pos -> original vertex (-1 padding)
+    TS_SEC_O2S,           // int32 [V] original vertex -> storage pos
+    TS_SEC_W,             // Real [Vstore] inverse mass (0 for padding)
+    TS_SEC_FACES,         // int32 [F][3] surface faces in storage positions
+    TS_SEC_FACES_ORIG,    // int32 [F][3] surface faces, original ids (plugin outputs)
+    TS_SEC_REST,          // Real [V][3] rest positions, original order (reset)
+    TS_SEC_COUNT
+};
+
+struct TsChunk {
+    int32_t kind, item_begin, item_count, slot_count;
+    int32_t region_off, val_off, conflicts, pad;
+};
+
+struct TsProgHeader {
+    int32_t magic, version, real_bytes, n_sections;
+    int32_t V, Vf, Vf_pad, Vstore;
+    int32_t F, B, VPT, G;
+    int32_t n_chunks, grasp_chunk, slot_capacity, n_att;
+    int32_t n_edge_items, n_tet_items, n_att_items, bank_conflicts;
+    int32_t n_slots_total, pad0, pad1, pad2;
+    int64_t off[TS_SEC_COUNT];
+    int64_t total_bytes;
+};

@@ -1,0 +1,114 @@
+// step_common.h -- host/device parameter blocks for the fused env-step kernel.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "program.h"
+
+// What one launch does (bit flags).
+enum TsModeBits {
+    TS_M_CMD_ACTIONS = 1 << 0,   // EnvBatch.step: targets = drag + clip(a)*scale, angle = held
+    TS_M_CMD_TARGETS = 1 << 1,   // Simulation.step(targets, angles)
+    TS_M_CMD_OVERRIDE = 1 << 2,  // pose supplied externally (validation)
+    TS_M_GRASP = 1 << 3,         // ToolBatch.update_grasps
+    TS_M_SUBSTEPS = 1 << 4,      // run_substeps
+    TS_M_CONTACTS = 1 << 5,      // detect + resolve contacts
+    TS_M_ENV = 1 << 6,           // reward / done / auto-reset / obs
+    TS_M_DETECT_ONLY = 1 << 7,   // plugin detect_contacts: write rows, no resolve
+    TS_M_EXT_GRASP = 1 << 8,     // plugin run_substeps: grasp vertex + drag from arrays
+    TS_M_CHECK_ACTIONS = 1 << 9  // abort (no state change) if *bad_flag != 0
+};
+
+// Scene constants (fp64 as in the reference; the kernel casts to Real where
+// the solver runs in Real).
+struct TsParams {
+    double h, damp, g[3], ks, kv, k_contact;
+    int32_t substeps, contact_iters;
+    double rcm[3], shaft_r, clamp_r, clamp_len, grasp_r2;
+    double start_axis[3], start_jaw[3], start_reach, start_clamp;
+    double held_angle, held_cos, held_sin;
+    double target[3], action_scale, success_thr;
+    double w_l, w_d, w_s, reward_scale;
+    double lo[3], hi[3];
+    int64_t max_steps;
+    double start_distance, target_obs[3];
+};
+
+// Decoded device program (pointers into the uploaded blob).
+struct TsDevProg {
+    int32_t V, Vf, Vf_pad, Vstore, F, B, VPT, G;
+    int32_t n_chunks, grasp_chunk, slot_cap, cbits_words;
+    const TsChunk *chunks;
+    const int4 *edge_idx;
+    const void *edge_par;
+    const int4 *tet_idx;
+    const int4 *tet_slot;
+    const void *tet_rv;
+    const int4 *att_idx;
+    const int4 *att_slot;
+    const void *att_par;
+    const void *att_anchor;
+    const int32_t *region;
+    const int32_t *valence;
+    const int32_t *static_cnt;
+    const int32_t *s2o;
+    const int32_t *o2s;
+    const void *w;
+    const int32_t *faces;
+    const int32_t *faces_orig;
+    const void *rest;
+};
+
+// Per-launch pointers (device).
+struct TsLaunch {
+    int32_t mode;
+    int64_t n_env;
+    // state
+    void *x, *v;
+    double *axis, *jaw, *reach, *clamp;
+    int64_t *grasp_vertex;
+    uint8_t *grasped;
+    int64_t *steps;
+    double *l_prev, *ep_return;
+    // inputs
+    const void *actions; int32_t actions_f32;
+    const double *targets, *angles;
+    const double *ovr_axis, *ovr_jaw, *ovr_reach, *ovr_clamp;
+    const uint8_t *ovr_clipped;
+    const int64_t *ext_gv;        // plugin run_substeps
+    const double *ext_drag;
+    const double *ext_caps;       // plugin detect: (N,3,7)
+    const int32_t *bad_flag;
+    // outputs
+    void *obs, *final_obs; int32_t obs_f64;
+    double *reward, *distance, *ret_out;
+    uint8_t *terminated, *truncated, *success, *diverged, *clipped, *rejected, *done_mask;
+    int32_t *contacts;
+    int64_t *len_out;
+    // plugin detect outputs (capacity 3F rows per env)
+    int32_t *det_count, *det_face, *det_cap;
+    double *det_depth, *det_dir, *det_bary;
+};
+
+// Shared-memory layout sizes (bytes) for one CTA.
+inline int ts_smem_bytes(const TsDevProg &P, int real_bytes) {
+    size_t b = 0;
+    b += (size_t)3 * P.Vstore * real_bytes;       // xs, ys, zs
+    b += (size_t)3 * P.slot_cap * real_bytes;     // slot buffer / contact records
+    b += (size_t)4 * P.Vf_pad;                    // degenerate-constraint counters
+    b += (size_t)4 * P.cbits_words;               // contact bitmap
+    b = (b + 15) / 16 * 16;
+    b += 2048;                                    // scalar block + capsule params
+    return (int)b;
+}
+
+template <typename Real>
+cudaError_t ts_launch_step(const TsDevProg &P, const TsParams &S, const TsLaunch &L, int grid,
+                           int smem, cudaStream_t stream);
+template <typename Real>
+cudaError_t ts_launch_reset(const TsDevProg &P, const TsParams &S, const TsLaunch &L,
+                            const uint8_t *mask, int observe_only, cudaStream_t stream);
+cudaError_t ts_launch_check_actions(const void *actions, int actions_f32, int64_t n,
+                                    int32_t *flag, cudaStream_t stream);
+cudaError_t ts_launch_uniform(double *out, int64_t n, uint64_t seed, uint64_t counter,
+                              cudaStream_t stream);

@@ -1,0 +1,8 @@
+// fp32 throughput build of the fused env step (compiled -fmad=false like the
+// fp64 build; the tool / env logic stays fp64 in both).
+#include "step_kernel.cuh"
+
+template cudaError_t ts_launch_step<float>(const TsDevProg &, const TsParams &, const TsLaunch &, int, int,
+                                           cudaStream_t);
+template cudaError_t ts_launch_reset<float>(const TsDevProg &, const TsParams &, const TsLaunch &,
+                                            const uint8_t *, int, cudaStream_t);

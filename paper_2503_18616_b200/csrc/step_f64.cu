@@ -1,0 +1,9 @@
+// fp64 build of the fused env step: compiled with -fmad=false so every
+// expression rounds exactly like the reference's C (-ffp-contract=off),
+// giving bitwise parity with the compiled CPU backend.
+#include "step_kernel.cuh"
+
+template cudaError_t ts_launch_step<double>(const TsDevProg &, const TsParams &, const TsLaunch &, int, int,
+                                            cudaStream_t);
+template cudaError_t ts_launch_reset<double>(const TsDevProg &, const TsParams &, const TsLaunch &,
+                                             const uint8_t *, int, cudaStream_t);

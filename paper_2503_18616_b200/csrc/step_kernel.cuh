@@ -1,0 +1,919 @@
+// step_kernel.cuh -- the fused tissue-reach environment step for sm_100a.
+//
+// One CTA owns one environment for the whole outer step (grid-stride over
+// environments).  Positions live in shared memory (SoA, storage order), each
+// free vertex's velocity lives in the registers of its owner thread, and the
+// step never touches HBM between loading the state and writing it back:
+//
+//   tool command + capsule rows     thread 0, fp64      tool.py:307-370
+//   grasp release / nearest vertex  block argmin, fp64  tool.py:372-389
+//   substeps x S:                                        _kernels.pyx:260-352
+//     predict                       owner threads
+//     per constraint chunk:
+//       phase 1  constraint-parallel: correction vectors -> slots (smem)
+//       phase 2  vertex-parallel: owner sums its slots in reference order
+//     apply + damping (+ next predict)   owner threads
+//   contacts: face-parallel AABB + PGD witness search,   _kernels.pyx:797-947
+//             then ordered sequential push-out            collision.py:55-73
+//   divergence guard                                      solver.py:357-365
+//   reward / done / auto-reset / obs                      env.py:144-197
+//
+// Real = double with -fmad=false reproduces the reference's fp64 arithmetic
+// bit for bit (same expression trees, same per-vertex summation order).
+// Real = float is the throughput build (same algorithm, fp32 storage).
+#pragma once
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "step_common.h"
+
+namespace tsk {
+
+template <typename Real> struct R4;
+template <> struct R4<float> { using T = float4; };
+template <> struct R4<double> { using T = double4; };
+
+__device__ __forceinline__ double cmin(double a, double b) { return (b < a) ? b : a; }   // Cython min()
+__device__ __forceinline__ double cmax(double a, double b) { return (b > a) ? b : a; }   // Cython max()
+__device__ __forceinline__ float cmin(float a, float b) { return (b < a) ? b : a; }
+__device__ __forceinline__ float cmax(float a, float b) { return (b > a) ? b : a; }
+
+__device__ __forceinline__ double dot3(const double *u, const double *w) {
+    return u[0] * w[0] + u[1] * w[1] + u[2] * w[2];
+}
+__device__ __forceinline__ void cross3(const double *u, const double *w, double *o) {
+    o[0] = u[1] * w[2] - u[2] * w[1];
+    o[1] = u[2] * w[0] - u[0] * w[2];
+    o[2] = u[0] * w[1] - u[1] * w[0];
+}
+__device__ __forceinline__ double norm3(const double *u) { return sqrt(dot3(u, u)); }
+
+struct Pose { double ax[3], jw[3], reach, clamp; };
+
+// perpendicular_unit, tool.py:55-62
+static __device__ void some_perpendicular(const double *a, double *out) {
+    const bool z = fabs(a[0]) > 0.9;
+    double ref[3] = {z ? 0.0 : 1.0, 0.0, z ? 1.0 : 0.0};
+    const double d = dot3(a, ref);
+    for (int c = 0; c < 3; ++c) out[c] = ref[c] - a[c] * d;
+    const double n = norm3(out);
+    for (int c = 0; c < 3; ++c) out[c] = out[c] / n;
+}
+
+// rotate_about_axis (Rodrigues), tool.py:47-52
+static __device__ void rodrigues(const double *vec, const double *k, double c, double s, double *out) {
+    double kx[3];
+    cross3(k, vec, kx);
+    const double kv = dot3(k, vec);
+    for (int i = 0; i < 3; ++i) out[i] = (vec[i] * c + kx[i] * s) + k[i] * kv * (1.0 - c);
+}
+
+// ToolBatch.apply_commands for one row, tool.py:307-345
+static __device__ __noinline__ void apply_command(const TsParams &S, Pose &p, const double *tgt, double angle,
+                              bool &clipped, bool &rejected) {
+    double b[3];
+    clipped = false;
+    for (int c = 0; c < 3; ++c) {
+        double t = tgt[c];
+        double m = t > S.lo[c] ? t : S.lo[c];        // np.maximum (finite inputs)
+        m = m < S.hi[c] ? m : S.hi[c];               // np.minimum
+        b[c] = m;
+        clipped |= (m != t);
+    }
+    double v1[3], v2[3];
+    for (int c = 0; c < 3; ++c) {
+        v1[c] = (S.rcm[c] + p.reach * p.ax[c]) - S.rcm[c];   // drag_points() - rcm
+        v2[c] = b[c] - S.rcm[c];
+    }
+    const double n1 = norm3(v1), n2 = norm3(v2);
+    rejected = n2 < 1e-9;
+    const double n2s = rejected ? 1.0 : n2;
+    double cosang = dot3(v1, v2) / (n1 * n2s);
+    cosang = cosang < -1.0 ? -1.0 : (cosang > 1.0 ? 1.0 : cosang);
+    double theta = acos(cosang);
+    double k[3];
+    cross3(v1, v2, k);
+    const double kn = norm3(k);
+    bool rot = (theta > 1e-9) && (kn > 0.0) && !rejected;
+    if (rot) { for (int c = 0; c < 3; ++c) k[c] = k[c] / kn; }
+    else { k[0] = k[1] = k[2] = 0.0; }
+    if ((theta > 1e-9) && (kn == 0.0) && !rejected) {
+        double u[3];
+        for (int c = 0; c < 3; ++c) u[c] = v1[c] / n1;
+        some_perpendicular(u, k);
+        rot = true;
+    }
+    if (!rot) theta = 0.0;
+    if (rejected) return;
+    if (rot) {
+        const double c = cos(theta), s = sin(theta);
+        double axn[3], jwn[3];
+        rodrigues(p.ax, k, c, s, axn);
+        const double na = norm3(axn);
+        for (int i = 0; i < 3; ++i) axn[i] = axn[i] / na;
+        rodrigues(p.jw, k, c, s, jwn);
+        const double d = dot3(axn, jwn);
+        for (int i = 0; i < 3; ++i) jwn[i] = jwn[i] - axn[i] * d;
+        const double nj = norm3(jwn);
+        for (int i = 0; i < 3; ++i) { p.ax[i] = axn[i]; p.jw[i] = jwn[i] / nj; }
+    }
+    p.reach = p.reach + (n2 - n1);
+    p.clamp = angle;
+}
+
+// ToolBatch.capsule_rows for one row, tool.py:347-370
+static __device__ __noinline__ void capsule_rows(const TsParams &S, const Pose &p, double rows[3][7]) {
+    double piv[3];
+    for (int c = 0; c < 3; ++c) piv[c] = S.rcm[c] + (p.reach - S.clamp_len) * p.ax[c];
+    double ca, sa;
+    if (p.clamp == S.held_angle) { ca = S.held_cos; sa = S.held_sin; }
+    else {
+        const double alpha = p.clamp * (3.141592653589793 / 180.0);  // np.radians
+        ca = cos(alpha); sa = sin(alpha);
+    }
+    double base[3] = {S.rcm[0], S.rcm[1], S.rcm[2]};
+    double dpb[3] = {piv[0] - base[0], piv[1] - base[1], piv[2] - base[2]};
+    if (norm3(dpb) < 1e-9)
+        for (int c = 0; c < 3; ++c) base[c] = piv[c] - 1e-6 * p.ax[c];
+    for (int c = 0; c < 3; ++c) {
+        const double da = ca * p.ax[c] + sa * p.jw[c];
+        const double db = ca * p.ax[c] - sa * p.jw[c];
+        rows[0][c] = base[c]; rows[0][3 + c] = piv[c];
+        rows[1][c] = piv[c]; rows[1][3 + c] = piv[c] + S.clamp_len * da;
+        rows[2][c] = piv[c]; rows[2][3 + c] = piv[c] + S.clamp_len * db;
+    }
+    rows[0][6] = S.shaft_r; rows[1][6] = S.clamp_r; rows[2][6] = S.clamp_r;
+}
+
+// ---------------------------------------------------------------------------
+// capsule SDF (Real), _kernels.pyx:732-794
+// ---------------------------------------------------------------------------
+template <typename Real>
+struct Cap { Real p0[3], seg[3], dd, radius, fb[3], lo[3], hi[3]; };
+
+template <typename Real>
+__device__ void make_cap(const double *row, Cap<Real> &C) {
+    for (int k = 0; k < 3; ++k) { C.p0[k] = (Real)row[k]; C.seg[k] = (Real)row[3 + k] - (Real)row[k]; }
+    C.radius = (Real)row[6];
+    C.dd = C.seg[0] * C.seg[0] + C.seg[1] * C.seg[1] + C.seg[2] * C.seg[2];
+    if (C.dd <= (Real)0) C.dd = (Real)1;
+    C.fb[0] = (Real)0; C.fb[1] = C.seg[2]; C.fb[2] = -C.seg[1];
+    Real fn = C.fb[0] * C.fb[0] + C.fb[1] * C.fb[1] + C.fb[2] * C.fb[2];
+    if (fn < (Real)1e-20) {
+        C.fb[0] = -C.seg[2]; C.fb[1] = (Real)0; C.fb[2] = C.seg[0];
+        fn = C.fb[0] * C.fb[0] + C.fb[1] * C.fb[1] + C.fb[2] * C.fb[2];
+    }
+    fn = sqrt(fn);
+    if (fn > (Real)0) { C.fb[0] /= fn; C.fb[1] /= fn; C.fb[2] /= fn; }
+    for (int k = 0; k < 3; ++k) {
+        C.lo[k] = cmin((Real)row[k], (Real)row[3 + k]) - C.radius;
+        C.hi[k] = cmax((Real)row[k], (Real)row[3 + k]) + C.radius;
+    }
+}
+
+template <typename Real>
+__device__ __forceinline__ Real cap_sd(const Cap<Real> &C, const Real *q, Real *grad) {
+    Real t = ((q[0] - C.p0[0]) * C.seg[0] + (q[1] - C.p0[1]) * C.seg[1] + (q[2] - C.p0[2]) * C.seg[2]) / C.dd;
+    if (t < (Real)0) t = (Real)0;
+    else if (t > (Real)1) t = (Real)1;
+    const Real dx = q[0] - (C.p0[0] + t * C.seg[0]);
+    const Real dy = q[1] - (C.p0[1] + t * C.seg[1]);
+    const Real dz = q[2] - (C.p0[2] + t * C.seg[2]);
+    const Real nrm = sqrt(dx * dx + dy * dy + dz * dz);
+    if (grad) {
+        if (nrm > (Real)1e-12) { grad[0] = dx / nrm; grad[1] = dy / nrm; grad[2] = dz / nrm; }
+        else { grad[0] = C.fb[0]; grad[1] = C.fb[1]; grad[2] = C.fb[2]; }
+    }
+    return nrm - C.radius;
+}
+
+template <typename Real>
+__device__ __forceinline__ void simplex3(Real *b) {
+    Real u0 = b[0], u1 = b[1], u2 = b[2], tmp, theta;
+    if (u0 < u1) { tmp = u0; u0 = u1; u1 = tmp; }
+    if (u1 < u2) { tmp = u1; u1 = u2; u2 = tmp; }
+    if (u0 < u1) { tmp = u0; u0 = u1; u1 = tmp; }
+    if (u2 - (u0 + u1 + u2 - (Real)1) / (Real)3 > (Real)0) theta = (u0 + u1 + u2 - (Real)1) / (Real)3;
+    else if (u1 - (u0 + u1 - (Real)1) / (Real)2 > (Real)0) theta = (u0 + u1 - (Real)1) / (Real)2;
+    else theta = u0 - (Real)1;
+    b[0] = cmax(b[0] - theta, (Real)0);
+    b[1] = cmax(b[1] - theta, (Real)0);
+    b[2] = cmax(b[2] - theta, (Real)0);
+}
+
+template <typename Real>
+__device__ __forceinline__ void bary_pt(const Real *b, const Real *pa, const Real *pb, const Real *pc, Real *o) {
+    o[0] = b[0] * pa[0] + b[1] * pb[0] + b[2] * pc[0];
+    o[1] = b[0] * pa[1] + b[1] * pb[1] + b[2] * pc[1];
+    o[2] = b[0] * pa[2] + b[1] * pb[2] + b[2] * pc[2];
+}
+
+// Narrow phase of one (face, capsule) pair that passed the AABB test.
+// Returns sd; fills depth/dir/bary when sd < 0.
+template <typename Real>
+__device__ __noinline__ Real witness(const Cap<Real> &C, const Real *pa, const Real *pb, const Real *pc, int iters,
+                        Real *dir, Real *bary) {
+    const Real s0 = cap_sd<Real>(C, pa, nullptr);
+    const Real s1 = cap_sd<Real>(C, pb, nullptr);
+    const Real s2 = cap_sd<Real>(C, pc, nullptr);
+    int vb = 0;
+    Real best = s0;
+    if (s1 < best) { vb = 1; best = s1; }
+    if (s2 < best) { vb = 2; best = s2; }
+    bary[0] = vb == 0 ? (Real)1 : (Real)0;
+    bary[1] = vb == 1 ? (Real)1 : (Real)0;
+    bary[2] = vb == 2 ? (Real)1 : (Real)0;
+    Real pt[3], g[3], gb[3];
+    Real step = (Real)0.5;
+    for (int it = 0; it < iters; ++it) {
+        bary_pt(bary, pa, pb, pc, pt);
+        cap_sd<Real>(C, pt, g);
+        gb[0] = g[0] * pa[0] + g[1] * pa[1] + g[2] * pa[2];
+        gb[1] = g[0] * pb[0] + g[1] * pb[1] + g[2] * pb[2];
+        gb[2] = g[0] * pc[0] + g[1] * pc[1] + g[2] * pc[2];
+        const Real mean_g = (gb[0] + gb[1] + gb[2]) / (Real)3;
+        gb[0] -= mean_g; gb[1] -= mean_g; gb[2] -= mean_g;
+        const Real mag = cmax(cmax(fabs(gb[0]), fabs(gb[1])), fabs(gb[2]));
+        bary[0] -= step * gb[0] / (mag + (Real)1e-30);
+        bary[1] -= step * gb[1] / (mag + (Real)1e-30);
+        bary[2] -= step * gb[2] / (mag + (Real)1e-30);
+        simplex3(bary);
+        step *= (Real)0.7;
+    }
+    bary_pt(bary, pa, pb, pc, pt);
+    Real sd = cap_sd<Real>(C, pt, g);
+    if (sd > best) {
+        bary[0] = vb == 0 ? (Real)1 : (Real)0;
+        bary[1] = vb == 1 ? (Real)1 : (Real)0;
+        bary[2] = vb == 2 ? (Real)1 : (Real)0;
+        bary_pt(bary, pa, pb, pc, pt);
+        sd = cap_sd<Real>(C, pt, g);
+    }
+    dir[0] = g[0]; dir[1] = g[1]; dir[2] = g[2];
+    return sd;
+}
+
+template <typename Real> __device__ __forceinline__ Real fused_sq3(Real a, Real b, Real c);
+// b @ b for the contact barycentrics: numpy dispatches to BLAS ddot, which
+// evaluates fma(b2,b2, fma(b1,b1, b0*b0)) on the reference hosts.
+template <> __device__ __forceinline__ double fused_sq3<double>(double a, double b, double c) {
+    return __fma_rn(c, c, __fma_rn(b, b, a * a));
+}
+template <> __device__ __forceinline__ float fused_sq3<float>(float a, float b, float c) {
+    return __fmaf_rn(c, c, __fmaf_rn(b, b, a * a));
+}
+
+// ---------------------------------------------------------------------------
+// shared scalar block
+// ---------------------------------------------------------------------------
+struct Scal {
+    double caps[3][7];
+    double drag[3];
+    Pose pose;
+    double red_key[32];
+    int red_idx[32];
+    int gv_orig;        // grasp vertex, original id (-1 none)
+    int gv_store;       // storage position (-1 none / pinned handled like free)
+    int need_search;
+    int diverged;
+    int done;
+    int n_contacts;
+    int clipped, rejected;
+    int abort;
+};
+
+template <typename Real>
+struct Smem {
+    Real *xs, *ys, *zs, *slx, *sly, *slz;
+    int *deg;
+    unsigned *cbits;
+    Scal *sc;
+    Cap<Real> *caps;
+};
+
+template <typename Real>
+__device__ __forceinline__ Smem<Real> carve(const TsDevProg &P, unsigned char *raw) {
+    Smem<Real> m;
+    m.xs = reinterpret_cast<Real *>(raw);
+    m.ys = m.xs + P.Vstore;
+    m.zs = m.ys + P.Vstore;
+    m.slx = m.zs + P.Vstore;
+    m.sly = m.slx + P.slot_cap;
+    m.slz = m.sly + P.slot_cap;
+    m.deg = reinterpret_cast<int *>(m.slz + P.slot_cap);
+    m.cbits = reinterpret_cast<unsigned *>(m.deg + P.Vf_pad);
+    size_t off = reinterpret_cast<unsigned char *>(m.cbits + P.cbits_words) - raw;
+    off = (off + 15) / 16 * 16;
+    m.sc = reinterpret_cast<Scal *>(raw + off);
+    m.caps = reinterpret_cast<Cap<Real> *>(raw + off + ((sizeof(Scal) + 15) / 16) * 16);
+    return m;
+}
+
+// ---------------------------------------------------------------------------
+// phase 1: constraint-parallel correction vectors into slots
+// ---------------------------------------------------------------------------
+template <typename Real>
+__device__ __forceinline__ void p1_edges(const TsDevProg &P, const Smem<Real> &m, const TsChunk &ch,
+                                         Real ks) {
+    using V4 = typename R4<Real>::T;
+    const int4 *idx = P.edge_idx + ch.item_begin;
+    const V4 *par = reinterpret_cast<const V4 *>(P.edge_par) + ch.item_begin;
+    for (int i = threadIdx.x; i < ch.item_count; i += blockDim.x) {
+        const int4 id = __ldg(idx + i);
+        const V4 pr = par[i];
+        const Real dx = m.xs[id.x] - m.xs[id.y];
+        const Real dy = m.ys[id.x] - m.ys[id.y];
+        const Real dz = m.zs[id.x] - m.zs[id.y];
+        const Real dist = sqrt(dx * dx + dy * dy + dz * dz);
+        const Real mm = (Real)0.5 + copysign((Real)0.5, dist - (Real)1e-12);
+        const Real scale = mm * ks * (dist - pr.x) / (dist * pr.w + ((Real)1 - mm));
+        const Real ca = -pr.y * scale;
+        const Real cb = pr.z * scale;
+        if (id.z >= 0) { m.slx[id.z] = ca * dx; m.sly[id.z] = ca * dy; m.slz[id.z] = ca * dz; }
+        if (id.w >= 0) { m.slx[id.w] = cb * dx; m.sly[id.w] = cb * dy; m.slz[id.w] = cb * dz; }
+        if (mm == (Real)0) {
+            if (id.z >= 0) atomicAdd(&m.deg[id.x], 1);
+            if (id.w >= 0) atomicAdd(&m.deg[id.y], 1);
+        }
+    }
+}
+
+template <typename Real>
+__device__ __forceinline__ void put_slot(const Smem<Real> &m, int s, Real c, Real gx, Real gy, Real gz) {
+    if (s >= 0) { m.slx[s] = c * gx; m.sly[s] = c * gy; m.slz[s] = c * gz; }
+}
+
+template <typename Real> __device__ __forceinline__ Real div6(Real a);
+template <> __device__ __forceinline__ double div6<double>(double a) { return a / 6.0; }
+template <> __device__ __forceinline__ float div6<float>(float a) { return a / 6.0f; }
+
+template <typename Real>
+__device__ __forceinline__ void p1_tets(const TsDevProg &P, const Smem<Real> &m, const TsChunk &ch, Real kv) {
+    const int4 *idx = P.tet_idx + ch.item_begin;
+    const int4 *slot = P.tet_slot + ch.item_begin;
+    const Real *rv = reinterpret_cast<const Real *>(P.tet_rv) + ch.item_begin;
+    for (int i = threadIdx.x; i < ch.item_count; i += blockDim.x) {
+        const int4 id = __ldg(idx + i);
+        const int4 sl = __ldg(slot + i);
+        const Real ax = m.xs[id.x], ay = m.ys[id.x], az = m.zs[id.x];
+        const Real bax = m.xs[id.y] - ax, bay = m.ys[id.y] - ay, baz = m.zs[id.y] - az;
+        const Real cax = m.xs[id.z] - ax, cay = m.ys[id.z] - ay, caz = m.zs[id.z] - az;
+        const Real dax = m.xs[id.w] - ax, day = m.ys[id.w] - ay, daz = m.zs[id.w] - az;
+        const Real gbx = div6(cay * daz - caz * day);
+        const Real gby = div6(caz * dax - cax * daz);
+        const Real gbz = div6(cax * day - cay * dax);
+        const Real gcx = div6(day * baz - daz * bay);
+        const Real gcy = div6(daz * bax - dax * baz);
+        const Real gcz = div6(dax * bay - day * bax);
+        const Real gdx = div6(bay * caz - baz * cay);
+        const Real gdy = div6(baz * cax - bax * caz);
+        const Real gdz = div6(bax * cay - bay * cax);
+        const Real gax = -(gbx + gcx + gdx);
+        const Real gay = -(gby + gcy + gdy);
+        const Real gaz = -(gbz + gcz + gdz);
+        const Real cval = (gdx * dax + gdy * day + gdz * daz) - rv[i];
+        const Real denom = gax * gax + gay * gay + gaz * gaz
+                         + gbx * gbx + gby * gby + gbz * gbz
+                         + gcx * gcx + gcy * gcy + gcz * gcz
+                         + gdx * gdx + gdy * gdy + gdz * gdz;
+        const Real mm = (Real)0.5 + copysign((Real)0.5, denom - (Real)1e-18);
+        const Real sc = -mm * kv * cval / (denom + ((Real)1 - mm));
+        put_slot(m, sl.x, sc, gax, gay, gaz);
+        put_slot(m, sl.y, sc, gbx, gby, gbz);
+        put_slot(m, sl.z, sc, gcx, gcy, gcz);
+        put_slot(m, sl.w, sc, gdx, gdy, gdz);
+        if (mm == (Real)0) {
+            if (sl.x >= 0) atomicAdd(&m.deg[id.x], 1);
+            if (sl.y >= 0) atomicAdd(&m.deg[id.y], 1);
+            if (sl.z >= 0) atomicAdd(&m.deg[id.z], 1);
+            if (sl.w >= 0) atomicAdd(&m.deg[id.w], 1);
+        }
+    }
+}
+
+template <typename Real>
+__device__ void p1_atts(const TsDevProg &P, const Smem<Real> &m, const TsChunk &ch) {
+    using V4 = typename R4<Real>::T;
+    const int4 *idx = P.att_idx + ch.item_begin;
+    const int4 *slot = P.att_slot + ch.item_begin;
+    const V4 *par = reinterpret_cast<const V4 *>(P.att_par) + ch.item_begin;
+    const V4 *anc = reinterpret_cast<const V4 *>(P.att_anchor) + ch.item_begin;
+    for (int i = threadIdx.x; i < ch.item_count; i += blockDim.x) {
+        const int4 id = idx[i];
+        const int4 sl = slot[i];
+        const V4 pr = par[i];   // rest, k, wv, wc
+        const V4 an = anc[i];   // ax, ay, az, is_face
+        const bool face = an.w != (Real)0;
+        Real cx, cy, cz;
+        if (face) {
+            cx = (m.xs[id.y] + m.xs[id.z] + m.xs[id.w]) / (Real)3;
+            cy = (m.ys[id.y] + m.ys[id.z] + m.ys[id.w]) / (Real)3;
+            cz = (m.zs[id.y] + m.zs[id.z] + m.zs[id.w]) / (Real)3;
+        } else { cx = an.x; cy = an.y; cz = an.z; }
+        const Real wsum = pr.z + pr.w;
+        const Real dx = m.xs[id.x] - cx, dy = m.ys[id.x] - cy, dz = m.zs[id.x] - cz;
+        const Real dist = sqrt(dx * dx + dy * dy + dz * dz);
+        const Real mm = dist > (Real)1e-12 ? (Real)1 : (Real)0;
+        const Real scale = mm * pr.y * (dist - pr.x) / (dist * wsum + ((Real)1 - mm));
+        const Real ca = -pr.z * scale;
+        put_slot(m, sl.x, ca, dx, dy, dz);
+        if (face) {
+            const Real cb = pr.w * scale / (Real)3;
+            put_slot(m, sl.y, cb, dx, dy, dz);
+            put_slot(m, sl.z, cb, dx, dy, dz);
+            put_slot(m, sl.w, cb, dx, dy, dz);
+        }
+        if (mm == (Real)0) {
+            if (sl.x >= 0) atomicAdd(&m.deg[id.x], 1);
+            if (face) {
+                if (sl.y >= 0) atomicAdd(&m.deg[id.y], 1);
+                if (sl.z >= 0) atomicAdd(&m.deg[id.z], 1);
+                if (sl.w >= 0) atomicAdd(&m.deg[id.w], 1);
+            }
+        }
+    }
+}
+
+// tool command + grasp release + capsule rows for one env (thread 0), tool.py:307-378
+static __device__ __noinline__ void t0_command(const TsDevProg &P, const TsParams &S, const TsLaunch &L, int64_t env, Scal &sc) {
+    const int mode = L.mode;
+    Pose p;
+    const bool has_tool = L.axis != nullptr;
+    if (has_tool) {
+        for (int c = 0; c < 3; ++c) { p.ax[c] = L.axis[3 * env + c]; p.jw[c] = L.jaw[3 * env + c]; }
+        p.reach = L.reach[env]; p.clamp = L.clamp[env];
+    }
+    bool clipped = false, rejected = false;
+    if (mode & TS_M_CMD_ACTIONS) {
+        double tgt[3];
+        for (int c = 0; c < 3; ++c) {
+            double a = L.actions_f32 ? (double)reinterpret_cast<const float *>(L.actions)[3 * env + c]
+                                     : reinterpret_cast<const double *>(L.actions)[3 * env + c];
+            a = a > 1.0 ? 1.0 : (a < -1.0 ? -1.0 : a);   // np.clip(actions, -1, 1)
+            tgt[c] = (S.rcm[c] + p.reach * p.ax[c]) + a * S.action_scale;
+        }
+        apply_command(S, p, tgt, S.held_angle, clipped, rejected);
+    } else if (mode & TS_M_CMD_TARGETS) {
+        double tgt[3] = {L.targets[3 * env], L.targets[3 * env + 1], L.targets[3 * env + 2]};
+        apply_command(S, p, tgt, L.angles ? L.angles[env] : p.clamp, clipped, rejected);
+    } else if (mode & TS_M_CMD_OVERRIDE) {
+        for (int c = 0; c < 3; ++c) { p.ax[c] = L.ovr_axis[3 * env + c]; p.jw[c] = L.ovr_jaw[3 * env + c]; }
+        p.reach = L.ovr_reach[env]; p.clamp = L.ovr_clamp[env];
+        clipped = L.ovr_clipped ? L.ovr_clipped[env] != 0 : false;
+    }
+    sc.clipped = clipped; sc.rejected = rejected;
+    int64_t gv = -1;
+    if (mode & TS_M_EXT_GRASP) {
+        gv = L.ext_gv[env];
+        for (int c = 0; c < 3; ++c) sc.drag[c] = L.ext_drag[3 * env + c];
+    } else if (has_tool) {
+        gv = L.grasp_vertex[env];
+        for (int c = 0; c < 3; ++c) sc.drag[c] = S.rcm[c] + p.reach * p.ax[c];
+    }
+    sc.need_search = 0;
+    if (mode & TS_M_GRASP) {
+        if (p.clamp >= 3.0) {            // GRASP_ENGAGE_DEG, tool.py:23, 374-378
+            if (gv >= 0) { L.grasped[env * P.V + gv] = 0; gv = -1; }
+        } else if (gv < 0) {
+            sc.need_search = 1;
+        }
+    }
+    sc.gv_orig = (int)gv;
+    sc.pose = p;
+    if (mode & TS_M_DETECT_ONLY) {
+        for (int r = 0; r < 3; ++r) for (int k = 0; k < 7; ++k) sc.caps[r][k] = L.ext_caps[(env * 3 + r) * 7 + k];
+    } else if (mode & TS_M_CONTACTS) {
+        capsule_rows(S, p, sc.caps);
+    }
+    sc.diverged = 0; sc.n_contacts = 0;
+}
+
+// reward / done / auto-reset / obs for one env (thread 0, fp64), env.py:160-197
+static __device__ __noinline__ void t0_env(const TsParams &S, const TsLaunch &L, int64_t env, int any_bad, Scal &sc) {
+    const int mode = L.mode;
+    Pose p = sc.pose;
+    const int64_t gv_new = sc.gv_orig;
+    int done = 0;
+    if (mode & TS_M_ENV) {
+        double drag[3], rel[3];
+        for (int c = 0; c < 3; ++c) { drag[c] = S.rcm[c] + p.reach * p.ax[c]; rel[c] = drag[c] - S.target[c]; }
+        // np.einsum("nq,nq->n") association on the reference hosts: (r0^2 + r2^2) + r1^2
+        const double l = sqrt((rel[0] * rel[0] + rel[2] * rel[2]) + rel[1] * rel[1]);
+        const bool success = l < S.success_thr;
+        const double lp = L.l_prev[env];
+        const double reward = S.reward_scale * (S.w_l * l + S.w_d * (l - lp) + S.w_s * (success ? 1.0 : 0.0));
+        const int64_t steps = L.steps[env] + 1;
+        const double ret = L.ep_return[env] + reward;
+        const bool div = any_bad != 0;
+        const bool term = success && !div;
+        const bool trunc = !term && (steps >= S.max_steps || div);
+        done = term || trunc;
+        if (L.reward) L.reward[env] = reward;
+        if (L.terminated) L.terminated[env] = term;
+        if (L.truncated) L.truncated[env] = trunc;
+        if (L.distance) L.distance[env] = l;
+        if (L.success) L.success[env] = success;
+        if (L.diverged) L.diverged[env] = div;
+        if (L.clipped) L.clipped[env] = sc.clipped;
+        if (L.contacts) L.contacts[env] = sc.n_contacts;
+        if (L.ret_out) L.ret_out[env] = ret;
+        if (L.len_out) L.len_out[env] = steps;
+        if (L.done_mask) L.done_mask[env] = done;
+        double o[6];
+        for (int c = 0; c < 3; ++c) { o[c] = 2.0 * (drag[c] - S.lo[c]) / (S.hi[c] - S.lo[c]) - 1.0; o[3 + c] = S.target_obs[c]; }
+        if (L.final_obs) {
+            for (int c = 0; c < 6; ++c) {
+                const double val = done ? o[c] : 0.0;
+                if (L.obs_f64) reinterpret_cast<double *>(L.final_obs)[6 * env + c] = val;
+                else reinterpret_cast<float *>(L.final_obs)[6 * env + c] = (float)val;
+            }
+        }
+        if (done) {
+            for (int c = 0; c < 3; ++c) { p.ax[c] = S.start_axis[c]; p.jw[c] = S.start_jaw[c]; }
+            p.reach = S.start_reach; p.clamp = S.start_clamp;
+            for (int c = 0; c < 3; ++c) o[c] = 2.0 * ((S.rcm[c] + p.reach * p.ax[c]) - S.lo[c]) / (S.hi[c] - S.lo[c]) - 1.0;
+            L.steps[env] = 0; L.ep_return[env] = 0.0; L.l_prev[env] = S.start_distance;
+        } else {
+            L.steps[env] = steps; L.ep_return[env] = ret; L.l_prev[env] = l;
+        }
+        if (L.obs) {
+            for (int c = 0; c < 6; ++c) {
+                if (L.obs_f64) reinterpret_cast<double *>(L.obs)[6 * env + c] = o[c];
+                else reinterpret_cast<float *>(L.obs)[6 * env + c] = (float)o[c];
+            }
+        }
+    } else {
+        if (L.diverged) L.diverged[env] = any_bad != 0;
+        if (L.clipped) L.clipped[env] = sc.clipped;
+        if (L.rejected) L.rejected[env] = sc.rejected;
+        if (L.contacts) L.contacts[env] = sc.n_contacts;
+    }
+    if (L.axis != nullptr && !(mode & TS_M_DETECT_ONLY) && !(mode & TS_M_EXT_GRASP)) {
+        for (int c = 0; c < 3; ++c) { L.axis[3 * env + c] = p.ax[c]; L.jaw[3 * env + c] = p.jw[c]; }
+        L.reach[env] = p.reach; L.clamp[env] = p.clamp;
+        L.grasp_vertex[env] = done ? -1 : gv_new;
+    }
+    sc.done = done;
+}
+
+// ---------------------------------------------------------------------------
+// the fused step kernel
+// ---------------------------------------------------------------------------
+template <typename Real, int VPT>
+__global__ void __launch_bounds__(512, sizeof(Real) == 4 ? 2 : 1) step_kernel(const __grid_constant__ TsDevProg P,
+                                                   const __grid_constant__ TsParams S,
+                                                   const __grid_constant__ TsLaunch L) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const Smem<Real> m = carve<Real>(P, smem_raw);
+    Scal &sc = *m.sc;
+    const int t = threadIdx.x;
+    const int B = blockDim.x;
+    const int lane = t & 31;
+    const int mode = L.mode;
+    const Real h = (Real)S.h, damp = (Real)S.damp;
+    const Real gx = (Real)S.g[0], gy = (Real)S.g[1], gz = (Real)S.g[2];
+    const Real ks = (Real)S.ks, kv = (Real)S.kv;
+    const Real *wst = reinterpret_cast<const Real *>(P.w);
+    const Real *rest = reinterpret_cast<const Real *>(P.rest);
+
+    if ((mode & TS_M_CHECK_ACTIONS) && *L.bad_flag) return;   // deferred ValidationError: no state change
+
+    for (int64_t env = blockIdx.x; env < L.n_env; env += gridDim.x) {
+        Real *xg = reinterpret_cast<Real *>(L.x) + env * (int64_t)P.V * 3;
+        Real *vg = reinterpret_cast<Real *>(L.v) + env * (int64_t)P.V * 3;
+
+        // ---- A. tool command (thread 0) overlapped with the state load ----
+        if (t == 0) t0_command(P, S, L, env, sc);
+        // state -> shared (storage order) / registers
+        for (int p = t; p < P.Vstore; p += B) {
+            const int o = P.s2o[p];
+            Real a = 0, b = 0, c = 0;
+            if (o >= 0) { a = xg[3 * o]; b = xg[3 * o + 1]; c = xg[3 * o + 2]; }
+            m.xs[p] = a; m.ys[p] = b; m.zs[p] = c;
+        }
+        Real vx[VPT], vy[VPT], vz[VPT];
+#pragma unroll
+        for (int r = 0; r < VPT; ++r) {
+            const int p = r * B + t;
+            vx[r] = vy[r] = vz[r] = 0;
+            if (p < P.Vf) {
+                const int o = P.s2o[p];
+                vx[r] = vg[3 * o]; vy[r] = vg[3 * o + 1]; vz[r] = vg[3 * o + 2];
+            }
+        }
+        for (int p = t; p < P.Vf_pad; p += B) m.deg[p] = 0;
+        for (int i = t; i < P.cbits_words; i += B) m.cbits[i] = 0u;
+        __syncthreads();
+
+        if (t < 3 && (mode & (TS_M_CONTACTS | TS_M_DETECT_ONLY))) make_cap<Real>(sc.caps[t], m.caps[t]);
+        // ---- B. grasp search: nearest free vertex (tool.py:380-389) ------
+        if (sc.need_search) {
+            double bk = INFINITY;
+            int bi = 0x7fffffff;
+            for (int p = t; p < P.Vf; p += B) {
+                const double r0 = (double)m.xs[p] - sc.drag[0];
+                const double r1 = (double)m.ys[p] - sc.drag[1];
+                const double r2 = (double)m.zs[p] - sc.drag[2];
+                double d2 = r0 * r0 + r1 * r1 + r2 * r2;
+                if (isnan(d2)) d2 = -INFINITY;      // numpy argmin returns the first NaN
+                const int o = P.s2o[p];
+                if (d2 < bk || (d2 == bk && o < bi)) { bk = d2; bi = o; }
+            }
+            for (int off = 16; off > 0; off >>= 1) {
+                const double ok = __shfl_xor_sync(0xffffffffu, bk, off);
+                const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+                if (ok < bk || (ok == bk && oi < bi)) { bk = ok; bi = oi; }
+            }
+            if (lane == 0) { sc.red_key[t >> 5] = bk; sc.red_idx[t >> 5] = bi; }
+            __syncthreads();
+            if (t == 0) {
+                for (int wi = 1; wi < (B >> 5); ++wi) {
+                    if (sc.red_key[wi] < bk || (sc.red_key[wi] == bk && sc.red_idx[wi] < bi)) {
+                        bk = sc.red_key[wi]; bi = sc.red_idx[wi];
+                    }
+                }
+                if (bi != 0x7fffffff && bk != -INFINITY && bk <= S.grasp_r2) {
+                    sc.gv_orig = bi;
+                    L.grasped[env * P.V + bi] = 1;
+                }
+            }
+            __syncthreads();
+        }
+        // grasp vertex in storage order (any vertex; pinned ones are never applied)
+        const int gvs = sc.gv_orig >= 0 ? P.o2s[sc.gv_orig] : -1;
+
+        // ---- C. substeps ---------------------------------------------------
+        if (mode & TS_M_SUBSTEPS) {
+            Real xr[VPT], yr[VPT], zr[VPT], accx[VPT], accy[VPT], accz[VPT];
+            int ndeg[VPT], gcnt[VPT];
+#pragma unroll
+            for (int r = 0; r < VPT; ++r) {
+                const int p = r * B + t;
+                accx[r] = accy[r] = accz[r] = 0; ndeg[r] = 0; gcnt[r] = 0;
+                xr[r] = yr[r] = zr[r] = 0;
+                if (p < P.Vf) {
+                    // predict for substep 0 (ts_lane_predict, _kernels.pyx:63-87)
+                    vx[r] += h * gx; xr[r] = m.xs[p] + h * vx[r];
+                    vy[r] += h * gy; yr[r] = m.ys[p] + h * vy[r];
+                    vz[r] += h * gz; zr[r] = m.zs[p] + h * vz[r];
+                    m.xs[p] = xr[r]; m.ys[p] = yr[r]; m.zs[p] = zr[r];
+                }
+            }
+            __syncthreads();
+            const double d0 = sc.drag[0], d1 = sc.drag[1], d2 = sc.drag[2];
+            for (int s = 0; s < S.substeps; ++s) {
+                for (int c = 0; c <= P.n_chunks; ++c) {
+                    // grasp contribution goes after all edge slots (_kernels.pyx:283-298)
+                    if (c == P.grasp_chunk) {
+#pragma unroll
+                        for (int r = 0; r < VPT; ++r) {
+                            const int p = r * B + t;
+                            if (p < P.Vf && p == gvs) {
+                                const Real dx = (Real)(d0 - (double)xr[r]);
+                                const Real dy = (Real)(d1 - (double)yr[r]);
+                                const Real dz = (Real)(d2 - (double)zr[r]);
+                                const Real dist = sqrt(dx * dx + dy * dy + dz * dz);
+                                if (!(dist <= (Real)1e-12)) { accx[r] += dx; accy[r] += dy; accz[r] += dz; gcnt[r] = 1; }
+                            }
+                        }
+                    }
+                    if (c == P.n_chunks) break;
+                    const TsChunk ch = P.chunks[c];
+                    if (ch.kind == TS_CHUNK_EDGE) p1_edges<Real>(P, m, ch, ks);
+                    else if (ch.kind == TS_CHUNK_TET) p1_tets<Real>(P, m, ch, kv);
+                    else p1_atts<Real>(P, m, ch);
+                    __syncthreads();
+                    // phase 2: owner gathers its slots in reference order
+#pragma unroll
+                    for (int r = 0; r < VPT; ++r) {
+                        const int p = r * B + t;
+                        if (p < P.Vf) {
+                            const int base = P.region[ch.region_off + (p >> 5)] + lane;
+                            const int val = P.valence[ch.val_off + p];
+                            Real ax = accx[r], ay = accy[r], az = accz[r];
+                            for (int k = 0; k < val; ++k) {
+                                const int sidx = base + 32 * k;
+                                ax += m.slx[sidx]; ay += m.sly[sidx]; az += m.slz[sidx];
+                            }
+                            accx[r] = ax; accy[r] = ay; accz[r] = az;
+                            const int dg = m.deg[p];
+                            if (dg) { ndeg[r] += dg; m.deg[p] = 0; }
+                        }
+                    }
+                    if (c + 1 < P.n_chunks) __syncthreads();   // slots are reused by the next chunk
+                }
+                // apply (ts_lane_apply, _kernels.pyx:213-244) + next predict
+#pragma unroll
+                for (int r = 0; r < VPT; ++r) {
+                    const int p = r * B + t;
+                    if (p < P.Vf) {
+                        const Real n = (Real)(P.static_cnt[p] - ndeg[r] + gcnt[r]);
+                        const Real mm = (Real)0.5 + copysign((Real)0.5, n - (Real)0.5);
+                        const Real inv = mm / (n + ((Real)1 - mm));
+                        const Real e0 = accx[r] * inv, e1 = accy[r] * inv, e2 = accz[r] * inv;
+                        xr[r] += e0; vx[r] += e0 / h;
+                        yr[r] += e1; vy[r] += e1 / h;
+                        zr[r] += e2; vz[r] += e2 / h;
+                        if (damp != (Real)1) { vx[r] *= damp; vy[r] *= damp; vz[r] *= damp; }
+                        if (s + 1 < S.substeps) {
+                            vx[r] += h * gx; xr[r] += h * vx[r];
+                            vy[r] += h * gy; yr[r] += h * vy[r];
+                            vz[r] += h * gz; zr[r] += h * vz[r];
+                        }
+                        m.xs[p] = xr[r]; m.ys[p] = yr[r]; m.zs[p] = zr[r];
+                        accx[r] = accy[r] = accz[r] = 0; ndeg[r] = 0; gcnt[r] = 0;
+                    }
+                }
+                __syncthreads();
+            }
+        }
+
+        // ---- D. contacts ---------------------------------------------------
+        if ((mode & (TS_M_CONTACTS | TS_M_DETECT_ONLY)) && P.F > 0) {
+            Cap<Real> *C = m.caps;   // built by threads 0..2 before the substeps
+            Real *rec = m.slx;   // 3F records x 7 reals (the slot buffer is free now)
+            for (int f = t; f < P.F; f += B) {
+                const int ia = P.faces[3 * f], ib = P.faces[3 * f + 1], ic = P.faces[3 * f + 2];
+                const Real pa[3] = {m.xs[ia], m.ys[ia], m.zs[ia]};
+                const Real pb[3] = {m.xs[ib], m.ys[ib], m.zs[ib]};
+                const Real pc[3] = {m.xs[ic], m.ys[ic], m.zs[ic]};
+#pragma unroll
+                for (int ci = 0; ci < 3; ++ci) {
+                    bool skip = false;
+                    for (int k = 0; k < 3; ++k) {
+                        const Real tlo = cmin(cmin(pa[k], pb[k]), pc[k]);
+                        const Real thi = cmax(cmax(pa[k], pb[k]), pc[k]);
+                        if (thi < C[ci].lo[k] || tlo > C[ci].hi[k]) { skip = true; break; }
+                    }
+                    if (skip) continue;
+                    Real dir[3], bary[3];
+                    const Real sd = witness<Real>(C[ci], pa, pb, pc, S.contact_iters, dir, bary);
+                    if (sd < (Real)0) {
+                        const int key = ci * P.F + f;
+                        Real *q = rec + 7 * key;
+                        q[0] = -sd; q[1] = dir[0]; q[2] = dir[1]; q[3] = dir[2];
+                        q[4] = bary[0]; q[5] = bary[1]; q[6] = bary[2];
+                        atomicOr(&m.cbits[key >> 5], 1u << (key & 31));
+                    }
+                }
+            }
+            __syncthreads();
+            if (t == 0) {
+                int count = 0;
+                for (int wi = 0; wi < P.cbits_words; ++wi) {
+                    unsigned bits = m.cbits[wi];
+                    while (bits) {
+                        const int b = __ffs(bits) - 1;
+                        bits &= bits - 1;
+                        const int key = wi * 32 + b;
+                        const int ci = key / P.F, f = key - ci * P.F;
+                        const Real *q = rec + 7 * key;
+                        if (mode & TS_M_DETECT_ONLY) {
+                            const int64_t row = env * 3 * (int64_t)P.F + count;
+                            L.det_face[row] = f; L.det_cap[row] = ci; L.det_depth[row] = (double)q[0];
+                            for (int k = 0; k < 3; ++k) { L.det_dir[3 * row + k] = (double)q[1 + k]; L.det_bary[3 * row + k] = (double)q[4 + k]; }
+                        } else {
+                            // collision.resolve_contact_arrays, sequential in emission order
+                            const Real b0 = q[4], b1 = q[5], b2 = q[6];
+                            const Real bb = fused_sq3<Real>(b0, b1, b2);
+                            if (bb > (Real)0) {
+                                const Real sc_ = (Real)S.k_contact * q[0] / bb;
+                                const Real px = sc_ * q[1], py = sc_ * q[2], pz = sc_ * q[3];
+                                const Real bj[3] = {b0, b1, b2};
+                                for (int j = 0; j < 3; ++j) {
+                                    const int vs = P.faces[3 * f + j];
+                                    if (wst[vs] > (Real)0) {
+                                        m.xs[vs] += bj[j] * px; m.ys[vs] += bj[j] * py; m.zs[vs] += bj[j] * pz;
+                                    }
+                                }
+                            }
+                        }
+                        ++count;
+                    }
+                }
+                sc.n_contacts = count;
+                if (mode & TS_M_DETECT_ONLY) L.det_count[env] = count;
+            }
+            __syncthreads();
+        }
+
+        // ---- E. divergence guard (solver.py:357-359) ----------------------
+        int bad = 0;
+        for (int p = t; p < P.Vstore; p += B)
+            bad |= !(isfinite(m.xs[p]) && isfinite(m.ys[p]) && isfinite(m.zs[p]));
+        const int any_bad = __syncthreads_or(bad);
+
+        // ---- F. env logic (thread 0, fp64; env.py:160-197) ----------------
+        if (t == 0) t0_env(S, L, env, any_bad, sc);
+        __syncthreads();
+
+        // ---- G. write back --------------------------------------------------
+        if (!(mode & TS_M_DETECT_ONLY)) {
+            const bool done = sc.done != 0;
+            if (done)
+                for (int i = t; i < P.V; i += B) L.grasped[env * P.V + i] = 0;
+#pragma unroll
+            for (int r = 0; r < VPT; ++r) {
+                const int p = r * B + t;
+                if (p < P.Vf) {
+                    const int o = P.s2o[p];
+                    if (done) {
+                        xg[3 * o] = rest[3 * o]; xg[3 * o + 1] = rest[3 * o + 1]; xg[3 * o + 2] = rest[3 * o + 2];
+                        vg[3 * o] = 0; vg[3 * o + 1] = 0; vg[3 * o + 2] = 0;
+                    } else {
+                        xg[3 * o] = m.xs[p]; xg[3 * o + 1] = m.ys[p]; xg[3 * o + 2] = m.zs[p];
+                        vg[3 * o] = vx[r]; vg[3 * o + 1] = vy[r]; vg[3 * o + 2] = vz[r];
+                    }
+                }
+            }
+            for (int p = P.Vf_pad + t; p < P.Vstore; p += B) {
+                const int o = P.s2o[p];
+                if (o < 0) continue;
+                if (done) { xg[3 * o] = rest[3 * o]; xg[3 * o + 1] = rest[3 * o + 1]; xg[3 * o + 2] = rest[3 * o + 2]; }
+                else if (mode & TS_M_CONTACTS) { xg[3 * o] = m.xs[p]; xg[3 * o + 1] = m.ys[p]; xg[3 * o + 2] = m.zs[p]; }
+                if (mode & TS_M_SUBSTEPS || done) { vg[3 * o] = 0; vg[3 * o + 1] = 0; vg[3 * o + 2] = 0; }
+            }
+        }
+        __syncthreads();   // shared scalars are reused by the next environment
+    }
+}
+
+// ---------------------------------------------------------------------------
+// reset / observe (EnvBatch.reset, env.py:123-142) -- one thread per (env, vertex)
+// ---------------------------------------------------------------------------
+template <typename Real>
+__global__ void reset_kernel(const TsDevProg P, const TsParams S, const TsLaunch L, const uint8_t *mask,
+                             int observe_only) {
+    const int64_t n = L.n_env;
+    const int64_t V = P.V;
+    const Real *rest = reinterpret_cast<const Real *>(P.rest);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n * V; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t env = i / V, vtx = i - env * V;
+        const bool sel = !observe_only && (mask == nullptr || mask[env] != 0);
+        if (sel) {
+            Real *x = reinterpret_cast<Real *>(L.x) + 3 * i;
+            Real *v = reinterpret_cast<Real *>(L.v) + 3 * i;
+            x[0] = rest[3 * vtx]; x[1] = rest[3 * vtx + 1]; x[2] = rest[3 * vtx + 2];
+            v[0] = 0; v[1] = 0; v[2] = 0;
+            L.grasped[i] = 0;
+        }
+        if (vtx == 0) {
+            if (sel) {
+                for (int c = 0; c < 3; ++c) { L.axis[3 * env + c] = S.start_axis[c]; L.jaw[3 * env + c] = S.start_jaw[c]; }
+                L.reach[env] = S.start_reach; L.clamp[env] = S.start_clamp;
+                L.grasp_vertex[env] = -1;
+                if (L.steps) L.steps[env] = 0;
+                if (L.ep_return) L.ep_return[env] = 0.0;
+                if (L.l_prev) L.l_prev[env] = S.start_distance;
+            }
+            if (L.obs) {
+                double ax[3], reach;
+                if (sel) { for (int c = 0; c < 3; ++c) ax[c] = S.start_axis[c]; reach = S.start_reach; }
+                else { for (int c = 0; c < 3; ++c) ax[c] = L.axis[3 * env + c]; reach = L.reach[env]; }
+                for (int c = 0; c < 6; ++c) {
+                    const double val = c < 3 ? 2.0 * ((S.rcm[c] + reach * ax[c]) - S.lo[c]) / (S.hi[c] - S.lo[c]) - 1.0
+                                             : S.target_obs[c - 3];
+                    if (L.obs_f64) reinterpret_cast<double *>(L.obs)[6 * env + c] = val;
+                    else reinterpret_cast<float *>(L.obs)[6 * env + c] = (float)val;
+                }
+            }
+        }
+    }
+}
+
+}  // namespace tsk
+
+// ---------------------------------------------------------------------------
+// launchers (instantiated per precision in step_f32.cu / step_f64.cu)
+// ---------------------------------------------------------------------------
+template <typename Real>
+cudaError_t ts_launch_step(const TsDevProg &P, const TsParams &S, const TsLaunch &L, int grid, int smem,
+                           cudaStream_t stream) {
+    void (*fn)(const TsDevProg, const TsParams, const TsLaunch) = nullptr;
+    switch (P.VPT) {
+        case 1: fn = tsk::step_kernel<Real, 1>; break;
+        case 2: fn = tsk::step_kernel<Real, 2>; break;
+        case 4: fn = tsk::step_kernel<Real, 4>; break;
+        case 8: fn = tsk::step_kernel<Real, 8>; break;
+        default:
+            if (P.VPT == 3) fn = tsk::step_kernel<Real, 4>;
+            else if (P.VPT <= 8) fn = tsk::step_kernel<Real, 8>;
+            else return cudaErrorInvalidValue;
+    }
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    fn<<<grid, P.B, smem, stream>>>(P, S, L);
+    return cudaGetLastError();
+}
+
+template <typename Real>
+cudaError_t ts_launch_reset(const TsDevProg &P, const TsParams &S, const TsLaunch &L, const uint8_t *mask,
+                            int observe_only, cudaStream_t stream) {
+    const int64_t total = L.n_env * (int64_t)(P.V > 0 ? P.V : 1);
+    int grid = (int)((total + 255) / 256);
+    if (grid > 65535 * 4) grid = 65535 * 4;
+    if (grid < 1) grid = 1;
+    tsk::reset_kernel<Real><<<grid, 256, 0, stream>>>(P, S, L, mask, observe_only);
+    return cudaGetLastError();
+}

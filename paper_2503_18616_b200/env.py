@@ -1,0 +1,283 @@
+"""Batched episodic reach task on the GPU -- drop-in for the reference ``EnvBatch`` (env.py:70-197).
+
+Same constructor, ``reset``/``step``/``observe``, attributes and error
+behaviour; the return values are CUDA tensors:
+
+* observations (N, 6): float32 (``precision="fp32"``, the policy dtype) or
+  float64 (``precision="fp64"``), overridable with ``obs_dtype``;
+* rewards (N,) float64; terminated / truncated (N,) bool;
+* ``info``: ``distance, success, diverged, clipped, contacts, episode_return,
+  episode_length, done_mask, final_observation`` (+ ``contacts_per_env``).
+  ``final_observation`` is always an (N, 6) tensor whose rows are zero where
+  ``done_mask`` is false (the reference returns None when no row is done);
+  ``contacts`` is evaluated lazily so a step never blocks the host.
+
+Every call to ``step`` is one launch of the fused sm_100a kernel
+(``csrc/step_kernel.cuh``), plus a one-block action check when the actions
+are already on the device and ``validate=True``.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .errors import ValidationError
+from .mesh import SceneConfig, load_scene
+from .solver import LazyInt, Simulation, _override_struct
+
+OBSERVATION_SIZE = 6
+ACTION_SIZE = 3
+
+
+@dataclass
+class EnvConfig:
+    """env.py:24-58."""
+
+    w_distance: float = -1.0
+    w_delta: float = -10.0
+    w_success: float = 100.0
+    success_threshold: float = 0.003
+    max_episode_steps: int = 200
+    action_scale: float = 0.005
+    reward_scale: float = 1.0
+    start: np.ndarray = field(default_factory=lambda: np.zeros(3))
+    target: np.ndarray = field(default_factory=lambda: np.zeros(3))
+    workspace_low: np.ndarray = field(default_factory=lambda: -np.ones(3))
+    workspace_high: np.ndarray = field(default_factory=lambda: np.ones(3))
+    held_clamp_angle: float = 2.0
+
+    @classmethod
+    def from_scene(cls, cfg: SceneConfig):
+        out = cls(w_distance=cfg.reward_distance_weight, w_delta=cfg.reward_delta_weight,
+                  w_success=cfg.reward_success_weight, success_threshold=cfg.success_threshold,
+                  max_episode_steps=cfg.max_episode_steps, action_scale=cfg.action_scale,
+                  reward_scale=cfg.reward_scale, start=np.asarray(cfg.tool_start, np.float64),
+                  target=np.asarray(cfg.target, np.float64),
+                  workspace_low=np.asarray(cfg.workspace_low, np.float64),
+                  workspace_high=np.asarray(cfg.workspace_high, np.float64),
+                  held_clamp_angle=cfg.clamp_angle)
+        for name, p in (("tool_start", out.start), ("target", out.target)):
+            if np.any(p < out.workspace_low) or np.any(p > out.workspace_high):
+                raise ValidationError(f"{name} lies outside the workspace box")
+        return out
+
+
+def compute_reward(distance, delta, success, cfg: EnvConfig):
+    """env.py:61-67 (numpy or torch)."""
+    if isinstance(distance, torch.Tensor):
+        s = success.to(torch.float64) if isinstance(success, torch.Tensor) else torch.as_tensor(success, dtype=torch.float64)
+    else:
+        s = np.asarray(success, dtype=np.float64)
+    return cfg.reward_scale * (cfg.w_distance * distance + cfg.w_delta * delta + cfg.w_success * s)
+
+
+class StepInfo(dict):
+    """info dict whose ``contacts`` total is computed on first access."""
+
+    def __getitem__(self, key):
+        val = dict.__getitem__(self, key)
+        return val.value() if isinstance(val, LazyInt) else val
+
+
+# output buffer layout of one step: (name, dtype, trailing shape)
+_OUTS = [("reward", torch.float64, ()), ("distance", torch.float64, ()),
+         ("episode_return", torch.float64, ()), ("episode_length", torch.int64, ()),
+         ("obs", None, (OBSERVATION_SIZE,)), ("final_obs", None, (OBSERVATION_SIZE,)),
+         ("contacts", torch.int32, ()), ("terminated", torch.bool, ()), ("truncated", torch.bool, ()),
+         ("success", torch.bool, ()), ("diverged", torch.bool, ()), ("clipped", torch.bool, ()),
+         ("done_mask", torch.bool, ())]
+
+
+class EnvBatch:
+    """N independent reach-task instances stepped as one batch on one GPU."""
+
+    observation_size = OBSERVATION_SIZE
+    action_size = ACTION_SIZE
+
+    def __init__(self, scene, num_envs: int = 1, seed: int = 0, backend: str = "auto",
+                 mode: str = "deterministic", threads: int | None = None, device=None,
+                 precision: str = "fp32", obs_dtype=None, layout=None):
+        if isinstance(scene, str):
+            mesh, rest, cfg = load_scene(scene)
+        else:
+            mesh, rest, cfg = scene
+        if num_envs < 1:
+            raise ValidationError("num_envs must be >= 1")
+        self.scene_config = cfg
+        self.config = EnvConfig.from_scene(cfg)
+        self.sim = Simulation(mesh, rest, cfg, num_instances=num_envs, backend=backend, mode=mode,
+                              threads=threads, device=device, precision=precision, layout=layout)
+        self.num_envs = num_envs
+        self.device = self.sim.device
+        self.precision = self.sim.precision
+        if obs_dtype is None:
+            obs_dtype = torch.float64 if self.precision == "fp64" else torch.float32
+        if obs_dtype not in (torch.float32, torch.float64):
+            raise ValidationError("obs_dtype must be torch.float32 or torch.float64")
+        self.obs_dtype = obs_dtype
+        self._ready = False
+        self.seed_value = seed
+        self._rng = None
+        self._bad_flag = torch.zeros(1, dtype=torch.int32, device=self.device)
+        self._pinned_actions = None
+        self._dev_actions = None
+        self._layout = self._out_layout()
+
+    # -- reference-named state (views of the device state) ------------------
+    @property
+    def _steps(self):
+        return self.sim._steps
+
+    @property
+    def _l_prev(self):
+        return self.sim._l_prev
+
+    @property
+    def _return(self):
+        return self.sim._return
+
+    # -- helpers ------------------------------------------------------------
+    def _normalize(self, p):
+        lo = torch.as_tensor(self.config.workspace_low, dtype=torch.float64, device=self.device)
+        hi = torch.as_tensor(self.config.workspace_high, dtype=torch.float64, device=self.device)
+        if not isinstance(p, torch.Tensor):
+            p = torch.as_tensor(np.asarray(p, np.float64), device=self.device)
+        return 2.0 * (p - lo) / (hi - lo) - 1.0
+
+    def _distances(self, idx=None):
+        drag = self.sim.tool.drag_points()
+        if idx is not None:
+            drag = drag[torch.as_tensor(np.atleast_1d(idx), device=self.device)]
+        rel = drag - torch.as_tensor(self.config.target, dtype=torch.float64, device=self.device)[None, :]
+        return torch.sqrt((rel[:, 0] * rel[:, 0] + rel[:, 2] * rel[:, 2]) + rel[:, 1] * rel[:, 1])
+
+    def _observe_all(self):
+        obs = torch.empty((self.num_envs, OBSERVATION_SIZE), dtype=self.obs_dtype, device=self.device)
+        st = self.sim.state_struct()
+        with torch.cuda.device(self.device):
+            N.check(self.sim.scene.lib.ts_env_observe(self.sim.scene.handle, ctypes.byref(st), self.num_envs,
+                                                      N.ptr(obs), int(self.obs_dtype == torch.float64),
+                                                      self.sim.stream_ptr()), "ts_env_observe")
+        return obs
+
+    def _observe_rows(self, idx):
+        return self._observe_all()[torch.as_tensor(np.asarray(idx), device=self.device)]
+
+    def observe(self, instance: int):
+        return self._observe_all()[int(instance)]
+
+    # -- episodic API ---------------------------------------------------------
+    def reset(self, indices=None, seed=None):
+        """env.py:123-142: restore rows to rest, tool at start; returns their observations."""
+        n = self.num_envs
+        if seed is not None:
+            self.seed_value = seed
+        if self._rng is None or seed is not None:
+            # per-instance RNGs are reserved by the reference (unused): keep the seeding contract
+            self._rng = np.random.SeedSequence(self.seed_value).generate_state(n)
+        mask = None
+        idx = None
+        if indices is not None:
+            idx = np.atleast_1d(np.asarray(indices))
+            m = np.zeros(n, np.uint8)
+            m[idx] = 1
+            mask = torch.as_tensor(m, device=self.device)
+        obs = torch.empty((n, OBSERVATION_SIZE), dtype=self.obs_dtype, device=self.device)
+        st = self.sim.state_struct()
+        with torch.cuda.device(self.device):
+            N.check(self.sim.scene.lib.ts_env_reset(self.sim.scene.handle, ctypes.byref(st), n, N.ptr(mask),
+                                                    N.ptr(obs), int(self.obs_dtype == torch.float64),
+                                                    self.sim.stream_ptr()), "ts_env_reset")
+        self._ready = True
+        return obs if idx is None else obs[torch.as_tensor(idx, device=self.device)]
+
+    def _out_layout(self):
+        n = self.num_envs
+        off = 0
+        layout = []
+        for name, dt, shape in _OUTS:
+            dt = self.obs_dtype if dt is None else dt
+            numel = n * int(np.prod(shape)) if shape else n
+            nbytes = numel * torch.tensor([], dtype=dt).element_size()
+            layout.append((name, dt, (n, *shape), off, nbytes))
+            off += (nbytes + 15) // 16 * 16
+        return layout, off
+
+    def _alloc_outputs(self):
+        layout, total = self._layout
+        buf = torch.empty(total, dtype=torch.uint8, device=self.device)
+        return {name: buf[off:off + nb].view(dt).view(shape) for name, dt, shape, off, nb in layout}
+
+    def _stage_actions(self, actions):
+        """(device pointer, is_f32, keepalive) for actions; validates like env.py:151-160."""
+        n = self.num_envs
+        if isinstance(actions, torch.Tensor) and actions.is_cuda:
+            if tuple(actions.shape) != (n, ACTION_SIZE):
+                raise ValidationError(f"actions must have shape {(n, ACTION_SIZE)}, got {tuple(actions.shape)}")
+            a = actions
+            if a.device != self.device:
+                a = a.to(self.device)
+            if a.dtype not in (torch.float32, torch.float64):
+                a = a.to(torch.float64)
+            a = a.contiguous()
+            return a, a.dtype == torch.float32, True
+        a = np.asarray(actions.cpu().numpy() if isinstance(actions, torch.Tensor) else actions, dtype=np.float64)
+        if a.shape != (n, ACTION_SIZE):
+            raise ValidationError(f"actions must have shape {(n, ACTION_SIZE)}, got {a.shape}")
+        if not np.all(np.isfinite(a)):
+            raise ValidationError("actions must be finite")
+        if self._pinned_actions is None:
+            self._pinned_actions = torch.empty((n, ACTION_SIZE), dtype=torch.float64, pin_memory=True)
+            self._dev_actions = torch.empty((n, ACTION_SIZE), dtype=torch.float64, device=self.device)
+            self._copy_done = torch.cuda.Event()
+        else:
+            self._copy_done.synchronize()   # previous H2D copy must have drained the pinned buffer
+        self._pinned_actions.numpy()[...] = a
+        with torch.cuda.device(self.device):
+            self._dev_actions.copy_(self._pinned_actions, non_blocking=True)
+            self._copy_done.record()
+        return self._dev_actions, False, False
+
+    def step(self, actions, validate=True, tool_override=None):
+        """env.py:144-197 on the GPU.  Returns (obs, reward, terminated, truncated, info).
+
+        Device-resident actions are checked for finiteness on the GPU; with
+        ``validate=True`` the call then waits for that verdict so a bad batch
+        raises ``ValidationError`` before returning (no state is modified).
+        """
+        if not self._ready:
+            raise RuntimeError("step called before reset")
+        n = self.num_envs
+        a, is_f32, on_device = self._stage_actions(actions)
+        out = self._alloc_outputs()
+        so = N.StepOut()
+        for name in ("obs", "reward", "terminated", "truncated", "distance", "success", "diverged",
+                     "clipped", "contacts", "episode_return", "episode_length", "done_mask", "final_obs"):
+            setattr(so, name, N.ptr(out[name]))
+        so.obs_f64 = int(self.obs_dtype == torch.float64)
+        ovr = None
+        if tool_override is not None:
+            ovr, _keep = _override_struct(tool_override, n, self.device)
+        check = on_device and validate
+        st = self.sim.state_struct()
+        with torch.cuda.device(self.device):
+            N.check(self.sim.scene.lib.ts_env_step(
+                self.sim.scene.handle, ctypes.byref(st), n, N.ptr(a), int(is_f32), ctypes.byref(so),
+                ctypes.byref(ovr) if ovr is not None else None,
+                N.ptr(self._bad_flag) if check else None, self.sim.stream_ptr()), "ts_env_step")
+        if check and int(self._bad_flag.item()) != 0:
+            raise ValidationError("actions must be finite")
+        self.sim.step_count += 1
+        contacts = out["contacts"]
+        info = StepInfo(
+            distance=out["distance"], success=out["success"], diverged=out["diverged"],
+            clipped=out["clipped"], contacts=LazyInt(lambda: int(contacts.sum().item())),
+            contacts_per_env=contacts, episode_return=out["episode_return"],
+            episode_length=out["episode_length"], done_mask=out["done_mask"],
+            final_observation=out["final_obs"])
+        return out["obs"], out["reward"], out["terminated"], out["truncated"], info

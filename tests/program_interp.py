@@ -1,0 +1,152 @@
+"""CPU interpreter of a compiled scene program (test infrastructure).
+
+Executes the kernel's substep data flow -- phase 1 (constraint corrections
+into slots) and phase 2 (owner gathers its slots in slot order) -- in numpy
+float64 straight from the program blob the sm_100a kernel consumes.  Because
+the arithmetic is plain IEEE fp64, the result must be bitwise equal to the
+oracle's (and so the reference's) substeps iff the compiler's slot layout,
+per-vertex order, counts and chunking are right.  This pins the scene
+compiler without a GPU.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+SECTIONS = ["CHUNK", "EDGE_IDX", "EDGE_PAR", "TET_IDX", "TET_SLOT", "TET_RV", "ATT_IDX", "ATT_SLOT",
+            "ATT_PAR", "ATT_ANCHOR", "REGION", "VALENCE", "STATIC_CNT", "S2O", "O2S", "W", "FACES",
+            "FACES_ORIG", "REST"]
+HDR_FIELDS = ["magic", "version", "real_bytes", "n_sections", "V", "Vf", "Vf_pad", "Vstore", "F", "B",
+              "VPT", "G", "n_chunks", "grasp_chunk", "slot_capacity", "n_att", "n_edge_items",
+              "n_tet_items", "n_att_items", "bank_conflicts", "n_slots_total", "pad0", "pad1", "pad2"]
+
+
+class Program:
+    def __init__(self, blob: np.ndarray):
+        b = blob.view(np.uint8)
+        ints = b[:96].view(np.int32)
+        self.h = dict(zip(HDR_FIELDS, (int(v) for v in ints)))
+        assert self.h["magic"] == 0x54534231
+        self.off = b[96:96 + 8 * len(SECTIONS)].view(np.int64)
+        self.b = b
+        rt = np.float64 if self.h["real_bytes"] == 8 else np.float32
+        H = self.h
+        nE, nT, nA = H["n_edge_items"], H["n_tet_items"], H["n_att_items"]
+        C, G, Vfp = H["n_chunks"], H["G"], H["Vf_pad"]
+        self.chunks = self.sec("CHUNK", np.int32, C * 8).reshape(C, 8)
+        self.edge_idx = self.sec("EDGE_IDX", np.int32, 4 * nE).reshape(nE, 4)
+        self.edge_par = self.sec("EDGE_PAR", rt, 4 * nE).reshape(nE, 4).astype(np.float64)
+        self.tet_idx = self.sec("TET_IDX", np.int32, 4 * nT).reshape(nT, 4)
+        self.tet_slot = self.sec("TET_SLOT", np.int32, 4 * nT).reshape(nT, 4)
+        self.tet_rv = self.sec("TET_RV", rt, nT).astype(np.float64)
+        self.att_idx = self.sec("ATT_IDX", np.int32, 4 * nA).reshape(nA, 4)
+        self.att_slot = self.sec("ATT_SLOT", np.int32, 4 * nA).reshape(nA, 4)
+        self.att_par = self.sec("ATT_PAR", rt, 4 * nA).reshape(nA, 4).astype(np.float64)
+        self.att_anchor = self.sec("ATT_ANCHOR", rt, 4 * nA).reshape(nA, 4).astype(np.float64)
+        self.region = self.sec("REGION", np.int32, C * G).reshape(C, G) if C * G else np.zeros((C, G), np.int32)
+        self.valence = self.sec("VALENCE", np.int32, C * Vfp).reshape(C, Vfp) if C * Vfp else np.zeros((C, Vfp), np.int32)
+        self.static_cnt = self.sec("STATIC_CNT", np.int32, Vfp)
+        self.s2o = self.sec("S2O", np.int32, H["Vstore"])
+        self.o2s = self.sec("O2S", np.int32, H["V"])
+        self.w = self.sec("W", rt, H["Vstore"]).astype(np.float64)
+        self.faces = self.sec("FACES", np.int32, 3 * H["F"]).reshape(-1, 3)
+
+    def sec(self, name, dtype, count):
+        o = int(self.off[SECTIONS.index(name)])
+        nbytes = count * np.dtype(dtype).itemsize
+        return self.b[o:o + nbytes].view(dtype).copy()
+
+
+def run_substeps(prog: Program, x, v, grasp_vertex, drag, g, h, substeps, damping, ks, kv):
+    """One env: x, v (V,3) float64 in place. Mirrors step_kernel.cuh section C."""
+    H = prog.h
+    Vf, Vst = H["Vf"], H["Vstore"]
+    s2o = prog.s2o
+    valid = s2o >= 0
+    xs = np.zeros((Vst, 3))
+    xs[valid] = x[s2o[valid]]
+    vf = v[s2o[:Vf]].copy()
+    damp = 1.0 if damping == 0.0 else max(0.0, 1.0 - damping * h)
+    gvs = prog.o2s[grasp_vertex] if grasp_vertex >= 0 else -1
+    scap = H["slot_capacity"]
+    lane = np.arange(Vf) % 32
+    grp = np.arange(Vf) // 32
+    # predict, substep 0
+    vf += h * np.asarray(g)[None, :]
+    xs[:Vf] = xs[:Vf] + h * vf
+    for s in range(substeps):
+        acc = np.zeros((Vf, 3))
+        cnt_adj = np.zeros(Vf, np.int64)
+        for c in range(H["n_chunks"] + 1):
+            if c == H["grasp_chunk"] and 0 <= gvs < Vf:
+                d = np.asarray(drag, np.float64) - xs[gvs]
+                dist = np.sqrt((d[0] * d[0] + d[1] * d[1]) + d[2] * d[2])
+                if not (dist <= 1e-12):
+                    acc[gvs] += d
+                    cnt_adj[gvs] += 1
+            if c == H["n_chunks"]:
+                break
+            kind, begin, count = prog.chunks[c, 0], prog.chunks[c, 1], prog.chunks[c, 2]
+            slots = np.full((scap, 3), np.nan)
+            deg = np.zeros(H["Vf_pad"], np.int64)
+            if kind == 0:
+                idx = prog.edge_idx[begin:begin + count]
+                par = prog.edge_par[begin:begin + count]
+                d = xs[idx[:, 0]] - xs[idx[:, 1]]
+                dist = np.sqrt((d[:, 0] * d[:, 0] + d[:, 1] * d[:, 1]) + d[:, 2] * d[:, 2])
+                m = 0.5 + np.copysign(0.5, dist - 1e-12)
+                scale = m * ks * (dist - par[:, 0]) / (dist * par[:, 3] + (1.0 - m))
+                ca = -par[:, 1] * scale
+                cb = par[:, 2] * scale
+                for col, coef, pos in ((2, ca, 0), (3, cb, 1)):
+                    sl = idx[:, col]
+                    ok = sl >= 0
+                    slots[sl[ok]] = coef[ok, None] * d[ok]
+                    np.add.at(deg, idx[ok & (m == 0), pos], 1)
+            elif kind == 2:
+                idx = prog.tet_idx[begin:begin + count]
+                sl = prog.tet_slot[begin:begin + count]
+                rv = prog.tet_rv[begin:begin + count]
+                pa = xs[idx[:, 0]]
+                ba, ca_, da = xs[idx[:, 1]] - pa, xs[idx[:, 2]] - pa, xs[idx[:, 3]] - pa
+
+                def cr(u, w):
+                    return np.stack([u[:, 1] * w[:, 2] - u[:, 2] * w[:, 1], u[:, 2] * w[:, 0] - u[:, 0] * w[:, 2],
+                                     u[:, 0] * w[:, 1] - u[:, 1] * w[:, 0]], axis=1)
+                gb, gc, gd = cr(ca_, da) / 6.0, cr(da, ba) / 6.0, cr(ba, ca_) / 6.0
+                ga = -((gb + gc) + gd)
+                cval = ((gd[:, 0] * da[:, 0] + gd[:, 1] * da[:, 1]) + gd[:, 2] * da[:, 2]) - rv
+                den = np.zeros(len(idx))
+                for gg in (ga, gb, gc, gd):
+                    for k in range(3):
+                        den = den + gg[:, k] * gg[:, k]
+                m = 0.5 + np.copysign(0.5, den - 1e-18)
+                scv = -m * kv * cval / (den + (1.0 - m))
+                for r, gg in enumerate((ga, gb, gc, gd)):
+                    ok = sl[:, r] >= 0
+                    slots[sl[ok, r]] = scv[ok, None] * gg[ok]
+                    np.add.at(deg, idx[ok & (m == 0), r], 1)
+            else:
+                raise NotImplementedError("attachment chunks are exercised on the GPU tests")
+            # phase 2
+            base = prog.region[c, grp] + lane
+            val = prog.valence[c, :Vf]
+            for k in range(int(val.max()) if len(val) else 0):
+                live = val > k
+                acc[live] += slots[base[live] + 32 * k]
+            cnt_adj -= deg[:Vf]
+        n = (prog.static_cnt[:Vf] + cnt_adj).astype(np.float64)
+        m = 0.5 + np.copysign(0.5, n - 0.5)
+        inv = m / (n + (1.0 - m))
+        e = acc * inv[:, None]
+        xs[:Vf] = xs[:Vf] + e
+        vf = vf + e / h
+        if damp != 1.0:
+            vf = vf * damp
+        if s + 1 < substeps:
+            vf = vf + h * np.asarray(g)[None, :]
+            xs[:Vf] = xs[:Vf] + h * vf
+    x[s2o[valid]] = xs[valid]
+    v[s2o[:Vf]] = vf
+    pinned = s2o[Vf:][s2o[Vf:] >= 0]
+    v[pinned] = 0.0
