@@ -1,0 +1,354 @@
+"""Benchmark: env-steps/s of the batched tissue-reach env step (4096 envs per GPU, full physics).
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl b200|reference]
+    python -m torch.distributed.run --nnodes=1 --nproc-per-node N --master-addr 127.0.0.1 \\
+        --master-port P bench.py --gpus N --steps K --warmup W
+
+A "step" is one EnvBatch.step over all envs of a GPU: tool command, grasp,
+10 substeps of the distance + tet-volume solver, capsule contact, reward /
+done / auto-reset -- ONE launch of the fused sm_100a kernel (plus one launch
+of the on-device uniform(-1,1) action generator).  Envs shard across GPUs
+with no data-path collective ("scaling": "weak"); the global env id indexes
+the action stream so a shard reproduces the single-GPU envs.
+
+value  : device-timed throughput (inputs resident in HBM), CUDA events per
+         step on the launching stream, L2 flushed between timed steps (state
+         38.5 MB < 126 MB L2), max over ranks.
+e2e    : the same metric through the public API with HOST numpy actions
+         (H2D through pinned memory) and the step result read back to the host
+         (D2H of obs, reward, terminated, truncated) inside the timed region.
+roofline: the binding roofline of this kernel is on-chip shared memory
+         (SURVEY.md §8(d)); achieved = 4,191,120 algorithmic B/env-step x envs
+         per launch / step-kernel time, peak = shared-memory bandwidth
+         measured on this GPU by ts_smem_probe.  The HBM view is reported
+         beside it (roofline_hbm, peak from MEASURED_PEAKS.json).
+cpu_baseline: the unmodified reference (oracle/_ref, compiled backend,
+         deterministic mode, 16 OpenMP threads) timed on this host on a bounded
+         sample of the same workload.
+--impl reference: that reference on the same config as a full bench line.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "env-steps/sec (XPBD tissue reach, 4096 envs)"
+UNIT = "env-steps/s"
+ENVS_PER_GPU = 4096
+V, E, T, SUBSTEPS = 392, 1831, 1170, 10
+# per substep 128 V + 88 E + 176 T bytes of canonical fp32 data flow,
+# plus 48 V of HBM state in/out and 64 B of I/O per env-step.
+ALG_BYTES_PER_ENV_STEP = SUBSTEPS * (128 * V + 88 * E + 176 * T) + 48 * V + 64     # 4,191,120
+HBM_BYTES_PER_ENV_STEP = 48 * V + 64                                              # 18,880
+REF_THREADS = 16
+
+
+def env_info():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            return json.load(fh), "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        time.sleep(0.25)
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = max(mx, float(parts[2]))
+            except ValueError:
+                continue
+            for name, flag in zip(names, parts[5:9]):
+                if flag.lower() == "active":
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# CPU reference (unmodified tissuesim from oracle/_ref; the oracle port if absent)
+# ---------------------------------------------------------------------------
+
+def reference_env(num_envs, seed=0):
+    ref_dir = os.path.join(ROOT, "oracle", "_ref")
+    scene = os.path.join(ROOT, "paper_2503_18616_b200", "scenes", "reach_1170.scene")
+    try:
+        sys.path.insert(0, ref_dir)
+        from tissuesim import backends
+        from tissuesim.env import EnvBatch as RefEnv
+        if not backends.HAVE_COMPILED:
+            raise ImportError("compiled backend missing")
+        env = RefEnv(scene, num_envs=num_envs, seed=seed, backend="compiled", mode="deterministic",
+                     threads=REF_THREADS)
+        return env, "reference", REF_THREADS
+    except Exception:
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        import oracle as O
+        from paper_2503_18616_b200.mesh import load_scene
+        env = O.OracleEnv(O.scene_from_loaded(*load_scene(scene)), num_envs)
+        return env, "port", 1
+
+
+def time_reference(num_envs, steps, warmup, seed=0):
+    env, kind, cores = reference_env(num_envs, seed)
+    env.reset(seed=seed) if kind == "reference" else env.reset()
+    rng = np.random.default_rng(seed)
+    for _ in range(warmup):
+        env.step(rng.uniform(-1.0, 1.0, (num_envs, 3)))
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        env.step(rng.uniform(-1.0, 1.0, (num_envs, 3)))
+    el = time.perf_counter() - t0
+    return num_envs * steps / el, el, kind, cores
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+
+def run_gpu(args):
+    import torch
+    import torch.distributed as dist
+
+    rank, world, local = env_info()
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+
+    from paper_2503_18616_b200 import EnvBatch, _native as N
+    from paper_2503_18616_b200.mesh import default_scene_path, load_scene
+
+    lib = N.load()
+    n = args.envs
+    first_env = rank * n
+    scene = load_scene(default_scene_path())
+    env = EnvBatch(scene, num_envs=n, device=dev, precision=args.precision)
+    env.reset(seed=0)
+    acts = torch.empty((n, 3), dtype=torch.float64, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    sptr = ctypes.c_void_p(stream.cuda_stream)
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)   # > 126 MB L2
+
+    def gen(i):
+        N.check(lib.ts_uniform_actions(N.ptr(acts), n, first_env, 12345, i, sptr), "ts_uniform_actions")
+
+    for i in range(args.warmup):
+        gen(i)
+        env.step(acts, validate=False)
+    torch.cuda.synchronize(dev)
+
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    kstart = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    launches0 = lib.ts_launch_count()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    with ClockSampler(local) as clocks:
+        for i in range(args.steps):
+            flush.fill_(i & 0xFF)                       # evict the state from L2 (untimed)
+            starts[i].record(stream)
+            gen(args.warmup + i)
+            kstart[i].record(stream)
+            env.step(acts, validate=False)
+            ends[i].record(stream)
+        torch.cuda.synchronize(dev)
+    launches = lib.ts_launch_count() - launches0
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    kern_ms = [s.elapsed_time(e) for s, e in zip(kstart, ends)]
+    total_ms = float(np.sum(step_ms))
+    t = torch.tensor([total_ms, float(np.sum(kern_ms))], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.barrier()
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms, kern_total_ms = float(t[0]), float(t[1])
+    value = world * n * args.steps / (total_ms * 1e-3)
+    kern_avg_ms = kern_total_ms / args.steps
+
+    # ---- end to end through the public API with host buffers -------------
+    rng = np.random.default_rng(1000 + rank)
+    host_actions = [rng.uniform(-1.0, 1.0, (n, 3)) for _ in range(args.steps)]
+    for i in range(min(2, args.warmup)):
+        o, r, te, tr, _ = env.step(host_actions[i])
+        o.cpu(), r.cpu(), te.cpu(), tr.cpu()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    d2h = 0
+    for i in range(args.steps):
+        o, r, te, tr, _ = env.step(host_actions[i])
+        res = (o.cpu(), r.cpu(), te.cpu(), tr.cpu())
+        d2h = sum(x.numel() * x.element_size() for x in res)
+    torch.cuda.synchronize(dev)
+    e2e_s = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
+    e2e_value = world * n * args.steps / float(e2e_s[0])
+
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    peaks, peak_src = measured_peaks()
+    smem_gbs = ctypes.c_double(0.0)
+    N.check(lib.ts_smem_probe(local, 20000, ctypes.byref(smem_gbs)), "ts_smem_probe")
+    per_launch_alg = ALG_BYTES_PER_ENV_STEP * n
+    achieved = per_launch_alg / (kern_avg_ms * 1e-3) / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if os.path.exists(prof):
+        with open(prof) as fh:
+            traffic = json.load(fh).get("dram_bytes_per_launch")
+    hbm_achieved = HBM_BYTES_PER_ENV_STEP * n / (kern_avg_ms * 1e-3) / 1e9
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32" if args.precision == "fp32" else "f64",
+        "data": "synthetic (uniform(-1,1) actions generated on device; scene reach_1170 from the in-tree preset)",
+        "config": {"workload": "config 3: 4096-env tissue reach, tet-volume + distance constraints, grasp + "
+                               "capsule contact, 10 substeps, auto-reset", "scene": "reach_1170 (V=392 E=1831 "
+                               "T=1170 F=540)", "envs_per_gpu": n, "global_envs": world * n,
+                   "precision": args.precision, "parallelism": f"env-sharded x{world} (no collective)",
+                   "l2": "flushed between timed steps (256 MiB write, untimed)"},
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": n * 3 * 8, "d2h_bytes_per_step": d2h},
+        "gpu_launches": int(launches),
+        "roofline": {"bound": "smem", "achieved": achieved, "peak": smem_gbs.value, "unit": "GB/s",
+                     "frac": achieved / smem_gbs.value, "traffic": traffic,
+                     "peak_source": "ts_smem_probe on this GPU (conflict-free LDS.128, all SMs)",
+                     "algorithmic_bytes_per_env_step": ALG_BYTES_PER_ENV_STEP,
+                     "kernel_ms": kern_avg_ms},
+        "roofline_hbm": {"bound": "hbm", "achieved": hbm_achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                         "frac": hbm_achieved / peaks["hbm_gbs"], "peak_source": peak_src,
+                         "algorithmic_bytes_per_env_step": HBM_BYTES_PER_ENV_STEP},
+        "clocks": clocks.summary(),
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        cpu_steps = max(2, args.cpu_steps)
+        val, el, kind, cores = time_reference(n, cpu_steps, 1)
+        line["cpu_baseline"] = {"value": val, "unit": UNIT, "cores": cores, "kind": kind,
+                                "sample": f"{cpu_steps} env steps x {n} envs after 1 warm-up step "
+                                          f"({el:.1f} s), reach_1170, compiled backend, deterministic mode, "
+                                          f"{cores} OpenMP threads on {os.cpu_count()} host cores"}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def run_reference(args):
+    rank, world, local = env_info()
+    if rank != 0:
+        return
+    n = args.envs
+    env, kind, cores = reference_env(n)
+    env.reset(seed=0) if kind == "reference" else env.reset()
+    rng = np.random.default_rng(0)
+    for _ in range(args.warmup):
+        env.step(rng.uniform(-1.0, 1.0, (n, 3)))
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        env.step(rng.uniform(-1.0, 1.0, (n, 3)))
+    el = time.perf_counter() - t0
+    val = n * args.steps / el
+    line = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": el * 1e3 / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (numpy uniform(-1,1) actions)",
+        "config": {"workload": "config 3: 4096-env tissue reach (reference CPU implementation)", "envs": n,
+                   "parallelism": f"{cores} OpenMP threads"},
+        "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": kind,
+                         "sample": f"{args.steps} env steps x {n} envs after {args.warmup} warm-up steps"},
+        "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=("b200", "reference"), default="b200")
+    ap.add_argument("--envs", type=int, default=ENVS_PER_GPU)
+    ap.add_argument("--precision", choices=("fp32", "fp64"), default="fp32")
+    ap.add_argument("--cpu-steps", type=int, default=25)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        ap.error("--warmup must be >= 3")
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -207,10 +207,15 @@ int32_t ts_detect_contacts(ts_handle *h, const void *x, int64_t num_envs, const 
                            int32_t *count, int32_t *face, int32_t *cap, double *depth,
                            double *dir, double *bary, void *stream);
 
-/* Uniform(-1,1) actions (N,3) float64 on device from a counter-based hash
- * (bench / synthetic rollouts). */
-int32_t ts_uniform_actions(double *actions, int64_t num_envs, uint64_t seed, uint64_t counter,
-                           void *stream);
+/* Uniform(-1,1) actions (N,3) float64 on device from a counter-based hash of
+ * (seed, counter, global env index first_env + i): a multi-GPU shard draws
+ * exactly the actions the single-GPU run draws for the same global envs. */
+int32_t ts_uniform_actions(double *actions, int64_t num_envs, int64_t first_env, uint64_t seed,
+                           uint64_t counter, void *stream);
+
+/* Measured shared-memory bandwidth of the device (GB/s, whole GPU): the
+ * roofline denominator for the on-chip-bound env step. */
+int32_t ts_smem_probe(int32_t device, int32_t iters, double *gbs_out);
 
 /* Kernel launches issued by this library since load (for bench accounting). */
 int64_t ts_launch_count(void);

@@ -311,10 +311,12 @@ int32_t ts_detect_contacts(ts_handle *h, const void *x, int64_t num_envs, const 
     return launch(h, L, reinterpret_cast<cudaStream_t>(stream));
 }
 
-int32_t ts_uniform_actions(double *actions, int64_t num_envs, uint64_t seed, uint64_t counter, void *stream) {
+int32_t ts_uniform_actions(double *actions, int64_t num_envs, int64_t first_env, uint64_t seed, uint64_t counter,
+                           void *stream) {
     if (!actions) return fail(TS_ERR_INVALID, "null argument");
     if (num_envs <= 0) return TS_OK;
-    cudaError_t e = ts_launch_uniform(actions, 3 * num_envs, seed, counter, reinterpret_cast<cudaStream_t>(stream));
+    cudaError_t e = ts_launch_uniform(actions, 3 * num_envs, 3 * first_env, seed, counter,
+                                      reinterpret_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return cuda_fail(e, "uniform kernel launch");
     g_launches.fetch_add(1);
     return TS_OK;
@@ -359,16 +361,73 @@ __device__ __forceinline__ uint64_t splitmix64(uint64_t z) {
     return z ^ (z >> 31);
 }
 
-__global__ void uniform_kernel(double *out, int64_t n, uint64_t seed, uint64_t counter) {
+// element i of the whole (multi-GPU) batch depends only on (seed, counter, global index)
+__global__ void uniform_kernel(double *out, int64_t n, int64_t first, uint64_t seed, uint64_t counter) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        const uint64_t r = splitmix64(seed ^ splitmix64(counter * 0x100000001B3ull + (uint64_t)i));
+        const uint64_t r = splitmix64(seed ^ splitmix64(counter * 0x100000001B3ull + (uint64_t)(i + first)));
         out[i] = 2.0 * ((double)(r >> 11) * (1.0 / 9007199254740992.0)) - 1.0;
     }
 }
 
-cudaError_t ts_launch_uniform(double *out, int64_t n, uint64_t seed, uint64_t counter, cudaStream_t stream) {
+cudaError_t ts_launch_uniform(double *out, int64_t n, int64_t first, uint64_t seed, uint64_t counter,
+                              cudaStream_t stream) {
     int grid = (int)((n + 255) / 256);
     if (grid > 4096) grid = 4096;
-    uniform_kernel<<<grid, 256, 0, stream>>>(out, n, seed, counter);
+    uniform_kernel<<<grid, 256, 0, stream>>>(out, n, first, seed, counter);
     return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// shared-memory bandwidth probe: the measured denominator of the roofline
+// (the env step is bound by on-chip shared memory, not HBM).  Every warp
+// streams conflict-free 128-bit loads over a 64 KiB buffer; bytes counted =
+// 16 B x 32 lanes per LDS.128 wavefront group.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(1024) smem_probe_kernel(int iters, float *sink) {
+    extern __shared__ float4 sbuf[];
+    const int n4 = 4096;   // 64 KiB
+    for (int i = threadIdx.x; i < n4; i += blockDim.x) sbuf[i] = make_float4(i, i + 1, i + 2, i + 3);
+    __syncthreads();
+    float4 acc = make_float4(0, 0, 0, 0);
+    int idx = threadIdx.x;
+#pragma unroll 1
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const float4 q = sbuf[(idx + k * 512) & (n4 - 1)];
+            acc.x += q.x; acc.y += q.y; acc.z += q.z; acc.w += q.w;
+        }
+        idx = (idx + 32) & (n4 - 1);
+    }
+    if (acc.x + acc.y + acc.z + acc.w == 1.2345f) sink[threadIdx.x] = acc.x;
+}
+
+extern "C" int32_t ts_smem_probe(int32_t device, int32_t iters, double *gbs_out) {
+    if (!gbs_out) return fail(TS_ERR_INVALID, "null argument");
+    cudaError_t e = cudaSetDevice(device);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    float *sink = nullptr;
+    e = cudaMalloc(&sink, 1024 * sizeof(float));
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc");
+    const int smem = 4096 * 16;
+    cudaFuncSetAttribute(smem_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    const int grid = sms * 2, block = 1024;
+    cudaEvent_t a, b;
+    cudaEventCreate(&a); cudaEventCreate(&b);
+    smem_probe_kernel<<<grid, block, smem>>>(iters / 10 + 1, sink);   // warm-up
+    cudaEventRecord(a);
+    smem_probe_kernel<<<grid, block, smem>>>(iters, sink);
+    cudaEventRecord(b);
+    e = cudaEventSynchronize(b);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, a, b);
+    cudaEventDestroy(a); cudaEventDestroy(b);
+    cudaFree(sink);
+    if (e != cudaSuccess) return cuda_fail(e, "smem probe");
+    g_launches.fetch_add(2);
+    const double bytes = (double)grid * block * (double)iters * 8.0 * 16.0;
+    *gbs_out = bytes / (ms * 1e-3) / 1e9;
+    return TS_OK;
 }

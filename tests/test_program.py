@@ -1,0 +1,131 @@
+"""The scene compiler's program (what the sm_100a kernel executes), pinned on CPU.
+
+* Interpreting the compiled program in fp64 must reproduce the oracle's
+  substeps bitwise -- for the benchmark scene, a small slab, several chunk
+  budgets and with/without the bank-aware schedule.  This proves the slot
+  layout encodes the reference's per-vertex accumulation order
+  (_kernels.pyx:260-352) independently of the GPU.
+* Structural invariants: every (constraint, free endpoint) incidence has
+  exactly one slot, slots are unique, warp-interleaved and in constraint order.
+* The bank-aware schedule is a permutation of the constraint items and
+  reduces phase-1 shared-memory conflicts.
+"""
+
+import numpy as np
+import pytest
+
+import oracle as O
+import program_interp as PI
+from conftest import build_slab_scene
+from paper_2503_18616_b200 import scene as S
+
+
+def _arrays(scene):
+    return S.SceneArrays.from_loaded(*scene)
+
+
+def _oracle_substeps(mesh, rest, cfg, x, v, gv, drag, att=None):
+    xa, va = x[None].copy(), v[None].copy()
+    a = att or dict(att_vertex=np.zeros(0), att_faces=np.zeros((0, 3)), att_is_face=np.zeros(0),
+                    att_anchor=np.zeros((0, 3)), att_rest=np.zeros(0), att_k=np.zeros(0))
+    O.run_substeps(xa, va, rest.inverse_mass, mesh.edges, rest.rest_length, cfg.k_s, mesh.tets, rest.rest_volume,
+                   cfg.k_v, a["att_vertex"], a["att_faces"], a["att_is_face"], a["att_anchor"], a["att_rest"],
+                   a["att_k"], np.array([gv]), drag[None], cfg.gravity, cfg.dt / cfg.substeps, cfg.substeps,
+                   cfg.damping)
+    return xa[0], va[0]
+
+
+@pytest.mark.parametrize("opts", [dict(), dict(max_chunk_slots=1024), dict(max_chunk_slots=200),
+                                  dict(schedule_banks=False), dict(block_threads=64)])
+def test_program_reproduces_oracle_bitwise(reach_scene, opts):
+    mesh, rest, cfg = reach_scene
+    blob, info = S.compile_program(_arrays(reach_scene), precision="fp64", **opts)
+    prog = PI.Program(blob)
+    rng = np.random.default_rng(1)
+    free = np.flatnonzero(rest.inverse_mass > 0)
+    x0 = mesh.positions_rest + rng.normal(0, 5e-4, mesh.positions_rest.shape) * (rest.inverse_mass > 0)[:, None]
+    v0 = rng.normal(0, 1e-2, x0.shape) * (rest.inverse_mass > 0)[:, None]
+    for gv in (-1, int(free[11]), int(free[-1])):
+        drag = x0[free[11]] + np.array([0.001, 0.002, -0.0005])
+        xa, va = _oracle_substeps(mesh, rest, cfg, x0, v0, gv, drag)
+        xb, vb = x0.copy(), v0.copy()
+        PI.run_substeps(prog, xb, vb, gv, drag, cfg.gravity, cfg.dt / cfg.substeps, cfg.substeps, cfg.damping,
+                        cfg.k_s, cfg.k_v)
+        assert np.array_equal(xa, xb) and np.array_equal(va, vb), (opts, gv)
+
+
+def test_program_degenerate_constraints_counted_like_reference():
+    """Coincident edge endpoints and collapsed tets drop out of the counts (m = 0 guards)."""
+    mesh, rest, cfg = build_slab_scene(3, 2, 2)
+    blob, _ = S.compile_program(_arrays((mesh, rest, cfg)), precision="fp64", max_chunk_slots=64)
+    prog = PI.Program(blob)
+    x0 = mesh.positions_rest.copy()
+    e = mesh.edges[5]
+    x0[e[1]] = x0[e[0]]          # coincident edge
+    t = mesh.tets[7]
+    x0[t[3]] = x0[t[0]]          # collapsed tet shares that corner
+    v0 = np.zeros_like(x0)
+    xa, va = _oracle_substeps(mesh, rest, cfg, x0, v0, -1, np.zeros(3))
+    xb, vb = x0.copy(), v0.copy()
+    PI.run_substeps(prog, xb, vb, -1, np.zeros(3), cfg.gravity, cfg.dt / cfg.substeps, cfg.substeps, cfg.damping,
+                    cfg.k_s, cfg.k_v)
+    assert np.array_equal(xa, xb) and np.array_equal(va, vb)
+
+
+def test_slot_structure(reach_scene):
+    mesh, rest, cfg = reach_scene
+    blob, info = S.compile_program(_arrays(reach_scene), precision="fp32")
+    p = PI.Program(blob)
+    H = p.h
+    Vf = H["Vf"]
+    w = rest.inverse_mass
+    # storage order: free first (sorted by incidence, descending), then pinned
+    assert np.all(w[p.s2o[:Vf]] > 0) and np.all(w[p.s2o[H["Vf_pad"]:][p.s2o[H["Vf_pad"]:] >= 0]] == 0)
+    assert np.array_equal(np.sort(p.s2o[p.s2o >= 0]), np.arange(mesh.vertex_count))
+    assert np.all(np.diff(p.static_cnt[:Vf]) <= 0)
+    expected = 0
+    for kind, items, roles in ((0, p.edge_idx, 2), (2, p.tet_idx, 4)):
+        slots = (p.edge_idx[:, 2:4] if kind == 0 else p.tet_slot)
+        used = []
+        for c in range(H["n_chunks"]):
+            if p.chunks[c, 0] != kind:
+                continue
+            b, n = p.chunks[c, 1], p.chunks[c, 2]
+            sl = slots[b:b + n]
+            idx = items[b:b + n, :roles]
+            assert np.all((sl >= 0) == (idx < H["Vf_pad"]))   # slots exactly for free endpoints
+            s = sl[sl >= 0]
+            assert len(np.unique(s)) == len(s)
+            # slot k of lane l sits at region + 32k + l: bank = owner lane
+            assert np.all(s % 32 == idx[sl >= 0] % 32)
+            used.append(len(s))
+        expected += sum(used)
+    assert expected == info["n_slots_total"] == p.static_cnt.sum()
+    # per-vertex incidence count equals the reference's count of live constraints touching it
+    inc = np.zeros(mesh.vertex_count, int)
+    for a, b in mesh.edges:
+        if w[a] + w[b] > 0:
+            inc[a] += w[a] > 0
+            inc[b] += w[b] > 0
+    for t in mesh.tets:
+        inc[t] += w[t] > 0
+    assert np.array_equal(p.static_cnt[:Vf], inc[p.s2o[:Vf]])
+
+
+def test_schedule_is_permutation_and_reduces_conflicts(reach_scene):
+    arr = _arrays(reach_scene)
+    b1, i1 = S.compile_program(arr, precision="fp32", schedule_banks=True)
+    b0, i0 = S.compile_program(arr, precision="fp32", schedule_banks=False)
+    p1, p0 = PI.Program(b1), PI.Program(b0)
+    for a, b in ((p1.edge_idx, p0.edge_idx), (p1.tet_idx, p0.tet_idx)):
+        assert sorted(map(tuple, a.tolist())) == sorted(map(tuple, b.tolist()))
+    assert i1["bank_conflicts_p1"] < i0["bank_conflicts_p1"]
+
+
+def test_compile_errors():
+    mesh, rest, cfg = build_slab_scene()
+    arr = _arrays((mesh, rest, cfg))
+    arr.edges = arr.edges.copy()
+    arr.edges[0, 0] = 10_000
+    with pytest.raises(Exception, match="out of range"):
+        S.compile_program(arr)

@@ -58,13 +58,13 @@ def timing(precision, n=4096, steps=20, warmup=5):
     lib = env.sim.scene.lib
     import ctypes
     for i in range(warmup):
-        lib.ts_uniform_actions(acts.data_ptr(), n, 1, i, ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+        lib.ts_uniform_actions(acts.data_ptr(), n, 0, 1, i, ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
         env.step(acts, validate=False)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for i in range(steps):
-        lib.ts_uniform_actions(acts.data_ptr(), n, 1, 100 + i, ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+        lib.ts_uniform_actions(acts.data_ptr(), n, 0, 1, 100 + i, ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
         env.step(acts, validate=False)
     e1.record()
     torch.cuda.synchronize()
