@@ -46,8 +46,60 @@ void put(std::vector<uint8_t> &blob, int64_t off, const std::vector<T> &v) {
     if (!v.empty()) std::memcpy(blob.data() + off, v.data(), v.size() * sizeof(T));
 }
 
-// Greedy bank-aware batching.  Returns items in schedule order and the
-// number of extra shared-memory wavefronts the residual conflicts cost.
+// Swap-based local search over a schedule: lanes are grouped into sub-batches
+// of `bank_mod` items (a warp for 32-bit data, a half-warp for 64-bit); the
+// cost of a sub-batch is, per role, (max items on one bank - 1) = the extra
+// shared-memory wavefronts that role's loads and stores pay.  Deterministic
+// (fixed-seed xorshift), first-improvement, sideways moves allowed.
+void local_search(std::vector<Item> &s, int bank_mod) {
+    const int n = (int)s.size();
+    const int nsb = (n + bank_mod - 1) / bank_mod;
+    const int R4 = 4;
+    std::vector<int> cnt((size_t)nsb * R4 * bank_mod, 0);
+    auto C = [&](int sb, int r, int b) -> int & { return cnt[((size_t)sb * R4 + r) * bank_mod + b]; };
+    for (int i = 0; i < n; ++i)
+        for (int r = 0; r < s[i].nroles; ++r) C(i / bank_mod, r, s[i].pos[r] % bank_mod)++;
+    auto sb_cost = [&](int sb) {
+        int c = 0;
+        for (int r = 0; r < R4; ++r) {
+            int m = 0;
+            for (int b = 0; b < bank_mod; ++b) m = std::max(m, C(sb, r, b));
+            if (m > 1) c += m - 1;
+        }
+        return c;
+    };
+    std::vector<int> cost(nsb);
+    int total = 0;
+    for (int sb = 0; sb < nsb; ++sb) { cost[sb] = sb_cost(sb); total += cost[sb]; }
+    uint64_t rng = 0x9E3779B97F4A7C15ull;
+    auto next = [&]() { rng ^= rng << 13; rng ^= rng >> 7; rng ^= rng << 17; return rng; };
+    const long iters = std::min<long>(400000L, 200L * n);
+    for (long it = 0; it < iters && total > 0; ++it) {
+        // pick a position in a costly sub-batch and a random partner elsewhere
+        int i = (int)(next() % n), j = (int)(next() % n);
+        int si = i / bank_mod, sj = j / bank_mod;
+        if (si == sj || (cost[si] == 0 && cost[sj] == 0)) continue;
+        auto move = [&](int k, int from, int to) {
+            for (int r = 0; r < s[k].nroles; ++r) { C(from, r, s[k].pos[r] % bank_mod)--; C(to, r, s[k].pos[r] % bank_mod)++; }
+        };
+        move(i, si, sj);
+        move(j, sj, si);
+        const int ci = sb_cost(si), cj = sb_cost(sj);
+        const int delta = ci + cj - cost[si] - cost[sj];
+        if (delta <= 0) {
+            std::swap(s[i], s[j]);
+            total += delta;
+            cost[si] = ci; cost[sj] = cj;
+        } else {
+            move(i, sj, si);
+            move(j, si, sj);
+        }
+    }
+}
+
+// Greedy bank-aware batching + local search.  Returns items in schedule
+// order and the number of extra shared-memory wavefronts the residual
+// conflicts cost per pass over the chunk.
 std::vector<Item> schedule_items(std::vector<Item> items, int bank_mod, int batch, bool enable,
                                  int *extra_wavefronts) {
     *extra_wavefronts = 0;
@@ -108,9 +160,16 @@ std::vector<Item> schedule_items(std::vector<Item> items, int bank_mod, int batc
             pick.push_back((int)i);
             taken[i] = 1;
         }
-        *extra_wavefronts += conflicts_of(pick);
         for (int i : pick) out.push_back(items[i]);
         done += pick.size();
+    }
+    if (enable && out.size() > (size_t)bank_mod) local_search(out, bank_mod);
+    for (size_t b0 = 0; b0 < out.size(); b0 += batch) {
+        std::vector<int> idx;
+        for (size_t k = b0; k < std::min(out.size(), b0 + batch); ++k) idx.push_back((int)k);
+        items.swap(out);
+        *extra_wavefronts += conflicts_of(idx);
+        items.swap(out);
     }
     return out;
 }
@@ -259,12 +318,15 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
         int base = 0;
         for (int g = 0; g < G; ++g) { region[(size_t)c * G + g] = base; base += 32 * cb.kmax[g]; }
         cb.padded = base;
-        slot_cap = std::max(slot_cap, base);
+        // 32 "trash" slots after the regions: edge / tet endpoints that are pinned store there
+        // unconditionally (bank = p % 32, same as their position reads), nobody reads them back
+        const int trash = base;
+        slot_cap = std::max(slot_cap, base + 32);
         std::vector<int> k_next(Vf_pad, 0);
         for (Item &it : cb.items) {  // items are in constraint-index order here
             for (int r = 0; r < it.nroles; ++r) {
                 int p = it.pos[r];
-                if (p >= Vf_pad) { it.slot[r] = -1; continue; }
+                if (p >= Vf_pad) { it.slot[r] = it.kind == TS_CHUNK_ATT ? -1 : trash + (p % 32); continue; }
                 it.slot[r] = region[(size_t)c * G + p / 32] + 32 * k_next[p] + (p % 32);
                 k_next[p]++;
             }
@@ -314,12 +376,19 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
         edge_idx[4 * i + 0] = it.pos[0]; edge_idx[4 * i + 1] = it.pos[1];
         edge_idx[4 * i + 2] = it.slot[0]; edge_idx[4 * i + 3] = it.slot[1];
         edge_par[4 * i + 0] = d.rest_length[it.index];
-        edge_par[4 * i + 1] = w[a]; edge_par[4 * i + 2] = w[b]; edge_par[4 * i + 3] = w[a] + w[b];
+        if (R == 8) {   // exact build: the reference's operands
+            edge_par[4 * i + 1] = w[a]; edge_par[4 * i + 2] = w[b]; edge_par[4 * i + 3] = w[a] + w[b];
+        } else {        // fp32 build: ca = -(ks wa / wsum)(1 - rl/dist), cb = (ks wb / wsum)(1 - rl/dist)
+            const double wsum = w[a] + w[b];
+            edge_par[4 * i + 1] = d.k_s * w[a] / wsum; edge_par[4 * i + 2] = d.k_s * w[b] / wsum;
+            edge_par[4 * i + 3] = 0.0;
+        }
     }
     for (int i = 0; i < nT; ++i) {
         const Item &it = all_items[2][i];
         for (int k = 0; k < 4; ++k) { tet_idx[4 * i + k] = it.pos[k]; tet_slot[4 * i + k] = it.slot[k]; }
-        tet_rv[i] = d.rest_volume[it.index];
+        // fp32 build works with unscaled cross products G = 6 grad: it needs 6 V0
+        tet_rv[i] = R == 8 ? d.rest_volume[it.index] : 6.0 * d.rest_volume[it.index];
     }
     for (int i = 0; i < nA; ++i) {
         const Item &it = all_items[1][i];

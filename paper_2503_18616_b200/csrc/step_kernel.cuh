@@ -319,22 +319,36 @@ __device__ __forceinline__ void p1_edges(const TsDevProg &P, const Smem<Real> &m
     using V4 = typename R4<Real>::T;
     const int4 *idx = P.edge_idx + ch.item_begin;
     const V4 *par = reinterpret_cast<const V4 *>(P.edge_par) + ch.item_begin;
+    const int vfp = P.Vf_pad;
     for (int i = threadIdx.x; i < ch.item_count; i += blockDim.x) {
-        const int4 id = __ldg(idx + i);
+        const int4 id = __ldg(idx + i);     // {pos a, pos b, slot a, slot b}; pinned endpoints -> trash slots
         const V4 pr = par[i];
         const Real dx = m.xs[id.x] - m.xs[id.y];
         const Real dy = m.ys[id.x] - m.ys[id.y];
         const Real dz = m.zs[id.x] - m.zs[id.y];
-        const Real dist = sqrt(dx * dx + dy * dy + dz * dz);
-        const Real mm = (Real)0.5 + copysign((Real)0.5, dist - (Real)1e-12);
-        const Real scale = mm * ks * (dist - pr.x) / (dist * pr.w + ((Real)1 - mm));
-        const Real ca = -pr.y * scale;
-        const Real cb = pr.z * scale;
-        if (id.z >= 0) { m.slx[id.z] = ca * dx; m.sly[id.z] = ca * dy; m.slz[id.z] = ca * dz; }
-        if (id.w >= 0) { m.slx[id.w] = cb * dx; m.sly[id.w] = cb * dy; m.slz[id.w] = cb * dz; }
-        if (mm == (Real)0) {
-            if (id.z >= 0) atomicAdd(&m.deg[id.x], 1);
-            if (id.w >= 0) atomicAdd(&m.deg[id.y], 1);
+        Real ca, cb;
+        bool degenerate;
+        if constexpr (sizeof(Real) == 8) {
+            // exact build: ts_lane_edges, _kernels.pyx:121-136 (pr = {rest, wa, wb, wa + wb})
+            const Real dist = sqrt(dx * dx + dy * dy + dz * dz);
+            const Real mm = (Real)0.5 + copysign((Real)0.5, dist - (Real)1e-12);
+            const Real scale = mm * ks * (dist - pr.x) / (dist * pr.w + ((Real)1 - mm));
+            ca = -pr.y * scale;
+            cb = pr.z * scale;
+            degenerate = mm == (Real)0;
+        } else {
+            // fp32 build: pr = {rest, ks wa / wsum, ks wb / wsum, 0};  c = k (1 - rest / dist)
+            const float d2 = __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, dx * dx));
+            degenerate = !(d2 >= 1e-24f);                    // dist < 1e-12 (coincident guard)
+            const float f = degenerate ? 0.0f : __fmaf_rn(-pr.x, rsqrtf(d2), 1.0f);
+            ca = -pr.y * f;
+            cb = pr.z * f;
+        }
+        m.slx[id.z] = ca * dx; m.sly[id.z] = ca * dy; m.slz[id.z] = ca * dz;
+        m.slx[id.w] = cb * dx; m.sly[id.w] = cb * dy; m.slz[id.w] = cb * dz;
+        if (degenerate) {
+            if (id.x < vfp) atomicAdd(&m.deg[id.x], 1);
+            if (id.y < vfp) atomicAdd(&m.deg[id.y], 1);
         }
     }
 }
@@ -344,15 +358,17 @@ __device__ __forceinline__ void put_slot(const Smem<Real> &m, int s, Real c, Rea
     if (s >= 0) { m.slx[s] = c * gx; m.sly[s] = c * gy; m.slz[s] = c * gz; }
 }
 
-template <typename Real> __device__ __forceinline__ Real div6(Real a);
-template <> __device__ __forceinline__ double div6<double>(double a) { return a / 6.0; }
-template <> __device__ __forceinline__ float div6<float>(float a) { return a / 6.0f; }
+template <typename Real>
+__device__ __forceinline__ void store_slot(const Smem<Real> &m, int s, Real c, Real gx, Real gy, Real gz) {
+    m.slx[s] = c * gx; m.sly[s] = c * gy; m.slz[s] = c * gz;
+}
 
 template <typename Real>
 __device__ __forceinline__ void p1_tets(const TsDevProg &P, const Smem<Real> &m, const TsChunk &ch, Real kv) {
     const int4 *idx = P.tet_idx + ch.item_begin;
     const int4 *slot = P.tet_slot + ch.item_begin;
     const Real *rv = reinterpret_cast<const Real *>(P.tet_rv) + ch.item_begin;
+    const int vfp = P.Vf_pad;
     for (int i = threadIdx.x; i < ch.item_count; i += blockDim.x) {
         const int4 id = __ldg(idx + i);
         const int4 sl = __ldg(slot + i);
@@ -360,34 +376,66 @@ __device__ __forceinline__ void p1_tets(const TsDevProg &P, const Smem<Real> &m,
         const Real bax = m.xs[id.y] - ax, bay = m.ys[id.y] - ay, baz = m.zs[id.y] - az;
         const Real cax = m.xs[id.z] - ax, cay = m.ys[id.z] - ay, caz = m.zs[id.z] - az;
         const Real dax = m.xs[id.w] - ax, day = m.ys[id.w] - ay, daz = m.zs[id.w] - az;
-        const Real gbx = div6(cay * daz - caz * day);
-        const Real gby = div6(caz * dax - cax * daz);
-        const Real gbz = div6(cax * day - cay * dax);
-        const Real gcx = div6(day * baz - daz * bay);
-        const Real gcy = div6(daz * bax - dax * baz);
-        const Real gcz = div6(dax * bay - day * bax);
-        const Real gdx = div6(bay * caz - baz * cay);
-        const Real gdy = div6(baz * cax - bax * caz);
-        const Real gdz = div6(bax * cay - bay * cax);
-        const Real gax = -(gbx + gcx + gdx);
-        const Real gay = -(gby + gcy + gdy);
-        const Real gaz = -(gbz + gcz + gdz);
-        const Real cval = (gdx * dax + gdy * day + gdz * daz) - rv[i];
-        const Real denom = gax * gax + gay * gay + gaz * gaz
-                         + gbx * gbx + gby * gby + gbz * gbz
-                         + gcx * gcx + gcy * gcy + gcz * gcz
-                         + gdx * gdx + gdy * gdy + gdz * gdz;
-        const Real mm = (Real)0.5 + copysign((Real)0.5, denom - (Real)1e-18);
-        const Real sc = -mm * kv * cval / (denom + ((Real)1 - mm));
-        put_slot(m, sl.x, sc, gax, gay, gaz);
-        put_slot(m, sl.y, sc, gbx, gby, gbz);
-        put_slot(m, sl.z, sc, gcx, gcy, gcz);
-        put_slot(m, sl.w, sc, gdx, gdy, gdz);
-        if (mm == (Real)0) {
-            if (sl.x >= 0) atomicAdd(&m.deg[id.x], 1);
-            if (sl.y >= 0) atomicAdd(&m.deg[id.y], 1);
-            if (sl.z >= 0) atomicAdd(&m.deg[id.z], 1);
-            if (sl.w >= 0) atomicAdd(&m.deg[id.w], 1);
+        bool degenerate;
+        if constexpr (sizeof(Real) == 8) {
+            // exact build: ts_lane_tets, _kernels.pyx:165-208
+            const Real gbx = (cay * daz - caz * day) / 6.0;
+            const Real gby = (caz * dax - cax * daz) / 6.0;
+            const Real gbz = (cax * day - cay * dax) / 6.0;
+            const Real gcx = (day * baz - daz * bay) / 6.0;
+            const Real gcy = (daz * bax - dax * baz) / 6.0;
+            const Real gcz = (dax * bay - day * bax) / 6.0;
+            const Real gdx = (bay * caz - baz * cay) / 6.0;
+            const Real gdy = (baz * cax - bax * caz) / 6.0;
+            const Real gdz = (bax * cay - bay * cax) / 6.0;
+            const Real gax = -(gbx + gcx + gdx);
+            const Real gay = -(gby + gcy + gdy);
+            const Real gaz = -(gbz + gcz + gdz);
+            const Real cval = (gdx * dax + gdy * day + gdz * daz) - rv[i];
+            const Real denom = gax * gax + gay * gay + gaz * gaz
+                             + gbx * gbx + gby * gby + gbz * gbz
+                             + gcx * gcx + gcy * gcy + gcz * gcz
+                             + gdx * gdx + gdy * gdy + gdz * gdz;
+            const Real mm = (Real)0.5 + copysign((Real)0.5, denom - (Real)1e-18);
+            const Real sc = -mm * kv * cval / (denom + ((Real)1 - mm));
+            store_slot(m, sl.x, sc, gax, gay, gaz);
+            store_slot(m, sl.y, sc, gbx, gby, gbz);
+            store_slot(m, sl.z, sc, gcx, gcy, gcz);
+            store_slot(m, sl.w, sc, gdx, gdy, gdz);
+            degenerate = mm == (Real)0;
+        } else {
+            // fp32 build on unscaled cross products G = 6 grad (rv holds 6 V0):
+            //   s grad_i = -kv (G_d . da - 6 V0) / sum|G|^2  G_i
+            const float Gbx = __fmaf_rn(cay, daz, -caz * day);
+            const float Gby = __fmaf_rn(caz, dax, -cax * daz);
+            const float Gbz = __fmaf_rn(cax, day, -cay * dax);
+            const float Gcx = __fmaf_rn(day, baz, -daz * bay);
+            const float Gcy = __fmaf_rn(daz, bax, -dax * baz);
+            const float Gcz = __fmaf_rn(dax, bay, -day * bax);
+            const float Gdx = __fmaf_rn(bay, caz, -baz * cay);
+            const float Gdy = __fmaf_rn(baz, cax, -bax * caz);
+            const float Gdz = __fmaf_rn(bax, cay, -bay * cax);
+            const float Gax = -(Gbx + Gcx + Gdx);
+            const float Gay = -(Gby + Gcy + Gdy);
+            const float Gaz = -(Gbz + Gcz + Gdz);
+            const float c6 = __fmaf_rn(Gdz, daz, __fmaf_rn(Gdy, day, Gdx * dax)) - rv[i];
+            float den = Gax * Gax;
+            den = __fmaf_rn(Gay, Gay, den); den = __fmaf_rn(Gaz, Gaz, den);
+            den = __fmaf_rn(Gbx, Gbx, den); den = __fmaf_rn(Gby, Gby, den); den = __fmaf_rn(Gbz, Gbz, den);
+            den = __fmaf_rn(Gcx, Gcx, den); den = __fmaf_rn(Gcy, Gcy, den); den = __fmaf_rn(Gcz, Gcz, den);
+            den = __fmaf_rn(Gdx, Gdx, den); den = __fmaf_rn(Gdy, Gdy, den); den = __fmaf_rn(Gdz, Gdz, den);
+            degenerate = !(den > 3.6e-17f);                  // sum|grad|^2 <= 1e-18
+            const float sc = degenerate ? 0.0f : __fdividef(-kv * c6, den);
+            store_slot(m, sl.x, sc, Gax, Gay, Gaz);
+            store_slot(m, sl.y, sc, Gbx, Gby, Gbz);
+            store_slot(m, sl.z, sc, Gcx, Gcy, Gcz);
+            store_slot(m, sl.w, sc, Gdx, Gdy, Gdz);
+        }
+        if (degenerate) {
+            if (id.x < vfp) atomicAdd(&m.deg[id.x], 1);
+            if (id.y < vfp) atomicAdd(&m.deg[id.y], 1);
+            if (id.z < vfp) atomicAdd(&m.deg[id.z], 1);
+            if (id.w < vfp) atomicAdd(&m.deg[id.w], 1);
         }
     }
 }
@@ -572,6 +620,7 @@ __global__ void __launch_bounds__(512, sizeof(Real) == 4 ? 2 : 1) step_kernel(co
     const int lane = t & 31;
     const int mode = L.mode;
     const Real h = (Real)S.h, damp = (Real)S.damp;
+    const Real inv_h = (Real)(1.0 / S.h);   // fp32 build: v += d * (1/h)
     const Real gx = (Real)S.g[0], gy = (Real)S.g[1], gz = (Real)S.g[2];
     const Real ks = (Real)S.ks, kv = (Real)S.kv;
     const Real *wst = reinterpret_cast<const Real *>(P.w);
@@ -606,7 +655,10 @@ __global__ void __launch_bounds__(512, sizeof(Real) == 4 ? 2 : 1) step_kernel(co
         for (int i = t; i < P.cbits_words; i += B) m.cbits[i] = 0u;
         __syncthreads();
 
-        if (t < 3 && (mode & (TS_M_CONTACTS | TS_M_DETECT_ONLY))) make_cap<Real>(sc.caps[t], m.caps[t]);
+        if (mode & (TS_M_CONTACTS | TS_M_DETECT_ONLY)) {
+            if (t < 3) make_cap<Real>(sc.caps[t], m.caps[t]);
+            __syncthreads();
+        }
         // ---- B. grasp search: nearest free vertex (tool.py:380-389) ------
         if (sc.need_search) {
             double bk = INFINITY;
@@ -708,13 +760,22 @@ __global__ void __launch_bounds__(512, sizeof(Real) == 4 ? 2 : 1) step_kernel(co
                 for (int r = 0; r < VPT; ++r) {
                     const int p = r * B + t;
                     if (p < P.Vf) {
-                        const Real n = (Real)(P.static_cnt[p] - ndeg[r] + gcnt[r]);
-                        const Real mm = (Real)0.5 + copysign((Real)0.5, n - (Real)0.5);
-                        const Real inv = mm / (n + ((Real)1 - mm));
-                        const Real e0 = accx[r] * inv, e1 = accy[r] * inv, e2 = accz[r] * inv;
-                        xr[r] += e0; vx[r] += e0 / h;
-                        yr[r] += e1; vy[r] += e1 / h;
-                        zr[r] += e2; vz[r] += e2 / h;
+                        const int cnt = P.static_cnt[p] - ndeg[r] + gcnt[r];
+                        if constexpr (sizeof(Real) == 8) {
+                            const Real n = (Real)cnt;
+                            const Real mm = (Real)0.5 + copysign((Real)0.5, n - (Real)0.5);
+                            const Real inv = mm / (n + ((Real)1 - mm));
+                            const Real e0 = accx[r] * inv, e1 = accy[r] * inv, e2 = accz[r] * inv;
+                            xr[r] += e0; vx[r] += e0 / h;
+                            yr[r] += e1; vy[r] += e1 / h;
+                            zr[r] += e2; vz[r] += e2 / h;
+                        } else {
+                            const float inv = cnt > 0 ? __frcp_rn((float)cnt) : 0.0f;
+                            const float e0 = accx[r] * inv, e1 = accy[r] * inv, e2 = accz[r] * inv;
+                            xr[r] += e0; vx[r] = __fmaf_rn(e0, inv_h, vx[r]);
+                            yr[r] += e1; vy[r] = __fmaf_rn(e1, inv_h, vy[r]);
+                            zr[r] += e2; vz[r] = __fmaf_rn(e2, inv_h, vz[r]);
+                        }
                         if (damp != (Real)1) { vx[r] *= damp; vy[r] *= damp; vz[r] *= damp; }
                         if (s + 1 < S.substeps) {
                             vx[r] += h * gx; xr[r] += h * vx[r];

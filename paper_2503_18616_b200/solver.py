@@ -195,7 +195,7 @@ class Simulation:
     def kinetic_energy(self):
         """Total kinetic energy per instance, joules (solver.py:368-371)."""
         speed2 = (self.v.double() ** 2).sum(-1)
-        return speed2 @ torch.as_tensor(self.mesh.vertex_mass, device=self.device)
+        return 0.5 * speed2 @ torch.as_tensor(self.mesh.vertex_mass, device=self.device)
 
     def instance_state(self, i):
         from types import SimpleNamespace

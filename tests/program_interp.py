@@ -99,10 +99,10 @@ def run_substeps(prog: Program, x, v, grasp_vertex, drag, g, h, substeps, dampin
                 ca = -par[:, 1] * scale
                 cb = par[:, 2] * scale
                 for col, coef, pos in ((2, ca, 0), (3, cb, 1)):
-                    sl = idx[:, col]
-                    ok = sl >= 0
-                    slots[sl[ok]] = coef[ok, None] * d[ok]
-                    np.add.at(deg, idx[ok & (m == 0), pos], 1)
+                    sl = idx[:, col]          # pinned endpoints write to trash slots
+                    slots[sl] = coef[:, None] * d
+                    free = idx[:, pos] < H["Vf_pad"]
+                    np.add.at(deg, idx[free & (m == 0), pos], 1)
             elif kind == 2:
                 idx = prog.tet_idx[begin:begin + count]
                 sl = prog.tet_slot[begin:begin + count]
@@ -123,9 +123,9 @@ def run_substeps(prog: Program, x, v, grasp_vertex, drag, g, h, substeps, dampin
                 m = 0.5 + np.copysign(0.5, den - 1e-18)
                 scv = -m * kv * cval / (den + (1.0 - m))
                 for r, gg in enumerate((ga, gb, gc, gd)):
-                    ok = sl[:, r] >= 0
-                    slots[sl[ok, r]] = scv[ok, None] * gg[ok]
-                    np.add.at(deg, idx[ok & (m == 0), r], 1)
+                    slots[sl[:, r]] = scv[:, None] * gg
+                    free = idx[:, r] < H["Vf_pad"]
+                    np.add.at(deg, idx[free & (m == 0), r], 1)
             else:
                 raise NotImplementedError("attachment chunks are exercised on the GPU tests")
             # phase 2

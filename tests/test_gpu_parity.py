@@ -203,19 +203,23 @@ def test_plugin_detect_contacts_bitwise_vs_reference_golden():
 
 
 def test_contacts_detected_on_random_tissue_states(reach_scene):
-    """Contact (face, capsule) lists of the kernel equal the oracle's on many deformed states."""
+    """Contact rows of the kernel equal the oracle's, bitwise, on many deformed states (capsules are
+    inflated by 1.5 mm because the step already pushed the tissue out of the real ones)."""
     from paper_2503_18616_b200 import backend
     ref = O.OracleEnv(O.scene_from_loaded(*reach_scene), 8)
     ref.reset()
     rng = np.random.default_rng(9)
     checked = 0
     for _ in range(150):
-        ref.step(rng.uniform(-1, 1, (8, 3)))
+        a = rng.uniform(-1, 1, (8, 3))
+        a[:, 1] = np.clip(a[:, 1] - 0.6, -1, 1)     # drive the tool into the tissue
+        ref.step(a)
         caps = ref.capsule_rows()
+        caps[:, :, 6] += 0.0015
         for i in range(8):
             a = O.detect_contacts(ref.x[i], ref.scene.faces, caps[i])
             b = backend.detect_contacts(ref.x[i], ref.scene.faces, caps[i])
             for u, w in zip(a, b):
                 assert np.array_equal(u, w)
             checked += len(a[0])
-    assert checked > 0
+    assert checked > 1000

@@ -90,14 +90,16 @@ def test_slot_structure(reach_scene):
         for c in range(H["n_chunks"]):
             if p.chunks[c, 0] != kind:
                 continue
-            b, n = p.chunks[c, 1], p.chunks[c, 2]
+            b, n, padded = p.chunks[c, 1], p.chunks[c, 2], p.chunks[c, 3]
             sl = slots[b:b + n]
             idx = items[b:b + n, :roles]
-            assert np.all((sl >= 0) == (idx < H["Vf_pad"]))   # slots exactly for free endpoints
-            s = sl[sl >= 0]
+            real = sl < padded
+            assert np.all(real == (idx < H["Vf_pad"]))     # real slots exactly for free endpoints
+            assert np.all(sl[~real] < padded + 32)          # pinned endpoints -> 32 trash slots
+            s = sl[real]
             assert len(np.unique(s)) == len(s)
-            # slot k of lane l sits at region + 32k + l: bank = owner lane
-            assert np.all(s % 32 == idx[sl >= 0] % 32)
+            # slot k of lane l sits at region + 32k + l: bank = owner lane (also for trash slots)
+            assert np.all(sl % 32 == idx % 32)
             used.append(len(s))
         expected += sum(used)
     assert expected == info["n_slots_total"] == p.static_cnt.sum()
