@@ -96,6 +96,7 @@ static void decode(ts_handle *h) {
     P.faces = reinterpret_cast<const int32_t *>(b + H->off[TS_SEC_FACES]);
     P.faces_orig = reinterpret_cast<const int32_t *>(b + H->off[TS_SEC_FACES_ORIG]);
     P.rest = b + H->off[TS_SEC_REST];
+    P.gsplit = reinterpret_cast<const int32_t *>(b + H->off[TS_SEC_GSPLIT]);
 }
 
 static void fill_params(const ts_scene_desc &d, TsParams &S) {

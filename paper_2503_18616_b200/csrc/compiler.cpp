@@ -265,37 +265,36 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
     }
 
     // ---- chunking by slot budget ---------------------------------------
+    // The reference's per-vertex accumulation order is the constraint sequence
+    // [live edges..., grasp, live attachments..., live tets...].  Chunks are
+    // contiguous ranges of that sequence (kinds may mix); the grasp is spliced
+    // into the chunk where the edges end, after each vertex's edge slots.
+    std::vector<Item> seq;
+    for (int k = 0; k < 3; ++k) seq.insert(seq.end(), kinds[k].begin(), kinds[k].end());
     const int budget = o.max_chunk_slots > 0 ? o.max_chunk_slots : (1 << 30);
-    struct ChunkBuild { int kind; std::vector<Item> items; std::vector<int> val; std::vector<int> kmax; int padded; };
+    struct ChunkBuild { std::vector<Item> items; std::vector<int> val; std::vector<int> kmax; int padded; };
     std::vector<ChunkBuild> chunks;
-    for (int k = 0; k < 3; ++k) {
+    {
         size_t i = 0;
-        while (i < kinds[k].size()) {
-            ChunkBuild c; c.kind = k == 0 ? TS_CHUNK_EDGE : (k == 1 ? TS_CHUNK_ATT : TS_CHUNK_TET);
+        while (i < seq.size()) {
+            ChunkBuild c;
             c.val.assign(Vf_pad, 0); c.kmax.assign(G, 0); c.padded = 0;
-            while (i < kinds[k].size()) {
-                const Item &it = kinds[k][i];
-                // padded size if added
+            while (i < seq.size()) {
+                const Item &it = seq[i];
                 int grow = 0;
-                std::vector<std::pair<int, int>> bumps;
+                std::vector<int> touched_g;
+                for (int r = 0; r < it.nroles; ++r) if (it.pos[r] < Vf_pad) c.val[it.pos[r]]++;
                 for (int r = 0; r < it.nroles; ++r) {
-                    int p = it.pos[r];
-                    if (p >= Vf_pad) continue;  // pinned: no slot
-                    bumps.push_back({p, 0});
-                }
-                // simulate
-                std::vector<int> tmpv; std::vector<int> touched_g;
-                for (auto &bp : bumps) { int p = bp.first; c.val[p]++; }
-                for (auto &bp : bumps) {
-                    int g = bp.first / 32;
-                    if (c.val[bp.first] > c.kmax[g]) { grow += 32 * (c.val[bp.first] - c.kmax[g]); c.kmax[g] = c.val[bp.first]; touched_g.push_back(g); }
+                    const int p = it.pos[r];
+                    if (p >= Vf_pad) continue;
+                    const int g = p / 32;
+                    if (c.val[p] > c.kmax[g]) { grow += 32 * (c.val[p] - c.kmax[g]); c.kmax[g] = c.val[p]; touched_g.push_back(g); }
                 }
                 if (!c.items.empty() && c.padded + grow > budget) {
-                    // roll back
-                    for (auto &bp : bumps) c.val[bp.first]--;
+                    for (int r = 0; r < it.nroles; ++r) if (it.pos[r] < Vf_pad) c.val[it.pos[r]]--;
                     for (int g : touched_g) {
-                        int m = 0; for (int q = 32 * g; q < 32 * g + 32; ++q) m = std::max(m, c.val[q]);
-                        c.kmax[g] = m;
+                        int mx = 0; for (int q = 32 * g; q < 32 * g + 32; ++q) mx = std::max(mx, c.val[q]);
+                        c.kmax[g] = mx;
                     }
                     break;
                 }
@@ -307,11 +306,22 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
         }
     }
     const int n_chunks = (int)chunks.size();
+    // grasp chunk: the chunk holding the first non-edge item (n_chunks if there is none)
     int grasp_chunk = n_chunks;
-    for (int c = 0; c < n_chunks; ++c) if (chunks[c].kind != TS_CHUNK_EDGE) { grasp_chunk = c; break; }
+    {
+        const size_t n_edges = kinds[0].size();
+        if (n_edges < seq.size()) {
+            size_t pos = 0;
+            for (int c = 0; c < n_chunks; ++c) {
+                if (n_edges < pos + chunks[c].items.size()) { grasp_chunk = c; break; }
+                pos += chunks[c].items.size();
+            }
+        }
+    }
 
     // ---- slot assignment (reference per-vertex order) -------------------
     std::vector<int32_t> region((size_t)n_chunks * G), valence((size_t)n_chunks * Vf_pad), static_cnt(Vf_pad, 0);
+    std::vector<int32_t> gsplit(Vf_pad, 0);
     int slot_cap = 0, n_slots_total = 0;
     for (int c = 0; c < n_chunks; ++c) {
         ChunkBuild &cb = chunks[c];
@@ -323,12 +333,13 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
         const int trash = base;
         slot_cap = std::max(slot_cap, base + 32);
         std::vector<int> k_next(Vf_pad, 0);
-        for (Item &it : cb.items) {  // items are in constraint-index order here
+        for (Item &it : cb.items) {  // items are in sequence order here
             for (int r = 0; r < it.nroles; ++r) {
                 int p = it.pos[r];
                 if (p >= Vf_pad) { it.slot[r] = it.kind == TS_CHUNK_ATT ? -1 : trash + (p % 32); continue; }
                 it.slot[r] = region[(size_t)c * G + p / 32] + 32 * k_next[p] + (p % 32);
                 k_next[p]++;
+                if (c == grasp_chunk && it.kind == TS_CHUNK_EDGE) gsplit[p] = k_next[p];
             }
         }
         for (int p = 0; p < Vf_pad; ++p) {
@@ -341,7 +352,7 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
     slot_cap = std::max(slot_cap, 7 * F);
     slot_cap = roundup(std::max(slot_cap, 32), 32);
 
-    // ---- phase-1 schedule ------------------------------------------------
+    // ---- phase-1 schedule (per chunk, per kind) ----------------------------
     const bool sched = o.schedule_banks >= 0;
     const int bank_mod = (R == 8) ? 16 : 32;
     int total_conf = 0;
@@ -349,20 +360,27 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
     std::vector<Item> all_items[3];
     for (int c = 0; c < n_chunks; ++c) {
         ChunkBuild &cb = chunks[c];
-        int conf = 0;
-        std::vector<Item> s = schedule_items(cb.items, bank_mod, 32, sched, &conf);
-        total_conf += conf;
-        int kidx = cb.kind == TS_CHUNK_EDGE ? 0 : (cb.kind == TS_CHUNK_ATT ? 1 : 2);
         TsChunk &r = chunk_rec[c];
-        r.kind = cb.kind;
-        r.item_begin = (int)all_items[kidx].size();
-        r.item_count = (int)s.size();
+        std::memset(&r, 0, sizeof(r));
+        int begin[3], count[3];
+        for (int k = 0; k < 3; ++k) {
+            const int kind = k == 0 ? TS_CHUNK_EDGE : (k == 1 ? TS_CHUNK_ATT : TS_CHUNK_TET);
+            std::vector<Item> part;
+            for (const Item &it : cb.items) if (it.kind == kind) part.push_back(it);
+            int conf = 0;
+            std::vector<Item> s = schedule_items(part, bank_mod, 32, sched && kind != TS_CHUNK_ATT, &conf);
+            r.conflicts += conf;
+            begin[k] = (int)all_items[k].size();
+            count[k] = (int)s.size();
+            all_items[k].insert(all_items[k].end(), s.begin(), s.end());
+        }
+        total_conf += r.conflicts;
+        r.edge_begin = begin[0]; r.edge_count = count[0];
+        r.att_begin = begin[1]; r.att_count = count[1];
+        r.tet_begin = begin[2]; r.tet_count = count[2];
         r.slot_count = cb.padded;
         r.region_off = c * G;
         r.val_off = c * Vf_pad;
-        r.conflicts = conf;
-        r.pad = 0;
-        all_items[kidx].insert(all_items[kidx].end(), s.begin(), s.end());
     }
 
     // ---- emit --------------------------------------------------------------
@@ -435,6 +453,7 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
     sz[TS_SEC_FACES] = 12LL * F;
     sz[TS_SEC_FACES_ORIG] = 12LL * F;
     sz[TS_SEC_REST] = 3LL * R * V;
+    sz[TS_SEC_GSPLIT] = 4LL * Vf_pad;
     TsProgHeader hdr{};
     hdr.magic = TS_PROG_MAGIC; hdr.version = TS_PROG_VERSION; hdr.real_bytes = R; hdr.n_sections = TS_SEC_COUNT;
     hdr.V = V; hdr.Vf = Vf; hdr.Vf_pad = Vf_pad; hdr.Vstore = Vstore;
@@ -460,6 +479,7 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
     put(blob, hdr.off[TS_SEC_O2S], o2s);
     put(blob, hdr.off[TS_SEC_FACES], faces_s);
     put(blob, hdr.off[TS_SEC_FACES_ORIG], faces_o);
+    put(blob, hdr.off[TS_SEC_GSPLIT], gsplit);
     auto put_real = [&](int sec, const std::vector<double> &v) {
         if (R == 8) put(blob, hdr.off[sec], v);
         else { std::vector<float> f(v.begin(), v.end()); put(blob, hdr.off[sec], f); }

@@ -43,12 +43,16 @@ enum TsSection {
     TS_SEC_FACES,         // int32 [F][3] surface faces in storage positions
     TS_SEC_FACES_ORIG,    // int32 [F][3] surface faces, original ids (plugin outputs)
     TS_SEC_REST,          // Real [V][3] rest positions, original order (reset)
+    TS_SEC_GSPLIT,        // int32 [Vf_pad] slots of p in the grasp chunk that precede the grasp
     TS_SEC_COUNT
 };
 
+// A chunk is a contiguous range of the reference's constraint sequence
+// [edges..., attachments..., tets...]; it may hold items of all three kinds.
 struct TsChunk {
-    int32_t kind, item_begin, item_count, slot_count;
-    int32_t region_off, val_off, conflicts, pad;
+    int32_t edge_begin, edge_count, att_begin, att_count;
+    int32_t tet_begin, tet_count, slot_count, region_off;
+    int32_t val_off, conflicts, pad0, pad1;
 };
 
 struct TsProgHeader {

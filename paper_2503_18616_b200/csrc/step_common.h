@@ -57,6 +57,7 @@ struct TsDevProg {
     const int32_t *faces;
     const int32_t *faces_orig;
     const void *rest;
+    const int32_t *gsplit;
 };
 
 // Per-launch pointers (device).

@@ -314,13 +314,13 @@ __device__ __forceinline__ Smem<Real> carve(const TsDevProg &P, unsigned char *r
 // phase 1: constraint-parallel correction vectors into slots
 // ---------------------------------------------------------------------------
 template <typename Real>
-__device__ __forceinline__ void p1_edges(const TsDevProg &P, const Smem<Real> &m, const TsChunk &ch,
+__device__ __forceinline__ void p1_edges(const TsDevProg &P, const Smem<Real> &m, int begin, int count,
                                          Real ks) {
     using V4 = typename R4<Real>::T;
-    const int4 *idx = P.edge_idx + ch.item_begin;
-    const V4 *par = reinterpret_cast<const V4 *>(P.edge_par) + ch.item_begin;
+    const int4 *idx = P.edge_idx + begin;
+    const V4 *par = reinterpret_cast<const V4 *>(P.edge_par) + begin;
     const int vfp = P.Vf_pad;
-    for (int i = threadIdx.x; i < ch.item_count; i += blockDim.x) {
+    for (int i = threadIdx.x; i < count; i += blockDim.x) {
         const int4 id = __ldg(idx + i);     // {pos a, pos b, slot a, slot b}; pinned endpoints -> trash slots
         const V4 pr = par[i];
         const Real dx = m.xs[id.x] - m.xs[id.y];
@@ -364,12 +364,12 @@ __device__ __forceinline__ void store_slot(const Smem<Real> &m, int s, Real c, R
 }
 
 template <typename Real>
-__device__ __forceinline__ void p1_tets(const TsDevProg &P, const Smem<Real> &m, const TsChunk &ch, Real kv) {
-    const int4 *idx = P.tet_idx + ch.item_begin;
-    const int4 *slot = P.tet_slot + ch.item_begin;
-    const Real *rv = reinterpret_cast<const Real *>(P.tet_rv) + ch.item_begin;
+__device__ __forceinline__ void p1_tets(const TsDevProg &P, const Smem<Real> &m, int begin, int count, Real kv) {
+    const int4 *idx = P.tet_idx + begin;
+    const int4 *slot = P.tet_slot + begin;
+    const Real *rv = reinterpret_cast<const Real *>(P.tet_rv) + begin;
     const int vfp = P.Vf_pad;
-    for (int i = threadIdx.x; i < ch.item_count; i += blockDim.x) {
+    for (int i = threadIdx.x; i < count; i += blockDim.x) {
         const int4 id = __ldg(idx + i);
         const int4 sl = __ldg(slot + i);
         const Real ax = m.xs[id.x], ay = m.ys[id.x], az = m.zs[id.x];
@@ -441,13 +441,13 @@ __device__ __forceinline__ void p1_tets(const TsDevProg &P, const Smem<Real> &m,
 }
 
 template <typename Real>
-__device__ void p1_atts(const TsDevProg &P, const Smem<Real> &m, const TsChunk &ch) {
+__device__ void p1_atts(const TsDevProg &P, const Smem<Real> &m, int begin, int count) {
     using V4 = typename R4<Real>::T;
-    const int4 *idx = P.att_idx + ch.item_begin;
-    const int4 *slot = P.att_slot + ch.item_begin;
-    const V4 *par = reinterpret_cast<const V4 *>(P.att_par) + ch.item_begin;
-    const V4 *anc = reinterpret_cast<const V4 *>(P.att_anchor) + ch.item_begin;
-    for (int i = threadIdx.x; i < ch.item_count; i += blockDim.x) {
+    const int4 *idx = P.att_idx + begin;
+    const int4 *slot = P.att_slot + begin;
+    const V4 *par = reinterpret_cast<const V4 *>(P.att_par) + begin;
+    const V4 *anc = reinterpret_cast<const V4 *>(P.att_anchor) + begin;
+    for (int i = threadIdx.x; i < count; i += blockDim.x) {
         const int4 id = idx[i];
         const int4 sl = slot[i];
         const V4 pr = par[i];   // rest, k, wv, wc
@@ -714,39 +714,47 @@ __global__ void __launch_bounds__(512, sizeof(Real) == 4 ? 2 : 1) step_kernel(co
             }
             __syncthreads();
             const double d0 = sc.drag[0], d1 = sc.drag[1], d2 = sc.drag[2];
+            // grasp contribution of owner slot r: after the vertex's edge slots (_kernels.pyx:283-298)
+            auto add_grasp = [&](int r) {
+                const int p = r * B + t;
+                if (p < P.Vf && p == gvs) {
+                    const Real dx = (Real)(d0 - (double)xr[r]);
+                    const Real dy = (Real)(d1 - (double)yr[r]);
+                    const Real dz = (Real)(d2 - (double)zr[r]);
+                    const Real dist = sqrt(dx * dx + dy * dy + dz * dz);
+                    if (!(dist <= (Real)1e-12)) { accx[r] += dx; accy[r] += dy; accz[r] += dz; gcnt[r] = 1; }
+                }
+            };
             for (int s = 0; s < S.substeps; ++s) {
-                for (int c = 0; c <= P.n_chunks; ++c) {
-                    // grasp contribution goes after all edge slots (_kernels.pyx:283-298)
-                    if (c == P.grasp_chunk) {
-#pragma unroll
-                        for (int r = 0; r < VPT; ++r) {
-                            const int p = r * B + t;
-                            if (p < P.Vf && p == gvs) {
-                                const Real dx = (Real)(d0 - (double)xr[r]);
-                                const Real dy = (Real)(d1 - (double)yr[r]);
-                                const Real dz = (Real)(d2 - (double)zr[r]);
-                                const Real dist = sqrt(dx * dx + dy * dy + dz * dz);
-                                if (!(dist <= (Real)1e-12)) { accx[r] += dx; accy[r] += dy; accz[r] += dz; gcnt[r] = 1; }
-                            }
-                        }
-                    }
-                    if (c == P.n_chunks) break;
+                for (int c = 0; c < P.n_chunks; ++c) {
                     const TsChunk ch = P.chunks[c];
-                    if (ch.kind == TS_CHUNK_EDGE) p1_edges<Real>(P, m, ch, ks);
-                    else if (ch.kind == TS_CHUNK_TET) p1_tets<Real>(P, m, ch, kv);
-                    else p1_atts<Real>(P, m, ch);
+                    // phase 1: every kind of the chunk, no barrier in between (disjoint slots)
+                    if (ch.edge_count) p1_edges<Real>(P, m, ch.edge_begin, ch.edge_count, ks);
+                    if (ch.att_count) p1_atts<Real>(P, m, ch.att_begin, ch.att_count);
+                    if (ch.tet_count) p1_tets<Real>(P, m, ch.tet_begin, ch.tet_count, kv);
                     __syncthreads();
                     // phase 2: owner gathers its slots in reference order
+                    const bool gchunk = c == P.grasp_chunk;
 #pragma unroll
                     for (int r = 0; r < VPT; ++r) {
                         const int p = r * B + t;
                         if (p < P.Vf) {
                             const int base = P.region[ch.region_off + (p >> 5)] + lane;
                             const int val = P.valence[ch.val_off + p];
+                            const int pre = gchunk ? P.gsplit[p] : val;
                             Real ax = accx[r], ay = accy[r], az = accz[r];
-                            for (int k = 0; k < val; ++k) {
+                            for (int k = 0; k < pre; ++k) {
                                 const int sidx = base + 32 * k;
                                 ax += m.slx[sidx]; ay += m.sly[sidx]; az += m.slz[sidx];
+                            }
+                            if (gchunk) {
+                                accx[r] = ax; accy[r] = ay; accz[r] = az;
+                                add_grasp(r);
+                                ax = accx[r]; ay = accy[r]; az = accz[r];
+                                for (int k = pre; k < val; ++k) {
+                                    const int sidx = base + 32 * k;
+                                    ax += m.slx[sidx]; ay += m.sly[sidx]; az += m.slz[sidx];
+                                }
                             }
                             accx[r] = ax; accy[r] = ay; accz[r] = az;
                             const int dg = m.deg[p];
@@ -754,6 +762,10 @@ __global__ void __launch_bounds__(512, sizeof(Real) == 4 ? 2 : 1) step_kernel(co
                         }
                     }
                     if (c + 1 < P.n_chunks) __syncthreads();   // slots are reused by the next chunk
+                }
+                if (P.grasp_chunk == P.n_chunks) {
+#pragma unroll
+                    for (int r = 0; r < VPT; ++r) add_grasp(r);
                 }
                 // apply (ts_lane_apply, _kernels.pyx:213-244) + next predict
 #pragma unroll

@@ -15,7 +15,7 @@ import numpy as np
 
 SECTIONS = ["CHUNK", "EDGE_IDX", "EDGE_PAR", "TET_IDX", "TET_SLOT", "TET_RV", "ATT_IDX", "ATT_SLOT",
             "ATT_PAR", "ATT_ANCHOR", "REGION", "VALENCE", "STATIC_CNT", "S2O", "O2S", "W", "FACES",
-            "FACES_ORIG", "REST"]
+            "FACES_ORIG", "REST", "GSPLIT"]
 HDR_FIELDS = ["magic", "version", "real_bytes", "n_sections", "V", "Vf", "Vf_pad", "Vstore", "F", "B",
               "VPT", "G", "n_chunks", "grasp_chunk", "slot_capacity", "n_att", "n_edge_items",
               "n_tet_items", "n_att_items", "bank_conflicts", "n_slots_total", "pad0", "pad1", "pad2"]
@@ -33,7 +33,9 @@ class Program:
         H = self.h
         nE, nT, nA = H["n_edge_items"], H["n_tet_items"], H["n_att_items"]
         C, G, Vfp = H["n_chunks"], H["G"], H["Vf_pad"]
-        self.chunks = self.sec("CHUNK", np.int32, C * 8).reshape(C, 8)
+        # TsChunk: edge_begin, edge_count, att_begin, att_count, tet_begin, tet_count, slot_count,
+        #          region_off, val_off, conflicts, pad, pad
+        self.chunks = self.sec("CHUNK", np.int32, C * 12).reshape(C, 12)
         self.edge_idx = self.sec("EDGE_IDX", np.int32, 4 * nE).reshape(nE, 4)
         self.edge_par = self.sec("EDGE_PAR", rt, 4 * nE).reshape(nE, 4).astype(np.float64)
         self.tet_idx = self.sec("TET_IDX", np.int32, 4 * nT).reshape(nT, 4)
@@ -50,6 +52,7 @@ class Program:
         self.o2s = self.sec("O2S", np.int32, H["V"])
         self.w = self.sec("W", rt, H["Vstore"]).astype(np.float64)
         self.faces = self.sec("FACES", np.int32, 3 * H["F"]).reshape(-1, 3)
+        self.gsplit = self.sec("GSPLIT", np.int32, Vfp)
 
     def sec(self, name, dtype, count):
         o = int(self.off[SECTIONS.index(name)])
@@ -77,21 +80,23 @@ def run_substeps(prog: Program, x, v, grasp_vertex, drag, g, h, substeps, dampin
     for s in range(substeps):
         acc = np.zeros((Vf, 3))
         cnt_adj = np.zeros(Vf, np.int64)
-        for c in range(H["n_chunks"] + 1):
-            if c == H["grasp_chunk"] and 0 <= gvs < Vf:
+        def add_grasp():
+            if 0 <= gvs < Vf:
                 d = np.asarray(drag, np.float64) - xs[gvs]
                 dist = np.sqrt((d[0] * d[0] + d[1] * d[1]) + d[2] * d[2])
                 if not (dist <= 1e-12):
                     acc[gvs] += d
                     cnt_adj[gvs] += 1
-            if c == H["n_chunks"]:
-                break
-            kind, begin, count = prog.chunks[c, 0], prog.chunks[c, 1], prog.chunks[c, 2]
+
+        for c in range(H["n_chunks"]):
+            eb, ec, ab, ac, tb, tc = (int(v) for v in prog.chunks[c, :6])
             slots = np.full((scap, 3), np.nan)
             deg = np.zeros(H["Vf_pad"], np.int64)
-            if kind == 0:
-                idx = prog.edge_idx[begin:begin + count]
-                par = prog.edge_par[begin:begin + count]
+            if ac:
+                raise NotImplementedError("attachment chunks are exercised on the GPU tests")
+            if ec:
+                idx = prog.edge_idx[eb:eb + ec]
+                par = prog.edge_par[eb:eb + ec]
                 d = xs[idx[:, 0]] - xs[idx[:, 1]]
                 dist = np.sqrt((d[:, 0] * d[:, 0] + d[:, 1] * d[:, 1]) + d[:, 2] * d[:, 2])
                 m = 0.5 + np.copysign(0.5, dist - 1e-12)
@@ -103,10 +108,10 @@ def run_substeps(prog: Program, x, v, grasp_vertex, drag, g, h, substeps, dampin
                     slots[sl] = coef[:, None] * d
                     free = idx[:, pos] < H["Vf_pad"]
                     np.add.at(deg, idx[free & (m == 0), pos], 1)
-            elif kind == 2:
-                idx = prog.tet_idx[begin:begin + count]
-                sl = prog.tet_slot[begin:begin + count]
-                rv = prog.tet_rv[begin:begin + count]
+            if tc:
+                idx = prog.tet_idx[tb:tb + tc]
+                sl = prog.tet_slot[tb:tb + tc]
+                rv = prog.tet_rv[tb:tb + tc]
                 pa = xs[idx[:, 0]]
                 ba, ca_, da = xs[idx[:, 1]] - pa, xs[idx[:, 2]] - pa, xs[idx[:, 3]] - pa
 
@@ -126,15 +131,21 @@ def run_substeps(prog: Program, x, v, grasp_vertex, drag, g, h, substeps, dampin
                     slots[sl[:, r]] = scv[:, None] * gg
                     free = idx[:, r] < H["Vf_pad"]
                     np.add.at(deg, idx[free & (m == 0), r], 1)
-            else:
-                raise NotImplementedError("attachment chunks are exercised on the GPU tests")
-            # phase 2
+            # phase 2: slots in order, the grasp spliced after the edge slots of the grasp chunk
             base = prog.region[c, grp] + lane
             val = prog.valence[c, :Vf]
-            for k in range(int(val.max()) if len(val) else 0):
-                live = val > k
+            pre = prog.gsplit[:Vf] if c == H["grasp_chunk"] else val
+            for k in range(int(pre.max()) if len(pre) else 0):
+                live = pre > k
                 acc[live] += slots[base[live] + 32 * k]
+            if c == H["grasp_chunk"]:
+                add_grasp()
+                for k in range(int(val.max()) if len(val) else 0):
+                    live = (val > k) & (k >= pre)
+                    acc[live] += slots[base[live] + 32 * k]
             cnt_adj -= deg[:Vf]
+        if H["grasp_chunk"] == H["n_chunks"]:
+            add_grasp()
         n = (prog.static_cnt[:Vf] + cnt_adj).astype(np.float64)
         m = 0.5 + np.copysign(0.5, n - 0.5)
         inv = m / (n + (1.0 - m))

@@ -88,9 +88,9 @@ def test_slot_structure(reach_scene):
         slots = (p.edge_idx[:, 2:4] if kind == 0 else p.tet_slot)
         used = []
         for c in range(H["n_chunks"]):
-            if p.chunks[c, 0] != kind:
+            b, n, padded = p.chunks[c, 2 * kind], p.chunks[c, 2 * kind + 1], p.chunks[c, 6]
+            if n == 0:
                 continue
-            b, n, padded = p.chunks[c, 1], p.chunks[c, 2], p.chunks[c, 3]
             sl = slots[b:b + n]
             idx = items[b:b + n, :roles]
             real = sl < padded
