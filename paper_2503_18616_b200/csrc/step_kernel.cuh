@@ -320,9 +320,15 @@ __device__ __forceinline__ void p1_edges(const TsDevProg &P, const Smem<Real> &m
     const int4 *idx = P.edge_idx + begin;
     const V4 *par = reinterpret_cast<const V4 *>(P.edge_par) + begin;
     const int vfp = P.Vf_pad;
-    for (int i = threadIdx.x; i < count; i += blockDim.x) {
-        const int4 id = __ldg(idx + i);     // {pos a, pos b, slot a, slot b}; pinned endpoints -> trash slots
-        const V4 pr = par[i];
+    const int stride = blockDim.x;
+    // topology of the next item is fetched one iteration ahead (hides the L2 latency)
+    int4 nid = make_int4(0, 0, 0, 0);
+    V4 npr{};
+    if ((int)threadIdx.x < count) { nid = __ldg(idx + threadIdx.x); npr = par[threadIdx.x]; }
+    for (int i = threadIdx.x; i < count; i += stride) {
+        const int4 id = nid;     // {pos a, pos b, slot a, slot b}; pinned endpoints -> trash slots
+        const V4 pr = npr;
+        if (i + stride < count) { nid = __ldg(idx + i + stride); npr = par[i + stride]; }
         const Real dx = m.xs[id.x] - m.xs[id.y];
         const Real dy = m.ys[id.x] - m.ys[id.y];
         const Real dz = m.zs[id.x] - m.zs[id.y];
@@ -369,9 +375,15 @@ __device__ __forceinline__ void p1_tets(const TsDevProg &P, const Smem<Real> &m,
     const int4 *slot = P.tet_slot + begin;
     const Real *rv = reinterpret_cast<const Real *>(P.tet_rv) + begin;
     const int vfp = P.Vf_pad;
-    for (int i = threadIdx.x; i < count; i += blockDim.x) {
-        const int4 id = __ldg(idx + i);
-        const int4 sl = __ldg(slot + i);
+    const int stride = blockDim.x;
+    int4 nid = make_int4(0, 0, 0, 0), nsl = make_int4(0, 0, 0, 0);
+    Real nrv = 0;
+    if ((int)threadIdx.x < count) { nid = __ldg(idx + threadIdx.x); nsl = __ldg(slot + threadIdx.x); nrv = rv[threadIdx.x]; }
+    for (int i = threadIdx.x; i < count; i += stride) {
+        const int4 id = nid;
+        const int4 sl = nsl;
+        const Real rvi = nrv;
+        if (i + stride < count) { nid = __ldg(idx + i + stride); nsl = __ldg(slot + i + stride); nrv = rv[i + stride]; }
         const Real ax = m.xs[id.x], ay = m.ys[id.x], az = m.zs[id.x];
         const Real bax = m.xs[id.y] - ax, bay = m.ys[id.y] - ay, baz = m.zs[id.y] - az;
         const Real cax = m.xs[id.z] - ax, cay = m.ys[id.z] - ay, caz = m.zs[id.z] - az;
@@ -391,7 +403,7 @@ __device__ __forceinline__ void p1_tets(const TsDevProg &P, const Smem<Real> &m,
             const Real gax = -(gbx + gcx + gdx);
             const Real gay = -(gby + gcy + gdy);
             const Real gaz = -(gbz + gcz + gdz);
-            const Real cval = (gdx * dax + gdy * day + gdz * daz) - rv[i];
+            const Real cval = (gdx * dax + gdy * day + gdz * daz) - rvi;
             const Real denom = gax * gax + gay * gay + gaz * gaz
                              + gbx * gbx + gby * gby + gbz * gbz
                              + gcx * gcx + gcy * gcy + gcz * gcz
@@ -418,7 +430,7 @@ __device__ __forceinline__ void p1_tets(const TsDevProg &P, const Smem<Real> &m,
             const float Gax = -(Gbx + Gcx + Gdx);
             const float Gay = -(Gby + Gcy + Gdy);
             const float Gaz = -(Gbz + Gcz + Gdz);
-            const float c6 = __fmaf_rn(Gdz, daz, __fmaf_rn(Gdy, day, Gdx * dax)) - rv[i];
+            const float c6 = __fmaf_rn(Gdz, daz, __fmaf_rn(Gdy, day, Gdx * dax)) - rvi;
             float den = Gax * Gax;
             den = __fmaf_rn(Gay, Gay, den); den = __fmaf_rn(Gaz, Gaz, den);
             den = __fmaf_rn(Gbx, Gbx, den); den = __fmaf_rn(Gby, Gby, den); den = __fmaf_rn(Gbz, Gbz, den);
@@ -743,6 +755,7 @@ __global__ void __launch_bounds__(512, sizeof(Real) == 4 ? 2 : 1) step_kernel(co
                             const int val = P.valence[ch.val_off + p];
                             const int pre = gchunk ? P.gsplit[p] : val;
                             Real ax = accx[r], ay = accy[r], az = accz[r];
+#pragma unroll 4
                             for (int k = 0; k < pre; ++k) {
                                 const int sidx = base + 32 * k;
                                 ax += m.slx[sidx]; ay += m.sly[sidx]; az += m.slz[sidx];
