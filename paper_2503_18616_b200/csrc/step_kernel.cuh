@@ -283,9 +283,20 @@ struct Scal {
     int abort;
 };
 
+// Component c of element i of an (n, 3) array-of-structs in shared memory.
+// Word 3i + c sits in bank (3i + c) mod 32; 3 is invertible mod 32 (and mod
+// 16 for 64-bit words), so lanes with distinct i mod 32 are conflict-free,
+// exactly as with separate component arrays, and the three components share
+// one address (immediate offsets 0/4/8) -- a third of the address arithmetic.
+template <typename Real>
+struct Strided {
+    Real *p;
+    __device__ __forceinline__ Real &operator[](int i) const { return p[3 * i]; }
+};
+
 template <typename Real>
 struct Smem {
-    Real *xs, *ys, *zs, *slx, *sly, *slz;
+    Strided<Real> xs, ys, zs, slx, sly, slz;   // positions (storage order), slots
     int *deg;
     unsigned *cbits;
     Scal *sc;
@@ -295,13 +306,11 @@ struct Smem {
 template <typename Real>
 __device__ __forceinline__ Smem<Real> carve(const TsDevProg &P, unsigned char *raw) {
     Smem<Real> m;
-    m.xs = reinterpret_cast<Real *>(raw);
-    m.ys = m.xs + P.Vstore;
-    m.zs = m.ys + P.Vstore;
-    m.slx = m.zs + P.Vstore;
-    m.sly = m.slx + P.slot_cap;
-    m.slz = m.sly + P.slot_cap;
-    m.deg = reinterpret_cast<int *>(m.slz + P.slot_cap);
+    Real *pos = reinterpret_cast<Real *>(raw);
+    Real *slots = pos + 3 * P.Vstore;
+    m.xs.p = pos; m.ys.p = pos + 1; m.zs.p = pos + 2;
+    m.slx.p = slots; m.sly.p = slots + 1; m.slz.p = slots + 2;
+    m.deg = reinterpret_cast<int *>(slots + 3 * P.slot_cap);
     m.cbits = reinterpret_cast<unsigned *>(m.deg + P.Vf_pad);
     size_t off = reinterpret_cast<unsigned char *>(m.cbits + P.cbits_words) - raw;
     off = (off + 15) / 16 * 16;
@@ -328,7 +337,10 @@ __device__ __forceinline__ void p1_edges(const TsDevProg &P, const Smem<Real> &m
     for (int i = threadIdx.x; i < count; i += stride) {
         const int4 id = nid;     // {pos a, pos b, slot a, slot b}; pinned endpoints -> trash slots
         const V4 pr = npr;
-        if (i + stride < count) { nid = __ldg(idx + i + stride); npr = par[i + stride]; }
+        {   // unconditional (clamped) prefetch: no branch in the loop body
+            const int j = min(i + stride, count - 1);
+            nid = __ldg(idx + j); npr = par[j];
+        }
         const Real dx = m.xs[id.x] - m.xs[id.y];
         const Real dy = m.ys[id.x] - m.ys[id.y];
         const Real dz = m.zs[id.x] - m.zs[id.y];
@@ -383,7 +395,10 @@ __device__ __forceinline__ void p1_tets(const TsDevProg &P, const Smem<Real> &m,
         const int4 id = nid;
         const int4 sl = nsl;
         const Real rvi = nrv;
-        if (i + stride < count) { nid = __ldg(idx + i + stride); nsl = __ldg(slot + i + stride); nrv = rv[i + stride]; }
+        {
+            const int j = min(i + stride, count - 1);
+            nid = __ldg(idx + j); nsl = __ldg(slot + j); nrv = rv[j];
+        }
         const Real ax = m.xs[id.x], ay = m.ys[id.x], az = m.zs[id.x];
         const Real bax = m.xs[id.y] - ax, bay = m.ys[id.y] - ay, baz = m.zs[id.y] - az;
         const Real cax = m.xs[id.z] - ax, cay = m.ys[id.z] - ay, caz = m.zs[id.z] - az;
@@ -818,7 +833,7 @@ __global__ void __launch_bounds__(512, sizeof(Real) == 4 ? 2 : 1) step_kernel(co
         // ---- D. contacts ---------------------------------------------------
         if ((mode & (TS_M_CONTACTS | TS_M_DETECT_ONLY)) && P.F > 0) {
             Cap<Real> *C = m.caps;   // built by threads 0..2 before the substeps
-            Real *rec = m.slx;   // 3F records x 7 reals (the slot buffer is free now)
+            Real *rec = m.slx.p;   // 3F records x 7 reals (the slot buffer is free now)
             for (int f = t; f < P.F; f += B) {
                 const int ia = P.faces[3 * f], ib = P.faces[3 * f + 1], ic = P.faces[3 * f + 2];
                 const Real pa[3] = {m.xs[ia], m.ys[ia], m.zs[ia]};
