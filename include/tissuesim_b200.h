@@ -92,6 +92,7 @@ typedef struct ts_layout_opts {
     int32_t max_chunk_slots;    /* slot budget per constraint chunk (0 = auto) */
     int32_t schedule_banks;     /* 1 = bank-conflict-aware item schedule (default), -1 = off */
     int32_t smem_budget;        /* bytes of shared memory per CTA to aim for (0 = auto) */
+    int32_t compact;            /* 16-bit item streams when possible (default), -1 = off */
 } ts_layout_opts;
 
 typedef struct ts_layout_info {
@@ -99,6 +100,7 @@ typedef struct ts_layout_info {
     int32_t n_free, n_store, slot_capacity, smem_bytes;
     int32_t n_edge_items, n_tet_items, n_att_items, n_slots_total;
     int32_t bank_conflicts_p1;  /* residual phase-1 conflicts of the schedule (extra wavefronts / substep) */
+    int32_t compact;            /* 1 when the program uses the 16-bit item streams */
     int64_t program_bytes;
 } ts_layout_info;
 

@@ -97,6 +97,10 @@ static void decode(ts_handle *h) {
     P.faces_orig = reinterpret_cast<const int32_t *>(b + H->off[TS_SEC_FACES_ORIG]);
     P.rest = b + H->off[TS_SEC_REST];
     P.gsplit = reinterpret_cast<const int32_t *>(b + H->off[TS_SEC_GSPLIT]);
+    P.compact = H->compact;
+    P.w_free = H->w_free;
+    P.edge_c = reinterpret_cast<const uint4 *>(b + H->off[TS_SEC_EDGE_C]);
+    P.tet_c = reinterpret_cast<const uint4 *>(b + H->off[TS_SEC_TET_C]);
 }
 
 static void fill_params(const ts_scene_desc &d, TsParams &S) {

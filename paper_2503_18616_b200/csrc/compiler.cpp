@@ -435,6 +435,36 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
     std::vector<double> rest(3 * (size_t)V);
     for (int i = 0; i < 3 * V; ++i) rest[i] = d.positions_rest[i];
 
+    // ---- compact 16-bit item streams ---------------------------------------
+    // Every mesh built by load_scene has one inverse mass for all free vertices
+    // (mesh.py:217: uniform mass), so an edge needs only its rest length: the
+    // per-endpoint weights follow from which endpoints are pinned.
+    double w_free = 0.0;
+    bool uniform = true;
+    for (int v = 0; v < V; ++v)
+        if (is_free(v)) {
+            if (w_free == 0.0) w_free = w[v];
+            else if (w[v] != w_free) uniform = false;
+        }
+    const bool compact = o.compact >= 0 && uniform && Vstore <= 65535 && slot_cap <= 65535;
+    std::vector<uint32_t> edge_c(compact ? 4 * (size_t)nE : 0), tet_c(compact ? 4 * (size_t)nT : 0);
+    if (compact) {
+        auto pk = [](int lo, int hi) { return (uint32_t)(lo & 0xffff) | ((uint32_t)(hi & 0xffff) << 16); };
+        for (int i = 0; i < nE; ++i) {
+            edge_c[4 * i + 0] = pk(edge_idx[4 * i + 0], edge_idx[4 * i + 1]);
+            edge_c[4 * i + 1] = pk(edge_idx[4 * i + 2], edge_idx[4 * i + 3]);
+            const double rl = edge_par[4 * i + 0];
+            if (R == 8) { std::memcpy(&edge_c[4 * i + 2], &rl, 8); }
+            else { const float f = (float)rl; std::memcpy(&edge_c[4 * i + 2], &f, 4); edge_c[4 * i + 3] = 0; }
+        }
+        for (int i = 0; i < nT; ++i) {
+            tet_c[4 * i + 0] = pk(tet_idx[4 * i + 0], tet_idx[4 * i + 1]);
+            tet_c[4 * i + 1] = pk(tet_idx[4 * i + 2], tet_idx[4 * i + 3]);
+            tet_c[4 * i + 2] = pk(tet_slot[4 * i + 0], tet_slot[4 * i + 1]);
+            tet_c[4 * i + 3] = pk(tet_slot[4 * i + 2], tet_slot[4 * i + 3]);
+        }
+    }
+
     // sizes (bytes) per section
     int64_t sz[TS_SEC_COUNT];
     sz[TS_SEC_CHUNK] = (int64_t)n_chunks * sizeof(TsChunk);
@@ -457,7 +487,11 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
     sz[TS_SEC_FACES_ORIG] = 12LL * F;
     sz[TS_SEC_REST] = 3LL * R * V;
     sz[TS_SEC_GSPLIT] = 4LL * Vf_pad;
+    sz[TS_SEC_EDGE_C] = 4LL * edge_c.size();
+    sz[TS_SEC_TET_C] = 4LL * tet_c.size();
     TsProgHeader hdr{};
+    hdr.compact = compact ? 1 : 0;
+    hdr.w_free = w_free;
     hdr.magic = TS_PROG_MAGIC; hdr.version = TS_PROG_VERSION; hdr.real_bytes = R; hdr.n_sections = TS_SEC_COUNT;
     hdr.V = V; hdr.Vf = Vf; hdr.Vf_pad = Vf_pad; hdr.Vstore = Vstore;
     hdr.F = F; hdr.B = B; hdr.VPT = VPT; hdr.G = G;
@@ -483,6 +517,8 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
     put(blob, hdr.off[TS_SEC_FACES], faces_s);
     put(blob, hdr.off[TS_SEC_FACES_ORIG], faces_o);
     put(blob, hdr.off[TS_SEC_GSPLIT], gsplit);
+    put(blob, hdr.off[TS_SEC_EDGE_C], edge_c);
+    put(blob, hdr.off[TS_SEC_TET_C], tet_c);
     auto put_real = [&](int sec, const std::vector<double> &v) {
         if (R == 8) put(blob, hdr.off[sec], v);
         else { std::vector<float> f(v.begin(), v.end()); put(blob, hdr.off[sec], f); }
@@ -498,7 +534,7 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
     info.precision = prec; info.block_threads = B; info.vertices_per_thread = VPT; info.n_chunks = n_chunks;
     info.n_free = Vf; info.n_store = Vstore; info.slot_capacity = slot_cap;
     info.n_edge_items = nE; info.n_tet_items = nT; info.n_att_items = nA; info.n_slots_total = n_slots_total;
-    info.bank_conflicts_p1 = total_conf; info.program_bytes = off;
+    info.bank_conflicts_p1 = total_conf; info.program_bytes = off; info.compact = compact ? 1 : 0;
     return TS_OK;
 }
 

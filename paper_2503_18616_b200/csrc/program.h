@@ -44,6 +44,10 @@ enum TsSection {
     TS_SEC_FACES_ORIG,    // int32 [F][3] surface faces, original ids (plugin outputs)
     TS_SEC_REST,          // Real [V][3] rest positions, original order (reset)
     TS_SEC_GSPLIT,        // int32 [Vf_pad] slots of p in the grasp chunk that precede the grasp
+    // compact 16-bit item streams (uniform free-vertex mass, < 65536 positions / slots):
+    // the whole phase-1 stream of reach_1170 fits in L1 and is shared by every CTA on an SM
+    TS_SEC_EDGE_C,        // uint4 {pa | pb << 16, sa | sb << 16, rest (fp32 bits | fp64 lo), fp64 hi}
+    TS_SEC_TET_C,         // uint4 {pa | pb << 16, pc | pd << 16, sa | sb << 16, sc | sd << 16}
     TS_SEC_COUNT
 };
 
@@ -61,7 +65,8 @@ struct TsProgHeader {
     int32_t F, B, VPT, G;
     int32_t n_chunks, grasp_chunk, slot_capacity, n_att;
     int32_t n_edge_items, n_tet_items, n_att_items, bank_conflicts;
-    int32_t n_slots_total, pad0, pad1, pad2;
+    int32_t n_slots_total, compact, pad1, pad2;
+    double w_free;   // the common inverse mass of free vertices (compact programs)
     int64_t off[TS_SEC_COUNT];
     int64_t total_bytes;
 };

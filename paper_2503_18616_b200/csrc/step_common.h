@@ -58,6 +58,10 @@ struct TsDevProg {
     const int32_t *faces_orig;
     const void *rest;
     const int32_t *gsplit;
+    int32_t compact;          // 1: use the 16-bit streams below
+    double w_free;            // common inverse mass of free vertices (compact programs)
+    const uint4 *edge_c;
+    const uint4 *tet_c;
 };
 
 // Per-launch pointers (device).

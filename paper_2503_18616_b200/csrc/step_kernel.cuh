@@ -322,52 +322,88 @@ __device__ __forceinline__ Smem<Real> carve(const TsDevProg &P, unsigned char *r
 // ---------------------------------------------------------------------------
 // phase 1: constraint-parallel correction vectors into slots
 // ---------------------------------------------------------------------------
+// One distance constraint: correction vectors for both endpoints into their slots.
+// fp64: (wa, wb, wsum) are the reference's operands; fp32: (wa, wb) carry the
+// folded coefficients ks wa / wsum, ks wb / wsum and wsum is unused.
+template <typename Real>
+__device__ __forceinline__ void edge_item(const Smem<Real> &m, int pa, int pb, int sa, int sb, Real rl, Real wa,
+                                          Real wb, Real wsum, Real ks, int vfp) {
+    const Real dx = m.xs[pa] - m.xs[pb];
+    const Real dy = m.ys[pa] - m.ys[pb];
+    const Real dz = m.zs[pa] - m.zs[pb];
+    Real ca, cb;
+    bool degenerate;
+    if constexpr (sizeof(Real) == 8) {
+        // exact build: ts_lane_edges, _kernels.pyx:121-136
+        const Real dist = sqrt(dx * dx + dy * dy + dz * dz);
+        const Real mm = (Real)0.5 + copysign((Real)0.5, dist - (Real)1e-12);
+        const Real scale = mm * ks * (dist - rl) / (dist * wsum + ((Real)1 - mm));
+        ca = -wa * scale;
+        cb = wb * scale;
+        degenerate = mm == (Real)0;
+    } else {
+        // fp32 build: c = k (1 - rest / dist)
+        const float d2 = __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, dx * dx));
+        degenerate = !(d2 >= 1e-24f);                    // dist < 1e-12 (coincident guard)
+        const float f = degenerate ? 0.0f : __fmaf_rn(-rl, rsqrtf(d2), 1.0f);
+        ca = -wa * f;
+        cb = wb * f;
+    }
+    m.slx[sa] = ca * dx; m.sly[sa] = ca * dy; m.slz[sa] = ca * dz;
+    m.slx[sb] = cb * dx; m.sly[sb] = cb * dy; m.slz[sb] = cb * dz;   // pinned endpoints -> trash slots
+    if (degenerate) {
+        if (pa < vfp) atomicAdd(&m.deg[pa], 1);
+        if (pb < vfp) atomicAdd(&m.deg[pb], 1);
+    }
+}
+
 template <typename Real>
 __device__ __forceinline__ void p1_edges(const TsDevProg &P, const Smem<Real> &m, int begin, int count,
                                          Real ks) {
+    const int vfp = P.Vf_pad;
+    const int stride = blockDim.x;
+    const int t = threadIdx.x;
+    if (P.compact) {
+        // 16-bit stream: {pa|pb, sa|sb, rest}; weights from the pinned flags (uniform free mass)
+        const uint4 *it = P.edge_c + begin;
+        const Real w = (Real)P.w_free;
+        uint4 nq = make_uint4(0, 0, 0, 0);
+        if (t < count) nq = __ldg(it + t);
+        for (int i = t; i < count; i += stride) {
+            const uint4 q = nq;
+            nq = __ldg(it + min(i + stride, count - 1));   // prefetch, branch-free
+            const int pa = q.x & 0xffff, pb = q.x >> 16, sa = q.y & 0xffff, sb = q.y >> 16;
+            Real rl, wa, wb, wsum;
+            if constexpr (sizeof(Real) == 8) {
+                rl = __hiloint2double((int)q.w, (int)q.z);
+                wa = pa < vfp ? w : (Real)0;
+                wb = pb < vfp ? w : (Real)0;
+                wsum = wa + wb;
+            } else {
+                rl = __uint_as_float(q.z);
+                const bool both = (pa < vfp) && (pb < vfp);
+                wa = wb = both ? (Real)0.5 * ks : ks;       // ks w / (w + w) or ks w / w
+                wsum = 0;
+            }
+            edge_item<Real>(m, pa, pb, sa, sb, rl, wa, wb, wsum, ks, vfp);
+        }
+        return;
+    }
     using V4 = typename R4<Real>::T;
     const int4 *idx = P.edge_idx + begin;
     const V4 *par = reinterpret_cast<const V4 *>(P.edge_par) + begin;
-    const int vfp = P.Vf_pad;
-    const int stride = blockDim.x;
     // topology of the next item is fetched one iteration ahead (hides the L2 latency)
     int4 nid = make_int4(0, 0, 0, 0);
     V4 npr{};
-    if ((int)threadIdx.x < count) { nid = __ldg(idx + threadIdx.x); npr = par[threadIdx.x]; }
-    for (int i = threadIdx.x; i < count; i += stride) {
-        const int4 id = nid;     // {pos a, pos b, slot a, slot b}; pinned endpoints -> trash slots
-        const V4 pr = npr;
+    if (t < count) { nid = __ldg(idx + t); npr = par[t]; }
+    for (int i = t; i < count; i += stride) {
+        const int4 id = nid;     // {pos a, pos b, slot a, slot b}
+        const V4 pr = npr;       // fp64 {rest, wa, wb, wa + wb}; fp32 {rest, ks wa/wsum, ks wb/wsum, 0}
         {   // unconditional (clamped) prefetch: no branch in the loop body
             const int j = min(i + stride, count - 1);
             nid = __ldg(idx + j); npr = par[j];
         }
-        const Real dx = m.xs[id.x] - m.xs[id.y];
-        const Real dy = m.ys[id.x] - m.ys[id.y];
-        const Real dz = m.zs[id.x] - m.zs[id.y];
-        Real ca, cb;
-        bool degenerate;
-        if constexpr (sizeof(Real) == 8) {
-            // exact build: ts_lane_edges, _kernels.pyx:121-136 (pr = {rest, wa, wb, wa + wb})
-            const Real dist = sqrt(dx * dx + dy * dy + dz * dz);
-            const Real mm = (Real)0.5 + copysign((Real)0.5, dist - (Real)1e-12);
-            const Real scale = mm * ks * (dist - pr.x) / (dist * pr.w + ((Real)1 - mm));
-            ca = -pr.y * scale;
-            cb = pr.z * scale;
-            degenerate = mm == (Real)0;
-        } else {
-            // fp32 build: pr = {rest, ks wa / wsum, ks wb / wsum, 0};  c = k (1 - rest / dist)
-            const float d2 = __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, dx * dx));
-            degenerate = !(d2 >= 1e-24f);                    // dist < 1e-12 (coincident guard)
-            const float f = degenerate ? 0.0f : __fmaf_rn(-pr.x, rsqrtf(d2), 1.0f);
-            ca = -pr.y * f;
-            cb = pr.z * f;
-        }
-        m.slx[id.z] = ca * dx; m.sly[id.z] = ca * dy; m.slz[id.z] = ca * dz;
-        m.slx[id.w] = cb * dx; m.sly[id.w] = cb * dy; m.slz[id.w] = cb * dz;
-        if (degenerate) {
-            if (id.x < vfp) atomicAdd(&m.deg[id.x], 1);
-            if (id.y < vfp) atomicAdd(&m.deg[id.y], 1);
-        }
+        edge_item<Real>(m, id.x, id.y, id.z, id.w, pr.x, pr.y, pr.z, pr.w, ks, vfp);
     }
 }
 
@@ -382,16 +418,35 @@ __device__ __forceinline__ void store_slot(const Smem<Real> &m, int s, Real c, R
 }
 
 template <typename Real>
+__device__ __forceinline__ void tet_item(const Smem<Real> &m, int4 id, int4 sl, Real rvi, Real kv, int vfp);
+
+template <typename Real>
 __device__ __forceinline__ void p1_tets(const TsDevProg &P, const Smem<Real> &m, int begin, int count, Real kv) {
-    const int4 *idx = P.tet_idx + begin;
-    const int4 *slot = P.tet_slot + begin;
     const Real *rv = reinterpret_cast<const Real *>(P.tet_rv) + begin;
     const int vfp = P.Vf_pad;
     const int stride = blockDim.x;
+    const int t = threadIdx.x;
+    if (P.compact) {
+        const uint4 *it = P.tet_c + begin;
+        uint4 nq = make_uint4(0, 0, 0, 0);
+        Real nrv = 0;
+        if (t < count) { nq = __ldg(it + t); nrv = rv[t]; }
+        for (int i = t; i < count; i += stride) {
+            const uint4 q = nq;
+            const Real rvi = nrv;
+            { const int j = min(i + stride, count - 1); nq = __ldg(it + j); nrv = rv[j]; }
+            const int4 id = make_int4(q.x & 0xffff, q.x >> 16, q.y & 0xffff, q.y >> 16);
+            const int4 sl = make_int4(q.z & 0xffff, q.z >> 16, q.w & 0xffff, q.w >> 16);
+            tet_item<Real>(m, id, sl, rvi, kv, vfp);
+        }
+        return;
+    }
+    const int4 *idx = P.tet_idx + begin;
+    const int4 *slot = P.tet_slot + begin;
     int4 nid = make_int4(0, 0, 0, 0), nsl = make_int4(0, 0, 0, 0);
     Real nrv = 0;
-    if ((int)threadIdx.x < count) { nid = __ldg(idx + threadIdx.x); nsl = __ldg(slot + threadIdx.x); nrv = rv[threadIdx.x]; }
-    for (int i = threadIdx.x; i < count; i += stride) {
+    if (t < count) { nid = __ldg(idx + t); nsl = __ldg(slot + t); nrv = rv[t]; }
+    for (int i = t; i < count; i += stride) {
         const int4 id = nid;
         const int4 sl = nsl;
         const Real rvi = nrv;
@@ -399,6 +454,14 @@ __device__ __forceinline__ void p1_tets(const TsDevProg &P, const Smem<Real> &m,
             const int j = min(i + stride, count - 1);
             nid = __ldg(idx + j); nsl = __ldg(slot + j); nrv = rv[j];
         }
+        tet_item<Real>(m, id, sl, rvi, kv, vfp);
+    }
+}
+
+// One volume constraint: correction vectors for its four vertices into their slots.
+template <typename Real>
+__device__ __forceinline__ void tet_item(const Smem<Real> &m, int4 id, int4 sl, Real rvi, Real kv, int vfp) {
+    {
         const Real ax = m.xs[id.x], ay = m.ys[id.x], az = m.zs[id.x];
         const Real bax = m.xs[id.y] - ax, bay = m.ys[id.y] - ay, baz = m.zs[id.y] - az;
         const Real cax = m.xs[id.z] - ax, cay = m.ys[id.z] - ay, caz = m.zs[id.z] - az;

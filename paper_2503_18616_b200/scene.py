@@ -151,12 +151,13 @@ class SceneArrays:
         return d
 
 
-def layout_opts(precision="fp32", block_threads=0, max_chunk_slots=0, schedule_banks=True):
+def layout_opts(precision="fp32", block_threads=0, max_chunk_slots=0, schedule_banks=True, compact=True):
     o = N.LayoutOpts()
     o.precision = N.TS_F64 if precision in ("fp64", "float64", "f64", N.TS_F64) else N.TS_F32
     o.block_threads = int(block_threads)
     o.max_chunk_slots = int(max_chunk_slots)
     o.schedule_banks = 1 if schedule_banks else -1
+    o.compact = 1 if compact else -1
     return o
 
 

@@ -15,10 +15,10 @@ import numpy as np
 
 SECTIONS = ["CHUNK", "EDGE_IDX", "EDGE_PAR", "TET_IDX", "TET_SLOT", "TET_RV", "ATT_IDX", "ATT_SLOT",
             "ATT_PAR", "ATT_ANCHOR", "REGION", "VALENCE", "STATIC_CNT", "S2O", "O2S", "W", "FACES",
-            "FACES_ORIG", "REST", "GSPLIT"]
+            "FACES_ORIG", "REST", "GSPLIT", "EDGE_C", "TET_C"]
 HDR_FIELDS = ["magic", "version", "real_bytes", "n_sections", "V", "Vf", "Vf_pad", "Vstore", "F", "B",
               "VPT", "G", "n_chunks", "grasp_chunk", "slot_capacity", "n_att", "n_edge_items",
-              "n_tet_items", "n_att_items", "bank_conflicts", "n_slots_total", "pad0", "pad1", "pad2"]
+              "n_tet_items", "n_att_items", "bank_conflicts", "n_slots_total", "compact", "pad1", "pad2"]
 
 
 class Program:
@@ -27,8 +27,13 @@ class Program:
         ints = b[:96].view(np.int32)
         self.h = dict(zip(HDR_FIELDS, (int(v) for v in ints)))
         assert self.h["magic"] == 0x54534231
-        self.off = b[96:96 + 8 * len(SECTIONS)].view(np.int64)
+        self.w_free = float(b[96:104].view(np.float64)[0])
+        self.off = b[104:104 + 8 * len(SECTIONS)].view(np.int64)
         self.b = b
+        if self.h["compact"]:
+            nE, nT = self.h["n_edge_items"], self.h["n_tet_items"]
+            self.edge_c = self.sec("EDGE_C", np.uint32, 4 * nE).reshape(nE, 4)
+            self.tet_c = self.sec("TET_C", np.uint32, 4 * nT).reshape(nT, 4)
         rt = np.float64 if self.h["real_bytes"] == 8 else np.float32
         H = self.h
         nE, nT, nA = H["n_edge_items"], H["n_tet_items"], H["n_att_items"]

@@ -124,6 +124,43 @@ def test_schedule_is_permutation_and_reduces_conflicts(reach_scene):
     assert i1["bank_conflicts_p1"] < i0["bank_conflicts_p1"]
 
 
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+def test_compact_streams_encode_the_full_program(reach_scene, precision):
+    """The 16-bit item streams the kernel reads for uniform-mass scenes carry exactly the full program:
+    same positions and slots, same rest lengths, and edge weights recoverable from the pinned flags."""
+    mesh, rest, cfg = reach_scene
+    blob, info = S.compile_program(_arrays(reach_scene), precision=precision)
+    p = PI.Program(blob)
+    assert info["compact"] == 1 and p.h["compact"] == 1
+    lo, hi = p.edge_c[:, 0] & 0xFFFF, p.edge_c[:, 0] >> 16
+    assert np.array_equal(lo, p.edge_idx[:, 0]) and np.array_equal(hi, p.edge_idx[:, 1])
+    assert np.array_equal(p.edge_c[:, 1] & 0xFFFF, p.edge_idx[:, 2])
+    assert np.array_equal(p.edge_c[:, 1] >> 16, p.edge_idx[:, 3])
+    if precision == "fp64":
+        rl = p.edge_c[:, 2:4].copy().view(np.float64)[:, 0]
+        vfp = p.h["Vf_pad"]
+        wa = np.where(p.edge_idx[:, 0] < vfp, p.w_free, 0.0)
+        wb = np.where(p.edge_idx[:, 1] < vfp, p.w_free, 0.0)
+        assert np.array_equal(wa, p.edge_par[:, 1]) and np.array_equal(wb, p.edge_par[:, 2])
+        assert np.array_equal(wa + wb, p.edge_par[:, 3])
+    else:
+        rl = p.edge_c[:, 2].copy().view(np.float32).astype(np.float64)
+    assert np.array_equal(rl, p.edge_par[:, 0])
+    for k in range(4):
+        assert np.array_equal((p.tet_c[:, k // 2] >> (16 * (k % 2))) & 0xFFFF, p.tet_idx[:, k])
+        assert np.array_equal((p.tet_c[:, 2 + k // 2] >> (16 * (k % 2))) & 0xFFFF, p.tet_slot[:, k])
+
+
+def test_nonuniform_mass_uses_full_streams(small_scene):
+    mesh, rest, cfg = small_scene
+    arr = _arrays(small_scene)
+    arr.inverse_mass = arr.inverse_mass.copy()
+    free = np.flatnonzero(arr.inverse_mass > 0)
+    arr.inverse_mass[free[0]] *= 2.0
+    _, info = S.compile_program(arr, precision="fp32")
+    assert info["compact"] == 0
+
+
 def test_compile_errors():
     mesh, rest, cfg = build_slab_scene()
     arr = _arrays((mesh, rest, cfg))

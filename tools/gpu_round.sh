@@ -1,5 +1,5 @@
 set -x
 python -m pytest tests -m gpu -q -x 2>&1 | tail -15 > gpurun_out/pytest_gpu.log
-TS_CHUNKS=0 TS_BLOCKS=0,448,512 python tools/tune.py > gpurun_out/tune.log 2>&1
+TS_CHUNKS=0 TS_BLOCKS=0,448 python tools/tune.py > gpurun_out/tune.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:step_kernel -s 3 -c 1 -o gpurun_out/prof_step_f32 python tools/profile_step.py > gpurun_out/ncu_full.log 2>&1
 tail -4 gpurun_out/pytest_gpu.log; cat gpurun_out/tune.log
