@@ -237,7 +237,10 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
     for (int i = 0; i < Vf; ++i) { s2o[i] = free_v[i]; o2s[free_v[i]] = i; }
     for (size_t i = 0; i < pinned_v.size(); ++i) { s2o[Vf_pad + i] = pinned_v[i]; o2s[pinned_v[i]] = Vf_pad + (int)i; }
 
-    int B = o.block_threads > 0 ? o.block_threads : std::min(512, std::max(64, Vf_pad));
+    // fp32: one thread per free vertex (3 CTAs/SM fit); fp64 runs 1 CTA/SM (shared memory), so it
+    // takes 1.5x the threads to widen phase 1 (measured on B200: 3.81 vs 4.30 ms at 4096 envs)
+    int B = o.block_threads > 0 ? o.block_threads
+                                : std::min(512, std::max(64, R == 8 ? roundup(Vf_pad * 3 / 2, 32) : Vf_pad));
     if (B % 32 != 0 || B < 32 || B > 512) { err = "block_threads must be a multiple of 32 in [32, 512]"; return TS_ERR_INVALID; }
     const int VPT = std::max(1, (Vf_pad + B - 1) / B);
     if (VPT > 8) { err = "mesh too large for one CTA per environment (more than 8 vertices per thread)"; return TS_ERR_UNSUPPORTED; }
