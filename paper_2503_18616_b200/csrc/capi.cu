@@ -62,7 +62,10 @@ int32_t ts_compile_program(const ts_scene_desc *desc, const ts_layout_opts *opts
     if (rc != TS_OK) return fail(rc, err);
     if (info) *info = inf;
     if (buf) {
-        if (*bytes < (int64_t)blob.size()) return fail(TS_ERR_INVALID, "buffer too small");
+        if (*bytes < (int64_t)blob.size()) {
+            *bytes = (int64_t)blob.size();   // report the size needed
+            return fail(TS_ERR_INVALID, "buffer too small");
+        }
         std::memcpy(buf, blob.data(), blob.size());
     }
     *bytes = (int64_t)blob.size();

@@ -19,6 +19,8 @@
 //    depend on this order, only shared-memory wavefronts do.
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <string>
@@ -37,6 +39,9 @@ struct Item {
     int nroles;
     int pos[4];        // storage positions of the roles
     int slot[4];       // slot id inside the chunk (-1 pinned endpoint)
+    int vid[4];        // original vertex ids of the roles
+    int chunk;
+    int sign = 1;      // fp32 tets: -1 after an odd corner permutation (signed volume flips)
 };
 
 inline int roundup(int x, int m) { return (x + m - 1) / m * m; }
@@ -174,6 +179,328 @@ std::vector<Item> schedule_items(std::vector<Item> items, int bank_mod, int batc
     return out;
 }
 
+// Extra shared-memory wavefronts of a scheduled item range (per role, per
+// sub-batch of `bank_mod` lanes: max items on one bank - 1).
+int batch_conflicts(const std::vector<Item> &items, int begin, int count, int bank_mod) {
+    int extra = 0;
+    for (int b0 = 0; b0 < count; b0 += bank_mod) {
+        for (int r = 0; r < 4; ++r) {
+            int cnt[32] = {0}, worst = 0;
+            for (int k = b0; k < std::min(count, b0 + bank_mod); ++k) {
+                const Item &it = items[begin + k];
+                if (r < it.nroles) worst = std::max(worst, ++cnt[it.pos[r] % bank_mod]);
+            }
+            if (worst > 1) extra += worst - 1;
+        }
+    }
+    return extra;
+}
+
+struct ListRef { std::vector<Item> *items; int begin, count; };
+
+// Joint refinement of the phase-1 bank pattern by simulated annealing over
+// three kinds of result-preserving moves:
+//   * swap two items of one (chunk, kind) list          -> which lanes run together;
+//   * swap the storage positions of two vertices of one warp group (or of the
+//     pinned pool)                                        -> which bank a vertex lives in;
+//     (a warp keeps the same vertices, so phase-2 balance and chunk padding are unchanged)
+//   * swap an edge's endpoints (bit-exact in both builds: every product only
+//     changes sign), or apply an orientation-preserving permutation to a tet's
+//     corners (fp32 build only: it changes the fp64 expression trees).
+// Deterministic (fixed-seed xorshift).  Slots are assigned afterwards from the
+// final positions, so the per-vertex summation order is untouched.
+void bank_refine(const std::vector<ListRef> &lists, std::vector<int> &o2s, std::vector<int> &s2o, int Vf,
+                 int Vf_pad, int bank_mod, bool permute_tets) {
+    struct Ref { int list, idx; };
+    std::vector<Ref> items;                 // global item id -> (list, index)
+    std::vector<int> sb_of, list_sb0;
+    int nsb = 0;
+    for (int l = 0; l < (int)lists.size(); ++l) {
+        list_sb0.push_back(nsb);
+        for (int i = 0; i < lists[l].count; ++i) { items.push_back({l, i}); sb_of.push_back(nsb + i / bank_mod); }
+        nsb += (lists[l].count + bank_mod - 1) / bank_mod;
+    }
+    const int n = (int)items.size();
+    if (n == 0) return;
+    auto item = [&](int g) -> Item & { const Ref &r = items[g]; return (*lists[r.list].items)[lists[r.list].begin + r.idx]; };
+    const int V = (int)o2s.size();
+    std::vector<std::vector<std::pair<int, int>>> inc(V);
+    for (int g = 0; g < n; ++g)
+        for (int r = 0; r < item(g).nroles; ++r) inc[item(g).vid[r]].push_back({g, r});
+    std::vector<int> cnt((size_t)nsb * 4 * bank_mod, 0), hist((size_t)nsb * 4 * 33, 0), mx((size_t)nsb * 4, 0);
+    for (int q = 0; q < nsb * 4; ++q) hist[(size_t)q * 33] = bank_mod;
+    auto add = [&](int sb, int r, int b, int delta) {
+        const int q = sb * 4 + r;
+        int &c = cnt[(size_t)q * bank_mod + b];
+        hist[(size_t)q * 33 + c]--;
+        c += delta;
+        hist[(size_t)q * 33 + c]++;
+        if (c > mx[q]) mx[q] = c;
+        while (mx[q] > 0 && hist[(size_t)q * 33 + mx[q]] == 0) mx[q]--;
+    };
+    auto bank = [&](int v) { return o2s[v] % bank_mod; };
+    for (int g = 0; g < n; ++g)
+        for (int r = 0; r < item(g).nroles; ++r) add(sb_of[g], r, bank(item(g).vid[r]), +1);
+    // objective: 4 x (extra wavefronts = max bank load - 1) + (items sharing a bank): the
+    // second term is a smooth surrogate that lets the search cross the plateaus of the first
+    auto sb_cost = [&](int sb) {
+        int c = 0;
+        for (int r = 0; r < 4; ++r) {
+            const int q = sb * 4 + r;
+            const int nz = bank_mod - hist[(size_t)q * 33];
+            int items_in = 0;
+            for (int k = 1; k <= mx[q]; ++k) items_in += k * hist[(size_t)q * 33 + k];
+            c += 4 * std::max(0, mx[q] - 1) + (items_in - nz);
+        }
+        return c;
+    };
+    long total = 0;
+    for (int sb = 0; sb < nsb; ++sb) total += sb_cost(sb);
+    uint64_t rng = 0x2545F4914F6CDD1Dull;
+    auto next = [&]() { rng ^= rng << 13; rng ^= rng >> 7; rng ^= rng << 17; return rng; };
+    auto unif = [&]() { return (double)(next() >> 11) * (1.0 / 9007199254740992.0); };
+    const int n_pinned = (int)std::count_if(s2o.begin() + Vf_pad, s2o.end(), [](int v) { return v >= 0; });
+    std::vector<int> touched;
+    auto collect = [&](int sb) { if (std::find(touched.begin(), touched.end(), sb) == touched.end()) touched.push_back(sb); };
+    long iters = std::min<long>(600000L, 150L * n);
+    if (const char *env = std::getenv("TS_REFINE_ITERS")) iters = std::atol(env);
+    const double T0 = 1.5, T1 = 0.05;
+    // best state seen (the schedule lists, the vertex positions)
+    long best = total;
+    std::vector<std::vector<Item>> best_lists;
+    std::vector<int> best_o2s = o2s, best_s2o = s2o;
+    auto snapshot = [&]() {
+        best_lists.clear();
+        for (const ListRef &l : lists)
+            best_lists.emplace_back(l.items->begin() + l.begin, l.items->begin() + l.begin + l.count);
+        best_o2s = o2s; best_s2o = s2o;
+    };
+    snapshot();
+    long last_snap = 0;
+    for (long it = 0; it < iters && total > 0; ++it) {
+        if (total < best && it - last_snap > 2000) { best = total; snapshot(); last_snap = it; }
+        const double T = T0 * std::pow(T1 / T0, (double)it / iters);
+        touched.clear();
+        const int kind = (int)(next() % 10);
+        // --- propose ---------------------------------------------------------
+        int g1 = -1, g2 = -1, u = -1, v = -1, perm = -1;
+        if (kind < 5) {                                   // item swap inside a list
+            g1 = (int)(next() % n);
+            const Ref r1 = items[g1];
+            const int cnt_l = lists[r1.list].count;
+            const int j = (int)(next() % cnt_l);
+            g2 = g1 - r1.idx + j;
+            if (sb_of[g1] == sb_of[g2]) continue;
+            collect(sb_of[g1]); collect(sb_of[g2]);
+        } else if (kind < 8) {                            // vertex swap inside a warp group / the pinned pool
+            u = item((int)(next() % n)).vid[next() % 2];
+            const int pu = o2s[u];
+            int pv;
+            if (pu < Vf_pad) {
+                const int g = pu / 32;
+                const int hi = std::min(Vf, 32 * g + 32);
+                pv = 32 * g + (int)(next() % (hi - 32 * g));
+            } else {
+                if (n_pinned < 2) continue;
+                pv = Vf_pad + (int)(next() % n_pinned);
+            }
+            v = s2o[pv];
+            if (v < 0 || v == u || bank(u) == bank(v)) continue;
+            for (auto &e : inc[u]) collect(sb_of[e.first]);
+            for (auto &e : inc[v]) collect(sb_of[e.first]);
+        } else {                                          // role permutation of one item
+            g1 = (int)(next() % n);
+            Item &x = item(g1);
+            if (x.kind == TS_CHUNK_EDGE) perm = 0;
+            else if (x.kind == TS_CHUNK_TET && permute_tets) perm = 1 + (int)(next() % 6);
+            else continue;
+            collect(sb_of[g1]);
+        }
+        long before = 0;
+        for (int sb : touched) before += sb_cost(sb);
+        // --- apply (as a reversible function) -----------------------------------
+        auto remove_item = [&](int g) { Item &x = item(g); for (int r = 0; r < x.nroles; ++r) add(sb_of[g], r, bank(x.vid[r]), -1); };
+        auto insert_item = [&](int g) { Item &x = item(g); for (int r = 0; r < x.nroles; ++r) add(sb_of[g], r, bank(x.vid[r]), +1); };
+        auto permute = [&](Item &x, int p) {
+            // edges: (a b) -> (b a); tets: the three double transpositions (orientation kept)
+            if (p == 0) std::swap(x.vid[0], x.vid[1]);
+            else {
+                // tets (fp32 build): one transposition of two corners; the signed volume flips, so
+                // the constraint is rewritten with -V0 (C' = -C, grad C' = -grad C: same correction)
+                static const int tr[6][2] = {{0, 1}, {0, 2}, {0, 3}, {1, 2}, {1, 3}, {2, 3}};
+                std::swap(x.vid[tr[p - 1][0]], x.vid[tr[p - 1][1]]);
+                x.sign = -x.sign;
+            }
+        };
+        auto swap_vertices = [&]() {
+            for (auto &e : inc[u]) add(sb_of[e.first], e.second, bank(u), -1);
+            for (auto &e : inc[v]) add(sb_of[e.first], e.second, bank(v), -1);
+            std::swap(o2s[u], o2s[v]);
+            s2o[o2s[u]] = u; s2o[o2s[v]] = v;
+            for (auto &e : inc[u]) add(sb_of[e.first], e.second, bank(u), +1);
+            for (auto &e : inc[v]) add(sb_of[e.first], e.second, bank(v), +1);
+        };
+        auto swap_items = [&]() {
+            remove_item(g1); remove_item(g2);
+            std::swap(item(g1), item(g2));
+            insert_item(g1); insert_item(g2);
+        };
+        auto fix_inc_after_swap = [&]() {
+            // after swapping item contents of g1 and g2, incidences (g1, r) <-> (g2, r)
+            std::vector<int> vs;
+            for (int g : {g1, g2}) for (int r = 0; r < item(g).nroles; ++r) vs.push_back(item(g).vid[r]);
+            std::sort(vs.begin(), vs.end());
+            vs.erase(std::unique(vs.begin(), vs.end()), vs.end());
+            for (int w : vs)
+                for (auto &e : inc[w]) {
+                    if (e.first == g1) e.first = g2;
+                    else if (e.first == g2) e.first = g1;
+                }
+        };
+        auto permute_item = [&](int p) {
+            Item &x = item(g1);
+            remove_item(g1);
+            // incidences carry the role index
+            for (int r = 0; r < x.nroles; ++r)
+                for (auto &e : inc[x.vid[r]]) if (e.first == g1 && e.second == r) e.second = -1 - r;
+            permute(x, p);
+            for (int r = 0; r < x.nroles; ++r)
+                for (auto &e : inc[x.vid[r]]) if (e.first == g1 && e.second < 0) { e.second = r; break; }
+            insert_item(g1);
+        };
+        if (g2 >= 0) { swap_items(); fix_inc_after_swap(); }
+        else if (u >= 0) swap_vertices();
+        else permute_item(perm);
+        long after = 0;
+        for (int sb : touched) after += sb_cost(sb);
+        const long delta = after - before;
+        if (delta <= 0 || unif() < std::exp(-(double)delta / T)) {
+            total += delta;
+            continue;
+        }
+        // --- revert ----------------------------------------------------------------
+        if (g2 >= 0) { swap_items(); fix_inc_after_swap(); }
+        else if (u >= 0) swap_vertices();
+        else {
+            // inverse permutations: every move above is an involution
+            permute_item(perm);
+        }
+    }
+    if (std::getenv("TS_DEBUG_REFINE")) {
+        long check = 0;
+        for (int sb = 0; sb < nsb; ++sb) check += sb_cost(sb);
+        std::fprintf(stderr, "bank_refine: tracked %ld recomputed %ld best %ld\n", total, check, best);
+    }
+    if (total > best) {   // restore the best state seen
+        for (size_t l = 0; l < lists.size(); ++l)
+            std::copy(best_lists[l].begin(), best_lists[l].end(), lists[l].items->begin() + lists[l].begin);
+        o2s = best_o2s; s2o = best_s2o;
+    }
+}
+
+// Conflict-free schedule of one edge list by bipartite edge colouring.
+// Every edge is an arc between the bank of its role-a vertex and the bank of
+// its role-b vertex; a warp batch (a half-warp for 64-bit data) is conflict-free
+// iff its arcs form a matching of the bank x bank bipartite graph.  Endpoints are
+// oriented to balance every bank's in/out degree (swapping roles is bit-exact),
+// then Koenig's theorem gives a colouring with max-degree colours; each colour
+// becomes one batch, padded with dummy edges between pinned vertices (they
+// write only trash slots and touch no counter).  Returns false (list untouched)
+// when there are no pinned vertices to build dummies from.
+bool edge_coloring_schedule(std::vector<Item> &list, const std::vector<int> &o2s, const std::vector<int> &s2o,
+                            int Vf_pad, int bank_mod) {
+    const int n = (int)list.size();
+    if (n < bank_mod) return false;
+    std::vector<int> pinned_by_bank[32];
+    for (int p = Vf_pad; p < (int)s2o.size(); ++p)
+        if (s2o[p] >= 0) pinned_by_bank[p % bank_mod].push_back(s2o[p]);
+    for (int b = 0; b < bank_mod; ++b)
+        if (pinned_by_bank[b].size() < 2) return false;
+    auto bank = [&](int v) { return o2s[v] % bank_mod; };
+    // orientation: greedy, then improving flips
+    std::vector<int> outd(bank_mod, 0), ind(bank_mod, 0);
+    for (Item &e : list) {
+        const int a = bank(e.vid[0]), b = bank(e.vid[1]);
+        if (std::max(outd[b] + 1, ind[a] + 1) < std::max(outd[a] + 1, ind[b] + 1)) std::swap(e.vid[0], e.vid[1]);
+        outd[bank(e.vid[0])]++; ind[bank(e.vid[1])]++;
+    }
+    for (int pass = 0; pass < 20; ++pass) {
+        bool changed = false;
+        for (Item &e : list) {
+            const int a = bank(e.vid[0]), b = bank(e.vid[1]);
+            if (a == b) continue;
+            const int cur = std::max(std::max(outd[a], ind[b]), std::max(outd[b], ind[a]));
+            const int alt = std::max(std::max(outd[a] - 1, ind[b] - 1), std::max(outd[b] + 1, ind[a] + 1));
+            if (alt < cur) {
+                outd[a]--; ind[b]--; outd[b]++; ind[a]++;
+                std::swap(e.vid[0], e.vid[1]);
+                changed = true;
+            }
+        }
+        if (!changed) break;
+    }
+    int delta = 0;
+    for (int b = 0; b < bank_mod; ++b) delta = std::max(delta, std::max(outd[b], ind[b]));
+    const int C = std::max(delta, (n + bank_mod - 1) / bank_mod);
+    // Koenig colouring: L[x][c] / R[y][c] = edge index using colour c at left bank x / right bank y
+    std::vector<int> L((size_t)bank_mod * C, -1), R((size_t)bank_mod * C, -1), col(n, -1);
+    auto Lc = [&](int x, int c) -> int & { return L[(size_t)x * C + c]; };
+    auto Rc = [&](int y, int c) -> int & { return R[(size_t)y * C + c]; };
+    for (int e = 0; e < n; ++e) {
+        const int x = bank(list[e].vid[0]), y = bank(list[e].vid[1]);
+        int a = 0; while (Lc(x, a) >= 0) ++a;
+        int b = 0; while (Rc(y, b) >= 0) ++b;
+        if (Rc(y, a) >= 0) {
+            // flip the a/b alternating path that starts at right node y with colour a
+            std::vector<int> path;
+            int node = y; bool right = true; int c = a;
+            while (true) {
+                const int f = right ? Rc(node, c) : Lc(node, c);
+                if (f < 0) break;
+                path.push_back(f);
+                node = right ? bank(list[f].vid[0]) : bank(list[f].vid[1]);
+                right = !right;
+                c = (c == a) ? b : a;
+            }
+            for (int f : path) {   // clear
+                Lc(bank(list[f].vid[0]), col[f]) = -1; Rc(bank(list[f].vid[1]), col[f]) = -1;
+            }
+            for (int f : path) {   // swap a <-> b
+                col[f] = (col[f] == a) ? b : a;
+                Lc(bank(list[f].vid[0]), col[f]) = f; Rc(bank(list[f].vid[1]), col[f]) = f;
+            }
+        }
+        col[e] = a;
+        Lc(x, a) = e; Rc(y, a) = e;
+    }
+    // batches = colour classes, each padded to bank_mod lanes with dummies on unused banks
+    std::vector<Item> out;
+    out.reserve((size_t)C * bank_mod);
+    for (int c = 0; c < C; ++c) {
+        std::vector<int> members;
+        std::vector<char> used_a(bank_mod, 0), used_b(bank_mod, 0);
+        for (int x = 0; x < bank_mod; ++x) {
+            const int e = Lc(x, c);
+            if (e >= 0) { members.push_back(e); used_a[x] = 1; used_b[bank(list[e].vid[1])] = 1; }
+        }
+        if (members.empty()) continue;
+        for (int e : members) out.push_back(list[e]);
+        int fa = 0, fb = 0;
+        for (int k = (int)members.size(); k < bank_mod; ++k) {
+            while (used_a[fa]) ++fa;
+            while (used_b[fb]) ++fb;
+            used_a[fa] = used_b[fb] = 1;
+            Item d{};
+            d.kind = TS_CHUNK_EDGE; d.index = -1; d.nroles = 2; d.chunk = list[0].chunk;
+            d.vid[0] = pinned_by_bank[fa][0];
+            d.vid[1] = pinned_by_bank[fb][fa == fb ? 1 : 0];
+            out.push_back(d);
+        }
+    }
+    list.swap(out);
+    return true;
+}
+
 template <typename Real>
 struct Real4T { Real x, y, z, w; };
 
@@ -251,19 +578,23 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
     std::vector<Item> kinds[3];
     for (int e = 0; e < E; ++e) if (edge_live[e]) {
         Item it{}; it.kind = TS_CHUNK_EDGE; it.index = e; it.nroles = 2;
-        it.pos[0] = P(d.edges[2 * e]); it.pos[1] = P(d.edges[2 * e + 1]);
+        it.vid[0] = d.edges[2 * e]; it.vid[1] = d.edges[2 * e + 1];
+        it.pos[0] = P(it.vid[0]); it.pos[1] = P(it.vid[1]);
         kinds[0].push_back(it);
     }
     for (int i = 0; i < A; ++i) if (att_live[i]) {
         Item it{}; it.kind = TS_CHUNK_ATT; it.index = i;
-        it.pos[0] = P(d.att_vertex[i]);
-        if (d.att_is_face[i]) { it.nroles = 4; for (int k = 0; k < 3; ++k) it.pos[1 + k] = P(d.att_faces[3 * i + k]); }
-        else it.nroles = 1;
+        it.vid[0] = d.att_vertex[i];
+        it.pos[0] = P(it.vid[0]);
+        if (d.att_is_face[i]) {
+            it.nroles = 4;
+            for (int k = 0; k < 3; ++k) { it.vid[1 + k] = d.att_faces[3 * i + k]; it.pos[1 + k] = P(it.vid[1 + k]); }
+        } else it.nroles = 1;
         kinds[1].push_back(it);
     }
     for (int t = 0; t < T; ++t) if (tet_live[t]) {
         Item it{}; it.kind = TS_CHUNK_TET; it.index = t; it.nroles = 4;
-        for (int k = 0; k < 4; ++k) it.pos[k] = P(d.tets[4 * t + k]);
+        for (int k = 0; k < 4; ++k) { it.vid[k] = d.tets[4 * t + k]; it.pos[k] = P(it.vid[k]); }
         kinds[2].push_back(it);
     }
 
@@ -325,27 +656,108 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
         }
     }
 
-    // ---- slot assignment (reference per-vertex order) -------------------
+    // ---- phase-1 schedule (per chunk, per kind) ----------------------------
+    const bool sched = o.schedule_banks >= 0;
+    const int bank_mod = (R == 8) ? 16 : 32;
+    std::vector<TsChunk> chunk_rec(n_chunks);
+    std::vector<Item> all_items[3];
+    for (int c = 0; c < n_chunks; ++c) {
+        ChunkBuild &cb = chunks[c];
+        TsChunk &r = chunk_rec[c];
+        std::memset(&r, 0, sizeof(r));
+        int begin[3], count[3];
+        for (int k = 0; k < 3; ++k) {
+            const int kind = k == 0 ? TS_CHUNK_EDGE : (k == 1 ? TS_CHUNK_ATT : TS_CHUNK_TET);
+            std::vector<Item> part;
+            for (const Item &it : cb.items) if (it.kind == kind) { part.push_back(it); part.back().chunk = c; }
+            int conf = 0;
+            std::vector<Item> s = schedule_items(part, bank_mod, 32, sched && kind != TS_CHUNK_ATT, &conf);
+            begin[k] = (int)all_items[k].size();
+            count[k] = (int)s.size();
+            all_items[k].insert(all_items[k].end(), s.begin(), s.end());
+        }
+        r.edge_begin = begin[0]; r.edge_count = count[0];
+        r.att_begin = begin[1]; r.att_count = count[1];
+        r.tet_begin = begin[2]; r.tet_count = count[2];
+        r.region_off = c * G;
+        r.val_off = c * Vf_pad;
+    }
+    // joint refinement: item order, vertex lanes inside each warp, role order (see bank_refine)
+    if (sched && o.schedule_banks != 2) {
+        std::vector<ListRef> lists;
+        for (int c = 0; c < n_chunks; ++c) {
+            if (chunk_rec[c].edge_count) lists.push_back({&all_items[0], chunk_rec[c].edge_begin, chunk_rec[c].edge_count});
+            if (chunk_rec[c].tet_count) lists.push_back({&all_items[2], chunk_rec[c].tet_begin, chunk_rec[c].tet_count});
+        }
+        bank_refine(lists, o2s, s2o, Vf, Vf_pad, bank_mod, /*permute_tets=*/R == 4);
+        // edges: exact conflict-free batches by bipartite edge colouring (with the final positions)
+        std::vector<Item> edges_out;
+        for (int c = 0; c < n_chunks; ++c) {
+            std::vector<Item> part(all_items[0].begin() + chunk_rec[c].edge_begin,
+                                   all_items[0].begin() + chunk_rec[c].edge_begin + chunk_rec[c].edge_count);
+            for (Item &it : part) for (int r = 0; r < it.nroles; ++r) it.pos[r] = o2s[it.vid[r]];
+            std::vector<Item> colored = part;
+            if (edge_coloring_schedule(colored, o2s, s2o, Vf_pad, bank_mod)) {
+                for (Item &it : colored) for (int r = 0; r < it.nroles; ++r) it.pos[r] = o2s[it.vid[r]];
+                if (batch_conflicts(colored, 0, (int)colored.size(), bank_mod) <
+                    batch_conflicts(part, 0, (int)part.size(), bank_mod))
+                    part.swap(colored);
+            }
+            chunk_rec[c].edge_begin = (int)edges_out.size();
+            chunk_rec[c].edge_count = (int)part.size();
+            edges_out.insert(edges_out.end(), part.begin(), part.end());
+        }
+        all_items[0].swap(edges_out);
+    }
+    // final positions of every role
+    for (int k = 0; k < 3; ++k)
+        for (Item &it : all_items[k])
+            for (int r = 0; r < it.nroles; ++r) it.pos[r] = o2s[it.vid[r]];
+    int total_conf = 0;
+    for (int c = 0; c < n_chunks; ++c) {
+        TsChunk &r = chunk_rec[c];
+        r.conflicts = batch_conflicts(all_items[0], r.edge_begin, r.edge_count, bank_mod) +
+                      batch_conflicts(all_items[2], r.tet_begin, r.tet_count, bank_mod);
+        total_conf += r.conflicts;
+    }
+
+    // ---- slot assignment (reference per-vertex order, final positions) --------
+    // Slots are numbered per vertex in the constraint sequence order (edges,
+    // attachments, tets, each by index) whatever the phase-1 schedule is.
     std::vector<int32_t> region((size_t)n_chunks * G), valence((size_t)n_chunks * Vf_pad), static_cnt(Vf_pad, 0);
     std::vector<int32_t> gsplit(Vf_pad, 0);
     int slot_cap = 0, n_slots_total = 0;
     for (int c = 0; c < n_chunks; ++c) {
-        ChunkBuild &cb = chunks[c];
+        TsChunk &rec = chunk_rec[c];
+        // items of this chunk in sequence order
+        std::vector<Item *> seqc;
+        for (int k = 0; k < 3; ++k) {
+            const int b0 = k == 0 ? rec.edge_begin : (k == 1 ? rec.att_begin : rec.tet_begin);
+            const int n0 = k == 0 ? rec.edge_count : (k == 1 ? rec.att_count : rec.tet_count);
+            std::vector<Item *> part;
+            for (int i = 0; i < n0; ++i) part.push_back(&all_items[k][b0 + i]);
+            std::sort(part.begin(), part.end(), [](const Item *x, const Item *y) { return x->index < y->index; });
+            seqc.insert(seqc.end(), part.begin(), part.end());
+        }
+        std::vector<int> kmax(G, 0), val(Vf_pad, 0);
+        for (Item *it : seqc)
+            for (int r = 0; r < it->nroles; ++r)
+                if (it->pos[r] < Vf_pad) { const int p = it->pos[r]; kmax[p / 32] = std::max(kmax[p / 32], ++val[p]); }
         int base = 0;
-        for (int g = 0; g < G; ++g) { region[(size_t)c * G + g] = base; base += 32 * cb.kmax[g]; }
-        cb.padded = base;
+        for (int g = 0; g < G; ++g) { region[(size_t)c * G + g] = base; base += 32 * kmax[g]; }
+        rec.slot_count = base;
         // 32 "trash" slots after the regions: edge / tet endpoints that are pinned store there
         // unconditionally (bank = p % 32, same as their position reads), nobody reads them back
         const int trash = base;
         slot_cap = std::max(slot_cap, base + 32);
         std::vector<int> k_next(Vf_pad, 0);
-        for (Item &it : cb.items) {  // items are in sequence order here
-            for (int r = 0; r < it.nroles; ++r) {
-                int p = it.pos[r];
-                if (p >= Vf_pad) { it.slot[r] = it.kind == TS_CHUNK_ATT ? -1 : trash + (p % 32); continue; }
-                it.slot[r] = region[(size_t)c * G + p / 32] + 32 * k_next[p] + (p % 32);
+        for (Item *it : seqc) {
+            for (int r = 0; r < it->nroles; ++r) {
+                const int p = it->pos[r];
+                if (p >= Vf_pad) { it->slot[r] = it->kind == TS_CHUNK_ATT ? -1 : trash + (p % 32); continue; }
+                it->slot[r] = region[(size_t)c * G + p / 32] + 32 * k_next[p] + (p % 32);
                 k_next[p]++;
-                if (c == grasp_chunk && it.kind == TS_CHUNK_EDGE) gsplit[p] = k_next[p];
+                if (c == grasp_chunk && it->kind == TS_CHUNK_EDGE) gsplit[p] = k_next[p];
             }
         }
         for (int p = 0; p < Vf_pad; ++p) {
@@ -358,37 +770,6 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
     slot_cap = std::max(slot_cap, 7 * F);
     slot_cap = roundup(std::max(slot_cap, 32), 32);
 
-    // ---- phase-1 schedule (per chunk, per kind) ----------------------------
-    const bool sched = o.schedule_banks >= 0;
-    const int bank_mod = (R == 8) ? 16 : 32;
-    int total_conf = 0;
-    std::vector<TsChunk> chunk_rec(n_chunks);
-    std::vector<Item> all_items[3];
-    for (int c = 0; c < n_chunks; ++c) {
-        ChunkBuild &cb = chunks[c];
-        TsChunk &r = chunk_rec[c];
-        std::memset(&r, 0, sizeof(r));
-        int begin[3], count[3];
-        for (int k = 0; k < 3; ++k) {
-            const int kind = k == 0 ? TS_CHUNK_EDGE : (k == 1 ? TS_CHUNK_ATT : TS_CHUNK_TET);
-            std::vector<Item> part;
-            for (const Item &it : cb.items) if (it.kind == kind) part.push_back(it);
-            int conf = 0;
-            std::vector<Item> s = schedule_items(part, bank_mod, 32, sched && kind != TS_CHUNK_ATT, &conf);
-            r.conflicts += conf;
-            begin[k] = (int)all_items[k].size();
-            count[k] = (int)s.size();
-            all_items[k].insert(all_items[k].end(), s.begin(), s.end());
-        }
-        total_conf += r.conflicts;
-        r.edge_begin = begin[0]; r.edge_count = count[0];
-        r.att_begin = begin[1]; r.att_count = count[1];
-        r.tet_begin = begin[2]; r.tet_count = count[2];
-        r.slot_count = cb.padded;
-        r.region_off = c * G;
-        r.val_off = c * Vf_pad;
-    }
-
     // ---- emit --------------------------------------------------------------
     const int nE = (int)all_items[0].size(), nA = (int)all_items[1].size(), nT = (int)all_items[2].size();
     std::vector<int32_t> edge_idx(4 * (size_t)nE), tet_idx(4 * (size_t)nT), tet_slot(4 * (size_t)nT);
@@ -396,9 +777,14 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
     std::vector<double> edge_par(4 * (size_t)nE), tet_rv(nT), att_par(4 * (size_t)nA), att_anc(4 * (size_t)nA);
     for (int i = 0; i < nE; ++i) {
         const Item &it = all_items[0][i];
-        int a = d.edges[2 * it.index], b = d.edges[2 * it.index + 1];
+        const int a = it.vid[0], b = it.vid[1];   // roles may be swapped by the bank refinement
         edge_idx[4 * i + 0] = it.pos[0]; edge_idx[4 * i + 1] = it.pos[1];
         edge_idx[4 * i + 2] = it.slot[0]; edge_idx[4 * i + 3] = it.slot[1];
+        if (it.index < 0) {   // padding lane of a colour class: pinned endpoints, trash slots only
+            edge_par[4 * i + 0] = 0.0; edge_par[4 * i + 1] = 0.0; edge_par[4 * i + 2] = 0.0;
+            edge_par[4 * i + 3] = 1.0;
+            continue;
+        }
         edge_par[4 * i + 0] = d.rest_length[it.index];
         if (R == 8) {   // exact build: the reference's operands
             edge_par[4 * i + 1] = w[a]; edge_par[4 * i + 2] = w[b]; edge_par[4 * i + 3] = w[a] + w[b];
@@ -412,7 +798,7 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
         const Item &it = all_items[2][i];
         for (int k = 0; k < 4; ++k) { tet_idx[4 * i + k] = it.pos[k]; tet_slot[4 * i + k] = it.slot[k]; }
         // fp32 build works with unscaled cross products G = 6 grad: it needs 6 V0
-        tet_rv[i] = R == 8 ? d.rest_volume[it.index] : 6.0 * d.rest_volume[it.index];
+        tet_rv[i] = R == 8 ? d.rest_volume[it.index] : it.sign * 6.0 * d.rest_volume[it.index];
     }
     for (int i = 0; i < nA; ++i) {
         const Item &it = all_items[1][i];

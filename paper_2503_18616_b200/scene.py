@@ -166,14 +166,21 @@ def compile_program(arrays: SceneArrays, **layout):
     lib = N.load()
     d = arrays.desc()
     o = layout_opts(**layout)
-    size = ctypes.c_int64(0)
     info = N.LayoutInfo()
-    N.check(lib.ts_compile_program(ctypes.byref(d), ctypes.byref(o), None, ctypes.byref(size),
-                                   ctypes.byref(info)), "ts_compile_program")
-    buf = np.zeros(size.value, np.uint8)
-    N.check(lib.ts_compile_program(ctypes.byref(d), ctypes.byref(o), N.ptr(buf), ctypes.byref(size),
-                                   ctypes.byref(info)), "ts_compile_program")
-    return buf, info.as_dict()
+    # generous first guess so the (seconds-long, bank-refined) compile runs once
+    guess = (1 << 20) + 512 * (len(arrays.edges) + len(arrays.tets) + len(arrays.att_vertex)) \
+        + 256 * arrays.n_vert + 64 * len(arrays.faces)
+    for _ in range(2):
+        buf = np.zeros(guess, np.uint8)
+        size = ctypes.c_int64(guess)
+        rc = lib.ts_compile_program(ctypes.byref(d), ctypes.byref(o), N.ptr(buf), ctypes.byref(size),
+                                    ctypes.byref(info))
+        if rc == N.TS_OK:
+            return buf[:size.value].copy(), info.as_dict()
+        if size.value <= guess:
+            N.check(rc, "ts_compile_program")
+        guess = int(size.value)
+    N.check(rc, "ts_compile_program")
 
 
 class DeviceScene:

@@ -82,7 +82,12 @@ def test_slot_structure(reach_scene):
     # storage order: free first (sorted by incidence, descending), then pinned
     assert np.all(w[p.s2o[:Vf]] > 0) and np.all(w[p.s2o[H["Vf_pad"]:][p.s2o[H["Vf_pad"]:] >= 0]] == 0)
     assert np.array_equal(np.sort(p.s2o[p.s2o >= 0]), np.arange(mesh.vertex_count))
-    assert np.all(np.diff(p.static_cnt[:Vf]) <= 0)
+    # warps own vertices of similar valence: the groups of 32 are the valence-sorted order
+    # (lanes inside a group may be permuted by the bank refinement)
+    sc = p.static_cnt[:Vf]
+    ref = np.sort(sc)[::-1]
+    for g in range(0, Vf, 32):
+        assert sorted(sc[g:g + 32]) == sorted(ref[g:g + 32])
     expected = 0
     for kind, items, roles in ((0, p.edge_idx, 2), (2, p.tet_idx, 4)):
         slots = (p.edge_idx[:, 2:4] if kind == 0 else p.tet_slot)
@@ -119,9 +124,24 @@ def test_schedule_is_permutation_and_reduces_conflicts(reach_scene):
     b1, i1 = S.compile_program(arr, precision="fp32", schedule_banks=True)
     b0, i0 = S.compile_program(arr, precision="fp32", schedule_banks=False)
     p1, p0 = PI.Program(b1), PI.Program(b0)
-    for a, b in ((p1.edge_idx, p0.edge_idx), (p1.tet_idx, p0.tet_idx)):
-        assert sorted(map(tuple, a.tolist())) == sorted(map(tuple, b.tolist()))
+
+    def constraints(p, idx, roles):
+        vf = p.h["Vf_pad"]
+        out = []
+        for row in idx[:, :roles]:
+            if np.all(row >= vf):          # padding lane (pinned-only dummy edge)
+                continue
+            out.append(tuple(sorted(int(p.s2o[q]) for q in row)))
+        return sorted(out)
+    for idx1, idx0, roles in ((p1.edge_idx, p0.edge_idx, 2), (p1.tet_idx, p0.tet_idx, 4)):
+        assert constraints(p1, idx1, roles) == constraints(p0, idx0, roles)
     assert i1["bank_conflicts_p1"] < i0["bank_conflicts_p1"]
+    # the edge lists are conflict-free by construction (bipartite edge colouring)
+    ex = 0
+    for b in range(0, len(p1.edge_idx), 32):
+        for r in range(2):
+            ex += np.bincount(p1.edge_idx[b:b + 32, r] % 32, minlength=32).max() - 1
+    assert ex == 0
 
 
 @pytest.mark.parametrize("precision", ["fp32", "fp64"])
@@ -141,8 +161,9 @@ def test_compact_streams_encode_the_full_program(reach_scene, precision):
         vfp = p.h["Vf_pad"]
         wa = np.where(p.edge_idx[:, 0] < vfp, p.w_free, 0.0)
         wb = np.where(p.edge_idx[:, 1] < vfp, p.w_free, 0.0)
-        assert np.array_equal(wa, p.edge_par[:, 1]) and np.array_equal(wb, p.edge_par[:, 2])
-        assert np.array_equal(wa + wb, p.edge_par[:, 3])
+        live = (p.edge_idx[:, 0] < vfp) | (p.edge_idx[:, 1] < vfp)   # skip padding lanes
+        assert np.array_equal(wa[live], p.edge_par[live, 1]) and np.array_equal(wb[live], p.edge_par[live, 2])
+        assert np.array_equal((wa + wb)[live], p.edge_par[live, 3])
     else:
         rl = p.edge_c[:, 2].copy().view(np.float32).astype(np.float64)
     assert np.array_equal(rl, p.edge_par[:, 0])

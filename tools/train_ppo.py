@@ -34,6 +34,9 @@ def main():
     ap.add_argument("--max-updates", type=int, default=150)
     ap.add_argument("--stop", type=float, default=80.0)
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--window", type=int, default=0,
+                    help="episodes in the trailing reward mean (0 = one per env of the whole job; "
+                         "100 = the reference's rule, ppo.py:405-413)")
     ap.add_argument("--precision", default="fp32")
     ap.add_argument("--out", default=None)
     args = ap.parse_args()
@@ -49,7 +52,8 @@ def main():
                    precision=args.precision)
     cfg = PPOConfig.for_num_envs(args.envs, horizon=args.horizon, minibatches=args.minibatches, epochs=args.epochs,
                                  learning_rate=args.lr, clip_range=args.clip, log_std_anneal_frac=args.anneal_frac,
-                                 seed=args.seed, stop_at_reward=args.stop)
+                                 seed=args.seed, stop_at_reward=args.stop,
+                                 stop_window=args.window or args.envs * world)
     cfg.total_steps = args.max_updates * cfg.steps_before_update
     t0 = time.perf_counter()
     stats = train(env, cfg, out_dir=args.out, verbose=(rank == 0))
@@ -60,7 +64,8 @@ def main():
             "metric": "wall-clock to trailing-100 mean reward > 80 (on-GPU PPO, tissue reach)",
             "reward_crossed_at_env_steps": stats.reward_crossed_at, "reward_crossed_wall_s": stats.reward_crossed_wall,
             "stopped_early_at": stats.stopped_early_at, "wall_s": wall, "updates": len(stats.rows),
-            "n_gpus": world, "envs_per_gpu": args.envs, "config": {k: getattr(cfg, k) for k in (
+            "n_gpus": world, "envs_per_gpu": args.envs, "stop_window": cfg.stop_window,
+            "config": {k: getattr(cfg, k) for k in (
                 "steps_before_update", "minibatch_size", "epochs", "learning_rate", "clip_range", "gamma",
                 "gae_lambda", "log_std_final", "log_std_anneal_frac", "total_steps")},
             "final_mean_reward": stats.rows[-1]["mean_ep_reward"] if stats.rows else None,
