@@ -38,7 +38,7 @@
 extern "C" {
 #endif
 
-#define TS_ABI_VERSION 1
+#define TS_ABI_VERSION 2
 
 enum ts_status {
     TS_OK = 0,
@@ -93,6 +93,8 @@ typedef struct ts_layout_opts {
     int32_t schedule_banks;     /* 1 = bank-conflict-aware item schedule (default), -1 = off */
     int32_t smem_budget;        /* bytes of shared memory per CTA to aim for (0 = auto) */
     int32_t compact;            /* 16-bit item streams when possible (default), -1 = off */
+    int32_t edge_gather;        /* 1 = distance constraints gathered by the owner of each free vertex,
+                                   -1 = constraint-parallel phase 1 + slots, 0 = auto (fp32 gather) */
 } ts_layout_opts;
 
 typedef struct ts_layout_info {
@@ -101,6 +103,8 @@ typedef struct ts_layout_info {
     int32_t n_edge_items, n_tet_items, n_att_items, n_slots_total;
     int32_t bank_conflicts_p1;  /* residual phase-1 conflicts of the schedule (extra wavefronts / substep) */
     int32_t compact;            /* 1 when the program uses the 16-bit item streams */
+    int32_t edge_gather;        /* 1 when distance constraints are owner-gathered */
+    int32_t n_edge_incidences;  /* (edge, free endpoint) records of the owner gather */
     int64_t program_bytes;
 } ts_layout_info;
 

@@ -37,6 +37,8 @@ struct ts_handle {
     ts_layout_info info{};
     int smem = 0;
     int max_grid = 0;   // 0 = one CTA per environment
+    TsCmd *cmd = nullptr;   // per-env command blocks (grown on demand)
+    int64_t cmd_cap = 0;
 };
 
 extern "C" {
@@ -104,6 +106,11 @@ static void decode(ts_handle *h) {
     P.w_free = H->w_free;
     P.edge_c = reinterpret_cast<const uint4 *>(b + H->off[TS_SEC_EDGE_C]);
     P.tet_c = reinterpret_cast<const uint4 *>(b + H->off[TS_SEC_TET_C]);
+    P.edge_gather = H->edge_gather;
+    P.einc_bytes = H->einc_bytes;
+    P.einc = b + H->off[TS_SEC_EINC];
+    P.eregion = reinterpret_cast<const int32_t *>(b + H->off[TS_SEC_EREGION]);
+    P.evalence = reinterpret_cast<const int32_t *>(b + H->off[TS_SEC_EVAL]);
 }
 
 static void fill_params(const ts_scene_desc &d, TsParams &S) {
@@ -166,6 +173,7 @@ int32_t ts_create(const ts_scene_desc *desc, const ts_layout_opts *opts, int32_t
 int32_t ts_destroy(ts_handle *h) {
     if (!h) return TS_OK;
     if (h->dev_blob) cudaFree(h->dev_blob);
+    if (h->cmd) cudaFree(h->cmd);
     delete h;
     return TS_OK;
 }
@@ -183,14 +191,29 @@ static void fill_state(TsLaunch &L, const ts_env_state *st) {
     L.steps = st->steps; L.l_prev = st->l_prev; L.ep_return = st->ep_return;
 }
 
-static int launch(ts_handle *h, const TsLaunch &L, cudaStream_t s) {
-    if (L.n_env <= 0) return TS_OK;
+// One step = command kernel (one thread per env) -> fused step kernel (one CTA per env)
+// -> epilogue kernel (one thread per env), stream ordered.
+static int launch(ts_handle *h, const TsLaunch &L_in, cudaStream_t s) {
+    if (L_in.n_env <= 0) return TS_OK;
+    if (L_in.n_env > h->cmd_cap) {
+        // grown outside the steady state (the first step at a batch size); not graph-capturable
+        TsCmd *nb = nullptr;
+        cudaError_t e = cudaMalloc(&nb, (size_t)L_in.n_env * sizeof(TsCmd));
+        if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(command blocks)");
+        if (h->cmd) { cudaStreamSynchronize(s); cudaFree(h->cmd); }
+        h->cmd = nb; h->cmd_cap = L_in.n_env;
+    }
+    TsLaunch L = L_in;
+    L.cmd = h->cmd;
     int grid = (int)std::min<int64_t>(L.n_env, h->max_grid > 0 ? h->max_grid : (int64_t)1 << 30);
-    if (grid > 2147483647) grid = 2147483647;
-    cudaError_t e = h->precision == TS_F64 ? ts_launch_step<double>(h->prog, h->params, L, grid, h->smem, s)
-                                           : ts_launch_step<float>(h->prog, h->params, L, grid, h->smem, s);
+    cudaError_t e = ts_launch_cmd(h->prog, h->params, L, s);
+    if (e != cudaSuccess) return cuda_fail(e, "command kernel launch");
+    e = h->precision == TS_F64 ? ts_launch_step<double>(h->prog, h->params, L, grid, h->smem, s)
+                               : ts_launch_step<float>(h->prog, h->params, L, grid, h->smem, s);
     if (e != cudaSuccess) return cuda_fail(e, "step kernel launch");
-    g_launches.fetch_add(1);
+    e = ts_launch_epilogue(h->prog, h->params, L, s);
+    if (e != cudaSuccess) return cuda_fail(e, "epilogue kernel launch");
+    g_launches.fetch_add(3);
     return TS_OK;
 }
 

@@ -19,7 +19,7 @@
 #include <stdint.h>
 
 #define TS_PROG_MAGIC 0x54534231  // "TSB1"
-#define TS_PROG_VERSION 1
+#define TS_PROG_VERSION 2
 
 enum TsChunkKind { TS_CHUNK_EDGE = 0, TS_CHUNK_ATT = 1, TS_CHUNK_TET = 2 };
 
@@ -48,6 +48,14 @@ enum TsSection {
     // the whole phase-1 stream of reach_1170 fits in L1 and is shared by every CTA on an SM
     TS_SEC_EDGE_C,        // uint4 {pa | pb << 16, sa | sb << 16, rest (fp32 bits | fp64 lo), fp64 hi}
     TS_SEC_TET_C,         // uint4 {pa | pb << 16, pc | pd << 16, sa | sb << 16, sc | sd << 16}
+    // owner-gathered distance constraints (edge_gather programs): every free vertex walks its own
+    // incident edges in edge-index order and recomputes each correction from the position
+    // snapshot, so edges need neither phase-1 items nor slots nor a barrier of their own
+    TS_SEC_EINC,          // records, warp-interleaved like slots: incidence k of lane l at
+                          //   eregion[g] + 32k + l.  einc_bytes = 8: {nbr pos, fp32 rest}
+                          //   (uniform-mass fp32); 16: {nbr pos, fp32 coef | 0, fp64/fp32 rest}
+    TS_SEC_EREGION,       // int32 [G] base record of group g
+    TS_SEC_EVAL,          // int32 [Vf_pad] live incident edges of p
     TS_SEC_COUNT
 };
 
@@ -65,7 +73,7 @@ struct TsProgHeader {
     int32_t F, B, VPT, G;
     int32_t n_chunks, grasp_chunk, slot_capacity, n_att;
     int32_t n_edge_items, n_tet_items, n_att_items, bank_conflicts;
-    int32_t n_slots_total, compact, pad1, pad2;
+    int32_t n_slots_total, compact, edge_gather, einc_bytes;
     double w_free;   // the common inverse mass of free vertices (compact programs)
     int64_t off[TS_SEC_COUNT];
     int64_t total_bytes;

@@ -62,6 +62,34 @@ struct TsDevProg {
     double w_free;            // common inverse mass of free vertices (compact programs)
     const uint4 *edge_c;
     const uint4 *tet_c;
+    int32_t edge_gather;      // 1: owner-gathered edges (records below), positions double-buffered
+    int32_t einc_bytes;       // 8 or 16
+    const void *einc;
+    const int32_t *eregion;
+    const int32_t *evalence;
+};
+
+// Tool pose of one env (ToolBatch row, tool.py:263-302), fp64.
+struct TsPose { double ax[3], jw[3], reach, clamp; };
+
+// Per-env command block: written by the per-env command kernel (tool command,
+// grasp release, capsule rows, the step's reward distance), read by the step
+// kernel (which adds the grasp search result, divergence and contact count)
+// and finished by the per-env epilogue kernel (reward / done / reset / obs).
+// The two scalar stages run one THREAD per env instead of one thread of a
+// 320-thread CTA while the rest of the CTA waits at a barrier.
+struct TsCmd {
+    double caps[3][7];        // capsule rows (tool.py:347-370)
+    double drag[3];           // drag point after the command
+    TsPose pose;              // tool pose after the command
+    double dist;              // env mode: |drag - target|, env.py:103-108
+    int32_t gv;               // grasp vertex (original id, -1 none) -- final after the step kernel
+    int32_t need_search;      // clamp engaged and nothing held: nearest-vertex search
+    int32_t clipped, rejected;
+    int32_t pre_done;         // env mode: success || steps + 1 >= max (done unless diverged)
+    int32_t any_bad;          // step kernel: non-finite position after the step
+    int32_t n_contacts;       // step kernel: contacts resolved
+    int32_t pad;
 };
 
 // Per-launch pointers (device).
@@ -93,12 +121,13 @@ struct TsLaunch {
     // plugin detect outputs (capacity 3F rows per env)
     int32_t *det_count, *det_face, *det_cap;
     double *det_depth, *det_dir, *det_bary;
+    TsCmd *cmd;                   // (n_env,) per-env command blocks (handle-owned scratch)
 };
 
 // Shared-memory layout sizes (bytes) for one CTA.
 inline int ts_smem_bytes(const TsDevProg &P, int real_bytes) {
     size_t b = 0;
-    b += (size_t)3 * P.Vstore * real_bytes;       // xs, ys, zs
+    b += (size_t)3 * P.Vstore * real_bytes * (P.edge_gather ? 2 : 1);   // positions (x2: ping-pong)
     b += (size_t)3 * P.slot_cap * real_bytes;     // slot buffer / contact records
     b += (size_t)4 * P.Vf_pad;                    // degenerate-constraint counters
     b += (size_t)4 * P.cbits_words;               // contact bitmap
@@ -107,9 +136,12 @@ inline int ts_smem_bytes(const TsDevProg &P, int real_bytes) {
     return (int)b;
 }
 
+// command kernel -> fused step kernel -> epilogue kernel, stream ordered
 template <typename Real>
 cudaError_t ts_launch_step(const TsDevProg &P, const TsParams &S, const TsLaunch &L, int grid,
                            int smem, cudaStream_t stream);
+cudaError_t ts_launch_cmd(const TsDevProg &P, const TsParams &S, const TsLaunch &L, cudaStream_t stream);
+cudaError_t ts_launch_epilogue(const TsDevProg &P, const TsParams &S, const TsLaunch &L, cudaStream_t stream);
 template <typename Real>
 cudaError_t ts_launch_reset(const TsDevProg &P, const TsParams &S, const TsLaunch &L,
                             const uint8_t *mask, int observe_only, cudaStream_t stream);

@@ -49,7 +49,7 @@ __device__ __forceinline__ void cross3(const double *u, const double *w, double 
 }
 __device__ __forceinline__ double norm3(const double *u) { return sqrt(dot3(u, u)); }
 
-struct Pose { double ax[3], jw[3], reach, clamp; };
+using Pose = TsPose;
 
 // perpendicular_unit, tool.py:55-62
 static __device__ void some_perpendicular(const double *a, double *out) {
@@ -270,17 +270,12 @@ template <> __device__ __forceinline__ float fused_sq3<float>(float a, float b, 
 struct Scal {
     double caps[3][7];
     double drag[3];
-    Pose pose;
     double red_key[32];
     int red_idx[32];
     int gv_orig;        // grasp vertex, original id (-1 none)
-    int gv_store;       // storage position (-1 none / pinned handled like free)
     int need_search;
-    int diverged;
     int done;
     int n_contacts;
-    int clipped, rejected;
-    int abort;
 };
 
 // Component c of element i of an (n, 3) array-of-structs in shared memory.
@@ -297,6 +292,7 @@ struct Strided {
 template <typename Real>
 struct Smem {
     Strided<Real> xs, ys, zs, slx, sly, slz;   // positions (storage order), slots
+    Real *alt;                                 // edge_gather: the other position buffer (ping-pong)
     int *deg;
     unsigned *cbits;
     Scal *sc;
@@ -307,7 +303,8 @@ template <typename Real>
 __device__ __forceinline__ Smem<Real> carve(const TsDevProg &P, unsigned char *raw) {
     Smem<Real> m;
     Real *pos = reinterpret_cast<Real *>(raw);
-    Real *slots = pos + 3 * P.Vstore;
+    m.alt = P.edge_gather ? pos + 3 * P.Vstore : pos;
+    Real *slots = pos + 3 * P.Vstore * (P.edge_gather ? 2 : 1);
     m.xs.p = pos; m.ys.p = pos + 1; m.zs.p = pos + 2;
     m.slx.p = slots; m.sly.p = slots + 1; m.slz.p = slots + 2;
     m.deg = reinterpret_cast<int *>(slots + 3 * P.slot_cap);
@@ -573,8 +570,75 @@ __device__ void p1_atts(const TsDevProg &P, const Smem<Real> &m, int begin, int 
     }
 }
 
+// ---------------------------------------------------------------------------
+// owner-gathered distance constraints (edge_gather programs)
+// ---------------------------------------------------------------------------
+// Free vertex p (owner lane `lane`, own predicted position (px, py, pz)) adds the
+// corrections of its live incident edges, in edge-index order, to (ax, ay, az).
+// fp64: -(w_p scale) (x_p - x_q) with the reference's scale expression
+// (ts_lane_edges, _kernels.pyx:121-136) -- bitwise the reference's per-endpoint
+// term, see compiler.cpp; fp32: -coef (1 - rest / dist) (x_p - x_q) with FMAs.
+template <typename Real>
+__device__ __forceinline__ void owner_edges(const TsDevProg &P, const Smem<Real> &m, int p, int lane, Real px,
+                                            Real py, Real pz, Real ks, Real &ax, Real &ay, Real &az, int &ndeg) {
+    const int ev = P.evalence[p];
+    const int rb = P.eregion[p >> 5] + lane;
+    if constexpr (sizeof(Real) == 8) {
+        const int4 *rec = reinterpret_cast<const int4 *>(P.einc) + rb;
+        const double *wst = reinterpret_cast<const double *>(P.w);
+        const double wp = wst[p];
+        for (int k = 0; k < ev; ++k) {
+            const int4 q = __ldg(rec + 32 * k);
+            const int nb = q.x;
+            const double rl = __hiloint2double(q.w, q.z);
+            const double wq = __ldg(wst + nb);
+            const double dx = px - m.xs[nb], dy = py - m.ys[nb], dz = pz - m.zs[nb];
+            const double dist = sqrt(dx * dx + dy * dy + dz * dz);
+            const double mm = 0.5 + copysign(0.5, dist - 1e-12);
+            const double scale = mm * ks * (dist - rl) / (dist * (wp + wq) + (1.0 - mm));
+            const double c = -(wp * scale);
+            ax = ax + c * dx; ay = ay + c * dy; az = az + c * dz;
+            ndeg += mm == 0.0;
+        }
+    } else if (P.einc_bytes == 8) {
+        // uniform free mass: coef = ks w / (w + w) = ks / 2, or ks when the neighbour is pinned
+        const uint2 *rec = reinterpret_cast<const uint2 *>(P.einc) + rb;
+        const int vfp = P.Vf_pad;
+        const float hks = 0.5f * ks;
+        uint2 q = ev > 0 ? __ldg(rec) : make_uint2(0, 0);
+        for (int k = 0; k < ev; ++k) {
+            const uint2 cur = q;
+            q = __ldg(rec + 32 * min(k + 1, ev - 1));    // next record, branch-free prefetch
+            const int nb = (int)cur.x;
+            const float rl = __uint_as_float(cur.y);
+            const float dx = px - m.xs[nb], dy = py - m.ys[nb], dz = pz - m.zs[nb];
+            const float d2 = __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, dx * dx));
+            const bool degenerate = !(d2 >= 1e-24f);
+            const float f = degenerate ? 0.0f : __fmaf_rn(-rl, rsqrtf(d2), 1.0f);
+            const float c = -(nb < vfp ? hks : ks) * f;
+            ax = __fmaf_rn(c, dx, ax); ay = __fmaf_rn(c, dy, ay); az = __fmaf_rn(c, dz, az);
+            ndeg += degenerate;
+        }
+    } else {
+        const int4 *rec = reinterpret_cast<const int4 *>(P.einc) + rb;
+        for (int k = 0; k < ev; ++k) {
+            const int4 q = __ldg(rec + 32 * k);
+            const int nb = q.x;
+            const float coef = __int_as_float(q.y), rl = __int_as_float(q.z);
+            const float dx = px - m.xs[nb], dy = py - m.ys[nb], dz = pz - m.zs[nb];
+            const float d2 = __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, dx * dx));
+            const bool degenerate = !(d2 >= 1e-24f);
+            const float f = degenerate ? 0.0f : __fmaf_rn(-rl, rsqrtf(d2), 1.0f);
+            const float c = -coef * f;
+            ax = __fmaf_rn(c, dx, ax); ay = __fmaf_rn(c, dy, ay); az = __fmaf_rn(c, dz, az);
+            ndeg += degenerate;
+        }
+    }
+}
+
 // tool command + grasp release + capsule rows for one env (thread 0), tool.py:307-378
-static __device__ __noinline__ void t0_command(const TsDevProg &P, const TsParams &S, const TsLaunch &L, int64_t env, Scal &sc) {
+static __device__ __forceinline__ void env_command(const TsDevProg &P, const TsParams &S, const TsLaunch &L,
+                                                   int64_t env, TsCmd &sc) {
     const int mode = L.mode;
     Pose p;
     const bool has_tool = L.axis != nullptr;
@@ -601,6 +665,17 @@ static __device__ __noinline__ void t0_command(const TsDevProg &P, const TsParam
         clipped = L.ovr_clipped ? L.ovr_clipped[env] != 0 : false;
     }
     sc.clipped = clipped; sc.rejected = rejected;
+    sc.pre_done = 0; sc.dist = 0.0;
+    if (mode & TS_M_ENV) {
+        // env.py:167-174: success and the step limit are known before the physics runs;
+        // only the divergence flag is added by the step kernel
+        double rel[3];
+        for (int c = 0; c < 3; ++c) rel[c] = (S.rcm[c] + p.reach * p.ax[c]) - S.target[c];
+        // np.einsum("nq,nq->n") association on the reference hosts: (r0^2 + r2^2) + r1^2
+        const double l = sqrt((rel[0] * rel[0] + rel[2] * rel[2]) + rel[1] * rel[1]);
+        sc.dist = l;
+        sc.pre_done = (l < S.success_thr) || (L.steps[env] + 1 >= S.max_steps);
+    }
     int64_t gv = -1;
     if (mode & TS_M_EXT_GRASP) {
         gv = L.ext_gv[env];
@@ -617,27 +692,28 @@ static __device__ __noinline__ void t0_command(const TsDevProg &P, const TsParam
             sc.need_search = 1;
         }
     }
-    sc.gv_orig = (int)gv;
+    sc.gv = (int)gv;
     sc.pose = p;
     if (mode & TS_M_DETECT_ONLY) {
         for (int r = 0; r < 3; ++r) for (int k = 0; k < 7; ++k) sc.caps[r][k] = L.ext_caps[(env * 3 + r) * 7 + k];
     } else if (mode & TS_M_CONTACTS) {
         capsule_rows(S, p, sc.caps);
     }
-    sc.diverged = 0; sc.n_contacts = 0;
+    sc.any_bad = 0; sc.n_contacts = 0;
 }
 
 // reward / done / auto-reset / obs for one env (thread 0, fp64), env.py:160-197
-static __device__ __noinline__ void t0_env(const TsParams &S, const TsLaunch &L, int64_t env, int any_bad, Scal &sc) {
+static __device__ __forceinline__ void env_epilogue(const TsParams &S, const TsLaunch &L, int64_t env,
+                                                    const TsCmd &sc) {
     const int mode = L.mode;
+    const int any_bad = sc.any_bad;
     Pose p = sc.pose;
-    const int64_t gv_new = sc.gv_orig;
+    const int64_t gv_new = sc.gv;
     int done = 0;
     if (mode & TS_M_ENV) {
-        double drag[3], rel[3];
-        for (int c = 0; c < 3; ++c) { drag[c] = S.rcm[c] + p.reach * p.ax[c]; rel[c] = drag[c] - S.target[c]; }
-        // np.einsum("nq,nq->n") association on the reference hosts: (r0^2 + r2^2) + r1^2
-        const double l = sqrt((rel[0] * rel[0] + rel[2] * rel[2]) + rel[1] * rel[1]);
+        double drag[3];
+        for (int c = 0; c < 3; ++c) drag[c] = S.rcm[c] + p.reach * p.ax[c];
+        const double l = sc.dist;
         const bool success = l < S.success_thr;
         const double lp = L.l_prev[env];
         const double reward = S.reward_scale * (S.w_l * l + S.w_d * (l - lp) + S.w_s * (success ? 1.0 : 0.0));
@@ -692,7 +768,25 @@ static __device__ __noinline__ void t0_env(const TsParams &S, const TsLaunch &L,
         L.reach[env] = p.reach; L.clamp[env] = p.clamp;
         L.grasp_vertex[env] = done ? -1 : gv_new;
     }
-    sc.done = done;
+}
+
+// per-env stages, one thread per environment
+static __global__ void __launch_bounds__(128) cmd_kernel(const __grid_constant__ TsDevProg P,
+                                                  const __grid_constant__ TsParams S,
+                                                  const __grid_constant__ TsLaunch L) {
+    if ((L.mode & TS_M_CHECK_ACTIONS) && *L.bad_flag) return;   // deferred ValidationError
+    for (int64_t env = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; env < L.n_env;
+         env += (int64_t)gridDim.x * blockDim.x)
+        env_command(P, S, L, env, L.cmd[env]);
+}
+
+static __global__ void __launch_bounds__(128) epilogue_kernel(const __grid_constant__ TsDevProg P,
+                                                       const __grid_constant__ TsParams S,
+                                                       const __grid_constant__ TsLaunch L) {
+    if ((L.mode & TS_M_CHECK_ACTIONS) && *L.bad_flag) return;
+    for (int64_t env = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; env < L.n_env;
+         env += (int64_t)gridDim.x * blockDim.x)
+        env_epilogue(S, L, env, L.cmd[env]);
 }
 
 // ---------------------------------------------------------------------------
@@ -703,7 +797,7 @@ __global__ void __launch_bounds__(512, sizeof(Real) == 4 ? 2 : 1) step_kernel(co
                                                    const __grid_constant__ TsParams S,
                                                    const __grid_constant__ TsLaunch L) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    const Smem<Real> m = carve<Real>(P, smem_raw);
+    Smem<Real> m = carve<Real>(P, smem_raw);
     Scal &sc = *m.sc;
     const int t = threadIdx.x;
     const int B = blockDim.x;
@@ -722,14 +816,21 @@ __global__ void __launch_bounds__(512, sizeof(Real) == 4 ? 2 : 1) step_kernel(co
         Real *xg = reinterpret_cast<Real *>(L.x) + env * (int64_t)P.V * 3;
         Real *vg = reinterpret_cast<Real *>(L.v) + env * (int64_t)P.V * 3;
 
-        // ---- A. tool command (thread 0) overlapped with the state load ----
-        if (t == 0) t0_command(P, S, L, env, sc);
+        // ---- A. the env's command block (cmd_kernel) + the state load ------
+        TsCmd &cmd = L.cmd[env];
+        if (t < 24) {
+            const double *src = t < 21 ? &cmd.caps[0][0] + t : cmd.drag + (t - 21);
+            (&sc.caps[0][0])[t] = *src;            // caps[21] and drag[3] are contiguous in Scal too
+        } else if (t == 24) {
+            sc.gv_orig = cmd.gv; sc.need_search = cmd.need_search; sc.n_contacts = 0;
+        }
         // state -> shared (storage order) / registers
         for (int p = t; p < P.Vstore; p += B) {
             const int o = P.s2o[p];
             Real a = 0, b = 0, c = 0;
             if (o >= 0) { a = xg[3 * o]; b = xg[3 * o + 1]; c = xg[3 * o + 2]; }
             m.xs[p] = a; m.ys[p] = b; m.zs[p] = c;
+            m.alt[3 * p] = a; m.alt[3 * p + 1] = b; m.alt[3 * p + 2] = c;   // pinned rows of the ping-pong
         }
         Real vx[VPT], vy[VPT], vz[VPT];
 #pragma unroll
@@ -833,6 +934,8 @@ __global__ void __launch_bounds__(512, sizeof(Real) == 4 ? 2 : 1) step_kernel(co
                             const int val = P.valence[ch.val_off + p];
                             const int pre = gchunk ? P.gsplit[p] : val;
                             Real ax = accx[r], ay = accy[r], az = accz[r];
+                            if (P.edge_gather && c == 0)   // edges come first in the reference order
+                                owner_edges<Real>(P, m, p, lane, xr[r], yr[r], zr[r], ks, ax, ay, az, ndeg[r]);
 #pragma unroll 4
                             for (int k = 0; k < pre; ++k) {
                                 const int sidx = base + 32 * k;
@@ -856,7 +959,13 @@ __global__ void __launch_bounds__(512, sizeof(Real) == 4 ? 2 : 1) step_kernel(co
                 }
                 if (P.grasp_chunk == P.n_chunks) {
 #pragma unroll
-                    for (int r = 0; r < VPT; ++r) add_grasp(r);
+                    for (int r = 0; r < VPT; ++r) {
+                        const int p = r * B + t;
+                        if (P.edge_gather && P.n_chunks == 0 && p < P.Vf)   // distance constraints only
+                            owner_edges<Real>(P, m, p, lane, xr[r], yr[r], zr[r], ks, accx[r], accy[r], accz[r],
+                                              ndeg[r]);
+                        add_grasp(r);
+                    }
                 }
                 // apply (ts_lane_apply, _kernels.pyx:213-244) + next predict
 #pragma unroll
@@ -885,11 +994,18 @@ __global__ void __launch_bounds__(512, sizeof(Real) == 4 ? 2 : 1) step_kernel(co
                             vy[r] += h * gy; yr[r] += h * vy[r];
                             vz[r] += h * gz; zr[r] += h * vz[r];
                         }
-                        m.xs[p] = xr[r]; m.ys[p] = yr[r]; m.zs[p] = zr[r];
+                        // edge_gather: other owners may still read this substep's snapshot -> ping-pong
+                        Real *dst = m.alt + 3 * p;
+                        dst[0] = xr[r]; dst[1] = yr[r]; dst[2] = zr[r];
                         accx[r] = accy[r] = accz[r] = 0; ndeg[r] = 0; gcnt[r] = 0;
                     }
                 }
                 __syncthreads();
+                if (P.edge_gather) {
+                    Real *cur = m.xs.p;
+                    m.xs.p = m.alt; m.ys.p = m.alt + 1; m.zs.p = m.alt + 2;
+                    m.alt = cur;
+                }
             }
         }
 
@@ -968,13 +1084,16 @@ __global__ void __launch_bounds__(512, sizeof(Real) == 4 ? 2 : 1) step_kernel(co
             bad |= !(isfinite(m.xs[p]) && isfinite(m.ys[p]) && isfinite(m.zs[p]));
         const int any_bad = __syncthreads_or(bad);
 
-        // ---- F. env logic (thread 0, fp64; env.py:160-197) ----------------
-        if (t == 0) t0_env(S, L, env, any_bad, sc);
-        __syncthreads();
+        // ---- F. hand the step's results to the epilogue kernel -------------
+        // done = terminated || truncated = success || steps >= max || diverged (env.py:173-175)
+        if (t == 0) {
+            cmd.gv = sc.gv_orig; cmd.any_bad = any_bad; cmd.n_contacts = sc.n_contacts;
+        }
+        const bool done_env = (mode & TS_M_ENV) && (cmd.pre_done || any_bad);
 
         // ---- G. write back --------------------------------------------------
         if (!(mode & TS_M_DETECT_ONLY)) {
-            const bool done = sc.done != 0;
+            const bool done = done_env;
             if (done)
                 for (int i = t; i < P.V; i += B) L.grasped[env * P.V + i] = 0;
 #pragma unroll
@@ -1081,3 +1200,20 @@ cudaError_t ts_launch_reset(const TsDevProg &P, const TsParams &S, const TsLaunc
     tsk::reset_kernel<Real><<<grid, 256, 0, stream>>>(P, S, L, mask, observe_only);
     return cudaGetLastError();
 }
+
+#ifdef TS_DEFINE_SCALAR_KERNELS
+static int scalar_grid(int64_t n) {
+    int64_t g = (n + 127) / 128;
+    return (int)(g < 1 ? 1 : (g > 65535 ? 65535 : g));
+}
+
+cudaError_t ts_launch_cmd(const TsDevProg &P, const TsParams &S, const TsLaunch &L, cudaStream_t stream) {
+    tsk::cmd_kernel<<<scalar_grid(L.n_env), 128, 0, stream>>>(P, S, L);
+    return cudaGetLastError();
+}
+
+cudaError_t ts_launch_epilogue(const TsDevProg &P, const TsParams &S, const TsLaunch &L, cudaStream_t stream) {
+    tsk::epilogue_kernel<<<scalar_grid(L.n_env), 128, 0, stream>>>(P, S, L);
+    return cudaGetLastError();
+}
+#endif

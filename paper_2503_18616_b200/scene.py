@@ -151,13 +151,17 @@ class SceneArrays:
         return d
 
 
-def layout_opts(precision="fp32", block_threads=0, max_chunk_slots=0, schedule_banks=True, compact=True):
+def layout_opts(precision="fp32", block_threads=0, max_chunk_slots=0, schedule_banks=True, compact=True,
+                edge_gather=None):
     o = N.LayoutOpts()
     o.precision = N.TS_F64 if precision in ("fp64", "float64", "f64", N.TS_F64) else N.TS_F32
     o.block_threads = int(block_threads)
     o.max_chunk_slots = int(max_chunk_slots)
     o.schedule_banks = 1 if schedule_banks else -1
     o.compact = 1 if compact else -1
+    # None: the compiler's choice (owner gather for fp32; fp64 keeps constraint-parallel slots,
+    # where the per-incidence IEEE sqrt / div of the gather cost more than they save)
+    o.edge_gather = 0 if edge_gather is None else (1 if edge_gather else -1)
     return o
 
 

@@ -15,10 +15,11 @@ import numpy as np
 
 SECTIONS = ["CHUNK", "EDGE_IDX", "EDGE_PAR", "TET_IDX", "TET_SLOT", "TET_RV", "ATT_IDX", "ATT_SLOT",
             "ATT_PAR", "ATT_ANCHOR", "REGION", "VALENCE", "STATIC_CNT", "S2O", "O2S", "W", "FACES",
-            "FACES_ORIG", "REST", "GSPLIT", "EDGE_C", "TET_C"]
+            "FACES_ORIG", "REST", "GSPLIT", "EDGE_C", "TET_C", "EINC", "EREGION", "EVAL"]
 HDR_FIELDS = ["magic", "version", "real_bytes", "n_sections", "V", "Vf", "Vf_pad", "Vstore", "F", "B",
               "VPT", "G", "n_chunks", "grasp_chunk", "slot_capacity", "n_att", "n_edge_items",
-              "n_tet_items", "n_att_items", "bank_conflicts", "n_slots_total", "compact", "pad1", "pad2"]
+              "n_tet_items", "n_att_items", "bank_conflicts", "n_slots_total", "compact", "edge_gather",
+              "einc_bytes"]
 
 
 class Program:
@@ -58,6 +59,29 @@ class Program:
         self.w = self.sec("W", rt, H["Vstore"]).astype(np.float64)
         self.faces = self.sec("FACES", np.int32, 3 * H["F"]).reshape(-1, 3)
         self.gsplit = self.sec("GSPLIT", np.int32, Vfp)
+        if H["edge_gather"]:
+            G = H["G"]
+            self.eregion = self.sec("EREGION", np.int32, G)
+            self.evalence = self.sec("EVAL", np.int32, Vfp)
+            eb = H["einc_bytes"]
+            n = int(self.eregion[-1] + 32 * self.evalence[32 * (G - 1):32 * G].max()) if G else 0
+            raw = self.sec("EINC", np.uint8, max(n, 1) * eb).reshape(-1, eb)
+            self.e_nbr = raw[:, 0:4].copy().view(np.int32)[:, 0]
+            if eb == 8:
+                self.e_rest = raw[:, 4:8].copy().view(np.float32)[:, 0].astype(np.float64)
+                self.e_coef = None
+            elif H["real_bytes"] == 8:
+                self.e_rest = raw[:, 8:16].copy().view(np.float64)[:, 0]
+                self.e_coef = None
+            else:
+                self.e_coef = raw[:, 4:8].copy().view(np.float32)[:, 0].astype(np.float64)
+                self.e_rest = raw[:, 8:12].copy().view(np.float32)[:, 0].astype(np.float64)
+
+    def edge_records(self, p):
+        """(neighbour storage positions, rest lengths) of free position p, in gather order."""
+        k = np.arange(int(self.evalence[p]))
+        r = self.eregion[p // 32] + 32 * k + p % 32
+        return self.e_nbr[r], self.e_rest[r]
 
     def sec(self, name, dtype, count):
         o = int(self.off[SECTIONS.index(name)])
@@ -85,6 +109,22 @@ def run_substeps(prog: Program, x, v, grasp_vertex, drag, g, h, substeps, dampin
     for s in range(substeps):
         acc = np.zeros((Vf, 3))
         cnt_adj = np.zeros(Vf, np.int64)
+        def owner_edges():
+            # owner-gathered distance constraints (step_kernel.cuh owner_edges, fp64 form)
+            for p in range(Vf):
+                nb, rl = prog.edge_records(p)
+                if len(nb) == 0:
+                    continue
+                d = xs[p][None, :] - xs[nb]
+                dist = np.sqrt((d[:, 0] * d[:, 0] + d[:, 1] * d[:, 1]) + d[:, 2] * d[:, 2])
+                m = 0.5 + np.copysign(0.5, dist - 1e-12)
+                wp = prog.w[p]
+                scale = m * ks * (dist - rl) / (dist * (wp + prog.w[nb]) + (1.0 - m))
+                corr = -(wp * scale)[:, None] * d
+                for k in range(len(nb)):          # sequential: the reference's summation order
+                    acc[p] += corr[k]
+                cnt_adj[p] -= int(np.sum(m == 0))
+
         def add_grasp():
             if 0 <= gvs < Vf:
                 d = np.asarray(drag, np.float64) - xs[gvs]
@@ -137,6 +177,8 @@ def run_substeps(prog: Program, x, v, grasp_vertex, drag, g, h, substeps, dampin
                     free = idx[:, r] < H["Vf_pad"]
                     np.add.at(deg, idx[free & (m == 0), r], 1)
             # phase 2: slots in order, the grasp spliced after the edge slots of the grasp chunk
+            if H["edge_gather"] and c == 0:
+                owner_edges()
             base = prog.region[c, grp] + lane
             val = prog.valence[c, :Vf]
             pre = prog.gsplit[:Vf] if c == H["grasp_chunk"] else val
@@ -150,6 +192,8 @@ def run_substeps(prog: Program, x, v, grasp_vertex, drag, g, h, substeps, dampin
                     acc[live] += slots[base[live] + 32 * k]
             cnt_adj -= deg[:Vf]
         if H["grasp_chunk"] == H["n_chunks"]:
+            if H["edge_gather"] and H["n_chunks"] == 0:
+                owner_edges()
             add_grasp()
         n = (prog.static_cnt[:Vf] + cnt_adj).astype(np.float64)
         m = 0.5 + np.copysign(0.5, n - 0.5)

@@ -28,10 +28,10 @@ REWARD_TOL = 1e-4          # north_star: per-step rewards within 1e-4
 POS_REL_TOL = 1e-5         # north_star: per-particle positions within 1e-5 relative (fp32) after 100 steps
 
 
-def run_pair(scene, precision, n, steps, seed, inject=True, record=None):
+def run_pair(scene, precision, n, steps, seed, inject=True, record=None, layout=None):
     ref = O.OracleEnv(O.scene_from_loaded(*scene), n)
     ref.reset()
-    gpu = EnvBatch(scene, num_envs=n, device="cuda:0", precision=precision)
+    gpu = EnvBatch(scene, num_envs=n, device="cuda:0", precision=precision, layout=layout)
     g_obs0 = gpu.reset().cpu().numpy()
     assert np.allclose(g_obs0, ref.observe_rows(np.arange(n)), atol=1e-7 if precision == "fp32" else 0)
     rng = np.random.default_rng(seed)
@@ -49,7 +49,10 @@ def run_pair(scene, precision, n, steps, seed, inject=True, record=None):
     return ref, gpu, out
 
 
-def test_fp64_bitwise_with_injected_tool_poses(reach_scene):
+@pytest.mark.parametrize("edge_gather", [False, True], ids=["edge-slots", "edge-gather"])
+def test_fp64_bitwise_with_injected_tool_poses(reach_scene, edge_gather):
+    """Both distance-constraint data flows (constraint-parallel slots, owner gather -- the fp32
+    default) reproduce the reference bit for bit in the fp64 build."""
     n, steps = 16, 100
 
     def check(s, ref, gpu, rec):
@@ -67,7 +70,9 @@ def test_fp64_bitwise_with_injected_tool_poses(reach_scene):
         assert np.array_equal(ginfo["distance"].cpu().numpy(), rinfo["distance"]), s
         if rinfo["final_observation"] is not None:
             assert np.array_equal(ginfo["final_observation"].cpu().numpy(), rinfo["final_observation"]), s
-    ref, gpu, out = run_pair(reach_scene, "fp64", n, steps, seed=5, record=check)
+    ref, gpu, out = run_pair(reach_scene, "fp64", n, steps, seed=5, record=check,
+                             layout=dict(edge_gather=edge_gather))
+    assert gpu.sim.scene.info["edge_gather"] == int(edge_gather)
     assert out[-1]["interacted"].sum() >= 2          # grasp and contact really happened
     assert sum(int(r["ref"][4]["contacts"]) for r in out) > 0
 

@@ -35,8 +35,12 @@ def _oracle_substeps(mesh, rest, cfg, x, v, gv, drag, att=None):
     return xa[0], va[0]
 
 
-@pytest.mark.parametrize("opts", [dict(), dict(max_chunk_slots=1024), dict(max_chunk_slots=200),
-                                  dict(schedule_banks=False), dict(block_threads=64)])
+@pytest.mark.parametrize("opts", [dict(edge_gather=True), dict(edge_gather=True, max_chunk_slots=1024),
+                                  dict(edge_gather=True, max_chunk_slots=200),
+                                  dict(edge_gather=True, schedule_banks=False),
+                                  dict(edge_gather=True, block_threads=64), dict(),
+                                  dict(edge_gather=False), dict(edge_gather=False, max_chunk_slots=1024),
+                                  dict(edge_gather=False, block_threads=64)])
 def test_program_reproduces_oracle_bitwise(reach_scene, opts):
     mesh, rest, cfg = reach_scene
     blob, info = S.compile_program(_arrays(reach_scene), precision="fp64", **opts)
@@ -54,10 +58,12 @@ def test_program_reproduces_oracle_bitwise(reach_scene, opts):
         assert np.array_equal(xa, xb) and np.array_equal(va, vb), (opts, gv)
 
 
-def test_program_degenerate_constraints_counted_like_reference():
+@pytest.mark.parametrize("gather", [True, False])
+def test_program_degenerate_constraints_counted_like_reference(gather):
     """Coincident edge endpoints and collapsed tets drop out of the counts (m = 0 guards)."""
     mesh, rest, cfg = build_slab_scene(3, 2, 2)
-    blob, _ = S.compile_program(_arrays((mesh, rest, cfg)), precision="fp64", max_chunk_slots=64)
+    blob, _ = S.compile_program(_arrays((mesh, rest, cfg)), precision="fp64", max_chunk_slots=64,
+                                edge_gather=gather)
     prog = PI.Program(blob)
     x0 = mesh.positions_rest.copy()
     e = mesh.edges[5]
@@ -72,19 +78,31 @@ def test_program_degenerate_constraints_counted_like_reference():
     assert np.array_equal(xa, xb) and np.array_equal(va, vb)
 
 
-def test_slot_structure(reach_scene):
+def _edge_incidence(mesh, w):
+    inc = np.zeros(mesh.vertex_count, int)
+    for a, b in mesh.edges:
+        if w[a] + w[b] > 0:
+            inc[a] += w[a] > 0
+            inc[b] += w[b] > 0
+    return inc
+
+
+@pytest.mark.parametrize("gather", [True, False])
+def test_slot_structure(reach_scene, gather):
     mesh, rest, cfg = reach_scene
-    blob, info = S.compile_program(_arrays(reach_scene), precision="fp32")
+    blob, info = S.compile_program(_arrays(reach_scene), precision="fp32", edge_gather=gather)
     p = PI.Program(blob)
     H = p.h
     Vf = H["Vf"]
     w = rest.inverse_mass
-    # storage order: free first (sorted by incidence, descending), then pinned
+    assert H["edge_gather"] == info["edge_gather"] == int(gather)
+    # storage order: free first (sorted by gather cost, descending), then pinned
     assert np.all(w[p.s2o[:Vf]] > 0) and np.all(w[p.s2o[H["Vf_pad"]:][p.s2o[H["Vf_pad"]:] >= 0]] == 0)
     assert np.array_equal(np.sort(p.s2o[p.s2o >= 0]), np.arange(mesh.vertex_count))
-    # warps own vertices of similar valence: the groups of 32 are the valence-sorted order
-    # (lanes inside a group may be permuted by the bank refinement)
-    sc = p.static_cnt[:Vf]
+    # warps own vertices of similar cost: the groups of 32 are the cost-sorted order
+    # (lanes inside a group may be permuted by the bank refinement); an owner-gathered edge
+    # weighs three slots
+    sc = p.static_cnt[:Vf] + (2 * p.evalence[:Vf] if gather else 0)
     ref = np.sort(sc)[::-1]
     for g in range(0, Vf, 32):
         assert sorted(sc[g:g + 32]) == sorted(ref[g:g + 32])
@@ -107,22 +125,41 @@ def test_slot_structure(reach_scene):
             assert np.all(sl % 32 == idx % 32)
             used.append(len(s))
         expected += sum(used)
-    assert expected == info["n_slots_total"] == p.static_cnt.sum()
+    n_inc = info["n_edge_incidences"] if gather else 0
+    assert expected == info["n_slots_total"] == p.static_cnt.sum() - n_inc
     # per-vertex incidence count equals the reference's count of live constraints touching it
-    inc = np.zeros(mesh.vertex_count, int)
-    for a, b in mesh.edges:
-        if w[a] + w[b] > 0:
-            inc[a] += w[a] > 0
-            inc[b] += w[b] > 0
+    inc = _edge_incidence(mesh, w)
+    if gather:
+        assert np.array_equal(p.evalence[:Vf], inc[p.s2o[:Vf]]) and n_inc == inc.sum()
     for t in mesh.tets:
         inc[t] += w[t] > 0
     assert np.array_equal(p.static_cnt[:Vf], inc[p.s2o[:Vf]])
 
 
+@pytest.mark.parametrize("precision", ["fp32", "fp64"])
+def test_edge_gather_records(reach_scene, precision):
+    """Owner-gathered edges: every free vertex lists exactly its live incident edges, in edge-index
+    order (the reference's accumulation order), warp-interleaved, with the right rest lengths."""
+    mesh, rest, cfg = reach_scene
+    blob, info = S.compile_program(_arrays(reach_scene), precision=precision, edge_gather=True)
+    p = PI.Program(blob)
+    w = rest.inverse_mass
+    assert p.h["einc_bytes"] == (8 if precision == "fp32" else 16)
+    assert info["n_edge_items"] == 0            # no phase-1 edge items, no edge slots
+    rt = np.float32 if precision == "fp32" else np.float64
+    for pos in range(p.h["Vf"]):
+        v = p.s2o[pos]
+        nb, rl = p.edge_records(pos)
+        want = [e for e, (a, b) in enumerate(mesh.edges) if (a == v or b == v) and w[a] + w[b] > 0]
+        other = [int(b if a == v else a) for a, b in mesh.edges[want]]
+        assert np.array_equal(p.s2o[nb], other)
+        assert np.array_equal(rl, rest.rest_length[want].astype(rt).astype(np.float64))
+
+
 def test_schedule_is_permutation_and_reduces_conflicts(reach_scene):
     arr = _arrays(reach_scene)
-    b1, i1 = S.compile_program(arr, precision="fp32", schedule_banks=True)
-    b0, i0 = S.compile_program(arr, precision="fp32", schedule_banks=False)
+    b1, i1 = S.compile_program(arr, precision="fp32", schedule_banks=True, edge_gather=False)
+    b0, i0 = S.compile_program(arr, precision="fp32", schedule_banks=False, edge_gather=False)
     p1, p0 = PI.Program(b1), PI.Program(b0)
 
     def constraints(p, idx, roles):
@@ -149,7 +186,7 @@ def test_compact_streams_encode_the_full_program(reach_scene, precision):
     """The 16-bit item streams the kernel reads for uniform-mass scenes carry exactly the full program:
     same positions and slots, same rest lengths, and edge weights recoverable from the pinned flags."""
     mesh, rest, cfg = reach_scene
-    blob, info = S.compile_program(_arrays(reach_scene), precision=precision)
+    blob, info = S.compile_program(_arrays(reach_scene), precision=precision, edge_gather=False)
     p = PI.Program(blob)
     assert info["compact"] == 1 and p.h["compact"] == 1
     lo, hi = p.edge_c[:, 0] & 0xFFFF, p.edge_c[:, 0] >> 16
