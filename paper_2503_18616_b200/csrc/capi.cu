@@ -133,6 +133,7 @@ static void fill_params(const ts_scene_desc &d, TsParams &S) {
     S.action_scale = d.action_scale; S.success_thr = d.success_threshold;
     S.w_l = d.w_distance; S.w_d = d.w_delta; S.w_s = d.w_success; S.reward_scale = d.reward_scale;
     S.max_steps = d.max_episode_steps; S.start_distance = d.start_distance;
+    ts_finish_params(S);
 }
 
 int32_t ts_create(const ts_scene_desc *desc, const ts_layout_opts *opts, int32_t device, ts_handle **out) {
@@ -324,6 +325,7 @@ int32_t ts_run_substeps(ts_handle *h, void *x, void *v, int64_t num_envs, const 
     for (int c = 0; c < 3; ++c) S.g[c] = gravity[c];
     if (damping == 0.0) S.damp = 1.0;
     else { double dv = 1.0 - damping * hstep; S.damp = (dv > 0.0) ? dv : 0.0; }
+    ts_finish_params(S);
     int rc = substeps > 0 ? launch(h, L, reinterpret_cast<cudaStream_t>(stream)) : TS_OK;
     h->params = saved;
     return rc;

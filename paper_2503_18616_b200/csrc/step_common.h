@@ -32,7 +32,15 @@ struct TsParams {
     double lo[3], hi[3];
     int64_t max_steps;
     double start_distance, target_obs[3];
+    // fp32 copies of the solver constants (read straight from the constant bank by the fp32 build)
+    float h_f, inv_h_f, damp_f, g_f[3], ks_f, hks_f, kv_f, pad_f;
 };
+
+inline void ts_finish_params(TsParams &S) {
+    S.h_f = (float)S.h; S.inv_h_f = (float)(1.0 / S.h); S.damp_f = (float)S.damp;
+    for (int c = 0; c < 3; ++c) S.g_f[c] = (float)S.g[c];
+    S.ks_f = (float)S.ks; S.hks_f = (float)(0.5 * S.ks); S.kv_f = (float)S.kv; S.pad_f = 0.0f;
+}
 
 // Decoded device program (pointers into the uploaded blob).
 struct TsDevProg {

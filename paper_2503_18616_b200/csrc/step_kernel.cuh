@@ -39,6 +39,22 @@ __device__ __forceinline__ double cmax(double a, double b) { return (b > a) ? b 
 __device__ __forceinline__ float cmin(float a, float b) { return (b < a) ? b : a; }
 __device__ __forceinline__ float cmax(float a, float b) { return (b > a) ? b : a; }
 
+// fp32 build: single-MUFU approximations (arguments are normal: guarded by the degeneracy tests)
+__device__ __forceinline__ float rsqrt_ftz(float x) {
+    float r;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+__device__ __forceinline__ float rcp_ftz(float x) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+// solver constant in the build's precision (fp32 copies live in TsParams, no F2F in the loops)
+template <typename Real> __device__ __forceinline__ Real prm(double d, float f);
+template <> __device__ __forceinline__ double prm<double>(double d, float) { return d; }
+template <> __device__ __forceinline__ float prm<float>(double, float f) { return f; }
+
 __device__ __forceinline__ double dot3(const double *u, const double *w) {
     return u[0] * w[0] + u[1] * w[1] + u[2] * w[2];
 }
@@ -283,16 +299,18 @@ struct Scal {
 // 16 for 64-bit words), so lanes with distinct i mod 32 are conflict-free,
 // exactly as with separate component arrays, and the three components share
 // one address (immediate offsets 0/4/8) -- a third of the address arithmetic.
-template <typename Real>
-struct Strided {
-    Real *p;
-    __device__ __forceinline__ Real &operator[](int i) const { return p[3 * i]; }
-};
 
 template <typename Real>
 struct Smem {
-    Strided<Real> xs, ys, zs, slx, sly, slz;   // positions (storage order), slots
-    Real *alt;                                 // edge_gather: the other position buffer (ping-pong)
+    Real *pos;      // positions (storage order), AoS: one address per vertex, components at +0/+1/+2
+    Real *alt;      // edge_gather: the other position buffer (ping-pong); == pos otherwise
+    Real *slot;     // slot buffer, AoS like the positions
+    __device__ __forceinline__ Real &X(int i) const { return pos[3 * i]; }
+    __device__ __forceinline__ Real &Y(int i) const { return pos[3 * i + 1]; }
+    __device__ __forceinline__ Real &Z(int i) const { return pos[3 * i + 2]; }
+    __device__ __forceinline__ Real &SX(int i) const { return slot[3 * i]; }
+    __device__ __forceinline__ Real &SY(int i) const { return slot[3 * i + 1]; }
+    __device__ __forceinline__ Real &SZ(int i) const { return slot[3 * i + 2]; }
     int *deg;
     unsigned *cbits;
     Scal *sc;
@@ -305,8 +323,8 @@ __device__ __forceinline__ Smem<Real> carve(const TsDevProg &P, unsigned char *r
     Real *pos = reinterpret_cast<Real *>(raw);
     m.alt = P.edge_gather ? pos + 3 * P.Vstore : pos;
     Real *slots = pos + 3 * P.Vstore * (P.edge_gather ? 2 : 1);
-    m.xs.p = pos; m.ys.p = pos + 1; m.zs.p = pos + 2;
-    m.slx.p = slots; m.sly.p = slots + 1; m.slz.p = slots + 2;
+    m.pos = pos;
+    m.slot = slots;
     m.deg = reinterpret_cast<int *>(slots + 3 * P.slot_cap);
     m.cbits = reinterpret_cast<unsigned *>(m.deg + P.Vf_pad);
     size_t off = reinterpret_cast<unsigned char *>(m.cbits + P.cbits_words) - raw;
@@ -325,9 +343,9 @@ __device__ __forceinline__ Smem<Real> carve(const TsDevProg &P, unsigned char *r
 template <typename Real>
 __device__ __forceinline__ void edge_item(const Smem<Real> &m, int pa, int pb, int sa, int sb, Real rl, Real wa,
                                           Real wb, Real wsum, Real ks, int vfp) {
-    const Real dx = m.xs[pa] - m.xs[pb];
-    const Real dy = m.ys[pa] - m.ys[pb];
-    const Real dz = m.zs[pa] - m.zs[pb];
+    const Real dx = m.X(pa) - m.X(pb);
+    const Real dy = m.Y(pa) - m.Y(pb);
+    const Real dz = m.Z(pa) - m.Z(pb);
     Real ca, cb;
     bool degenerate;
     if constexpr (sizeof(Real) == 8) {
@@ -342,12 +360,12 @@ __device__ __forceinline__ void edge_item(const Smem<Real> &m, int pa, int pb, i
         // fp32 build: c = k (1 - rest / dist)
         const float d2 = __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, dx * dx));
         degenerate = !(d2 >= 1e-24f);                    // dist < 1e-12 (coincident guard)
-        const float f = degenerate ? 0.0f : __fmaf_rn(-rl, rsqrtf(d2), 1.0f);
+        const float f = degenerate ? 0.0f : __fmaf_rn(-rl, rsqrt_ftz(d2), 1.0f);
         ca = -wa * f;
         cb = wb * f;
     }
-    m.slx[sa] = ca * dx; m.sly[sa] = ca * dy; m.slz[sa] = ca * dz;
-    m.slx[sb] = cb * dx; m.sly[sb] = cb * dy; m.slz[sb] = cb * dz;   // pinned endpoints -> trash slots
+    m.SX(sa) = ca * dx; m.SY(sa) = ca * dy; m.SZ(sa) = ca * dz;
+    m.SX(sb) = cb * dx; m.SY(sb) = cb * dy; m.SZ(sb) = cb * dz;   // pinned endpoints -> trash slots
     if (degenerate) {
         if (pa < vfp) atomicAdd(&m.deg[pa], 1);
         if (pb < vfp) atomicAdd(&m.deg[pb], 1);
@@ -406,12 +424,12 @@ __device__ __forceinline__ void p1_edges(const TsDevProg &P, const Smem<Real> &m
 
 template <typename Real>
 __device__ __forceinline__ void put_slot(const Smem<Real> &m, int s, Real c, Real gx, Real gy, Real gz) {
-    if (s >= 0) { m.slx[s] = c * gx; m.sly[s] = c * gy; m.slz[s] = c * gz; }
+    if (s >= 0) { m.SX(s) = c * gx; m.SY(s) = c * gy; m.SZ(s) = c * gz; }
 }
 
 template <typename Real>
 __device__ __forceinline__ void store_slot(const Smem<Real> &m, int s, Real c, Real gx, Real gy, Real gz) {
-    m.slx[s] = c * gx; m.sly[s] = c * gy; m.slz[s] = c * gz;
+    m.SX(s) = c * gx; m.SY(s) = c * gy; m.SZ(s) = c * gz;
 }
 
 template <typename Real>
@@ -459,10 +477,10 @@ __device__ __forceinline__ void p1_tets(const TsDevProg &P, const Smem<Real> &m,
 template <typename Real>
 __device__ __forceinline__ void tet_item(const Smem<Real> &m, int4 id, int4 sl, Real rvi, Real kv, int vfp) {
     {
-        const Real ax = m.xs[id.x], ay = m.ys[id.x], az = m.zs[id.x];
-        const Real bax = m.xs[id.y] - ax, bay = m.ys[id.y] - ay, baz = m.zs[id.y] - az;
-        const Real cax = m.xs[id.z] - ax, cay = m.ys[id.z] - ay, caz = m.zs[id.z] - az;
-        const Real dax = m.xs[id.w] - ax, day = m.ys[id.w] - ay, daz = m.zs[id.w] - az;
+        const Real ax = m.X(id.x), ay = m.Y(id.x), az = m.Z(id.x);
+        const Real bax = m.X(id.y) - ax, bay = m.Y(id.y) - ay, baz = m.Z(id.y) - az;
+        const Real cax = m.X(id.z) - ax, cay = m.Y(id.z) - ay, caz = m.Z(id.z) - az;
+        const Real dax = m.X(id.w) - ax, day = m.Y(id.w) - ay, daz = m.Z(id.w) - az;
         bool degenerate;
         if constexpr (sizeof(Real) == 8) {
             // exact build: ts_lane_tets, _kernels.pyx:165-208
@@ -512,7 +530,7 @@ __device__ __forceinline__ void tet_item(const Smem<Real> &m, int4 id, int4 sl, 
             den = __fmaf_rn(Gcx, Gcx, den); den = __fmaf_rn(Gcy, Gcy, den); den = __fmaf_rn(Gcz, Gcz, den);
             den = __fmaf_rn(Gdx, Gdx, den); den = __fmaf_rn(Gdy, Gdy, den); den = __fmaf_rn(Gdz, Gdz, den);
             degenerate = !(den > 3.6e-17f);                  // sum|grad|^2 <= 1e-18
-            const float sc = degenerate ? 0.0f : __fdividef(-kv * c6, den);
+            const float sc = degenerate ? 0.0f : (-kv * c6) * rcp_ftz(den);
             store_slot(m, sl.x, sc, Gax, Gay, Gaz);
             store_slot(m, sl.y, sc, Gbx, Gby, Gbz);
             store_slot(m, sl.z, sc, Gcx, Gcy, Gcz);
@@ -542,12 +560,12 @@ __device__ void p1_atts(const TsDevProg &P, const Smem<Real> &m, int begin, int 
         const bool face = an.w != (Real)0;
         Real cx, cy, cz;
         if (face) {
-            cx = (m.xs[id.y] + m.xs[id.z] + m.xs[id.w]) / (Real)3;
-            cy = (m.ys[id.y] + m.ys[id.z] + m.ys[id.w]) / (Real)3;
-            cz = (m.zs[id.y] + m.zs[id.z] + m.zs[id.w]) / (Real)3;
+            cx = (m.X(id.y) + m.X(id.z) + m.X(id.w)) / (Real)3;
+            cy = (m.Y(id.y) + m.Y(id.z) + m.Y(id.w)) / (Real)3;
+            cz = (m.Z(id.y) + m.Z(id.z) + m.Z(id.w)) / (Real)3;
         } else { cx = an.x; cy = an.y; cz = an.z; }
         const Real wsum = pr.z + pr.w;
-        const Real dx = m.xs[id.x] - cx, dy = m.ys[id.x] - cy, dz = m.zs[id.x] - cz;
+        const Real dx = m.X(id.x) - cx, dy = m.Y(id.x) - cy, dz = m.Z(id.x) - cz;
         const Real dist = sqrt(dx * dx + dy * dy + dz * dz);
         const Real mm = dist > (Real)1e-12 ? (Real)1 : (Real)0;
         const Real scale = mm * pr.y * (dist - pr.x) / (dist * wsum + ((Real)1 - mm));
@@ -592,7 +610,7 @@ __device__ __forceinline__ void owner_edges(const TsDevProg &P, const Smem<Real>
             const int nb = q.x;
             const double rl = __hiloint2double(q.w, q.z);
             const double wq = __ldg(wst + nb);
-            const double dx = px - m.xs[nb], dy = py - m.ys[nb], dz = pz - m.zs[nb];
+            const double dx = px - m.X(nb), dy = py - m.Y(nb), dz = pz - m.Z(nb);
             const double dist = sqrt(dx * dx + dy * dy + dz * dz);
             const double mm = 0.5 + copysign(0.5, dist - 1e-12);
             const double scale = mm * ks * (dist - rl) / (dist * (wp + wq) + (1.0 - mm));
@@ -604,17 +622,17 @@ __device__ __forceinline__ void owner_edges(const TsDevProg &P, const Smem<Real>
         // uniform free mass: coef = ks w / (w + w) = ks / 2, or ks when the neighbour is pinned
         const uint2 *rec = reinterpret_cast<const uint2 *>(P.einc) + rb;
         const int vfp = P.Vf_pad;
-        const float hks = 0.5f * ks;
+        const float hks = 0.5f * ks;   // == TsParams::hks_f
         uint2 q = ev > 0 ? __ldg(rec) : make_uint2(0, 0);
         for (int k = 0; k < ev; ++k) {
             const uint2 cur = q;
             q = __ldg(rec + 32 * min(k + 1, ev - 1));    // next record, branch-free prefetch
             const int nb = (int)cur.x;
             const float rl = __uint_as_float(cur.y);
-            const float dx = px - m.xs[nb], dy = py - m.ys[nb], dz = pz - m.zs[nb];
+            const float dx = px - m.X(nb), dy = py - m.Y(nb), dz = pz - m.Z(nb);
             const float d2 = __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, dx * dx));
             const bool degenerate = !(d2 >= 1e-24f);
-            const float f = degenerate ? 0.0f : __fmaf_rn(-rl, rsqrtf(d2), 1.0f);
+            const float f = degenerate ? 0.0f : __fmaf_rn(-rl, rsqrt_ftz(d2), 1.0f);
             const float c = -(nb < vfp ? hks : ks) * f;
             ax = __fmaf_rn(c, dx, ax); ay = __fmaf_rn(c, dy, ay); az = __fmaf_rn(c, dz, az);
             ndeg += degenerate;
@@ -625,10 +643,10 @@ __device__ __forceinline__ void owner_edges(const TsDevProg &P, const Smem<Real>
             const int4 q = __ldg(rec + 32 * k);
             const int nb = q.x;
             const float coef = __int_as_float(q.y), rl = __int_as_float(q.z);
-            const float dx = px - m.xs[nb], dy = py - m.ys[nb], dz = pz - m.zs[nb];
+            const float dx = px - m.X(nb), dy = py - m.Y(nb), dz = pz - m.Z(nb);
             const float d2 = __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, dx * dx));
             const bool degenerate = !(d2 >= 1e-24f);
-            const float f = degenerate ? 0.0f : __fmaf_rn(-rl, rsqrtf(d2), 1.0f);
+            const float f = degenerate ? 0.0f : __fmaf_rn(-rl, rsqrt_ftz(d2), 1.0f);
             const float c = -coef * f;
             ax = __fmaf_rn(c, dx, ax); ay = __fmaf_rn(c, dy, ay); az = __fmaf_rn(c, dz, az);
             ndeg += degenerate;
@@ -803,10 +821,10 @@ __global__ void __launch_bounds__(512, sizeof(Real) == 4 ? 2 : 1) step_kernel(co
     const int B = blockDim.x;
     const int lane = t & 31;
     const int mode = L.mode;
-    const Real h = (Real)S.h, damp = (Real)S.damp;
-    const Real inv_h = (Real)(1.0 / S.h);   // fp32 build: v += d * (1/h)
-    const Real gx = (Real)S.g[0], gy = (Real)S.g[1], gz = (Real)S.g[2];
-    const Real ks = (Real)S.ks, kv = (Real)S.kv;
+    const Real h = prm<Real>(S.h, S.h_f), damp = prm<Real>(S.damp, S.damp_f);
+    const Real inv_h = prm<Real>(1.0 / S.h, S.inv_h_f);   // fp32 build: v += d * (1/h)
+    const Real gx = prm<Real>(S.g[0], S.g_f[0]), gy = prm<Real>(S.g[1], S.g_f[1]), gz = prm<Real>(S.g[2], S.g_f[2]);
+    const Real ks = prm<Real>(S.ks, S.ks_f), kv = prm<Real>(S.kv, S.kv_f);
     const Real *wst = reinterpret_cast<const Real *>(P.w);
     const Real *rest = reinterpret_cast<const Real *>(P.rest);
 
@@ -829,7 +847,7 @@ __global__ void __launch_bounds__(512, sizeof(Real) == 4 ? 2 : 1) step_kernel(co
             const int o = P.s2o[p];
             Real a = 0, b = 0, c = 0;
             if (o >= 0) { a = xg[3 * o]; b = xg[3 * o + 1]; c = xg[3 * o + 2]; }
-            m.xs[p] = a; m.ys[p] = b; m.zs[p] = c;
+            m.X(p) = a; m.Y(p) = b; m.Z(p) = c;
             m.alt[3 * p] = a; m.alt[3 * p + 1] = b; m.alt[3 * p + 2] = c;   // pinned rows of the ping-pong
         }
         Real vx[VPT], vy[VPT], vz[VPT];
@@ -855,9 +873,9 @@ __global__ void __launch_bounds__(512, sizeof(Real) == 4 ? 2 : 1) step_kernel(co
             double bk = INFINITY;
             int bi = 0x7fffffff;
             for (int p = t; p < P.Vf; p += B) {
-                const double r0 = (double)m.xs[p] - sc.drag[0];
-                const double r1 = (double)m.ys[p] - sc.drag[1];
-                const double r2 = (double)m.zs[p] - sc.drag[2];
+                const double r0 = (double)m.X(p) - sc.drag[0];
+                const double r1 = (double)m.Y(p) - sc.drag[1];
+                const double r2 = (double)m.Z(p) - sc.drag[2];
                 double d2 = r0 * r0 + r1 * r1 + r2 * r2;
                 if (isnan(d2)) d2 = -INFINITY;      // numpy argmin returns the first NaN
                 const int o = P.s2o[p];
@@ -897,10 +915,10 @@ __global__ void __launch_bounds__(512, sizeof(Real) == 4 ? 2 : 1) step_kernel(co
                 xr[r] = yr[r] = zr[r] = 0;
                 if (p < P.Vf) {
                     // predict for substep 0 (ts_lane_predict, _kernels.pyx:63-87)
-                    vx[r] += h * gx; xr[r] = m.xs[p] + h * vx[r];
-                    vy[r] += h * gy; yr[r] = m.ys[p] + h * vy[r];
-                    vz[r] += h * gz; zr[r] = m.zs[p] + h * vz[r];
-                    m.xs[p] = xr[r]; m.ys[p] = yr[r]; m.zs[p] = zr[r];
+                    vx[r] += h * gx; xr[r] = m.X(p) + h * vx[r];
+                    vy[r] += h * gy; yr[r] = m.Y(p) + h * vy[r];
+                    vz[r] += h * gz; zr[r] = m.Z(p) + h * vz[r];
+                    m.X(p) = xr[r]; m.Y(p) = yr[r]; m.Z(p) = zr[r];
                 }
             }
             __syncthreads();
@@ -939,7 +957,7 @@ __global__ void __launch_bounds__(512, sizeof(Real) == 4 ? 2 : 1) step_kernel(co
 #pragma unroll 4
                             for (int k = 0; k < pre; ++k) {
                                 const int sidx = base + 32 * k;
-                                ax += m.slx[sidx]; ay += m.sly[sidx]; az += m.slz[sidx];
+                                ax += m.SX(sidx); ay += m.SY(sidx); az += m.SZ(sidx);
                             }
                             if (gchunk) {
                                 accx[r] = ax; accy[r] = ay; accz[r] = az;
@@ -947,7 +965,7 @@ __global__ void __launch_bounds__(512, sizeof(Real) == 4 ? 2 : 1) step_kernel(co
                                 ax = accx[r]; ay = accy[r]; az = accz[r];
                                 for (int k = pre; k < val; ++k) {
                                     const int sidx = base + 32 * k;
-                                    ax += m.slx[sidx]; ay += m.sly[sidx]; az += m.slz[sidx];
+                                    ax += m.SX(sidx); ay += m.SY(sidx); az += m.SZ(sidx);
                                 }
                             }
                             accx[r] = ax; accy[r] = ay; accz[r] = az;
@@ -982,7 +1000,7 @@ __global__ void __launch_bounds__(512, sizeof(Real) == 4 ? 2 : 1) step_kernel(co
                             yr[r] += e1; vy[r] += e1 / h;
                             zr[r] += e2; vz[r] += e2 / h;
                         } else {
-                            const float inv = cnt > 0 ? __frcp_rn((float)cnt) : 0.0f;
+                            const float inv = cnt > 0 ? rcp_ftz((float)cnt) : 0.0f;
                             const float e0 = accx[r] * inv, e1 = accy[r] * inv, e2 = accz[r] * inv;
                             xr[r] += e0; vx[r] = __fmaf_rn(e0, inv_h, vx[r]);
                             yr[r] += e1; vy[r] = __fmaf_rn(e1, inv_h, vy[r]);
@@ -1002,8 +1020,8 @@ __global__ void __launch_bounds__(512, sizeof(Real) == 4 ? 2 : 1) step_kernel(co
                 }
                 __syncthreads();
                 if (P.edge_gather) {
-                    Real *cur = m.xs.p;
-                    m.xs.p = m.alt; m.ys.p = m.alt + 1; m.zs.p = m.alt + 2;
+                    Real *cur = m.pos;
+                    m.pos = m.alt;
                     m.alt = cur;
                 }
             }
@@ -1012,12 +1030,12 @@ __global__ void __launch_bounds__(512, sizeof(Real) == 4 ? 2 : 1) step_kernel(co
         // ---- D. contacts ---------------------------------------------------
         if ((mode & (TS_M_CONTACTS | TS_M_DETECT_ONLY)) && P.F > 0) {
             Cap<Real> *C = m.caps;   // built by threads 0..2 before the substeps
-            Real *rec = m.slx.p;   // 3F records x 7 reals (the slot buffer is free now)
+            Real *rec = m.slot;   // 3F records x 7 reals (the slot buffer is free now)
             for (int f = t; f < P.F; f += B) {
                 const int ia = P.faces[3 * f], ib = P.faces[3 * f + 1], ic = P.faces[3 * f + 2];
-                const Real pa[3] = {m.xs[ia], m.ys[ia], m.zs[ia]};
-                const Real pb[3] = {m.xs[ib], m.ys[ib], m.zs[ib]};
-                const Real pc[3] = {m.xs[ic], m.ys[ic], m.zs[ic]};
+                const Real pa[3] = {m.X(ia), m.Y(ia), m.Z(ia)};
+                const Real pb[3] = {m.X(ib), m.Y(ib), m.Z(ib)};
+                const Real pc[3] = {m.X(ic), m.Y(ic), m.Z(ic)};
 #pragma unroll
                 for (int ci = 0; ci < 3; ++ci) {
                     bool skip = false;
@@ -1064,7 +1082,7 @@ __global__ void __launch_bounds__(512, sizeof(Real) == 4 ? 2 : 1) step_kernel(co
                                 for (int j = 0; j < 3; ++j) {
                                     const int vs = P.faces[3 * f + j];
                                     if (wst[vs] > (Real)0) {
-                                        m.xs[vs] += bj[j] * px; m.ys[vs] += bj[j] * py; m.zs[vs] += bj[j] * pz;
+                                        m.X(vs) += bj[j] * px; m.Y(vs) += bj[j] * py; m.Z(vs) += bj[j] * pz;
                                     }
                                 }
                             }
@@ -1081,7 +1099,7 @@ __global__ void __launch_bounds__(512, sizeof(Real) == 4 ? 2 : 1) step_kernel(co
         // ---- E. divergence guard (solver.py:357-359) ----------------------
         int bad = 0;
         for (int p = t; p < P.Vstore; p += B)
-            bad |= !(isfinite(m.xs[p]) && isfinite(m.ys[p]) && isfinite(m.zs[p]));
+            bad |= !(isfinite(m.X(p)) && isfinite(m.Y(p)) && isfinite(m.Z(p)));
         const int any_bad = __syncthreads_or(bad);
 
         // ---- F. hand the step's results to the epilogue kernel -------------
@@ -1105,7 +1123,7 @@ __global__ void __launch_bounds__(512, sizeof(Real) == 4 ? 2 : 1) step_kernel(co
                         xg[3 * o] = rest[3 * o]; xg[3 * o + 1] = rest[3 * o + 1]; xg[3 * o + 2] = rest[3 * o + 2];
                         vg[3 * o] = 0; vg[3 * o + 1] = 0; vg[3 * o + 2] = 0;
                     } else {
-                        xg[3 * o] = m.xs[p]; xg[3 * o + 1] = m.ys[p]; xg[3 * o + 2] = m.zs[p];
+                        xg[3 * o] = m.X(p); xg[3 * o + 1] = m.Y(p); xg[3 * o + 2] = m.Z(p);
                         vg[3 * o] = vx[r]; vg[3 * o + 1] = vy[r]; vg[3 * o + 2] = vz[r];
                     }
                 }
@@ -1114,7 +1132,7 @@ __global__ void __launch_bounds__(512, sizeof(Real) == 4 ? 2 : 1) step_kernel(co
                 const int o = P.s2o[p];
                 if (o < 0) continue;
                 if (done) { xg[3 * o] = rest[3 * o]; xg[3 * o + 1] = rest[3 * o + 1]; xg[3 * o + 2] = rest[3 * o + 2]; }
-                else if (mode & TS_M_CONTACTS) { xg[3 * o] = m.xs[p]; xg[3 * o + 1] = m.ys[p]; xg[3 * o + 2] = m.zs[p]; }
+                else if (mode & TS_M_CONTACTS) { xg[3 * o] = m.X(p); xg[3 * o + 1] = m.Y(p); xg[3 * o + 2] = m.Z(p); }
                 if (mode & TS_M_SUBSTEPS || done) { vg[3 * o] = 0; vg[3 * o + 1] = 0; vg[3 * o + 2] = 0; }
             }
         }

@@ -13,7 +13,8 @@ def num(x):
         return 0.0
 
 
-def main(rep, top=40):
+def parse(rep):
+    """[(file:line, source text, instructions, stall samples, smem wavefronts)] per CUDA source line."""
     out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source=cuda,sass"],
                          capture_output=True, text=True).stdout
     lines = out.splitlines()
@@ -45,6 +46,23 @@ def main(rep, top=40):
             cur[3] += num(r[i_samp])
             if i_wf is not None:
                 cur[4] += num(r[i_wf])
+    return rows
+
+
+def phases(rep, ranges, fname=""):
+    """Instruction / stall shares of named [first, last) line ranges of one source file."""
+    rows = parse(rep)
+    tot_i = sum(r[2] for r in rows)
+    tot_s = sum(r[3] for r in rows)
+    out = []
+    for name, a, b in ranges:
+        sel = [r for r in rows if r[0].split(":")[0] == fname and a <= int(r[0].split(":")[1]) < b]
+        out.append((name, 100 * sum(r[2] for r in sel) / tot_i, 100 * sum(r[3] for r in sel) / tot_s))
+    return out
+
+
+def main(rep, top=40):
+    rows = parse(rep)
     tot_i = sum(r[2] for r in rows)
     tot_s = sum(r[3] for r in rows)
     print(f"total inst {tot_i:.4g}  samples {tot_s:.4g}")
