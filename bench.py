@@ -6,8 +6,10 @@
 
 A "step" is one EnvBatch.step over all envs of a GPU: tool command, grasp,
 10 substeps of the distance + tet-volume solver, capsule contact, reward /
-done / auto-reset -- ONE launch of the fused sm_100a kernel (plus one launch
-of the on-device uniform(-1,1) action generator).  Envs shard across GPUs
+done / auto-reset -- three stream-ordered launches: the per-env command
+kernel (one thread per env), the fused sm_100a step kernel (one CTA per env)
+and the per-env epilogue kernel, plus the on-device uniform(-1,1) action
+generator.  Envs shard across GPUs
 with no data-path collective ("scaling": "weak"); the global env id indexes
 the action stream so a shard reproduces the single-GPU envs.
 
@@ -19,7 +21,8 @@ e2e    : the same metric through the public API with HOST numpy actions
          (D2H of obs, reward, terminated, truncated) inside the timed region.
 roofline: the binding roofline of this kernel is on-chip shared memory
          (SURVEY.md §8(d)); achieved = 4,191,120 algorithmic B/env-step x envs
-         per launch / step-kernel time, peak = shared-memory bandwidth
+         per launch / step-kernel time (CUDA events around that kernel alone,
+         recorded by the library on its stream), peak = shared-memory bandwidth
          measured on this GPU by ts_smem_probe.  The HBM view is reported
          beside it (roofline_hbm, peak from MEASURED_PEAKS.json).
 cpu_baseline: the unmodified reference (oracle/_ref, compiled backend,
@@ -205,6 +208,8 @@ def run_gpu(args):
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     kstart = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     launches0 = lib.ts_launch_count()
+    handle = env.sim.scene.handle
+    N.check(lib.ts_kernel_timing(handle, 1, args.steps), "ts_kernel_timing")   # events around the step kernel
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
@@ -219,15 +224,19 @@ def run_gpu(args):
         torch.cuda.synchronize(dev)
     launches = lib.ts_launch_count() - launches0
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
-    kern_ms = [s.elapsed_time(e) for s, e in zip(kstart, ends)]
+    envstep_ms = [s.elapsed_time(e) for s, e in zip(kstart, ends)]   # command + step + epilogue kernels
     total_ms = float(np.sum(step_ms))
-    t = torch.tensor([total_ms, float(np.sum(kern_ms))], dtype=torch.float64, device=dev)
+    sk_ms, sk_n = ctypes.c_double(0.0), ctypes.c_int64(0)
+    N.check(lib.ts_kernel_time(handle, ctypes.byref(sk_ms), ctypes.byref(sk_n)), "ts_kernel_time")
+    N.check(lib.ts_kernel_timing(handle, 0, 0), "ts_kernel_timing")
+    assert sk_n.value == args.steps, (sk_n.value, args.steps)
+    t = torch.tensor([total_ms, float(np.sum(envstep_ms)), sk_ms.value], dtype=torch.float64, device=dev)
     if world > 1:
         dist.barrier()
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    total_ms, kern_total_ms = float(t[0]), float(t[1])
+    total_ms, envstep_total_ms, kern_total_ms = float(t[0]), float(t[1]), float(t[2])
     value = world * n * args.steps / (total_ms * 1e-3)
-    kern_avg_ms = kern_total_ms / args.steps
+    kern_avg_ms = kern_total_ms / args.steps     # the fused step kernel alone (CUDA events on its stream)
 
     # ---- end to end through the public API with host buffers -------------
     rng = np.random.default_rng(1000 + rank)
@@ -284,7 +293,9 @@ def run_gpu(args):
                      "frac": achieved / smem_gbs.value, "traffic": traffic,
                      "peak_source": "ts_smem_probe on this GPU (conflict-free LDS.128, all SMs)",
                      "algorithmic_bytes_per_env_step": ALG_BYTES_PER_ENV_STEP,
-                     "kernel_ms": kern_avg_ms},
+                     "kernel": "tsk::step_kernel<float, 1> (fused substeps + grasp + contacts)",
+                     "kernel_ms": kern_avg_ms, "env_step_ms": envstep_total_ms / args.steps,
+                     "envs_per_launch": n},
         "roofline_hbm": {"bound": "hbm", "achieved": hbm_achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                          "frac": hbm_achieved / peaks["hbm_gbs"], "peak_source": peak_src,
                          "algorithmic_bytes_per_env_step": HBM_BYTES_PER_ENV_STEP},

@@ -226,6 +226,14 @@ int32_t ts_smem_probe(int32_t device, int32_t iters, double *gbs_out);
 /* Kernel launches issued by this library since load (for bench accounting). */
 int64_t ts_launch_count(void);
 
+/* Device time of the fused step kernel alone (the roofline's denominator): while enabled, every
+ * step-kernel launch of this handle is bracketed by CUDA events on its own stream (capacity
+ * `max_launches`, further launches are not timed).  ts_kernel_time waits for the recorded
+ * events, returns the summed milliseconds and the number of timed launches, and clears them.
+ * enable = 0 releases the events. */
+int32_t ts_kernel_timing(ts_handle *h, int32_t enable, int32_t max_launches);
+int32_t ts_kernel_time(ts_handle *h, double *total_ms, int64_t *launches);
+
 #ifdef __cplusplus
 }
 #endif

@@ -39,6 +39,8 @@ struct ts_handle {
     int max_grid = 0;   // 0 = one CTA per environment
     TsCmd *cmd = nullptr;   // per-env command blocks (grown on demand)
     int64_t cmd_cap = 0;
+    std::vector<cudaEvent_t> tev;   // step-kernel timing events (pairs), see ts_kernel_timing
+    int64_t tev_used = 0;
 };
 
 extern "C" {
@@ -175,6 +177,7 @@ int32_t ts_destroy(ts_handle *h) {
     if (!h) return TS_OK;
     if (h->dev_blob) cudaFree(h->dev_blob);
     if (h->cmd) cudaFree(h->cmd);
+    for (cudaEvent_t ev : h->tev) cudaEventDestroy(ev);
     delete h;
     return TS_OK;
 }
@@ -209,9 +212,12 @@ static int launch(ts_handle *h, const TsLaunch &L_in, cudaStream_t s) {
     int grid = (int)std::min<int64_t>(L.n_env, h->max_grid > 0 ? h->max_grid : (int64_t)1 << 30);
     cudaError_t e = ts_launch_cmd(h->prog, h->params, L, s);
     if (e != cudaSuccess) return cuda_fail(e, "command kernel launch");
+    const bool timed = 2 * h->tev_used + 1 < (int64_t)h->tev.size();
+    if (timed) cudaEventRecord(h->tev[2 * h->tev_used], s);
     e = h->precision == TS_F64 ? ts_launch_step<double>(h->prog, h->params, L, grid, h->smem, s)
                                : ts_launch_step<float>(h->prog, h->params, L, grid, h->smem, s);
     if (e != cudaSuccess) return cuda_fail(e, "step kernel launch");
+    if (timed) cudaEventRecord(h->tev[2 * h->tev_used++ + 1], s);
     e = ts_launch_epilogue(h->prog, h->params, L, s);
     if (e != cudaSuccess) return cuda_fail(e, "epilogue kernel launch");
     g_launches.fetch_add(3);
@@ -352,6 +358,38 @@ int32_t ts_uniform_actions(double *actions, int64_t num_envs, int64_t first_env,
                                       reinterpret_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return cuda_fail(e, "uniform kernel launch");
     g_launches.fetch_add(1);
+    return TS_OK;
+}
+
+int32_t ts_kernel_timing(ts_handle *h, int32_t enable, int32_t max_launches) {
+    if (!h) return fail(TS_ERR_INVALID, "null argument");
+    for (cudaEvent_t ev : h->tev) cudaEventDestroy(ev);
+    h->tev.clear();
+    h->tev_used = 0;
+    if (!enable) return TS_OK;
+    if (max_launches < 1) return fail(TS_ERR_INVALID, "max_launches must be >= 1");
+    h->tev.resize(2 * (size_t)max_launches);
+    for (auto &ev : h->tev) {
+        cudaError_t e = cudaEventCreate(&ev);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaEventCreate");
+    }
+    return TS_OK;
+}
+
+int32_t ts_kernel_time(ts_handle *h, double *total_ms, int64_t *launches) {
+    if (!h || !total_ms || !launches) return fail(TS_ERR_INVALID, "null argument");
+    double tot = 0.0;
+    for (int64_t i = 0; i < h->tev_used; ++i) {
+        cudaError_t e = cudaEventSynchronize(h->tev[2 * i + 1]);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaEventSynchronize");
+        float ms = 0.0f;
+        e = cudaEventElapsedTime(&ms, h->tev[2 * i], h->tev[2 * i + 1]);
+        if (e != cudaSuccess) return cuda_fail(e, "cudaEventElapsedTime");
+        tot += ms;
+    }
+    *total_ms = tot;
+    *launches = h->tev_used;
+    h->tev_used = 0;
     return TS_OK;
 }
 
