@@ -95,6 +95,8 @@ typedef struct ts_layout_opts {
     int32_t compact;            /* 16-bit item streams when possible (default), -1 = off */
     int32_t edge_gather;        /* 1 = distance constraints gathered by the owner of each free vertex,
                                    -1 = constraint-parallel phase 1 + slots, 0 = auto (fp32 gather) */
+    int32_t cluster_size;       /* CTAs per environment: 0 = auto (one CTA when the mesh fits, else the
+                                   smallest thread-block cluster that holds it), 1 = one CTA, 2..16 */
 } ts_layout_opts;
 
 typedef struct ts_layout_info {
@@ -105,6 +107,8 @@ typedef struct ts_layout_info {
     int32_t compact;            /* 1 when the program uses the 16-bit item streams */
     int32_t edge_gather;        /* 1 when distance constraints are owner-gathered */
     int32_t n_edge_incidences;  /* (edge, free endpoint) records of the owner gather */
+    int32_t slot_budget;        /* slot budget per chunk the compiler used */
+    int32_t cluster_size;       /* CTAs per environment (1, or the thread-block cluster size) */
     int64_t program_bytes;
 } ts_layout_info;
 

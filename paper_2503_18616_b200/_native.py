@@ -48,7 +48,7 @@ class SceneDesc(ctypes.Structure):
 class LayoutOpts(ctypes.Structure):
     _fields_ = [("precision", _I32), ("block_threads", _I32), ("max_chunk_slots", _I32),
                 ("schedule_banks", _I32), ("smem_budget", _I32), ("compact", _I32),
-                ("edge_gather", _I32)]
+                ("edge_gather", _I32), ("cluster_size", _I32)]
 
 
 class LayoutInfo(ctypes.Structure):
@@ -57,6 +57,7 @@ class LayoutInfo(ctypes.Structure):
                 ("smem_bytes", _I32), ("n_edge_items", _I32), ("n_tet_items", _I32),
                 ("n_att_items", _I32), ("n_slots_total", _I32), ("bank_conflicts_p1", _I32),
                 ("compact", _I32), ("edge_gather", _I32), ("n_edge_incidences", _I32),
+                ("slot_budget", _I32), ("cluster_size", _I32),
                 ("program_bytes", _I64)]
 
     def as_dict(self):

@@ -56,10 +56,12 @@ class _AttSpec:
 
 
 def _scene_for(w, edges, rest_len, ks, tets, rest_vol, kv, att_vertex, att_faces, att_is_face,
-               att_anchor, att_rest, att_k, precision, faces=None, iters=8):
+               att_anchor, att_rest, att_k, precision, faces=None, iters=8, layout=None):
+    layout = dict(layout or {})
     key = _key(w, edges, rest_len, tets, rest_vol, att_vertex, att_faces, att_is_face, att_anchor,
                att_rest, att_k, faces if faces is not None else np.zeros(0),
-               extra=(float(ks), float(kv), precision, int(iters), torch.cuda.current_device()))
+               extra=(float(ks), float(kv), precision, int(iters), torch.cuda.current_device(),
+                      sorted(layout.items())))
     sc = _CACHE.get(key)
     if sc is not None:
         return sc
@@ -76,7 +78,7 @@ def _scene_for(w, edges, rest_len, ks, tets, rest_vol, kv, att_vertex, att_faces
                       np.zeros((0, 3), np.int32) if faces is None else faces, cfg,
                       attachments=atts, surface_faces=att_faces if len(atts) else None,
                       contact_iterations=iters)
-    sc = DeviceScene(arr, torch.cuda.current_device(), precision=precision)
+    sc = DeviceScene(arr, torch.cuda.current_device(), precision=precision, **layout)
     if len(_CACHE) > 32:
         _CACHE.clear()
     _CACHE[key] = sc
@@ -86,7 +88,7 @@ def _scene_for(w, edges, rest_len, ks, tets, rest_vol, kv, att_vertex, att_faces
 def run_substeps(x, v, w, edges, rest_len, ks, tets, rest_vol, kv,
                  att_vertex, att_faces, att_is_face, att_anchor, att_rest, att_k,
                  grasp_vertex, drag_points, g, h, substeps, damping,
-                 acc=None, cnt=None, threads=1, parallel=False, scratch=None):
+                 acc=None, cnt=None, threads=1, parallel=False, scratch=None, *, layout=None):
     """In place on x, v (N, V, 3).  Same arguments as _kernels.run_substeps (_kernels.pyx:577-585)."""
     x_np, v_np = x, v
     if x_np.dtype not in (np.float32, np.float64):
@@ -96,7 +98,7 @@ def run_substeps(x, v, w, edges, rest_len, ks, tets, rest_vol, kv,
     if n_env == 0 or n_vert == 0:
         return None
     sc = _scene_for(np.asarray(w, np.float64), edges, rest_len, ks, tets, rest_vol, kv, att_vertex,
-                    att_faces, att_is_face, att_anchor, att_rest, att_k, precision)
+                    att_faces, att_is_face, att_anchor, att_rest, att_k, precision, layout=layout)
     dev = torch.device("cuda", torch.cuda.current_device())
     xt = torch.as_tensor(np.ascontiguousarray(x_np), device=dev)
     vt = torch.as_tensor(np.ascontiguousarray(v_np), device=dev)
@@ -111,7 +113,7 @@ def run_substeps(x, v, w, edges, rest_len, ks, tets, rest_vol, kv,
     return None
 
 
-def detect_contacts(pos, faces, caps, iters=8):
+def detect_contacts(pos, faces, caps, iters=8, *, layout=None):
     """Contacts of one position set (V, 3) against capsule rows (C, 7), capsule-major order."""
     pos = np.ascontiguousarray(pos, np.float64)
     faces = np.ascontiguousarray(faces, np.int32).reshape(-1, 3)
@@ -130,7 +132,7 @@ def detect_contacts(pos, faces, caps, iters=8):
     rows[:nc] = caps
     sc = _scene_for(np.ones(nv), np.zeros((0, 2), np.int32), np.zeros(0), 1.0, np.zeros((0, 4), np.int32),
                     np.zeros(0), 1.0, np.zeros(0, np.int32), np.zeros((0, 3), np.int32), np.zeros(0, np.uint8),
-                    np.zeros((0, 3)), np.zeros(0), np.zeros(0), "fp64", faces=faces, iters=iters)
+                    np.zeros((0, 3)), np.zeros(0), np.zeros(0), "fp64", faces=faces, iters=iters, layout=layout)
     dev = torch.device("cuda", torch.cuda.current_device())
     x = torch.as_tensor(pos[None], device=dev)
     c = torch.as_tensor(rows[None], device=dev)

@@ -6,12 +6,8 @@
 #include <vector>
 
 #include "../../include/tissuesim_b200.h"
+#include "compiler.h"
 #include "step_common.h"
-
-namespace ts {
-int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector<uint8_t> &blob,
-                    ts_layout_info &info, std::string &err);
-}
 
 namespace {
 thread_local std::string g_err;
@@ -41,6 +37,9 @@ struct ts_handle {
     int64_t cmd_cap = 0;
     std::vector<cudaEvent_t> tev;   // step-kernel timing events (pairs), see ts_kernel_timing
     int64_t tev_used = 0;
+    int cluster_k = 1;                  // > 1: thread-block cluster program (large meshes)
+    std::vector<TsDevProg> parts;       // decoded part programs (host copies)
+    TsDevProg *dev_parts = nullptr;     // the same, on the device (cluster kernel argument)
 };
 
 extern "C" {
@@ -55,6 +54,19 @@ static ts_layout_opts default_opts() {
     return o;
 }
 
+// One CTA per env when the mesh fits (or cluster_size == 1), else a K-CTA cluster program.
+static int compile_any(const ts_scene_desc &d, const ts_layout_opts &o, std::vector<uint8_t> &blob,
+                       ts_layout_info &inf, std::string &err) {
+    if (o.cluster_size >= 2) return ts::compile_cluster(d, o, o.cluster_size, blob, inf, err);
+    int rc = ts::compile_program(d, o, blob, inf, err);
+    if (rc == TS_ERR_UNSUPPORTED && o.cluster_size == 0) {
+        std::string e2;
+        rc = ts::compile_cluster(d, o, 0, blob, inf, e2);
+        if (rc != TS_OK) err += "; " + e2;
+    }
+    return rc;
+}
+
 int32_t ts_compile_program(const ts_scene_desc *desc, const ts_layout_opts *opts, void *buf, int64_t *bytes,
                            ts_layout_info *info) {
     if (!desc || !bytes) return fail(TS_ERR_INVALID, "null argument");
@@ -62,7 +74,7 @@ int32_t ts_compile_program(const ts_scene_desc *desc, const ts_layout_opts *opts
     std::vector<uint8_t> blob;
     ts_layout_info inf;
     std::string err;
-    int rc = ts::compile_program(*desc, o, blob, inf, err);
+    int rc = compile_any(*desc, o, blob, inf, err);
     if (rc != TS_OK) return fail(rc, err);
     if (info) *info = inf;
     if (buf) {
@@ -76,10 +88,8 @@ int32_t ts_compile_program(const ts_scene_desc *desc, const ts_layout_opts *opts
     return TS_OK;
 }
 
-static void decode(ts_handle *h) {
-    const TsProgHeader *H = reinterpret_cast<const TsProgHeader *>(h->host_blob.data());
-    const uint8_t *b = reinterpret_cast<const uint8_t *>(h->dev_blob);
-    TsDevProg &P = h->prog;
+static void decode_part(const uint8_t *host, const uint8_t *b, TsDevProg &P) {
+    const TsProgHeader *H = reinterpret_cast<const TsProgHeader *>(host);
     P.V = H->V; P.Vf = H->Vf; P.Vf_pad = H->Vf_pad; P.Vstore = H->Vstore;
     P.F = H->F; P.B = H->B; P.VPT = H->VPT; P.G = H->G;
     P.n_chunks = H->n_chunks; P.grasp_chunk = H->grasp_chunk; P.slot_cap = H->slot_capacity;
@@ -113,6 +123,11 @@ static void decode(ts_handle *h) {
     P.einc = b + H->off[TS_SEC_EINC];
     P.eregion = reinterpret_cast<const int32_t *>(b + H->off[TS_SEC_EREGION]);
     P.evalence = reinterpret_cast<const int32_t *>(b + H->off[TS_SEC_EVAL]);
+    P.face_gid = reinterpret_cast<const int32_t *>(b + H->off[TS_SEC_FACE_GID]);
+    P.Vown = H->Vown; P.cluster_k = H->cluster_k; P.cluster_rank = H->cluster_rank;
+    P.send_off = reinterpret_cast<const int32_t *>(b + H->off[TS_SEC_SEND_OFF]);
+    P.send = reinterpret_cast<const int32_t *>(b + H->off[TS_SEC_SEND]);
+    P.face_own = reinterpret_cast<const int32_t *>(b + H->off[TS_SEC_FACE_OWN]);
 }
 
 static void fill_params(const ts_scene_desc &d, TsParams &S) {
@@ -135,6 +150,7 @@ static void fill_params(const ts_scene_desc &d, TsParams &S) {
     S.action_scale = d.action_scale; S.success_thr = d.success_threshold;
     S.w_l = d.w_distance; S.w_d = d.w_delta; S.w_s = d.w_success; S.reward_scale = d.reward_scale;
     S.max_steps = d.max_episode_steps; S.start_distance = d.start_distance;
+    S.n_face = d.n_face;
     ts_finish_params(S);
 }
 
@@ -147,7 +163,7 @@ int32_t ts_create(const ts_scene_desc *desc, const ts_layout_opts *opts, int32_t
     h->device = device;
     h->precision = o.precision;
     std::string err;
-    int rc = ts::compile_program(*desc, o, h->host_blob, h->info, err);
+    int rc = compile_any(*desc, o, h->host_blob, h->info, err);
     if (rc != TS_OK) { delete h; return fail(rc, err); }
     cudaError_t e = cudaSetDevice(device);
     if (e != cudaSuccess) { delete h; return cuda_fail(e, "cudaSetDevice"); }
@@ -155,10 +171,26 @@ int32_t ts_create(const ts_scene_desc *desc, const ts_layout_opts *opts, int32_t
     if (e != cudaSuccess) { delete h; return cuda_fail(e, "cudaMalloc(program)"); }
     e = cudaMemcpy(h->dev_blob, h->host_blob.data(), h->host_blob.size(), cudaMemcpyHostToDevice);
     if (e != cudaSuccess) { cudaFree(h->dev_blob); delete h; return cuda_fail(e, "cudaMemcpy(program)"); }
-    decode(h);
-    fill_params(*desc, h->params);
+    const uint8_t *hb = h->host_blob.data();
+    const uint8_t *db = reinterpret_cast<const uint8_t *>(h->dev_blob);
     const int R = o.precision == TS_F64 ? 8 : 4;
-    h->smem = ts_smem_bytes(h->prog, R);
+    if (reinterpret_cast<const TsClusterHeader *>(hb)->magic == TS_CLUSTER_MAGIC) {
+        const TsClusterHeader *CH = reinterpret_cast<const TsClusterHeader *>(hb);
+        h->cluster_k = CH->K;
+        h->parts.resize(CH->K);
+        for (int r = 0; r < CH->K; ++r) decode_part(hb + CH->part_off[r], db + CH->part_off[r], h->parts[r]);
+        h->prog = h->parts[0];
+        h->smem = 0;
+        for (int r = 0; r < CH->K; ++r) h->smem = std::max(h->smem, ts_smem_bytes(h->parts[r], R));
+        e = cudaMalloc(&h->dev_parts, sizeof(TsDevProg) * CH->K);
+        if (e == cudaSuccess)
+            e = cudaMemcpy(h->dev_parts, h->parts.data(), sizeof(TsDevProg) * CH->K, cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) { cudaFree(h->dev_blob); delete h; return cuda_fail(e, "cluster programs"); }
+    } else {
+        decode_part(hb, db, h->prog);
+        h->smem = ts_smem_bytes(h->prog, R);
+    }
+    fill_params(*desc, h->params);
     int max_smem = 0;
     cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
     if (h->smem > max_smem) {
@@ -177,6 +209,7 @@ int32_t ts_destroy(ts_handle *h) {
     if (!h) return TS_OK;
     if (h->dev_blob) cudaFree(h->dev_blob);
     if (h->cmd) cudaFree(h->cmd);
+    if (h->dev_parts) cudaFree(h->dev_parts);
     for (cudaEvent_t ev : h->tev) cudaEventDestroy(ev);
     delete h;
     return TS_OK;
@@ -214,8 +247,15 @@ static int launch(ts_handle *h, const TsLaunch &L_in, cudaStream_t s) {
     if (e != cudaSuccess) return cuda_fail(e, "command kernel launch");
     const bool timed = 2 * h->tev_used + 1 < (int64_t)h->tev.size();
     if (timed) cudaEventRecord(h->tev[2 * h->tev_used], s);
-    e = h->precision == TS_F64 ? ts_launch_step<double>(h->prog, h->params, L, grid, h->smem, s)
-                               : ts_launch_step<float>(h->prog, h->params, L, grid, h->smem, s);
+    if (h->cluster_k > 1)
+        e = h->precision == TS_F64
+                ? ts_launch_cluster_step<double>(h->dev_parts, h->prog.VPT, h->cluster_k, h->prog.B, h->params, L,
+                                                 grid, h->smem, s)
+                : ts_launch_cluster_step<float>(h->dev_parts, h->prog.VPT, h->cluster_k, h->prog.B, h->params, L,
+                                                grid, h->smem, s);
+    else
+        e = h->precision == TS_F64 ? ts_launch_step<double>(h->prog, h->params, L, grid, h->smem, s)
+                                   : ts_launch_step<float>(h->prog, h->params, L, grid, h->smem, s);
     if (e != cudaSuccess) return cuda_fail(e, "step kernel launch");
     if (timed) cudaEventRecord(h->tev[2 * h->tev_used++ + 1], s);
     e = ts_launch_epilogue(h->prog, h->params, L, s);

@@ -27,6 +27,7 @@
 #include <vector>
 
 #include "../../include/tissuesim_b200.h"
+#include "compiler.h"
 #include "program.h"
 
 namespace ts {
@@ -45,6 +46,9 @@ struct Item {
 };
 
 inline int roundup(int x, int m) { return (x + m - 1) / m * m; }
+
+// effort of the bank-conflict searches (cluster parts compile K programs twice: a tenth)
+thread_local double g_search_effort = 1.0;
 
 template <typename T>
 void put(std::vector<uint8_t> &blob, int64_t off, const std::vector<T> &v) {
@@ -78,7 +82,7 @@ void local_search(std::vector<Item> &s, int bank_mod) {
     for (int sb = 0; sb < nsb; ++sb) { cost[sb] = sb_cost(sb); total += cost[sb]; }
     uint64_t rng = 0x9E3779B97F4A7C15ull;
     auto next = [&]() { rng ^= rng << 13; rng ^= rng >> 7; rng ^= rng << 17; return rng; };
-    const long iters = std::min<long>(400000L, 200L * n);
+    const long iters = (long)(g_search_effort * std::min<long>(400000L, 200L * n));
     for (long it = 0; it < iters && total > 0; ++it) {
         // pick a position in a costly sub-batch and a random partner elsewhere
         int i = (int)(next() % n), j = (int)(next() % n);
@@ -210,7 +214,7 @@ struct ListRef { std::vector<Item> *items; int begin, count; };
 // Deterministic (fixed-seed xorshift).  Slots are assigned afterwards from the
 // final positions, so the per-vertex summation order is untouched.
 void bank_refine(const std::vector<ListRef> &lists, std::vector<int> &o2s, std::vector<int> &s2o, int Vf,
-                 int Vf_pad, int bank_mod, bool permute_tets) {
+                 int Vf_pad, int Vown, int bank_mod, bool permute_tets) {
     struct Ref { int list, idx; };
     std::vector<Ref> items;                 // global item id -> (list, index)
     std::vector<int> sb_of, list_sb0;
@@ -259,10 +263,12 @@ void bank_refine(const std::vector<ListRef> &lists, std::vector<int> &o2s, std::
     uint64_t rng = 0x2545F4914F6CDD1Dull;
     auto next = [&]() { rng ^= rng << 13; rng ^= rng >> 7; rng ^= rng << 17; return rng; };
     auto unif = [&]() { return (double)(next() >> 11) * (1.0 / 9007199254740992.0); };
-    const int n_pinned = (int)std::count_if(s2o.begin() + Vf_pad, s2o.end(), [](int v) { return v >= 0; });
+    // pools a vertex may move in: its warp group (free), the owned pinned block, the halo block
+    const int n_pinned = (int)std::count_if(s2o.begin() + Vf_pad, s2o.begin() + Vown, [](int v) { return v >= 0; });
+    const int n_halo = (int)std::count_if(s2o.begin() + Vown, s2o.end(), [](int v) { return v >= 0; });
     std::vector<int> touched;
     auto collect = [&](int sb) { if (std::find(touched.begin(), touched.end(), sb) == touched.end()) touched.push_back(sb); };
-    long iters = std::min<long>(600000L, 150L * n);
+    long iters = (long)(g_search_effort * std::min<long>(600000L, 150L * n));
     if (const char *env = std::getenv("TS_REFINE_ITERS")) iters = std::atol(env);
     const double T0 = 1.5, T1 = 0.05;
     // best state seen (the schedule lists, the vertex positions)
@@ -300,9 +306,12 @@ void bank_refine(const std::vector<ListRef> &lists, std::vector<int> &o2s, std::
                 const int g = pu / 32;
                 const int hi = std::min(Vf, 32 * g + 32);
                 pv = 32 * g + (int)(next() % (hi - 32 * g));
-            } else {
+            } else if (pu < Vown) {
                 if (n_pinned < 2) continue;
                 pv = Vf_pad + (int)(next() % n_pinned);
+            } else {
+                if (n_halo < 2) continue;
+                pv = Vown + (int)(next() % n_halo);
             }
             v = s2o[pv];
             if (v < 0 || v == u || bank(u) == bank(v)) continue;
@@ -507,7 +516,9 @@ struct Real4T { Real x, y, z, w; };
 }  // namespace
 
 int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector<uint8_t> &blob,
-                    ts_layout_info &info, std::string &err) {
+                    ts_layout_info &info, std::string &err, const PartSpec *part) {
+    if (part && (int)part->own.size() != d.n_vert) { err = "part ownership mask size"; return TS_ERR_INVALID; }
+    g_search_effort = part ? 0.1 : 1.0;
     const int V = d.n_vert, E = d.n_edge, T = d.n_tet, F = d.n_face, A = d.n_att;
     const int prec = o.precision;
     if (prec != TS_F32 && prec != TS_F64) { err = "precision must be TS_F32 or TS_F64"; return TS_ERR_INVALID; }
@@ -525,12 +536,16 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
     }
     const double *w = d.inverse_mass;
     auto is_free = [&](int v) { return w[v] > 0.0; };
+    // cluster part: this CTA of the env's cluster owns (updates, writes back) part->own vertices
+    // and reads a halo of other parts' vertices, refreshed over DSMEM every substep
+    auto own = [&](int v) { return !part || part->own[v] != 0; };
+    auto own_free = [&](int v) { return is_free(v) && own(v); };
 
     // edge_gather: distance constraints are gathered by the owner thread of each free vertex
     // (no phase-1 items, no slots); only attachments and tets go through slots
     // (default for fp32; fp64 keeps slots: measured on B200, 4096 envs, reach_1170:
     // fp32 0.867 vs 0.949 ms/step, fp64 4.47 vs 3.83 ms/step)
-    const bool eg = o.edge_gather > 0 || (o.edge_gather == 0 && o.precision == TS_F32);
+    const bool eg = part || o.edge_gather > 0 || (o.edge_gather == 0 && o.precision == TS_F32);
 
     // ---- live constraints and per-vertex incidence counts ---------------
     std::vector<int> inc(V, 0), inc_e(V, 0);
@@ -559,9 +574,48 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
         if (any) for (int k = 0; k < 4; ++k) inc[q[k]] += is_free(q[k]);
     }
 
+    // ---- local vertex set (parts: owned + halo) ---------------------------
+    std::vector<char> local(V, part ? 0 : 1);
+    auto local_tet = [&](int t) {
+        if (!tet_live[t]) return false;
+        if (!part) return true;
+        for (int k = 0; k < 4; ++k) if (own_free(d.tets[4 * t + k])) return true;
+        return false;
+    };
+    auto local_edge = [&](int e) {
+        return edge_live[e] && (!part || own_free(d.edges[2 * e]) || own_free(d.edges[2 * e + 1]));
+    };
+    auto local_att = [&](int i) {
+        if (!att_live[i]) return false;
+        if (!part || own_free(d.att_vertex[i])) return true;
+        if (d.att_is_face[i]) for (int k = 0; k < 3; ++k) if (own_free(d.att_faces[3 * i + k])) return true;
+        return false;
+    };
+    std::vector<int> faces_local;
+    if (part) {
+        for (int v = 0; v < V; ++v) if (own(v)) local[v] = 1;
+        for (int e = 0; e < E; ++e) if (local_edge(e)) local[d.edges[2 * e]] = local[d.edges[2 * e + 1]] = 1;
+        for (int t = 0; t < T; ++t) if (local_tet(t)) for (int k = 0; k < 4; ++k) local[d.tets[4 * t + k]] = 1;
+        for (int i = 0; i < A; ++i) if (local_att(i)) {
+            local[d.att_vertex[i]] = 1;
+            if (d.att_is_face[i]) for (int k = 0; k < 3; ++k) local[d.att_faces[3 * i + k]] = 1;
+        }
+        faces_local = part->faces;
+        for (int f : faces_local) for (int k = 0; k < 3; ++k) local[d.faces[3 * f + k]] = 1;
+    } else {
+        faces_local.resize(F);
+        std::iota(faces_local.begin(), faces_local.end(), 0);
+    }
+    const int Floc = (int)faces_local.size();
+
     // ---- storage order -------------------------------------------------
-    std::vector<int> free_v, pinned_v;
-    for (int v = 0; v < V; ++v) (is_free(v) ? free_v : pinned_v).push_back(v);
+    // [owned free (cost-sorted) | pad | owned pinned | pad | halo (other parts' vertices) | pad]
+    std::vector<int> free_v, pinned_v, halo_v;
+    for (int v = 0; v < V; ++v) {
+        if (!local[v]) continue;
+        if (!own(v)) halo_v.push_back(v);
+        else (is_free(v) ? free_v : pinned_v).push_back(v);
+    }
     // warps own vertices of similar per-substep gather cost: an owner-gathered edge costs about
     // three slot reads (it recomputes the correction), a slot one
     std::vector<int> cost(V);
@@ -569,15 +623,22 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
     std::stable_sort(free_v.begin(), free_v.end(), [&](int a, int b) { return cost[a] > cost[b]; });
     const int Vf = (int)free_v.size();
     const int Vf_pad = roundup(Vf, 32);
-    const int Vstore = Vf_pad + roundup((int)pinned_v.size(), 32);
+    const int Vown = Vf_pad + roundup((int)pinned_v.size(), 32);
+    int Vstore = Vown + roundup((int)halo_v.size(), 32);
+    if (part && part->force_Vstore) {
+        if (part->force_Vstore < Vstore) { err = "forced Vstore too small"; return TS_ERR_INVALID; }
+        Vstore = part->force_Vstore;
+    }
     std::vector<int> s2o(Vstore, -1), o2s(V, -1);
     for (int i = 0; i < Vf; ++i) { s2o[i] = free_v[i]; o2s[free_v[i]] = i; }
     for (size_t i = 0; i < pinned_v.size(); ++i) { s2o[Vf_pad + i] = pinned_v[i]; o2s[pinned_v[i]] = Vf_pad + (int)i; }
+    for (size_t i = 0; i < halo_v.size(); ++i) { s2o[Vown + i] = halo_v[i]; o2s[halo_v[i]] = Vown + (int)i; }
 
     // fp32: one thread per free vertex (3 CTAs/SM fit); fp64 runs 1 CTA/SM (shared memory), so it
     // takes 1.5x the threads to widen phase 1 (measured on B200: 3.81 vs 4.30 ms at 4096 envs)
     int B = o.block_threads > 0 ? o.block_threads
                                 : std::min(512, std::max(64, R == 8 ? roundup(Vf_pad * 3 / 2, 32) : Vf_pad));
+    if (part && part->force_B) B = part->force_B;
     if (B % 32 != 0 || B < 32 || B > 512) { err = "block_threads must be a multiple of 32 in [32, 512]"; return TS_ERR_INVALID; }
     const int VPT = std::max(1, (Vf_pad + B - 1) / B);
     if (VPT > 8) { err = "mesh too large for one CTA per environment (more than 8 vertices per thread)"; return TS_ERR_UNSUPPORTED; }
@@ -586,13 +647,13 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
     // ---- items per kind (constraint index order) -----------------------
     auto P = [&](int v) { return o2s[v]; };
     std::vector<Item> kinds[3];
-    for (int e = 0; e < E; ++e) if (edge_live[e]) {
+    for (int e = 0; e < E; ++e) if (local_edge(e)) {
         Item it{}; it.kind = TS_CHUNK_EDGE; it.index = e; it.nroles = 2;
         it.vid[0] = d.edges[2 * e]; it.vid[1] = d.edges[2 * e + 1];
         it.pos[0] = P(it.vid[0]); it.pos[1] = P(it.vid[1]);
         kinds[0].push_back(it);
     }
-    for (int i = 0; i < A; ++i) if (att_live[i]) {
+    for (int i = 0; i < A; ++i) if (local_att(i)) {
         Item it{}; it.kind = TS_CHUNK_ATT; it.index = i;
         it.vid[0] = d.att_vertex[i];
         it.pos[0] = P(it.vid[0]);
@@ -602,7 +663,7 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
         } else it.nroles = 1;
         kinds[1].push_back(it);
     }
-    for (int t = 0; t < T; ++t) if (tet_live[t]) {
+    for (int t = 0; t < T; ++t) if (local_tet(t)) {
         Item it{}; it.kind = TS_CHUNK_TET; it.index = t; it.nroles = 4;
         for (int k = 0; k < 4; ++k) { it.vid[k] = d.tets[4 * t + k]; it.pos[k] = P(it.vid[k]); }
         kinds[2].push_back(it);
@@ -615,7 +676,17 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
     // into the chunk where the edges end, after each vertex's edge slots.
     std::vector<Item> seq;
     for (int k = eg ? 1 : 0; k < 3; ++k) seq.insert(seq.end(), kinds[k].begin(), kinds[k].end());
-    const int budget = o.max_chunk_slots > 0 ? o.max_chunk_slots : (1 << 30);
+    // slot budget per chunk: explicit, or what the CTA's shared memory leaves next to the positions
+    int budget = o.max_chunk_slots > 0 ? o.max_chunk_slots : (1 << 30);
+    if (o.max_chunk_slots <= 0) {
+        const int fixed = ts_smem_layout_bytes(Vstore, 0, Vf_pad, Floc, R, eg ? 1 : 0);
+        const int avail = (TS_SMEM_LIMIT - fixed) / (3 * R) - 32;    // minus the 32 trash slots
+        if (avail < 7 * Floc || avail < 64) {
+            err = "mesh too large for one CTA per environment (shared memory); use a cluster program";
+            return TS_ERR_UNSUPPORTED;
+        }
+        budget = avail;
+    }
     struct ChunkBuild { std::vector<Item> items; std::vector<int> val; std::vector<int> kmax; int padded; };
     std::vector<ChunkBuild> chunks;
     {
@@ -700,7 +771,7 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
             if (chunk_rec[c].edge_count) lists.push_back({&all_items[0], chunk_rec[c].edge_begin, chunk_rec[c].edge_count});
             if (chunk_rec[c].tet_count) lists.push_back({&all_items[2], chunk_rec[c].tet_begin, chunk_rec[c].tet_count});
         }
-        bank_refine(lists, o2s, s2o, Vf, Vf_pad, bank_mod, /*permute_tets=*/R == 4);
+        bank_refine(lists, o2s, s2o, Vf, Vf_pad, Vown, bank_mod, /*permute_tets=*/R == 4);
         // edges: exact conflict-free batches by bipartite edge colouring (with the final positions)
         std::vector<Item> edges_out;
         for (int c = 0; c < n_chunks; ++c) {
@@ -778,8 +849,12 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
         }
     }
     // contact records reuse the slot buffer: 3F records x 7 reals <= 3 arrays x S reals
-    slot_cap = std::max(slot_cap, 7 * F);
+    slot_cap = std::max(slot_cap, 7 * Floc);
     slot_cap = roundup(std::max(slot_cap, 32), 32);
+    if (part && part->force_slot_cap) {
+        if (part->force_slot_cap < slot_cap) { err = "forced slot capacity too small"; return TS_ERR_INVALID; }
+        slot_cap = part->force_slot_cap;
+    }
 
     // ---- emit --------------------------------------------------------------
     const int nE = (int)all_items[0].size(), nA = (int)all_items[1].size(), nT = (int)all_items[2].size();
@@ -830,8 +905,12 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
     }
     std::vector<double> wst(Vstore, 0.0);
     for (int p = 0; p < Vstore; ++p) if (s2o[p] >= 0) wst[p] = w[s2o[p]];
-    std::vector<int32_t> faces_s(3 * (size_t)F), faces_o(3 * (size_t)F);
-    for (int i = 0; i < 3 * F; ++i) { faces_o[i] = d.faces[i]; faces_s[i] = o2s[d.faces[i]]; }
+    std::vector<int32_t> faces_s(3 * (size_t)Floc), faces_o(3 * (size_t)Floc), face_gid(Floc);
+    for (int i = 0; i < Floc; ++i) {
+        const int f = faces_local[i];
+        face_gid[i] = f;
+        for (int k = 0; k < 3; ++k) { faces_o[3 * i + k] = d.faces[3 * f + k]; faces_s[3 * i + k] = o2s[d.faces[3 * f + k]]; }
+    }
     std::vector<double> rest(3 * (size_t)V);
     for (int i = 0; i < 3 * V; ++i) rest[i] = d.positions_rest[i];
 
@@ -880,8 +959,8 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
         for (int e = 0; e < E; ++e) {
             if (!edge_live[e]) continue;
             const int a = d.edges[2 * e], b = d.edges[2 * e + 1];
-            if (is_free(a)) lists[o2s[a]].push_back(e);
-            if (is_free(b)) lists[o2s[b]].push_back(e);
+            if (own_free(a)) lists[o2s[a]].push_back(e);
+            if (own_free(b)) lists[o2s[b]].push_back(e);
         }
         int base = 0;
         for (int g = 0; g < G; ++g) {
@@ -900,7 +979,9 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
                 const int e = lists[p][k];
                 const int a = d.edges[2 * e], b = d.edges[2 * e + 1];
                 const int q = a == self ? b : a;
-                const int32_t nbr = o2s[q];
+                // bit 31: the neighbour is pinned (w = 0); with uniform free mass that fixes the
+                // weight ratio (compact fp32 records), and halo neighbours of a cluster part are free
+                const int32_t nbr = o2s[q] | (is_free(q) ? 0 : (int32_t)0x80000000u);
                 uint8_t *rec = einc.data() + (size_t)(eregion[p / 32] + 32 * k + p % 32) * einc_bytes;
                 std::memcpy(rec, &nbr, 4);
                 const double rl = d.rest_length[e];
@@ -916,6 +997,22 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
                     std::memcpy(rec + 8, &f, 4);
                 }
             }
+        }
+    }
+
+    // ---- cluster part: halo sends and face-vertex owners ----------------------
+    std::vector<int32_t> send_off, send, face_own;
+    if (part && part->halo_of) {
+        send_off.assign(Vf_pad + 1, 0);
+        for (int p = 0; p < Vf_pad; ++p) {
+            if (p < Vf)
+                for (const auto &rp : (*part->halo_of)[s2o[p]]) send.push_back((rp.first << 20) | rp.second);
+            send_off[p + 1] = (int32_t)send.size();
+        }
+        face_own.assign(3 * (size_t)Floc, -1);
+        for (int i = 0; i < 3 * Floc; ++i) {
+            const int v = faces_o[i];
+            if (is_free(v)) face_own[i] = ((*part->owner_rank)[v] << 20) | (*part->owner_pos)[v];
         }
     }
 
@@ -937,8 +1034,8 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
     sz[TS_SEC_S2O] = 4LL * Vstore;
     sz[TS_SEC_O2S] = 4LL * V;
     sz[TS_SEC_W] = (int64_t)R * Vstore;
-    sz[TS_SEC_FACES] = 12LL * F;
-    sz[TS_SEC_FACES_ORIG] = 12LL * F;
+    sz[TS_SEC_FACES] = 12LL * Floc;
+    sz[TS_SEC_FACES_ORIG] = 12LL * Floc;
     sz[TS_SEC_REST] = 3LL * R * V;
     sz[TS_SEC_GSPLIT] = 4LL * Vf_pad;
     sz[TS_SEC_EDGE_C] = 4LL * edge_c.size();
@@ -946,12 +1043,17 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
     sz[TS_SEC_EINC] = (int64_t)einc.size();
     sz[TS_SEC_EREGION] = 4LL * eregion.size();
     sz[TS_SEC_EVAL] = 4LL * evalence.size();
+    sz[TS_SEC_FACE_GID] = 4LL * face_gid.size();
+    sz[TS_SEC_SEND_OFF] = 4LL * send_off.size();
+    sz[TS_SEC_SEND] = 4LL * send.size();
+    sz[TS_SEC_FACE_OWN] = 4LL * face_own.size();
     TsProgHeader hdr{};
     hdr.compact = compact ? 1 : 0;
     hdr.w_free = w_free;
     hdr.magic = TS_PROG_MAGIC; hdr.version = TS_PROG_VERSION; hdr.real_bytes = R; hdr.n_sections = TS_SEC_COUNT;
     hdr.V = V; hdr.Vf = Vf; hdr.Vf_pad = Vf_pad; hdr.Vstore = Vstore;
-    hdr.F = F; hdr.B = B; hdr.VPT = VPT; hdr.G = G;
+    hdr.F = Floc; hdr.B = B; hdr.VPT = VPT; hdr.G = G;
+    hdr.Vown = Vown; hdr.cluster_k = part ? part->K : 1; hdr.cluster_rank = part ? part->rank : 0;
     hdr.n_chunks = n_chunks; hdr.grasp_chunk = grasp_chunk; hdr.slot_capacity = slot_cap; hdr.n_att = nA;
     hdr.n_edge_items = nE; hdr.n_tet_items = nT; hdr.n_att_items = nA; hdr.bank_conflicts = total_conf;
     hdr.n_slots_total = n_slots_total;
@@ -980,6 +1082,10 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
     put(blob, hdr.off[TS_SEC_EINC], einc);
     put(blob, hdr.off[TS_SEC_EREGION], eregion);
     put(blob, hdr.off[TS_SEC_EVAL], evalence);
+    put(blob, hdr.off[TS_SEC_FACE_GID], face_gid);
+    put(blob, hdr.off[TS_SEC_SEND_OFF], send_off);
+    put(blob, hdr.off[TS_SEC_SEND], send);
+    put(blob, hdr.off[TS_SEC_FACE_OWN], face_own);
     auto put_real = [&](int sec, const std::vector<double> &v) {
         if (R == 8) put(blob, hdr.off[sec], v);
         else { std::vector<float> f(v.begin(), v.end()); put(blob, hdr.off[sec], f); }
@@ -997,7 +1103,158 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
     info.n_edge_items = nE; info.n_tet_items = nT; info.n_att_items = nA; info.n_slots_total = n_slots_total;
     info.bank_conflicts_p1 = total_conf; info.program_bytes = off; info.compact = compact ? 1 : 0;
     info.edge_gather = eg ? 1 : 0; info.n_edge_incidences = n_einc;
+    info.slot_budget = budget; info.cluster_size = part ? part->K : 1;
     return TS_OK;
+}
+
+
+// ---------------------------------------------------------------------------
+// cluster programs (large meshes): K parts, one per CTA of an env's cluster
+// ---------------------------------------------------------------------------
+namespace {
+
+// recursive coordinate bisection of the free vertices (balanced counts, compact parts)
+void rcb(const double *X, std::vector<int> &idx, int lo, int hi, int part0, int nparts, std::vector<int> &part_of) {
+    if (nparts <= 1 || hi - lo <= 1) {
+        for (int i = lo; i < hi; ++i) part_of[idx[i]] = part0;
+        return;
+    }
+    double mn[3] = {1e300, 1e300, 1e300}, mx[3] = {-1e300, -1e300, -1e300};
+    for (int i = lo; i < hi; ++i)
+        for (int c = 0; c < 3; ++c) { mn[c] = std::min(mn[c], X[3 * idx[i] + c]); mx[c] = std::max(mx[c], X[3 * idx[i] + c]); }
+    int axis = 0;
+    for (int c = 1; c < 3; ++c) if (mx[c] - mn[c] > mx[axis] - mn[axis]) axis = c;
+    std::stable_sort(idx.begin() + lo, idx.begin() + hi, [&](int a, int b) {
+        const double xa = X[3 * a + axis], xb = X[3 * b + axis];
+        return xa < xb || (xa == xb && a < b);
+    });
+    const int left = nparts / 2;
+    const int mid = lo + (int)((int64_t)(hi - lo) * left / nparts);
+    rcb(X, idx, lo, mid, part0, left, part_of);
+    rcb(X, idx, mid, hi, part0 + left, nparts - left, part_of);
+}
+
+const int32_t *prog_section(const std::vector<uint8_t> &blob, int sec) {
+    const TsProgHeader *H = reinterpret_cast<const TsProgHeader *>(blob.data());
+    return reinterpret_cast<const int32_t *>(blob.data() + H->off[sec]);
+}
+
+}  // namespace
+
+int compile_cluster(const ts_scene_desc &d, const ts_layout_opts &o_in, int K, std::vector<uint8_t> &blob,
+                    ts_layout_info &info, std::string &err) {
+    const int V = d.n_vert, E = d.n_edge, F = d.n_face;
+    if (V <= 0) { err = "cluster programs need vertices"; return TS_ERR_INVALID; }
+    for (int i = 0; i < 2 * E; ++i) if (d.edges[i] < 0 || d.edges[i] >= V) { err = "edge vertex index out of range"; return TS_ERR_INVALID; }
+    for (int i = 0; i < 3 * F; ++i) if (d.faces[i] < 0 || d.faces[i] >= V) { err = "face vertex index out of range"; return TS_ERR_INVALID; }
+    const int R = o_in.precision == TS_F64 ? 8 : 4;
+    std::vector<int> tries;
+    if (K == 0) tries = {2, 4, 8, 16};
+    else tries = {K};
+    std::string last_err = "no cluster size fits";
+    for (int k : tries) {
+        if (k < 2 || k > TS_MAX_CLUSTER) { err = "cluster size must be in [2, 16]"; return TS_ERR_INVALID; }
+        // ---- partition: free vertices by RCB, pinned ones follow a free neighbour -------
+        const double *w = d.inverse_mass;
+        std::vector<int> part_of(V, 0), freev;
+        for (int v = 0; v < V; ++v) if (w[v] > 0.0) freev.push_back(v);
+        rcb(d.positions_rest, freev, 0, (int)freev.size(), 0, k, part_of);
+        std::vector<char> placed(V, 0);
+        for (int v : freev) placed[v] = 1;
+        for (int e = 0; e < E; ++e) {   // first edge (by index) to a free vertex decides a pinned vertex
+            const int a = d.edges[2 * e], b = d.edges[2 * e + 1];
+            if (!placed[a] && placed[b] && w[b] > 0.0) { part_of[a] = part_of[b]; placed[a] = 2; }
+            if (!placed[b] && placed[a] && w[a] > 0.0) { part_of[b] = part_of[a]; placed[b] = 2; }
+        }
+        std::vector<PartSpec> ps(k);
+        for (int r = 0; r < k; ++r) {
+            ps[r].rank = r; ps[r].K = k;
+            ps[r].own.assign(V, 0);
+        }
+        for (int v = 0; v < V; ++v) ps[part_of[v]].own[v] = 1;
+        for (int f = 0; f < F; ++f) {   // a face goes to the owner of its first free vertex
+            int r = part_of[d.faces[3 * f]];
+            for (int j = 0; j < 3; ++j) if (w[d.faces[3 * f + j]] > 0.0) { r = part_of[d.faces[3 * f + j]]; break; }
+            ps[r].faces.push_back(f);
+        }
+        // ---- pass 1: natural sizes, storage orders ------------------------------------
+        // (again with a common slot budget if the parts' largest sizes together overflow)
+        ts_layout_opts o = o_in;
+        std::vector<std::vector<uint8_t>> blobs(k);
+        std::vector<ts_layout_info> infos(k);
+        bool ok = true;
+        int maxB = 0, maxVs = 0, maxSl = 0;
+        for (int attempt = 0; attempt < 2; ++attempt) {
+            ok = true;
+            for (int r = 0; r < k && ok; ++r) {
+                std::string e2;
+                if (compile_program(d, o, blobs[r], infos[r], e2, &ps[r]) != TS_OK) { ok = false; last_err = e2; }
+            }
+            if (!ok) break;
+            maxB = maxVs = maxSl = 0;
+            int maxVfp = 0, maxF = 0;
+            for (int r = 0; r < k; ++r) {
+                const TsProgHeader *H = reinterpret_cast<const TsProgHeader *>(blobs[r].data());
+                maxB = std::max(maxB, infos[r].block_threads);
+                maxVs = std::max(maxVs, infos[r].n_store);
+                maxSl = std::max(maxSl, infos[r].slot_capacity);
+                maxVfp = std::max(maxVfp, H->Vf_pad);
+                maxF = std::max(maxF, H->F);
+            }
+            if (ts_smem_layout_bytes(maxVs, maxSl, maxVfp, maxF, R, 1) <= TS_SMEM_LIMIT) break;
+            ok = false;
+            last_err = "cluster part exceeds shared memory";
+            const int fixed = ts_smem_layout_bytes(maxVs, 0, maxVfp, maxF, R, 1);
+            const int common = (TS_SMEM_LIMIT - fixed) / (3 * R) - 32 - 32 * 64;   // margin: region padding
+            if (common < 7 * maxF || common < 256) break;
+            o.max_chunk_slots = common;
+        }
+        if (!ok) continue;
+        std::vector<std::vector<int>> o2s(k);
+        std::vector<int> owner_rank(V, -1), owner_pos(V, -1);
+        std::vector<std::vector<std::pair<int, int>>> halo_of(V);
+        for (int r = 0; r < k; ++r) {
+            const int32_t *q = prog_section(blobs[r], TS_SEC_O2S);
+            o2s[r].assign(q, q + V);
+            for (int v = 0; v < V; ++v) {
+                if (o2s[r][v] < 0) continue;
+                if (ps[r].own[v]) { owner_rank[v] = r; owner_pos[v] = o2s[r][v]; }
+                else halo_of[v].push_back({r, o2s[r][v]});
+            }
+        }
+        // ---- pass 2: common layout sizes + halo sends / face owners ---------------------
+        for (int r = 0; r < k && ok; ++r) {
+            ps[r].force_B = maxB; ps[r].force_Vstore = maxVs; ps[r].force_slot_cap = maxSl;
+            ps[r].halo_of = &halo_of; ps[r].owner_rank = &owner_rank; ps[r].owner_pos = &owner_pos;
+            ts_layout_opts o2 = o;
+            o2.max_chunk_slots = infos[r].slot_budget;   // the same chunking as pass 1
+            std::string e2;
+            if (compile_program(d, o2, blobs[r], infos[r], e2, &ps[r]) != TS_OK) { ok = false; last_err = e2; break; }
+            const int32_t *q = prog_section(blobs[r], TS_SEC_O2S);
+            if (!std::equal(q, q + V, o2s[r].begin())) { err = "cluster part storage order changed between passes"; return TS_ERR_INVALID; }
+        }
+        if (!ok) continue;
+        // ---- assemble ---------------------------------------------------------------------
+        TsClusterHeader ch{};
+        ch.magic = TS_CLUSTER_MAGIC; ch.K = k; ch.n_vert = V; ch.n_face = F;
+        int64_t off = ((int64_t)sizeof(TsClusterHeader) + 255) / 256 * 256;
+        for (int r = 0; r < k; ++r) {
+            ch.part_off[r] = off; ch.part_bytes[r] = (int64_t)blobs[r].size();
+            off += ((int64_t)blobs[r].size() + 255) / 256 * 256;
+        }
+        ch.total_bytes = off;
+        blob.assign((size_t)off, 0);
+        std::memcpy(blob.data(), &ch, sizeof(ch));
+        for (int r = 0; r < k; ++r) std::memcpy(blob.data() + ch.part_off[r], blobs[r].data(), blobs[r].size());
+        info = infos[0];
+        int nfree = 0, nslots = 0, ninc = 0;
+        for (int r = 0; r < k; ++r) { nfree += infos[r].n_free; nslots += infos[r].n_slots_total; ninc += infos[r].n_edge_incidences; }
+        info.n_free = nfree; info.n_slots_total = nslots; info.n_edge_incidences = ninc;
+        info.cluster_size = k; info.program_bytes = off;
+        return TS_OK;
+    }
+    err = last_err;
+    return TS_ERR_UNSUPPORTED;
 }
 
 }  // namespace ts

@@ -56,6 +56,11 @@ enum TsSection {
                           //   (uniform-mass fp32); 16: {nbr pos, fp32 coef | 0, fp64/fp32 rest}
     TS_SEC_EREGION,       // int32 [G] base record of group g
     TS_SEC_EVAL,          // int32 [Vf_pad] live incident edges of p
+    TS_SEC_FACE_GID,      // int32 [F] global surface-face index of local face i (contact order key)
+    // cluster parts only (one CTA of an env's thread-block cluster):
+    TS_SEC_SEND_OFF,      // int32 [Vf_pad + 1] CSR offsets of the halo sends of owned free vertex p
+    TS_SEC_SEND,          // int32 [n] (dest rank << 20) | dest storage position
+    TS_SEC_FACE_OWN,      // int32 [F][3] (owner rank << 20) | owner position of a free face vertex, -1 pinned
     TS_SEC_COUNT
 };
 
@@ -67,6 +72,30 @@ struct TsChunk {
     int32_t val_off, conflicts, pad0, pad1;
 };
 
+// Shared memory one CTA needs for a program (the kernel's carve, step_kernel.cuh): positions
+// (x2 when ping-ponged), slot buffer / contact records, degenerate counters, contact bitmap,
+// scalar block.
+inline int ts_smem_layout_bytes(int Vstore, int slot_cap, int Vf_pad, int F, int real_bytes, int ping_pong) {
+    size_t b = 0;
+    b += (size_t)3 * Vstore * real_bytes * (ping_pong ? 2 : 1);
+    b += (size_t)3 * slot_cap * real_bytes;
+    b += (size_t)4 * Vf_pad;
+    b += (size_t)4 * ((3 * F + 31) / 32);
+    b = (b + 15) / 16 * 16;
+    b += 2048;
+    return (int)b;
+}
+#define TS_SMEM_LIMIT 232448   // B200 opt-in shared memory per CTA (227 KiB)
+
+// A cluster program: K part programs, one per CTA rank of an environment's cluster.
+#define TS_CLUSTER_MAGIC 0x54534331  // "TSC1"
+#define TS_MAX_CLUSTER 16
+struct TsClusterHeader {
+    int32_t magic, K, n_vert, n_face;
+    int64_t part_off[TS_MAX_CLUSTER], part_bytes[TS_MAX_CLUSTER];
+    int64_t total_bytes;
+};
+
 struct TsProgHeader {
     int32_t magic, version, real_bytes, n_sections;
     int32_t V, Vf, Vf_pad, Vstore;
@@ -74,6 +103,7 @@ struct TsProgHeader {
     int32_t n_chunks, grasp_chunk, slot_capacity, n_att;
     int32_t n_edge_items, n_tet_items, n_att_items, bank_conflicts;
     int32_t n_slots_total, compact, edge_gather, einc_bytes;
+    int32_t Vown, cluster_k, cluster_rank, pad3;   // Vown: end of the owned (written-back) positions
     double w_free;   // the common inverse mass of free vertices (compact programs)
     int64_t off[TS_SEC_COUNT];
     int64_t total_bytes;

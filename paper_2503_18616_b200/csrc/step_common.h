@@ -32,6 +32,7 @@ struct TsParams {
     double lo[3], hi[3];
     int64_t max_steps;
     double start_distance, target_obs[3];
+    int64_t n_face;           // surface faces of the whole mesh (detect_contacts row capacity 3F)
     // fp32 copies of the solver constants (read straight from the constant bank by the fp32 build)
     float h_f, inv_h_f, damp_f, g_f[3], ks_f, hks_f, kv_f, pad_f;
 };
@@ -75,6 +76,13 @@ struct TsDevProg {
     const void *einc;
     const int32_t *eregion;
     const int32_t *evalence;
+    const int32_t *face_gid;  // [F] global face index (contact emission key)
+    // cluster parts (cluster_k > 1): one CTA of an env's thread-block cluster
+    int32_t Vown;             // end of the owned (written-back) storage positions
+    int32_t cluster_k, cluster_rank;
+    const int32_t *send_off;  // [Vf_pad + 1]
+    const int32_t *send;      // (rank << 20) | storage position of a halo copy
+    const int32_t *face_own;  // [F][3] (rank << 20) | position of a free face vertex's owner, -1 pinned
 };
 
 // Tool pose of one env (ToolBatch row, tool.py:263-302), fp64.
@@ -134,20 +142,17 @@ struct TsLaunch {
 
 // Shared-memory layout sizes (bytes) for one CTA.
 inline int ts_smem_bytes(const TsDevProg &P, int real_bytes) {
-    size_t b = 0;
-    b += (size_t)3 * P.Vstore * real_bytes * (P.edge_gather ? 2 : 1);   // positions (x2: ping-pong)
-    b += (size_t)3 * P.slot_cap * real_bytes;     // slot buffer / contact records
-    b += (size_t)4 * P.Vf_pad;                    // degenerate-constraint counters
-    b += (size_t)4 * P.cbits_words;               // contact bitmap
-    b = (b + 15) / 16 * 16;
-    b += 2048;                                    // scalar block + capsule params
-    return (int)b;
+    return ts_smem_layout_bytes(P.Vstore, P.slot_cap, P.Vf_pad, P.F, real_bytes, P.edge_gather);
 }
 
 // command kernel -> fused step kernel -> epilogue kernel, stream ordered
 template <typename Real>
 cudaError_t ts_launch_step(const TsDevProg &P, const TsParams &S, const TsLaunch &L, int grid,
                            int smem, cudaStream_t stream);
+// large meshes: `n_clusters` clusters of K CTAs (part programs `parts`, device array)
+template <typename Real>
+cudaError_t ts_launch_cluster_step(const TsDevProg *parts, int VPT, int K, int B, const TsParams &S,
+                                   const TsLaunch &L, int n_clusters, int smem, cudaStream_t stream);
 cudaError_t ts_launch_cmd(const TsDevProg &P, const TsParams &S, const TsLaunch &L, cudaStream_t stream);
 cudaError_t ts_launch_epilogue(const TsDevProg &P, const TsParams &S, const TsLaunch &L, cudaStream_t stream);
 template <typename Real>

@@ -7,3 +7,5 @@ template cudaError_t ts_launch_step<float>(const TsDevProg &, const TsParams &, 
                                            cudaStream_t);
 template cudaError_t ts_launch_reset<float>(const TsDevProg &, const TsParams &, const TsLaunch &,
                                             const uint8_t *, int, cudaStream_t);
+template cudaError_t ts_launch_cluster_step<float>(const TsDevProg *, int, int, int, const TsParams &, const TsLaunch &,
+                                                  int, int, cudaStream_t);

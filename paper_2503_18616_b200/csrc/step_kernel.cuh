@@ -292,6 +292,12 @@ struct Scal {
     int need_search;
     int done;
     int n_contacts;
+    // cluster mode: per-rank exchange slots (used in rank 0's copy) and local results
+    double cl_key[TS_MAX_CLUSTER];
+    int cl_idx[TS_MAX_CLUSTER];
+    int cl_flag[TS_MAX_CLUSTER];
+    int n_list;
+    int any_bad;
 };
 
 // Component c of element i of an (n, 3) array-of-structs in shared memory.
@@ -319,18 +325,21 @@ struct Smem {
 
 template <typename Real>
 __device__ __forceinline__ Smem<Real> carve(const TsDevProg &P, unsigned char *raw) {
+    // [scalar block | capsules | positions | ping-pong positions | slots | degenerate counters |
+    //  contact bitmap]: everything a cluster peer addresses over DSMEM (scalars, positions,
+    //  slot / record buffer, the contact key list in the counters) sits at the same offset in
+    //  every CTA of the cluster (parts share Vstore and the slot capacity)
+    static_assert(((sizeof(Scal) + 15) / 16) * 16 + 3 * sizeof(Cap<Real>) <= 2048, "scalar block");
     Smem<Real> m;
-    Real *pos = reinterpret_cast<Real *>(raw);
+    m.sc = reinterpret_cast<Scal *>(raw);
+    m.caps = reinterpret_cast<Cap<Real> *>(raw + ((sizeof(Scal) + 15) / 16) * 16);
+    Real *pos = reinterpret_cast<Real *>(raw + 2048);
     m.alt = P.edge_gather ? pos + 3 * P.Vstore : pos;
     Real *slots = pos + 3 * P.Vstore * (P.edge_gather ? 2 : 1);
     m.pos = pos;
     m.slot = slots;
     m.deg = reinterpret_cast<int *>(slots + 3 * P.slot_cap);
     m.cbits = reinterpret_cast<unsigned *>(m.deg + P.Vf_pad);
-    size_t off = reinterpret_cast<unsigned char *>(m.cbits + P.cbits_words) - raw;
-    off = (off + 15) / 16 * 16;
-    m.sc = reinterpret_cast<Scal *>(raw + off);
-    m.caps = reinterpret_cast<Cap<Real> *>(raw + off + ((sizeof(Scal) + 15) / 16) * 16);
     return m;
 }
 
@@ -607,7 +616,7 @@ __device__ __forceinline__ void owner_edges(const TsDevProg &P, const Smem<Real>
         const double wp = wst[p];
         for (int k = 0; k < ev; ++k) {
             const int4 q = __ldg(rec + 32 * k);
-            const int nb = q.x;
+            const int nb = q.x & 0x7fffffff;
             const double rl = __hiloint2double(q.w, q.z);
             const double wq = __ldg(wst + nb);
             const double dx = px - m.X(nb), dy = py - m.Y(nb), dz = pz - m.Z(nb);
@@ -620,20 +629,20 @@ __device__ __forceinline__ void owner_edges(const TsDevProg &P, const Smem<Real>
         }
     } else if (P.einc_bytes == 8) {
         // uniform free mass: coef = ks w / (w + w) = ks / 2, or ks when the neighbour is pinned
+        // (record bit 31)
         const uint2 *rec = reinterpret_cast<const uint2 *>(P.einc) + rb;
-        const int vfp = P.Vf_pad;
         const float hks = 0.5f * ks;   // == TsParams::hks_f
         uint2 q = ev > 0 ? __ldg(rec) : make_uint2(0, 0);
         for (int k = 0; k < ev; ++k) {
             const uint2 cur = q;
             q = __ldg(rec + 32 * min(k + 1, ev - 1));    // next record, branch-free prefetch
-            const int nb = (int)cur.x;
+            const int nb = (int)(cur.x & 0x7fffffffu);
             const float rl = __uint_as_float(cur.y);
             const float dx = px - m.X(nb), dy = py - m.Y(nb), dz = pz - m.Z(nb);
             const float d2 = __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, dx * dx));
             const bool degenerate = !(d2 >= 1e-24f);
             const float f = degenerate ? 0.0f : __fmaf_rn(-rl, rsqrt_ftz(d2), 1.0f);
-            const float c = -(nb < vfp ? hks : ks) * f;
+            const float c = -((int)cur.x < 0 ? ks : hks) * f;
             ax = __fmaf_rn(c, dx, ax); ay = __fmaf_rn(c, dy, ay); az = __fmaf_rn(c, dz, az);
             ndeg += degenerate;
         }
@@ -641,7 +650,7 @@ __device__ __forceinline__ void owner_edges(const TsDevProg &P, const Smem<Real>
         const int4 *rec = reinterpret_cast<const int4 *>(P.einc) + rb;
         for (int k = 0; k < ev; ++k) {
             const int4 q = __ldg(rec + 32 * k);
-            const int nb = q.x;
+            const int nb = q.x & 0x7fffffff;
             const float coef = __int_as_float(q.y), rl = __int_as_float(q.z);
             const float dx = px - m.X(nb), dy = py - m.Y(nb), dz = pz - m.Z(nb);
             const float d2 = __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, dx * dx));
@@ -808,14 +817,82 @@ static __global__ void __launch_bounds__(128) epilogue_kernel(const __grid_const
 }
 
 // ---------------------------------------------------------------------------
-// the fused step kernel
+// thread-block cluster primitives (large-mesh mode: one cluster of K CTAs per env)
 // ---------------------------------------------------------------------------
-template <typename Real, int VPT>
-__global__ void __launch_bounds__(512, sizeof(Real) == 4 ? 2 : 1) step_kernel(const __grid_constant__ TsDevProg P,
-                                                   const __grid_constant__ TsParams S,
-                                                   const __grid_constant__ TsLaunch L) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    Smem<Real> m = carve<Real>(P, smem_raw);
+namespace cl {
+__device__ __forceinline__ unsigned rank() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ unsigned cluster_id() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%clusterid.x;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ unsigned n_clusters() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%nclusterid.x;" : "=r"(r));
+    return r;
+}
+// all threads of all CTAs of the cluster; release/acquire orders the DSMEM traffic around it
+__device__ __forceinline__ void sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t saddr(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+// the same shared-memory offset in CTA `r` of the cluster
+__device__ __forceinline__ uint32_t map(uint32_t a, unsigned r) {
+    uint32_t o;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(o) : "r"(a), "r"(r));
+    return o;
+}
+__device__ __forceinline__ void st(uint32_t a, float v) { asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(a), "f"(v) : "memory"); }
+__device__ __forceinline__ void st(uint32_t a, double v) { asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory"); }
+__device__ __forceinline__ void st(uint32_t a, int v) { asm volatile("st.shared::cluster.s32 [%0], %1;" ::"r"(a), "r"(v) : "memory"); }
+template <typename T> __device__ __forceinline__ T ld(uint32_t a);
+template <> __device__ __forceinline__ float ld<float>(uint32_t a) {
+    float v;
+    asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(a) : "memory");
+    return v;
+}
+template <> __device__ __forceinline__ double ld<double>(uint32_t a) {
+    double v;
+    asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(a) : "memory");
+    return v;
+}
+template <> __device__ __forceinline__ int ld<int>(uint32_t a) {
+    int v;
+    asm volatile("ld.shared::cluster.s32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+    return v;
+}
+template <> __device__ __forceinline__ unsigned ld<unsigned>(uint32_t a) {
+    unsigned v;
+    asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(a) : "memory");
+    return v;
+}
+}  // namespace cl
+
+// Cluster parts: push owned free vertex p's position (x, y, z) into the halo copies other CTAs
+// keep of it, in their buffer at the same shared-memory offset as `buf` here.
+template <typename Real>
+__device__ __forceinline__ void halo_send(const TsDevProg &P, const Real *buf, int p, Real x, Real y, Real z) {
+    const int k1 = P.send_off[p + 1];
+    for (int k = P.send_off[p]; k < k1; ++k) {
+        const int sd = P.send[k];
+        const uint32_t a = cl::map(cl::saddr(buf + 3 * (sd & 0xfffff)), (unsigned)sd >> 20);
+        cl::st(a, x); cl::st(a + sizeof(Real), y); cl::st(a + 2 * sizeof(Real), z);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// the fused step of one environment
+// ---------------------------------------------------------------------------
+// CL = false: this CTA owns the whole env.  CL = true: this CTA is rank `rank` of the env's
+// cluster (program P = progs[rank]); it owns part of the vertices and keeps a halo of the rest
+// current over DSMEM; grasp search, contacts and the divergence flag are cluster-wide.
+template <typename Real, int VPT, bool CL>
+__device__ __forceinline__ void step_env(const TsDevProg &P, const TsDevProg *progs, const TsParams &S,
+                                         const TsLaunch &L, Smem<Real> &m, int64_t env, unsigned rank) {
     Scal &sc = *m.sc;
     const int t = threadIdx.x;
     const int B = blockDim.x;
@@ -827,236 +904,256 @@ __global__ void __launch_bounds__(512, sizeof(Real) == 4 ? 2 : 1) step_kernel(co
     const Real ks = prm<Real>(S.ks, S.ks_f), kv = prm<Real>(S.kv, S.kv_f);
     const Real *wst = reinterpret_cast<const Real *>(P.w);
     const Real *rest = reinterpret_cast<const Real *>(P.rest);
+    const int K = CL ? P.cluster_k : 1;
 
-    if ((mode & TS_M_CHECK_ACTIONS) && *L.bad_flag) return;   // deferred ValidationError: no state change
+    Real *xg = reinterpret_cast<Real *>(L.x) + env * (int64_t)P.V * 3;
+    Real *vg = reinterpret_cast<Real *>(L.v) + env * (int64_t)P.V * 3;
 
-    for (int64_t env = blockIdx.x; env < L.n_env; env += gridDim.x) {
-        Real *xg = reinterpret_cast<Real *>(L.x) + env * (int64_t)P.V * 3;
-        Real *vg = reinterpret_cast<Real *>(L.v) + env * (int64_t)P.V * 3;
-
-        // ---- A. the env's command block (cmd_kernel) + the state load ------
-        TsCmd &cmd = L.cmd[env];
-        if (t < 24) {
-            const double *src = t < 21 ? &cmd.caps[0][0] + t : cmd.drag + (t - 21);
-            (&sc.caps[0][0])[t] = *src;            // caps[21] and drag[3] are contiguous in Scal too
-        } else if (t == 24) {
-            sc.gv_orig = cmd.gv; sc.need_search = cmd.need_search; sc.n_contacts = 0;
-        }
-        // state -> shared (storage order) / registers
-        for (int p = t; p < P.Vstore; p += B) {
+    // ---- A. the env's command block (cmd_kernel) + the state load ------
+    TsCmd &cmd = L.cmd[env];
+    if (t < 24) {
+        const double *src = t < 21 ? &cmd.caps[0][0] + t : cmd.drag + (t - 21);
+        (&sc.caps[0][0])[t] = *src;            // caps[21] and drag[3] are contiguous in Scal too
+    } else if (t == 24) {
+        sc.gv_orig = cmd.gv; sc.need_search = cmd.need_search; sc.n_contacts = 0;
+    }
+    // state -> shared (storage order) / registers
+    for (int p = t; p < P.Vstore; p += B) {
+        const int o = P.s2o[p];
+        Real a = 0, b = 0, c = 0;
+        if (o >= 0) { a = xg[3 * o]; b = xg[3 * o + 1]; c = xg[3 * o + 2]; }
+        m.X(p) = a; m.Y(p) = b; m.Z(p) = c;
+        m.alt[3 * p] = a; m.alt[3 * p + 1] = b; m.alt[3 * p + 2] = c;   // pinned rows of the ping-pong
+    }
+    Real vx[VPT], vy[VPT], vz[VPT];
+#pragma unroll
+    for (int r = 0; r < VPT; ++r) {
+        const int p = r * B + t;
+        vx[r] = vy[r] = vz[r] = 0;
+        if (p < P.Vf) {
             const int o = P.s2o[p];
-            Real a = 0, b = 0, c = 0;
-            if (o >= 0) { a = xg[3 * o]; b = xg[3 * o + 1]; c = xg[3 * o + 2]; }
-            m.X(p) = a; m.Y(p) = b; m.Z(p) = c;
-            m.alt[3 * p] = a; m.alt[3 * p + 1] = b; m.alt[3 * p + 2] = c;   // pinned rows of the ping-pong
+            vx[r] = vg[3 * o]; vy[r] = vg[3 * o + 1]; vz[r] = vg[3 * o + 2];
         }
-        Real vx[VPT], vy[VPT], vz[VPT];
+    }
+    for (int p = t; p < P.Vf_pad; p += B) m.deg[p] = 0;
+    for (int i = t; i < P.cbits_words; i += B) m.cbits[i] = 0u;
+    if constexpr (CL) cl::sync();   // every CTA holds its halo before anyone pushes into it
+    else __syncthreads();
+
+    if (mode & (TS_M_CONTACTS | TS_M_DETECT_ONLY)) {
+        if (t < 3) make_cap<Real>(sc.caps[t], m.caps[t]);
+        __syncthreads();
+    }
+    // ---- B. grasp search: nearest free vertex (tool.py:380-389) ------
+    if (sc.need_search) {
+        double bk = INFINITY;
+        int bi = 0x7fffffff;
+        for (int p = t; p < P.Vf; p += B) {
+            const double r0 = (double)m.X(p) - sc.drag[0];
+            const double r1 = (double)m.Y(p) - sc.drag[1];
+            const double r2 = (double)m.Z(p) - sc.drag[2];
+            double d2 = r0 * r0 + r1 * r1 + r2 * r2;
+            if (isnan(d2)) d2 = -INFINITY;      // numpy argmin returns the first NaN
+            const int o = P.s2o[p];
+            if (d2 < bk || (d2 == bk && o < bi)) { bk = d2; bi = o; }
+        }
+        for (int off = 16; off > 0; off >>= 1) {
+            const double ok = __shfl_xor_sync(0xffffffffu, bk, off);
+            const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
+            if (ok < bk || (ok == bk && oi < bi)) { bk = ok; bi = oi; }
+        }
+        if (lane == 0) { sc.red_key[t >> 5] = bk; sc.red_idx[t >> 5] = bi; }
+        __syncthreads();
+        if (t == 0) {
+            for (int wi = 1; wi < (B >> 5); ++wi) {
+                if (sc.red_key[wi] < bk || (sc.red_key[wi] == bk && sc.red_idx[wi] < bi)) {
+                    bk = sc.red_key[wi]; bi = sc.red_idx[wi];
+                }
+            }
+            if constexpr (CL) {   // cluster-wide argmin: every part's winner to rank 0
+                cl::st(cl::map(cl::saddr(&sc.cl_key[rank]), 0), bk);
+                cl::st(cl::map(cl::saddr(&sc.cl_idx[rank]), 0), bi);
+            }
+        }
+        if constexpr (CL) {
+            cl::sync();
+            if (t == 0) {
+                for (int r = 0; r < K; ++r) {
+                    const double ok = cl::ld<double>(cl::map(cl::saddr(&sc.cl_key[r]), 0));
+                    const int oi = cl::ld<int>(cl::map(cl::saddr(&sc.cl_idx[r]), 0));
+                    if (r == 0 || ok < bk || (ok == bk && oi < bi)) { bk = ok; bi = oi; }
+                }
+            }
+        }
+        if (t == 0) {
+            if (bi != 0x7fffffff && bk != -INFINITY && bk <= S.grasp_r2) {
+                sc.gv_orig = bi;
+                if (rank == 0) L.grasped[env * P.V + bi] = 1;
+            }
+        }
+        __syncthreads();
+    }
+    // grasp vertex in storage order (any vertex; pinned ones are never applied)
+    const int gvs = sc.gv_orig >= 0 ? P.o2s[sc.gv_orig] : -1;
+
+    // ---- C. substeps ---------------------------------------------------
+    if (mode & TS_M_SUBSTEPS) {
+        Real xr[VPT], yr[VPT], zr[VPT], accx[VPT], accy[VPT], accz[VPT];
+        int ndeg[VPT], gcnt[VPT];
 #pragma unroll
         for (int r = 0; r < VPT; ++r) {
             const int p = r * B + t;
-            vx[r] = vy[r] = vz[r] = 0;
+            accx[r] = accy[r] = accz[r] = 0; ndeg[r] = 0; gcnt[r] = 0;
+            xr[r] = yr[r] = zr[r] = 0;
             if (p < P.Vf) {
-                const int o = P.s2o[p];
-                vx[r] = vg[3 * o]; vy[r] = vg[3 * o + 1]; vz[r] = vg[3 * o + 2];
+                // predict for substep 0 (ts_lane_predict, _kernels.pyx:63-87)
+                vx[r] += h * gx; xr[r] = m.X(p) + h * vx[r];
+                vy[r] += h * gy; yr[r] = m.Y(p) + h * vy[r];
+                vz[r] += h * gz; zr[r] = m.Z(p) + h * vz[r];
+                m.X(p) = xr[r]; m.Y(p) = yr[r]; m.Z(p) = zr[r];
+                if constexpr (CL) halo_send<Real>(P, m.pos, p, xr[r], yr[r], zr[r]);
             }
         }
-        for (int p = t; p < P.Vf_pad; p += B) m.deg[p] = 0;
-        for (int i = t; i < P.cbits_words; i += B) m.cbits[i] = 0u;
-        __syncthreads();
-
-        if (mode & (TS_M_CONTACTS | TS_M_DETECT_ONLY)) {
-            if (t < 3) make_cap<Real>(sc.caps[t], m.caps[t]);
-            __syncthreads();
-        }
-        // ---- B. grasp search: nearest free vertex (tool.py:380-389) ------
-        if (sc.need_search) {
-            double bk = INFINITY;
-            int bi = 0x7fffffff;
-            for (int p = t; p < P.Vf; p += B) {
-                const double r0 = (double)m.X(p) - sc.drag[0];
-                const double r1 = (double)m.Y(p) - sc.drag[1];
-                const double r2 = (double)m.Z(p) - sc.drag[2];
-                double d2 = r0 * r0 + r1 * r1 + r2 * r2;
-                if (isnan(d2)) d2 = -INFINITY;      // numpy argmin returns the first NaN
-                const int o = P.s2o[p];
-                if (d2 < bk || (d2 == bk && o < bi)) { bk = d2; bi = o; }
+        if constexpr (CL) cl::sync();
+        else __syncthreads();
+        const double d0 = sc.drag[0], d1 = sc.drag[1], d2 = sc.drag[2];
+        // grasp contribution of owner slot r: after the vertex's edges (_kernels.pyx:283-298)
+        auto add_grasp = [&](int r) {
+            const int p = r * B + t;
+            if (p < P.Vf && p == gvs) {
+                const Real dx = (Real)(d0 - (double)xr[r]);
+                const Real dy = (Real)(d1 - (double)yr[r]);
+                const Real dz = (Real)(d2 - (double)zr[r]);
+                const Real dist = sqrt(dx * dx + dy * dy + dz * dz);
+                if (!(dist <= (Real)1e-12)) { accx[r] += dx; accy[r] += dy; accz[r] += dz; gcnt[r] = 1; }
             }
-            for (int off = 16; off > 0; off >>= 1) {
-                const double ok = __shfl_xor_sync(0xffffffffu, bk, off);
-                const int oi = __shfl_xor_sync(0xffffffffu, bi, off);
-                if (ok < bk || (ok == bk && oi < bi)) { bk = ok; bi = oi; }
-            }
-            if (lane == 0) { sc.red_key[t >> 5] = bk; sc.red_idx[t >> 5] = bi; }
-            __syncthreads();
-            if (t == 0) {
-                for (int wi = 1; wi < (B >> 5); ++wi) {
-                    if (sc.red_key[wi] < bk || (sc.red_key[wi] == bk && sc.red_idx[wi] < bi)) {
-                        bk = sc.red_key[wi]; bi = sc.red_idx[wi];
-                    }
-                }
-                if (bi != 0x7fffffff && bk != -INFINITY && bk <= S.grasp_r2) {
-                    sc.gv_orig = bi;
-                    L.grasped[env * P.V + bi] = 1;
-                }
-            }
-            __syncthreads();
-        }
-        // grasp vertex in storage order (any vertex; pinned ones are never applied)
-        const int gvs = sc.gv_orig >= 0 ? P.o2s[sc.gv_orig] : -1;
-
-        // ---- C. substeps ---------------------------------------------------
-        if (mode & TS_M_SUBSTEPS) {
-            Real xr[VPT], yr[VPT], zr[VPT], accx[VPT], accy[VPT], accz[VPT];
-            int ndeg[VPT], gcnt[VPT];
-#pragma unroll
-            for (int r = 0; r < VPT; ++r) {
-                const int p = r * B + t;
-                accx[r] = accy[r] = accz[r] = 0; ndeg[r] = 0; gcnt[r] = 0;
-                xr[r] = yr[r] = zr[r] = 0;
-                if (p < P.Vf) {
-                    // predict for substep 0 (ts_lane_predict, _kernels.pyx:63-87)
-                    vx[r] += h * gx; xr[r] = m.X(p) + h * vx[r];
-                    vy[r] += h * gy; yr[r] = m.Y(p) + h * vy[r];
-                    vz[r] += h * gz; zr[r] = m.Z(p) + h * vz[r];
-                    m.X(p) = xr[r]; m.Y(p) = yr[r]; m.Z(p) = zr[r];
-                }
-            }
-            __syncthreads();
-            const double d0 = sc.drag[0], d1 = sc.drag[1], d2 = sc.drag[2];
-            // grasp contribution of owner slot r: after the vertex's edge slots (_kernels.pyx:283-298)
-            auto add_grasp = [&](int r) {
-                const int p = r * B + t;
-                if (p < P.Vf && p == gvs) {
-                    const Real dx = (Real)(d0 - (double)xr[r]);
-                    const Real dy = (Real)(d1 - (double)yr[r]);
-                    const Real dz = (Real)(d2 - (double)zr[r]);
-                    const Real dist = sqrt(dx * dx + dy * dy + dz * dz);
-                    if (!(dist <= (Real)1e-12)) { accx[r] += dx; accy[r] += dy; accz[r] += dz; gcnt[r] = 1; }
-                }
-            };
-            for (int s = 0; s < S.substeps; ++s) {
-                for (int c = 0; c < P.n_chunks; ++c) {
-                    const TsChunk ch = P.chunks[c];
-                    // phase 1: every kind of the chunk, no barrier in between (disjoint slots)
-                    if (ch.edge_count) p1_edges<Real>(P, m, ch.edge_begin, ch.edge_count, ks);
-                    if (ch.att_count) p1_atts<Real>(P, m, ch.att_begin, ch.att_count);
-                    if (ch.tet_count) p1_tets<Real>(P, m, ch.tet_begin, ch.tet_count, kv);
-                    __syncthreads();
-                    // phase 2: owner gathers its slots in reference order
-                    const bool gchunk = c == P.grasp_chunk;
-#pragma unroll
-                    for (int r = 0; r < VPT; ++r) {
-                        const int p = r * B + t;
-                        if (p < P.Vf) {
-                            const int base = P.region[ch.region_off + (p >> 5)] + lane;
-                            const int val = P.valence[ch.val_off + p];
-                            const int pre = gchunk ? P.gsplit[p] : val;
-                            Real ax = accx[r], ay = accy[r], az = accz[r];
-                            if (P.edge_gather && c == 0)   // edges come first in the reference order
-                                owner_edges<Real>(P, m, p, lane, xr[r], yr[r], zr[r], ks, ax, ay, az, ndeg[r]);
-#pragma unroll 4
-                            for (int k = 0; k < pre; ++k) {
-                                const int sidx = base + 32 * k;
-                                ax += m.SX(sidx); ay += m.SY(sidx); az += m.SZ(sidx);
-                            }
-                            if (gchunk) {
-                                accx[r] = ax; accy[r] = ay; accz[r] = az;
-                                add_grasp(r);
-                                ax = accx[r]; ay = accy[r]; az = accz[r];
-                                for (int k = pre; k < val; ++k) {
-                                    const int sidx = base + 32 * k;
-                                    ax += m.SX(sidx); ay += m.SY(sidx); az += m.SZ(sidx);
-                                }
-                            }
-                            accx[r] = ax; accy[r] = ay; accz[r] = az;
-                            const int dg = m.deg[p];
-                            if (dg) { ndeg[r] += dg; m.deg[p] = 0; }
-                        }
-                    }
-                    if (c + 1 < P.n_chunks) __syncthreads();   // slots are reused by the next chunk
-                }
-                if (P.grasp_chunk == P.n_chunks) {
-#pragma unroll
-                    for (int r = 0; r < VPT; ++r) {
-                        const int p = r * B + t;
-                        if (P.edge_gather && P.n_chunks == 0 && p < P.Vf)   // distance constraints only
-                            owner_edges<Real>(P, m, p, lane, xr[r], yr[r], zr[r], ks, accx[r], accy[r], accz[r],
-                                              ndeg[r]);
-                        add_grasp(r);
-                    }
-                }
-                // apply (ts_lane_apply, _kernels.pyx:213-244) + next predict
+        };
+        for (int s = 0; s < S.substeps; ++s) {
+            for (int c = 0; c < P.n_chunks; ++c) {
+                const TsChunk ch = P.chunks[c];
+                // phase 1: every kind of the chunk, no barrier in between (disjoint slots)
+                if (ch.edge_count) p1_edges<Real>(P, m, ch.edge_begin, ch.edge_count, ks);
+                if (ch.att_count) p1_atts<Real>(P, m, ch.att_begin, ch.att_count);
+                if (ch.tet_count) p1_tets<Real>(P, m, ch.tet_begin, ch.tet_count, kv);
+                __syncthreads();
+                // phase 2: owner gathers its slots in reference order
+                const bool gchunk = c == P.grasp_chunk;
 #pragma unroll
                 for (int r = 0; r < VPT; ++r) {
                     const int p = r * B + t;
                     if (p < P.Vf) {
-                        const int cnt = P.static_cnt[p] - ndeg[r] + gcnt[r];
-                        if constexpr (sizeof(Real) == 8) {
-                            const Real n = (Real)cnt;
-                            const Real mm = (Real)0.5 + copysign((Real)0.5, n - (Real)0.5);
-                            const Real inv = mm / (n + ((Real)1 - mm));
-                            const Real e0 = accx[r] * inv, e1 = accy[r] * inv, e2 = accz[r] * inv;
-                            xr[r] += e0; vx[r] += e0 / h;
-                            yr[r] += e1; vy[r] += e1 / h;
-                            zr[r] += e2; vz[r] += e2 / h;
-                        } else {
-                            const float inv = cnt > 0 ? rcp_ftz((float)cnt) : 0.0f;
-                            const float e0 = accx[r] * inv, e1 = accy[r] * inv, e2 = accz[r] * inv;
-                            xr[r] += e0; vx[r] = __fmaf_rn(e0, inv_h, vx[r]);
-                            yr[r] += e1; vy[r] = __fmaf_rn(e1, inv_h, vy[r]);
-                            zr[r] += e2; vz[r] = __fmaf_rn(e2, inv_h, vz[r]);
+                        const int base = P.region[ch.region_off + (p >> 5)] + lane;
+                        const int val = P.valence[ch.val_off + p];
+                        const int pre = gchunk ? P.gsplit[p] : val;
+                        Real ax = accx[r], ay = accy[r], az = accz[r];
+                        if (P.edge_gather && c == 0)   // edges come first in the reference order
+                            owner_edges<Real>(P, m, p, lane, xr[r], yr[r], zr[r], ks, ax, ay, az, ndeg[r]);
+#pragma unroll 4
+                        for (int k = 0; k < pre; ++k) {
+                            const int sidx = base + 32 * k;
+                            ax += m.SX(sidx); ay += m.SY(sidx); az += m.SZ(sidx);
                         }
-                        if (damp != (Real)1) { vx[r] *= damp; vy[r] *= damp; vz[r] *= damp; }
-                        if (s + 1 < S.substeps) {
-                            vx[r] += h * gx; xr[r] += h * vx[r];
-                            vy[r] += h * gy; yr[r] += h * vy[r];
-                            vz[r] += h * gz; zr[r] += h * vz[r];
+                        if (gchunk) {
+                            accx[r] = ax; accy[r] = ay; accz[r] = az;
+                            add_grasp(r);
+                            ax = accx[r]; ay = accy[r]; az = accz[r];
+                            for (int k = pre; k < val; ++k) {
+                                const int sidx = base + 32 * k;
+                                ax += m.SX(sidx); ay += m.SY(sidx); az += m.SZ(sidx);
+                            }
                         }
-                        // edge_gather: other owners may still read this substep's snapshot -> ping-pong
-                        Real *dst = m.alt + 3 * p;
-                        dst[0] = xr[r]; dst[1] = yr[r]; dst[2] = zr[r];
-                        accx[r] = accy[r] = accz[r] = 0; ndeg[r] = 0; gcnt[r] = 0;
+                        accx[r] = ax; accy[r] = ay; accz[r] = az;
+                        const int dg = m.deg[p];
+                        if (dg) { ndeg[r] += dg; m.deg[p] = 0; }
                     }
                 }
-                __syncthreads();
-                if (P.edge_gather) {
-                    Real *cur = m.pos;
-                    m.pos = m.alt;
-                    m.alt = cur;
+                if (c + 1 < P.n_chunks) __syncthreads();   // slots are reused by the next chunk
+            }
+            if (P.grasp_chunk == P.n_chunks) {
+#pragma unroll
+                for (int r = 0; r < VPT; ++r) {
+                    const int p = r * B + t;
+                    if (P.edge_gather && P.n_chunks == 0 && p < P.Vf)   // distance constraints only
+                        owner_edges<Real>(P, m, p, lane, xr[r], yr[r], zr[r], ks, accx[r], accy[r], accz[r],
+                                          ndeg[r]);
+                    add_grasp(r);
+                }
+            }
+            // apply (ts_lane_apply, _kernels.pyx:213-244) + next predict
+#pragma unroll
+            for (int r = 0; r < VPT; ++r) {
+                const int p = r * B + t;
+                if (p < P.Vf) {
+                    const int cnt = P.static_cnt[p] - ndeg[r] + gcnt[r];
+                    if constexpr (sizeof(Real) == 8) {
+                        const Real n = (Real)cnt;
+                        const Real mm = (Real)0.5 + copysign((Real)0.5, n - (Real)0.5);
+                        const Real inv = mm / (n + ((Real)1 - mm));
+                        const Real e0 = accx[r] * inv, e1 = accy[r] * inv, e2 = accz[r] * inv;
+                        xr[r] += e0; vx[r] += e0 / h;
+                        yr[r] += e1; vy[r] += e1 / h;
+                        zr[r] += e2; vz[r] += e2 / h;
+                    } else {
+                        const float inv = cnt > 0 ? rcp_ftz((float)cnt) : 0.0f;
+                        const float e0 = accx[r] * inv, e1 = accy[r] * inv, e2 = accz[r] * inv;
+                        xr[r] += e0; vx[r] = __fmaf_rn(e0, inv_h, vx[r]);
+                        yr[r] += e1; vy[r] = __fmaf_rn(e1, inv_h, vy[r]);
+                        zr[r] += e2; vz[r] = __fmaf_rn(e2, inv_h, vz[r]);
+                    }
+                    if (damp != (Real)1) { vx[r] *= damp; vy[r] *= damp; vz[r] *= damp; }
+                    if (s + 1 < S.substeps) {
+                        vx[r] += h * gx; xr[r] += h * vx[r];
+                        vy[r] += h * gy; yr[r] += h * vy[r];
+                        vz[r] += h * gz; zr[r] += h * vz[r];
+                    }
+                    // edge_gather: other owners may still read this substep's snapshot -> ping-pong
+                    Real *dst = m.alt + 3 * p;
+                    dst[0] = xr[r]; dst[1] = yr[r]; dst[2] = zr[r];
+                    if constexpr (CL) halo_send<Real>(P, m.alt, p, xr[r], yr[r], zr[r]);
+                    accx[r] = accy[r] = accz[r] = 0; ndeg[r] = 0; gcnt[r] = 0;
+                }
+            }
+            if constexpr (CL) cl::sync();
+            else __syncthreads();
+            if (P.edge_gather) {
+                Real *cur = m.pos;
+                m.pos = m.alt;
+                m.alt = cur;
+            }
+        }
+    }
+
+    // ---- D. contacts ---------------------------------------------------
+    if ((mode & (TS_M_CONTACTS | TS_M_DETECT_ONLY)) && (CL || P.F > 0)) {
+        Cap<Real> *C = m.caps;   // built by threads 0..2 before the substeps
+        Real *rec = m.slot;   // 3F records x 7 reals (the slot buffer is free now)
+        for (int f = t; f < P.F; f += B) {
+            const int ia = P.faces[3 * f], ib = P.faces[3 * f + 1], ic = P.faces[3 * f + 2];
+            const Real pa[3] = {m.X(ia), m.Y(ia), m.Z(ia)};
+            const Real pb[3] = {m.X(ib), m.Y(ib), m.Z(ib)};
+            const Real pc[3] = {m.X(ic), m.Y(ic), m.Z(ic)};
+#pragma unroll
+            for (int ci = 0; ci < 3; ++ci) {
+                bool skip = false;
+                for (int k = 0; k < 3; ++k) {
+                    const Real tlo = cmin(cmin(pa[k], pb[k]), pc[k]);
+                    const Real thi = cmax(cmax(pa[k], pb[k]), pc[k]);
+                    if (thi < C[ci].lo[k] || tlo > C[ci].hi[k]) { skip = true; break; }
+                }
+                if (skip) continue;
+                Real dir[3], bary[3];
+                const Real sd = witness<Real>(C[ci], pa, pb, pc, S.contact_iters, dir, bary);
+                if (sd < (Real)0) {
+                    const int key = ci * P.F + f;
+                    Real *q = rec + 7 * key;
+                    q[0] = -sd; q[1] = dir[0]; q[2] = dir[1]; q[3] = dir[2];
+                    q[4] = bary[0]; q[5] = bary[1]; q[6] = bary[2];
+                    atomicOr(&m.cbits[key >> 5], 1u << (key & 31));
                 }
             }
         }
-
-        // ---- D. contacts ---------------------------------------------------
-        if ((mode & (TS_M_CONTACTS | TS_M_DETECT_ONLY)) && P.F > 0) {
-            Cap<Real> *C = m.caps;   // built by threads 0..2 before the substeps
-            Real *rec = m.slot;   // 3F records x 7 reals (the slot buffer is free now)
-            for (int f = t; f < P.F; f += B) {
-                const int ia = P.faces[3 * f], ib = P.faces[3 * f + 1], ic = P.faces[3 * f + 2];
-                const Real pa[3] = {m.X(ia), m.Y(ia), m.Z(ia)};
-                const Real pb[3] = {m.X(ib), m.Y(ib), m.Z(ib)};
-                const Real pc[3] = {m.X(ic), m.Y(ic), m.Z(ic)};
-#pragma unroll
-                for (int ci = 0; ci < 3; ++ci) {
-                    bool skip = false;
-                    for (int k = 0; k < 3; ++k) {
-                        const Real tlo = cmin(cmin(pa[k], pb[k]), pc[k]);
-                        const Real thi = cmax(cmax(pa[k], pb[k]), pc[k]);
-                        if (thi < C[ci].lo[k] || tlo > C[ci].hi[k]) { skip = true; break; }
-                    }
-                    if (skip) continue;
-                    Real dir[3], bary[3];
-                    const Real sd = witness<Real>(C[ci], pa, pb, pc, S.contact_iters, dir, bary);
-                    if (sd < (Real)0) {
-                        const int key = ci * P.F + f;
-                        Real *q = rec + 7 * key;
-                        q[0] = -sd; q[1] = dir[0]; q[2] = dir[1]; q[3] = dir[2];
-                        q[4] = bary[0]; q[5] = bary[1]; q[6] = bary[2];
-                        atomicOr(&m.cbits[key >> 5], 1u << (key & 31));
-                    }
-                }
-            }
-            __syncthreads();
+        __syncthreads();
+        if constexpr (!CL) {
             if (t == 0) {
                 int count = 0;
                 for (int wi = 0; wi < P.cbits_words; ++wi) {
@@ -1069,7 +1166,7 @@ __global__ void __launch_bounds__(512, sizeof(Real) == 4 ? 2 : 1) step_kernel(co
                         const Real *q = rec + 7 * key;
                         if (mode & TS_M_DETECT_ONLY) {
                             const int64_t row = env * 3 * (int64_t)P.F + count;
-                            L.det_face[row] = f; L.det_cap[row] = ci; L.det_depth[row] = (double)q[0];
+                            L.det_face[row] = P.face_gid[f]; L.det_cap[row] = ci; L.det_depth[row] = (double)q[0];
                             for (int k = 0; k < 3; ++k) { L.det_dir[3 * row + k] = (double)q[1 + k]; L.det_bary[3 * row + k] = (double)q[4 + k]; }
                         } else {
                             // collision.resolve_contact_arrays, sequential in emission order
@@ -1094,50 +1191,160 @@ __global__ void __launch_bounds__(512, sizeof(Real) == 4 ? 2 : 1) step_kernel(co
                 if (mode & TS_M_DETECT_ONLY) L.det_count[env] = count;
             }
             __syncthreads();
-        }
-
-        // ---- E. divergence guard (solver.py:357-359) ----------------------
-        int bad = 0;
-        for (int p = t; p < P.Vstore; p += B)
-            bad |= !(isfinite(m.X(p)) && isfinite(m.Y(p)) && isfinite(m.Z(p)));
-        const int any_bad = __syncthreads_or(bad);
-
-        // ---- F. hand the step's results to the epilogue kernel -------------
-        // done = terminated || truncated = success || steps >= max || diverged (env.py:173-175)
-        if (t == 0) {
-            cmd.gv = sc.gv_orig; cmd.any_bad = any_bad; cmd.n_contacts = sc.n_contacts;
-        }
-        const bool done_env = (mode & TS_M_ENV) && (cmd.pre_done || any_bad);
-
-        // ---- G. write back --------------------------------------------------
-        if (!(mode & TS_M_DETECT_ONLY)) {
-            const bool done = done_env;
-            if (done)
-                for (int i = t; i < P.V; i += B) L.grasped[env * P.V + i] = 0;
-#pragma unroll
-            for (int r = 0; r < VPT; ++r) {
-                const int p = r * B + t;
-                if (p < P.Vf) {
-                    const int o = P.s2o[p];
-                    if (done) {
-                        xg[3 * o] = rest[3 * o]; xg[3 * o + 1] = rest[3 * o + 1]; xg[3 * o + 2] = rest[3 * o + 2];
-                        vg[3 * o] = 0; vg[3 * o + 1] = 0; vg[3 * o + 2] = 0;
-                    } else {
-                        xg[3 * o] = m.X(p); xg[3 * o + 1] = m.Y(p); xg[3 * o + 2] = m.Z(p);
-                        vg[3 * o] = vx[r]; vg[3 * o + 1] = vy[r]; vg[3 * o + 2] = vz[r];
+        } else {
+            // every part lists its contact keys in (capsule, local face) order -- local faces are
+            // ascending global faces -- into its (now free) degenerate-counter array
+            if (t == 0) {
+                int n = 0;
+                for (int wi = 0; wi < P.cbits_words; ++wi) {
+                    unsigned bits = m.cbits[wi];
+                    while (bits && n < P.Vf_pad) {
+                        const int b = __ffs(bits) - 1;
+                        bits &= bits - 1;
+                        m.deg[n++] = wi * 32 + b;
                     }
                 }
+                sc.n_list = n;
             }
-            for (int p = P.Vf_pad + t; p < P.Vstore; p += B) {
+            cl::sync();
+            // rank 0 merges the K lists in emission order (capsule-major, global face minor) and
+            // applies the push-outs sequentially to the owners' positions (collision.py:55-73)
+            if (rank == 0 && t == 0) {
+                int count = 0;
+                int head[TS_MAX_CLUSTER], nl[TS_MAX_CLUSTER];
+                for (int r = 0; r < K; ++r) {
+                    head[r] = 0;
+                    nl[r] = cl::ld<int>(cl::map(cl::saddr(&sc.n_list), r));
+                }
+                for (int ci = 0; ci < 3; ++ci) {
+                    while (true) {
+                        int best_r = -1, best_g = 0x7fffffff, best_f = 0;
+                        for (int r = 0; r < K; ++r) {
+                            if (head[r] >= nl[r]) continue;
+                            const TsDevProg &Q = progs[r];
+                            const int key = cl::ld<int>(cl::map(cl::saddr(&m.deg[head[r]]), r));
+                            const int kc = key / Q.F;
+                            if (kc != ci) continue;
+                            const int f = key - kc * Q.F;
+                            const int g = Q.face_gid[f];
+                            if (g < best_g) { best_g = g; best_r = r; best_f = f; }
+                        }
+                        if (best_r < 0) break;
+                        const TsDevProg &Q = progs[best_r];
+                        const int key = ci * Q.F + best_f;
+                        const uint32_t qa = cl::map(cl::saddr(rec + 7 * key), best_r);
+                        Real q[7];
+                        for (int k = 0; k < 7; ++k) q[k] = cl::ld<Real>(qa + k * sizeof(Real));
+                        if (mode & TS_M_DETECT_ONLY) {
+                            const int64_t row = env * 3 * (int64_t)S.n_face + count;
+                            L.det_face[row] = best_g; L.det_cap[row] = ci; L.det_depth[row] = (double)q[0];
+                            for (int k = 0; k < 3; ++k) { L.det_dir[3 * row + k] = (double)q[1 + k]; L.det_bary[3 * row + k] = (double)q[4 + k]; }
+                        } else {
+                            const Real b0 = q[4], b1 = q[5], b2 = q[6];
+                            const Real bb = fused_sq3<Real>(b0, b1, b2);
+                            if (bb > (Real)0) {
+                                const Real sc_ = (Real)S.k_contact * q[0] / bb;
+                                const Real px = sc_ * q[1], py = sc_ * q[2], pz = sc_ * q[3];
+                                const Real bj[3] = {b0, b1, b2};
+                                for (int j = 0; j < 3; ++j) {
+                                    const int ow = Q.face_own[3 * best_f + j];
+                                    if (ow < 0) continue;   // pinned
+                                    const uint32_t a = cl::map(cl::saddr(m.pos + 3 * (ow & 0xfffff)), (unsigned)ow >> 20);
+                                    cl::st(a, cl::ld<Real>(a) + bj[j] * px);
+                                    cl::st(a + sizeof(Real), cl::ld<Real>(a + sizeof(Real)) + bj[j] * py);
+                                    cl::st(a + 2 * sizeof(Real), cl::ld<Real>(a + 2 * sizeof(Real)) + bj[j] * pz);
+                                }
+                            }
+                        }
+                        ++head[best_r];
+                        ++count;
+                    }
+                }
+                sc.n_contacts = count;
+                if (mode & TS_M_DETECT_ONLY) L.det_count[env] = count;
+            }
+            cl::sync();
+        }
+    }
+
+    // ---- E. divergence guard (solver.py:357-359) ----------------------
+    int bad = 0;
+    for (int p = t; p < P.Vown; p += B)
+        bad |= !(isfinite(m.X(p)) && isfinite(m.Y(p)) && isfinite(m.Z(p)));
+    int any_bad = __syncthreads_or(bad);
+    if constexpr (CL) {
+        if (t == 0) cl::st(cl::map(cl::saddr(&sc.cl_flag[rank]), 0), any_bad);
+        cl::sync();
+        if (t == 0) {
+            int a = 0;
+            for (int r = 0; r < K; ++r) a |= cl::ld<int>(cl::map(cl::saddr(&sc.cl_flag[r]), 0));
+            sc.any_bad = a;
+        }
+        __syncthreads();
+        any_bad = sc.any_bad;
+    }
+
+    // ---- F. hand the step's results to the epilogue kernel -------------
+    // done = terminated || truncated = success || steps >= max || diverged (env.py:173-175)
+    if (t == 0 && rank == 0) {
+        cmd.gv = sc.gv_orig; cmd.any_bad = any_bad; cmd.n_contacts = sc.n_contacts;
+    }
+    const bool done_env = (mode & TS_M_ENV) && (cmd.pre_done || any_bad);
+
+    // ---- G. write back (owned vertices) ----------------------------------
+    if (!(mode & TS_M_DETECT_ONLY)) {
+        const bool done = done_env;
+        if (done)
+            for (int i = t * K + (int)rank; i < P.V; i += B * K) L.grasped[env * P.V + i] = 0;
+#pragma unroll
+        for (int r = 0; r < VPT; ++r) {
+            const int p = r * B + t;
+            if (p < P.Vf) {
                 const int o = P.s2o[p];
-                if (o < 0) continue;
-                if (done) { xg[3 * o] = rest[3 * o]; xg[3 * o + 1] = rest[3 * o + 1]; xg[3 * o + 2] = rest[3 * o + 2]; }
-                else if (mode & TS_M_CONTACTS) { xg[3 * o] = m.X(p); xg[3 * o + 1] = m.Y(p); xg[3 * o + 2] = m.Z(p); }
-                if (mode & TS_M_SUBSTEPS || done) { vg[3 * o] = 0; vg[3 * o + 1] = 0; vg[3 * o + 2] = 0; }
+                if (done) {
+                    xg[3 * o] = rest[3 * o]; xg[3 * o + 1] = rest[3 * o + 1]; xg[3 * o + 2] = rest[3 * o + 2];
+                    vg[3 * o] = 0; vg[3 * o + 1] = 0; vg[3 * o + 2] = 0;
+                } else {
+                    xg[3 * o] = m.X(p); xg[3 * o + 1] = m.Y(p); xg[3 * o + 2] = m.Z(p);
+                    vg[3 * o] = vx[r]; vg[3 * o + 1] = vy[r]; vg[3 * o + 2] = vz[r];
+                }
             }
         }
-        __syncthreads();   // shared scalars are reused by the next environment
+        for (int p = P.Vf_pad + t; p < P.Vown; p += B) {
+            const int o = P.s2o[p];
+            if (o < 0) continue;
+            if (done) { xg[3 * o] = rest[3 * o]; xg[3 * o + 1] = rest[3 * o + 1]; xg[3 * o + 2] = rest[3 * o + 2]; }
+            else if (mode & TS_M_CONTACTS) { xg[3 * o] = m.X(p); xg[3 * o + 1] = m.Y(p); xg[3 * o + 2] = m.Z(p); }
+            if (mode & TS_M_SUBSTEPS || done) { vg[3 * o] = 0; vg[3 * o + 1] = 0; vg[3 * o + 2] = 0; }
+        }
     }
+    if constexpr (CL) cl::sync();   // no CTA of the cluster still reads this one's shared memory
+    else __syncthreads();           // shared scalars are reused by the next environment
+}
+
+template <typename Real, int VPT>
+__global__ void __launch_bounds__(512, sizeof(Real) == 4 ? 2 : 1) step_kernel(const __grid_constant__ TsDevProg P,
+                                                   const __grid_constant__ TsParams S,
+                                                   const __grid_constant__ TsLaunch L) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    Smem<Real> m = carve<Real>(P, smem_raw);
+    if ((L.mode & TS_M_CHECK_ACTIONS) && *L.bad_flag) return;   // deferred ValidationError: no state change
+    for (int64_t env = blockIdx.x; env < L.n_env; env += gridDim.x)
+        step_env<Real, VPT, false>(P, nullptr, S, L, m, env, 0);
+}
+
+// Large-mesh mode: a thread-block cluster of K CTAs per environment (grid = K x clusters).
+template <typename Real, int VPT>
+__global__ void __launch_bounds__(512, 1) cluster_step_kernel(const TsDevProg *__restrict__ progs,
+                                                              const __grid_constant__ TsParams S,
+                                                              const __grid_constant__ TsLaunch L) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const unsigned rank = cl::rank();
+    const TsDevProg &P = progs[rank];
+    Smem<Real> m = carve<Real>(P, smem_raw);
+    if ((L.mode & TS_M_CHECK_ACTIONS) && *L.bad_flag) return;   // the same verdict in every CTA
+    for (int64_t env = cl::cluster_id(); env < L.n_env; env += cl::n_clusters())
+        step_env<Real, VPT, true>(P, progs, S, L, m, env, rank);
 }
 
 // ---------------------------------------------------------------------------
@@ -1205,6 +1412,37 @@ cudaError_t ts_launch_step(const TsDevProg &P, const TsParams &S, const TsLaunch
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     fn<<<grid, P.B, smem, stream>>>(P, S, L);
+    return cudaGetLastError();
+}
+
+template <typename Real>
+cudaError_t ts_launch_cluster_step(const TsDevProg *parts, int VPT, int K, int B, const TsParams &S,
+                                   const TsLaunch &L, int n_clusters, int smem, cudaStream_t stream) {
+    void (*fn)(const TsDevProg *, const TsParams, const TsLaunch) = nullptr;
+    if (VPT <= 1) fn = tsk::cluster_step_kernel<Real, 1>;
+    else if (VPT <= 2) fn = tsk::cluster_step_kernel<Real, 2>;
+    else if (VPT <= 4) fn = tsk::cluster_step_kernel<Real, 4>;
+    else return cudaErrorInvalidValue;
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    if (K > 8) {
+        e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        if (e != cudaSuccess) return e;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(n_clusters * K), 1, 1);
+    cfg.blockDim = dim3((unsigned)B, 1, 1);
+    cfg.dynamicSmemBytes = (size_t)smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = (unsigned)K;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, fn, parts, S, L);
+    if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
 

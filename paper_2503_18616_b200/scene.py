@@ -152,7 +152,7 @@ class SceneArrays:
 
 
 def layout_opts(precision="fp32", block_threads=0, max_chunk_slots=0, schedule_banks=True, compact=True,
-                edge_gather=None):
+                edge_gather=None, cluster_size=0):
     o = N.LayoutOpts()
     o.precision = N.TS_F64 if precision in ("fp64", "float64", "f64", N.TS_F64) else N.TS_F32
     o.block_threads = int(block_threads)
@@ -162,6 +162,7 @@ def layout_opts(precision="fp32", block_threads=0, max_chunk_slots=0, schedule_b
     # None: the compiler's choice (owner gather for fp32; fp64 keeps constraint-parallel slots,
     # where the per-incidence IEEE sqrt / div of the gather cost more than they save)
     o.edge_gather = 0 if edge_gather is None else (1 if edge_gather else -1)
+    o.cluster_size = int(cluster_size)
     return o
 
 

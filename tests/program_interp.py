@@ -15,21 +15,23 @@ import numpy as np
 
 SECTIONS = ["CHUNK", "EDGE_IDX", "EDGE_PAR", "TET_IDX", "TET_SLOT", "TET_RV", "ATT_IDX", "ATT_SLOT",
             "ATT_PAR", "ATT_ANCHOR", "REGION", "VALENCE", "STATIC_CNT", "S2O", "O2S", "W", "FACES",
-            "FACES_ORIG", "REST", "GSPLIT", "EDGE_C", "TET_C", "EINC", "EREGION", "EVAL"]
+            "FACES_ORIG", "REST", "GSPLIT", "EDGE_C", "TET_C", "EINC", "EREGION", "EVAL", "FACE_GID",
+            "SEND_OFF", "SEND", "FACE_OWN"]
 HDR_FIELDS = ["magic", "version", "real_bytes", "n_sections", "V", "Vf", "Vf_pad", "Vstore", "F", "B",
               "VPT", "G", "n_chunks", "grasp_chunk", "slot_capacity", "n_att", "n_edge_items",
               "n_tet_items", "n_att_items", "bank_conflicts", "n_slots_total", "compact", "edge_gather",
-              "einc_bytes"]
+              "einc_bytes", "Vown", "cluster_k", "cluster_rank", "pad3"]
 
 
 class Program:
     def __init__(self, blob: np.ndarray):
         b = blob.view(np.uint8)
-        ints = b[:96].view(np.int32)
+        ints = b[:4 * len(HDR_FIELDS)].view(np.int32)
         self.h = dict(zip(HDR_FIELDS, (int(v) for v in ints)))
         assert self.h["magic"] == 0x54534231
-        self.w_free = float(b[96:104].view(np.float64)[0])
-        self.off = b[104:104 + 8 * len(SECTIONS)].view(np.int64)
+        o = 4 * len(HDR_FIELDS)
+        self.w_free = float(b[o:o + 8].view(np.float64)[0])
+        self.off = b[o + 8:o + 8 + 8 * len(SECTIONS)].view(np.int64)
         self.b = b
         if self.h["compact"]:
             nE, nT = self.h["n_edge_items"], self.h["n_tet_items"]
@@ -66,7 +68,9 @@ class Program:
             eb = H["einc_bytes"]
             n = int(self.eregion[-1] + 32 * self.evalence[32 * (G - 1):32 * G].max()) if G else 0
             raw = self.sec("EINC", np.uint8, max(n, 1) * eb).reshape(-1, eb)
-            self.e_nbr = raw[:, 0:4].copy().view(np.int32)[:, 0]
+            word = raw[:, 0:4].copy().view(np.uint32)[:, 0]
+            self.e_nbr = (word & 0x7FFFFFFF).astype(np.int32)
+            self.e_nbr_pinned = (word >> 31).astype(bool)       # bit 31: neighbour pinned (w = 0)
             if eb == 8:
                 self.e_rest = raw[:, 4:8].copy().view(np.float32)[:, 0].astype(np.float64)
                 self.e_coef = None
@@ -89,24 +93,35 @@ class Program:
         return self.b[o:o + nbytes].view(dtype).copy()
 
 
-def run_substeps(prog: Program, x, v, grasp_vertex, drag, g, h, substeps, damping, ks, kv):
-    """One env: x, v (V,3) float64 in place. Mirrors step_kernel.cuh section C."""
-    H = prog.h
-    Vf, Vst = H["Vf"], H["Vstore"]
-    s2o = prog.s2o
-    valid = s2o >= 0
-    xs = np.zeros((Vst, 3))
-    xs[valid] = x[s2o[valid]]
-    vf = v[s2o[:Vf]].copy()
-    damp = 1.0 if damping == 0.0 else max(0.0, 1.0 - damping * h)
-    gvs = prog.o2s[grasp_vertex] if grasp_vertex >= 0 else -1
-    scap = H["slot_capacity"]
-    lane = np.arange(Vf) % 32
-    grp = np.arange(Vf) // 32
-    # predict, substep 0
-    vf += h * np.asarray(g)[None, :]
-    xs[:Vf] = xs[:Vf] + h * vf
-    for s in range(substeps):
+class PartRun:
+    """Section C of step_kernel.cuh for one program (or one cluster part) in fp64."""
+
+    def __init__(self, prog: Program, x, v, grasp_vertex, drag, g, h, damping, ks, kv):
+        self.prog, self.g, self.h, self.ks, self.kv = prog, np.asarray(g, np.float64), h, ks, kv
+        self.drag = np.asarray(drag, np.float64)
+        H = prog.h
+        self.Vf = Vf = H["Vf"]
+        s2o = prog.s2o
+        self.valid = s2o >= 0
+        self.xs = np.zeros((H["Vstore"], 3))
+        self.xs[self.valid] = x[s2o[self.valid]]
+        self.vf = v[s2o[:Vf]].copy()
+        self.damp = 1.0 if damping == 0.0 else max(0.0, 1.0 - damping * h)
+        o = prog.o2s[grasp_vertex] if grasp_vertex >= 0 else -1
+        self.gvs = o
+
+    def predict(self):
+        self.vf += self.h * self.g[None, :]
+        self.xs[:self.Vf] = self.xs[:self.Vf] + self.h * self.vf
+
+    def accumulate(self):
+        """Corrections of one substep from the current snapshot: (acc, count adjustment)."""
+        prog, xs, Vf, ks, kv = self.prog, self.xs, self.Vf, self.ks, self.kv
+        H = prog.h
+        gvs, drag = self.gvs, self.drag
+        scap = H["slot_capacity"]
+        lane = np.arange(Vf) % 32
+        grp = np.arange(Vf) // 32
         acc = np.zeros((Vf, 3))
         cnt_adj = np.zeros(Vf, np.int64)
         def owner_edges():
@@ -195,18 +210,77 @@ def run_substeps(prog: Program, x, v, grasp_vertex, drag, g, h, substeps, dampin
             if H["edge_gather"] and H["n_chunks"] == 0:
                 owner_edges()
             add_grasp()
+        return acc, cnt_adj
+
+    def apply(self, acc, cnt_adj, last):
+        prog, Vf, h = self.prog, self.Vf, self.h
         n = (prog.static_cnt[:Vf] + cnt_adj).astype(np.float64)
         m = 0.5 + np.copysign(0.5, n - 0.5)
         inv = m / (n + (1.0 - m))
         e = acc * inv[:, None]
-        xs[:Vf] = xs[:Vf] + e
-        vf = vf + e / h
-        if damp != 1.0:
-            vf = vf * damp
-        if s + 1 < substeps:
-            vf = vf + h * np.asarray(g)[None, :]
-            xs[:Vf] = xs[:Vf] + h * vf
-    x[s2o[valid]] = xs[valid]
-    v[s2o[:Vf]] = vf
-    pinned = s2o[Vf:][s2o[Vf:] >= 0]
-    v[pinned] = 0.0
+        self.xs[:Vf] = self.xs[:Vf] + e
+        self.vf = self.vf + e / h
+        if self.damp != 1.0:
+            self.vf = self.vf * self.damp
+        if not last:
+            self.vf = self.vf + h * self.g[None, :]
+            self.xs[:Vf] = self.xs[:Vf] + h * self.vf
+
+    def write_back(self, x, v):
+        prog, Vf = self.prog, self.Vf
+        s2o = prog.s2o
+        own = np.zeros(len(s2o), bool)
+        own[:prog.h["Vown"]] = True
+        sel = self.valid & own
+        x[s2o[sel]] = self.xs[sel]
+        v[s2o[:Vf]] = self.vf
+        pinned = s2o[Vf:prog.h["Vown"]]
+        v[pinned[pinned >= 0]] = 0.0
+
+
+def run_substeps(prog: Program, x, v, grasp_vertex, drag, g, h, substeps, damping, ks, kv):
+    """One env: x, v (V,3) float64 in place. Mirrors step_kernel.cuh section C."""
+    run = PartRun(prog, x, v, grasp_vertex, drag, g, h, damping, ks, kv)
+    run.predict()
+    for s in range(substeps):
+        acc, cnt = run.accumulate()
+        run.apply(acc, cnt, s + 1 == substeps)
+    run.write_back(x, v)
+
+
+def cluster_parts(blob: np.ndarray):
+    """The part programs of a cluster program (TsClusterHeader + K part blobs)."""
+    b = blob.view(np.uint8)
+    magic, K = (int(q) for q in b[:8].view(np.int32))
+    assert magic == 0x54534331, hex(magic)
+    off = b[16:16 + 8 * 16].view(np.int64)
+    size = b[16 + 8 * 16:16 + 16 * 16].view(np.int64)
+    return [Program(b[int(off[r]):int(off[r]) + int(size[r])].copy()) for r in range(K)]
+
+
+def run_substeps_cluster(parts, x, v, grasp_vertex, drag, g, h, substeps, damping, ks, kv):
+    """The cluster kernel's data flow on CPU: every part computes its owned vertices from its
+    local snapshot, then the owners refresh every halo copy (the DSMEM sends)."""
+    runs = [PartRun(p, x, v, grasp_vertex, drag, g, h, damping, ks, kv) for p in parts]
+    owner = {}
+    for r, p in enumerate(parts):
+        for q in range(p.h["Vf"]):
+            owner[int(p.s2o[q])] = (r, q)
+
+    def refresh():
+        for r, p in enumerate(parts):
+            for q in range(p.h["Vown"], p.h["Vstore"]):
+                o = int(p.s2o[q])
+                if o >= 0 and o in owner:
+                    rr, qq = owner[o]
+                    runs[r].xs[q] = runs[rr].xs[qq]
+    for run in runs:
+        run.predict()
+    refresh()
+    for s in range(substeps):
+        upd = [run.accumulate() for run in runs]
+        for run, (acc, cnt) in zip(runs, upd):
+            run.apply(acc, cnt, s + 1 == substeps)
+        refresh()
+    for run in runs:
+        run.write_back(x, v)

@@ -226,3 +226,82 @@ def test_compile_errors():
     arr.edges[0, 0] = 10_000
     with pytest.raises(Exception, match="out of range"):
         S.compile_program(arr)
+
+
+# ---------------------------------------------------------------------------
+# cluster programs (large-mesh mode: one thread-block cluster of K CTAs per env)
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("k", [2, 4, 16])
+def test_cluster_program_reproduces_oracle_bitwise(reach_scene, k):
+    """K parts, each owning a block of vertices and reading a halo refreshed by the owners every
+    substep, reproduce the reference's substeps bit for bit (fp64 program, CPU interpreter)."""
+    mesh, rest, cfg = reach_scene
+    blob, info = S.compile_program(_arrays(reach_scene), precision="fp64", cluster_size=k)
+    assert info["cluster_size"] == k
+    parts = PI.cluster_parts(blob)
+    assert len(parts) == k
+    rng = np.random.default_rng(3)
+    free = np.flatnonzero(rest.inverse_mass > 0)
+    x0 = mesh.positions_rest + rng.normal(0, 5e-4, mesh.positions_rest.shape) * (rest.inverse_mass > 0)[:, None]
+    v0 = rng.normal(0, 1e-2, x0.shape) * (rest.inverse_mass > 0)[:, None]
+    for gv in (-1, int(free[17])):
+        drag = x0[free[17]] + np.array([0.001, -0.002, 0.0005])
+        xa, va = _oracle_substeps(mesh, rest, cfg, x0, v0, gv, drag)
+        xb, vb = x0.copy(), v0.copy()
+        PI.run_substeps_cluster(parts, xb, vb, gv, drag, cfg.gravity, cfg.dt / cfg.substeps, cfg.substeps,
+                                cfg.damping, cfg.k_s, cfg.k_v)
+        assert np.array_equal(xa, xb) and np.array_equal(va, vb), (k, gv)
+
+
+def test_cluster_parts_partition_and_halo_sends(reach_scene):
+    """Every vertex is owned by exactly one part; every halo copy is fed by exactly one send of its
+    owner; every surface face is handled by exactly one part that holds its three vertices."""
+    mesh, rest, cfg = reach_scene
+    k = 4
+    blob, info = S.compile_program(_arrays(reach_scene), precision="fp32", cluster_size=k)
+    parts = PI.cluster_parts(blob)
+    V = mesh.vertex_count
+    owners = np.zeros(V, int)
+    loc = []
+    for r, p in enumerate(parts):
+        H = p.h
+        assert H["cluster_k"] == k and H["cluster_rank"] == r
+        own = p.s2o[:H["Vown"]]
+        owners[own[own >= 0]] += 1
+        loc.append({int(o): q for q, o in enumerate(p.s2o) if o >= 0})
+    assert np.all(owners == 1)
+    # sends: (rank, pos) pairs of owned free vertex q must be exactly its halo copies elsewhere
+    for r, p in enumerate(parts):
+        H = p.h
+        off = p.sec("SEND_OFF", np.int32, H["Vf_pad"] + 1)
+        snd = p.sec("SEND", np.int32, int(off[-1]))
+        for q in range(H["Vf"]):
+            o = int(p.s2o[q])
+            got = sorted((int(s) >> 20, int(s) & 0xFFFFF) for s in snd[off[q]:off[q + 1]])
+            want = sorted((rr, loc[rr][o]) for rr in range(k) if rr != r and o in loc[rr])
+            assert got == want
+    # faces: a partition of the surface, ascending global ids per part, vertices local
+    gids = []
+    for r, p in enumerate(parts):
+        g = p.sec("FACE_GID", np.int32, p.h["F"])
+        assert np.all(np.diff(g) > 0)
+        gids.extend(g.tolist())
+        for i, f in enumerate(g):
+            assert all(int(vv) in loc[r] for vv in mesh.surface_faces[f])
+    assert sorted(gids) == list(range(len(mesh.surface_faces)))
+    # equal shared-memory layout across ranks (DSMEM addresses coincide)
+    assert len({(p.h["Vstore"], p.h["slot_capacity"], p.h["B"]) for p in parts}) == 1
+
+
+def test_large_presets_compile_to_clusters():
+    """Table II-right meshes: the 52359-tet slab does not fit one CTA, and compiles to a cluster."""
+    import tempfile
+    from paper_2503_18616_b200.mesh import load_scene, make_slab_scene
+    d = tempfile.mkdtemp()
+    sc = load_scene(make_slab_scene(d, tets=52359))
+    blob, info = S.compile_program(_arrays(sc), precision="fp32")
+    assert 2 <= info["cluster_size"] <= 16
+    assert info["n_free"] == int((sc[1].inverse_mass > 0).sum())
+    with pytest.raises(Exception, match="too large|shared memory"):
+        S.compile_program(_arrays(sc), precision="fp32", cluster_size=1)
