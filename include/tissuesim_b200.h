@@ -223,6 +223,11 @@ int32_t ts_detect_contacts(ts_handle *h, const void *x, int64_t num_envs, const 
 int32_t ts_uniform_actions(double *actions, int64_t num_envs, int64_t first_env, uint64_t seed,
                            uint64_t counter, void *stream);
 
+/* The same draw with the counter in DEVICE memory (uint64), incremented by the call in stream
+ * order: a captured CUDA graph replays a fresh action batch every time. */
+int32_t ts_uniform_actions_dev(double *actions, int64_t num_envs, int64_t first_env, uint64_t seed,
+                               uint64_t *counter, void *stream);
+
 /* Measured shared-memory bandwidth of the device (GB/s, whole GPU): the
  * roofline denominator for the on-chip-bound env step. */
 int32_t ts_smem_probe(int32_t device, int32_t iters, double *gbs_out);

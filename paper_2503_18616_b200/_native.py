@@ -99,6 +99,7 @@ _SIGNATURES = {
     "ts_detect_contacts": ([_P, _P, _I64, _P, _P, _P, _P, _P, _P, _P, _P], _I32),
     "ts_uniform_actions": ([_P, _I64, _I64, ctypes.c_uint64, ctypes.c_uint64, _P], _I32),
     "ts_smem_probe": ([_I32, _I32, _P], _I32),
+    "ts_uniform_actions_dev": ([_P, _I64, _I64, ctypes.c_uint64, _P, _P], _I32),
     "ts_kernel_timing": ([_P, _I32, _I32], _I32),
     "ts_kernel_time": ([_P, _P, _P], _I32),
 }

@@ -433,6 +433,17 @@ int32_t ts_kernel_time(ts_handle *h, double *total_ms, int64_t *launches) {
     return TS_OK;
 }
 
+int32_t ts_uniform_actions_dev(double *actions, int64_t num_envs, int64_t first_env, uint64_t seed,
+                               uint64_t *counter, void *stream) {
+    if (!actions || !counter) return fail(TS_ERR_INVALID, "null argument");
+    if (num_envs <= 0) return TS_OK;
+    cudaError_t e = ts_launch_uniform_dev(actions, 3 * num_envs, 3 * first_env, seed, counter,
+                                          reinterpret_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "uniform kernel launch");
+    g_launches.fetch_add(2);
+    return TS_OK;
+}
+
 int32_t ts_set_max_grid(ts_handle *h, int32_t max_grid) {
     if (!h) return fail(TS_ERR_INVALID, "null argument");
     h->max_grid = max_grid;
@@ -473,7 +484,9 @@ __device__ __forceinline__ uint64_t splitmix64(uint64_t z) {
 }
 
 // element i of the whole (multi-GPU) batch depends only on (seed, counter, global index)
-__global__ void uniform_kernel(double *out, int64_t n, int64_t first, uint64_t seed, uint64_t counter) {
+__global__ void uniform_kernel(double *out, int64_t n, int64_t first, uint64_t seed, uint64_t counter,
+                               uint64_t *dev_counter) {
+    if (dev_counter) counter = *dev_counter;   // graph replays: the counter lives on the device
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const uint64_t r = splitmix64(seed ^ splitmix64(counter * 0x100000001B3ull + (uint64_t)(i + first)));
         out[i] = 2.0 * ((double)(r >> 11) * (1.0 / 9007199254740992.0)) - 1.0;
@@ -484,7 +497,20 @@ cudaError_t ts_launch_uniform(double *out, int64_t n, int64_t first, uint64_t se
                               cudaStream_t stream) {
     int grid = (int)((n + 255) / 256);
     if (grid > 4096) grid = 4096;
-    uniform_kernel<<<grid, 256, 0, stream>>>(out, n, first, seed, counter);
+    uniform_kernel<<<grid, 256, 0, stream>>>(out, n, first, seed, counter, nullptr);
+    return cudaGetLastError();
+}
+
+__global__ void counter_kernel(uint64_t *c) { *c += 1; }
+
+cudaError_t ts_launch_uniform_dev(double *out, int64_t n, int64_t first, uint64_t seed, uint64_t *counter,
+                                  cudaStream_t stream) {
+    int grid = (int)((n + 255) / 256);
+    if (grid > 4096) grid = 4096;
+    uniform_kernel<<<grid, 256, 0, stream>>>(out, n, first, seed, 0, counter);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    counter_kernel<<<1, 1, 0, stream>>>(counter);   // stream order: after every read of *counter
     return cudaGetLastError();
 }
 

@@ -160,5 +160,7 @@ cudaError_t ts_launch_reset(const TsDevProg &P, const TsParams &S, const TsLaunc
                             const uint8_t *mask, int observe_only, cudaStream_t stream);
 cudaError_t ts_launch_check_actions(const void *actions, int actions_f32, int64_t n,
                                     int32_t *flag, cudaStream_t stream);
+cudaError_t ts_launch_uniform_dev(double *out, int64_t n, int64_t first, uint64_t seed, uint64_t *counter,
+                                  cudaStream_t stream);
 cudaError_t ts_launch_uniform(double *out, int64_t n, int64_t first, uint64_t seed, uint64_t counter,
                               cudaStream_t stream);

@@ -243,6 +243,42 @@ class EnvBatch:
             self._copy_done.record()
         return self._dev_actions, False, False
 
+    def capture_step(self, actions, pre=None, warmup=2):
+        """CUDA-graph one whole env step (command, fused step and epilogue kernels) for the
+        device-resident ``actions`` tensor, which the caller refills in place between replays
+        (or ``pre``, a callable captured in front of the step -- e.g. an on-device action draw).
+
+        Runs ``warmup`` real steps first (graph capture needs the lazily-grown device buffers to
+        exist), then captures.  Returns ``replay() -> (obs, reward, terminated, truncated, info)``;
+        the outputs live in fixed buffers that every replay overwrites.
+        """
+        if not self._ready:
+            raise RuntimeError("step called before reset")
+        if not (isinstance(actions, torch.Tensor) and actions.is_cuda):
+            raise ValidationError("capture_step needs device-resident actions")
+        dev = self.device
+        side = torch.cuda.Stream(dev)
+        side.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(side):
+            for _ in range(warmup):
+                if pre is not None:
+                    pre()
+                self.step(actions, validate=False)
+        torch.cuda.current_stream(dev).wait_stream(side)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            if pre is not None:
+                pre()
+            out = self.step(actions, validate=False)
+        self.sim.step_count -= 1          # the capture itself executes nothing
+
+        def replay():
+            graph.replay()
+            self.sim.step_count += 1
+            return out
+        replay.graph = graph
+        return replay
+
     def step(self, actions, validate=True, tool_override=None):
         """env.py:144-197 on the GPU.  Returns (obs, reward, terminated, truncated, info).
 
