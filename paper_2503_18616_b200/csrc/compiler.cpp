@@ -926,7 +926,12 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
             else if (w[v] != w_free) uniform = false;
         }
     const bool compact = o.compact >= 0 && uniform && Vstore <= 65535 && slot_cap <= 65535;
-    std::vector<uint32_t> edge_c(compact ? 4 * (size_t)nE : 0), tet_c(compact ? 4 * (size_t)nT : 0);
+    // fp32 gather programs: the compact tet stream and the edge records carry BYTE offsets
+    // (12 x position / slot index) so the kernel addresses shared memory without multiplies;
+    // the streams are padded by one CTA's worth of zero items so prefetches need no clamp
+    const bool boff = compact && eg && R == 4 && 12 * Vstore <= 65535 && 12 * slot_cap <= 65535;
+    const int scale_b = boff ? 12 : 1;
+    std::vector<uint32_t> edge_c(compact ? 4 * (size_t)nE : 0), tet_c(compact ? 4 * ((size_t)nT + B) : 0);
     if (compact) {
         auto pk = [](int lo, int hi) { return (uint32_t)(lo & 0xffff) | ((uint32_t)(hi & 0xffff) << 16); };
         for (int i = 0; i < nE; ++i) {
@@ -937,10 +942,10 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
             else { const float f = (float)rl; std::memcpy(&edge_c[4 * i + 2], &f, 4); edge_c[4 * i + 3] = 0; }
         }
         for (int i = 0; i < nT; ++i) {
-            tet_c[4 * i + 0] = pk(tet_idx[4 * i + 0], tet_idx[4 * i + 1]);
-            tet_c[4 * i + 1] = pk(tet_idx[4 * i + 2], tet_idx[4 * i + 3]);
-            tet_c[4 * i + 2] = pk(tet_slot[4 * i + 0], tet_slot[4 * i + 1]);
-            tet_c[4 * i + 3] = pk(tet_slot[4 * i + 2], tet_slot[4 * i + 3]);
+            tet_c[4 * i + 0] = pk(scale_b * tet_idx[4 * i + 0], scale_b * tet_idx[4 * i + 1]);
+            tet_c[4 * i + 1] = pk(scale_b * tet_idx[4 * i + 2], scale_b * tet_idx[4 * i + 3]);
+            tet_c[4 * i + 2] = pk(scale_b * tet_slot[4 * i + 0], scale_b * tet_slot[4 * i + 1]);
+            tet_c[4 * i + 3] = pk(scale_b * tet_slot[4 * i + 2], scale_b * tet_slot[4 * i + 3]);
         }
     }
 
@@ -969,7 +974,7 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
             eregion[g] = base;
             base += 32 * kmax;
         }
-        einc.assign((size_t)std::max(base, 1) * einc_bytes, 0);
+        einc.assign(((size_t)base + 32) * einc_bytes, 0);   // + one padding row: unclamped prefetch
         for (int p = 0; p < Vf; ++p) {
             const int self = s2o[p];
             evalence[p] = (int)lists[p].size();
@@ -981,7 +986,7 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
                 const int q = a == self ? b : a;
                 // bit 31: the neighbour is pinned (w = 0); with uniform free mass that fixes the
                 // weight ratio (compact fp32 records), and halo neighbours of a cluster part are free
-                const int32_t nbr = o2s[q] | (is_free(q) ? 0 : (int32_t)0x80000000u);
+                const int32_t nbr = (boff ? 12 * o2s[q] : o2s[q]) | (is_free(q) ? 0 : (int32_t)0x80000000u);
                 uint8_t *rec = einc.data() + (size_t)(eregion[p / 32] + 32 * k + p % 32) * einc_bytes;
                 std::memcpy(rec, &nbr, 4);
                 const double rl = d.rest_length[e];
@@ -1023,7 +1028,7 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
     sz[TS_SEC_EDGE_PAR] = 4LL * R * nE;
     sz[TS_SEC_TET_IDX] = 16LL * nT;
     sz[TS_SEC_TET_SLOT] = 16LL * nT;
-    sz[TS_SEC_TET_RV] = (int64_t)R * nT;
+    sz[TS_SEC_TET_RV] = (int64_t)R * (nT + B);   // padded like the compact stream
     sz[TS_SEC_ATT_IDX] = 16LL * nA;
     sz[TS_SEC_ATT_SLOT] = 16LL * nA;
     sz[TS_SEC_ATT_PAR] = 4LL * R * nA;
@@ -1054,6 +1059,7 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
     hdr.V = V; hdr.Vf = Vf; hdr.Vf_pad = Vf_pad; hdr.Vstore = Vstore;
     hdr.F = Floc; hdr.B = B; hdr.VPT = VPT; hdr.G = G;
     hdr.Vown = Vown; hdr.cluster_k = part ? part->K : 1; hdr.cluster_rank = part ? part->rank : 0;
+    hdr.boff = boff ? 1 : 0;
     hdr.n_chunks = n_chunks; hdr.grasp_chunk = grasp_chunk; hdr.slot_capacity = slot_cap; hdr.n_att = nA;
     hdr.n_edge_items = nE; hdr.n_tet_items = nT; hdr.n_att_items = nA; hdr.bank_conflicts = total_conf;
     hdr.n_slots_total = n_slots_total;

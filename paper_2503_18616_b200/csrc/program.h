@@ -72,6 +72,8 @@ struct TsChunk {
     int32_t val_off, conflicts, pad0, pad1;
 };
 
+#define TS_SMEM_HEAD 2048       // scalar block + capsule parameters, at the start of shared memory
+
 // Shared memory one CTA needs for a program (the kernel's carve, step_kernel.cuh): positions
 // (x2 when ping-ponged), slot buffer / contact records, degenerate counters, contact bitmap,
 // scalar block.
@@ -82,7 +84,7 @@ inline int ts_smem_layout_bytes(int Vstore, int slot_cap, int Vf_pad, int F, int
     b += (size_t)4 * Vf_pad;
     b += (size_t)4 * ((3 * F + 31) / 32);
     b = (b + 15) / 16 * 16;
-    b += 2048;
+    b += TS_SMEM_HEAD;
     return (int)b;
 }
 #define TS_SMEM_LIMIT 232448   // B200 opt-in shared memory per CTA (227 KiB)
@@ -103,7 +105,8 @@ struct TsProgHeader {
     int32_t n_chunks, grasp_chunk, slot_capacity, n_att;
     int32_t n_edge_items, n_tet_items, n_att_items, bank_conflicts;
     int32_t n_slots_total, compact, edge_gather, einc_bytes;
-    int32_t Vown, cluster_k, cluster_rank, pad3;   // Vown: end of the owned (written-back) positions
+    int32_t Vown, cluster_k, cluster_rank, boff;   // Vown: end of the owned (written-back) positions;
+                                                   // boff: fp32 compact streams hold byte offsets
     double w_free;   // the common inverse mass of free vertices (compact programs)
     int64_t off[TS_SEC_COUNT];
     int64_t total_bytes;

@@ -325,20 +325,21 @@ struct Smem {
 
 template <typename Real>
 __device__ __forceinline__ Smem<Real> carve(const TsDevProg &P, unsigned char *raw) {
-    // [scalar block | capsules | positions | ping-pong positions | slots | degenerate counters |
-    //  contact bitmap]: everything a cluster peer addresses over DSMEM (scalars, positions,
-    //  slot / record buffer, the contact key list in the counters) sits at the same offset in
-    //  every CTA of the cluster (parts share Vstore and the slot capacity)
-    static_assert(((sizeof(Scal) + 15) / 16) * 16 + 3 * sizeof(Cap<Real>) <= 2048, "scalar block");
+    // [scalar block | capsules | slots | positions | ping-pong positions | degenerate counters |
+    //  contact bitmap]: the slot buffer sits at a constant offset (no per-use address
+    //  arithmetic in phase 1), and everything a cluster peer addresses over DSMEM (scalars,
+    //  slots / contact records, positions, the contact key list in the counters) sits at the same
+    //  offset in every CTA of the cluster (parts share Vstore and the slot capacity)
+    static_assert(((sizeof(Scal) + 15) / 16) * 16 + 3 * sizeof(Cap<Real>) <= TS_SMEM_HEAD, "scalar block");
     Smem<Real> m;
     m.sc = reinterpret_cast<Scal *>(raw);
     m.caps = reinterpret_cast<Cap<Real> *>(raw + ((sizeof(Scal) + 15) / 16) * 16);
-    Real *pos = reinterpret_cast<Real *>(raw + 2048);
-    m.alt = P.edge_gather ? pos + 3 * P.Vstore : pos;
-    Real *slots = pos + 3 * P.Vstore * (P.edge_gather ? 2 : 1);
-    m.pos = pos;
+    Real *slots = reinterpret_cast<Real *>(raw + TS_SMEM_HEAD);
+    Real *pos = slots + 3 * P.slot_cap;
     m.slot = slots;
-    m.deg = reinterpret_cast<int *>(slots + 3 * P.slot_cap);
+    m.pos = pos;
+    m.alt = P.edge_gather ? pos + 3 * P.Vstore : pos;
+    m.deg = reinterpret_cast<int *>(pos + 3 * P.Vstore * (P.edge_gather ? 2 : 1));
     m.cbits = reinterpret_cast<unsigned *>(m.deg + P.Vf_pad);
     return m;
 }
@@ -444,12 +445,76 @@ __device__ __forceinline__ void store_slot(const Smem<Real> &m, int s, Real c, R
 template <typename Real>
 __device__ __forceinline__ void tet_item(const Smem<Real> &m, int4 id, int4 sl, Real rvi, Real kv, int vfp);
 
+// fp32 tet item on byte-offset streams (boff programs): q = {a | b << 16, c | d << 16, slot a | b << 16,
+// slot c | d << 16}, all byte offsets into the position / slot buffers (no index multiplies)
+__device__ __forceinline__ void tet_item_b(const char *pb, char *sb, int *deg, uint4 q, float rvi, float kv,
+                                           unsigned vfp_b) {
+    const unsigned oa = q.x & 0xffffu, ob = q.x >> 16, oc = q.y & 0xffffu, od = q.y >> 16;
+    auto ld = [&](unsigned o) { return *reinterpret_cast<const float *>(pb + o); };
+    const float ax = ld(oa), ay = ld(oa + 4), az = ld(oa + 8);
+    const float bax = ld(ob) - ax, bay = ld(ob + 4) - ay, baz = ld(ob + 8) - az;
+    const float cax = ld(oc) - ax, cay = ld(oc + 4) - ay, caz = ld(oc + 8) - az;
+    const float dax = ld(od) - ax, day = ld(od + 4) - ay, daz = ld(od + 8) - az;
+    // unscaled cross products G = 6 grad (rv holds 6 V0), as tet_item's fp32 branch
+    const float Gbx = __fmaf_rn(cay, daz, -caz * day);
+    const float Gby = __fmaf_rn(caz, dax, -cax * daz);
+    const float Gbz = __fmaf_rn(cax, day, -cay * dax);
+    const float Gcx = __fmaf_rn(day, baz, -daz * bay);
+    const float Gcy = __fmaf_rn(daz, bax, -dax * baz);
+    const float Gcz = __fmaf_rn(dax, bay, -day * bax);
+    const float Gdx = __fmaf_rn(bay, caz, -baz * cay);
+    const float Gdy = __fmaf_rn(baz, cax, -bax * caz);
+    const float Gdz = __fmaf_rn(bax, cay, -bay * cax);
+    const float Gax = -(Gbx + Gcx + Gdx);
+    const float Gay = -(Gby + Gcy + Gdy);
+    const float Gaz = -(Gbz + Gcz + Gdz);
+    const float c6 = __fmaf_rn(Gdz, daz, __fmaf_rn(Gdy, day, Gdx * dax)) - rvi;
+    float den = Gax * Gax;
+    den = __fmaf_rn(Gay, Gay, den); den = __fmaf_rn(Gaz, Gaz, den);
+    den = __fmaf_rn(Gbx, Gbx, den); den = __fmaf_rn(Gby, Gby, den); den = __fmaf_rn(Gbz, Gbz, den);
+    den = __fmaf_rn(Gcx, Gcx, den); den = __fmaf_rn(Gcy, Gcy, den); den = __fmaf_rn(Gcz, Gcz, den);
+    den = __fmaf_rn(Gdx, Gdx, den); den = __fmaf_rn(Gdy, Gdy, den); den = __fmaf_rn(Gdz, Gdz, den);
+    const bool degenerate = !(den > 3.6e-17f);                  // sum|grad|^2 <= 1e-18
+    const float sc = degenerate ? 0.0f : (-kv * c6) * rcp_ftz(den);
+    auto st3 = [&](unsigned o, float gx, float gy, float gz) {
+        float *d = reinterpret_cast<float *>(sb + o);
+        d[0] = sc * gx; d[1] = sc * gy; d[2] = sc * gz;
+    };
+    st3(q.z & 0xffffu, Gax, Gay, Gaz);
+    st3(q.z >> 16, Gbx, Gby, Gbz);
+    st3(q.w & 0xffffu, Gcx, Gcy, Gcz);
+    st3(q.w >> 16, Gdx, Gdy, Gdz);
+    if (degenerate) {
+        if (oa < vfp_b) atomicAdd(&deg[oa / 12], 1);
+        if (ob < vfp_b) atomicAdd(&deg[ob / 12], 1);
+        if (oc < vfp_b) atomicAdd(&deg[oc / 12], 1);
+        if (od < vfp_b) atomicAdd(&deg[od / 12], 1);
+    }
+}
+
 template <typename Real>
 __device__ __forceinline__ void p1_tets(const TsDevProg &P, const Smem<Real> &m, int begin, int count, Real kv) {
     const Real *rv = reinterpret_cast<const Real *>(P.tet_rv) + begin;
     const int vfp = P.Vf_pad;
     const int stride = blockDim.x;
     const int t = threadIdx.x;
+    if constexpr (sizeof(Real) == 4) {
+        if (P.boff) {   // byte-offset stream, padded by a CTA's worth of items: unclamped prefetch
+            const uint4 *it = P.tet_c + begin;
+            const char *pb = reinterpret_cast<const char *>(m.pos);
+            char *sb = reinterpret_cast<char *>(m.slot);   // == shared base + TS_SMEM_HEAD
+            uint4 nq = __ldg(it + t);
+            float nrv = __ldg(rv + t);
+            for (int i = t; i < count; i += stride) {
+                const uint4 q = nq;
+                const float rvi = nrv;
+                nq = __ldg(it + i + stride);
+                nrv = __ldg(rv + i + stride);
+                tet_item_b(pb, sb, m.deg, q, rvi, kv, 12u * (unsigned)vfp);
+            }
+            return;
+        }
+    }
     if (P.compact) {
         const uint4 *it = P.tet_c + begin;
         uint4 nq = make_uint4(0, 0, 0, 0);
@@ -626,6 +691,26 @@ __device__ __forceinline__ void owner_edges(const TsDevProg &P, const Smem<Real>
             const double c = -(wp * scale);
             ax = ax + c * dx; ay = ay + c * dy; az = az + c * dz;
             ndeg += mm == 0.0;
+        }
+    } else if (P.einc_bytes == 8 && P.boff) {
+        // byte-offset records, padded by one row: the prefetch of record k + 1 needs no clamp
+        const uint2 *rec = reinterpret_cast<const uint2 *>(P.einc) + rb;
+        const char *pb = reinterpret_cast<const char *>(m.pos);
+        const float hks = 0.5f * ks;
+        uint2 q = __ldg(rec);
+        for (int k = 0; k < ev; ++k) {
+            const uint2 cur = q;
+            q = __ldg(rec + 32 * (k + 1));
+            const unsigned nb = cur.x & 0x7fffffffu;
+            const float rl = __uint_as_float(cur.y);
+            const float *nq = reinterpret_cast<const float *>(pb + nb);
+            const float dx = px - nq[0], dy = py - nq[1], dz = pz - nq[2];
+            const float d2 = __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, dx * dx));
+            const bool degenerate = !(d2 >= 1e-24f);
+            const float f = degenerate ? 0.0f : __fmaf_rn(-rl, rsqrt_ftz(d2), 1.0f);
+            const float c = -((int)cur.x < 0 ? ks : hks) * f;
+            ax = __fmaf_rn(c, dx, ax); ay = __fmaf_rn(c, dy, ay); az = __fmaf_rn(c, dz, az);
+            ndeg += degenerate;
         }
     } else if (P.einc_bytes == 8) {
         // uniform free mass: coef = ks w / (w + w) = ks / 2, or ks when the neighbour is pinned

@@ -20,7 +20,7 @@ SECTIONS = ["CHUNK", "EDGE_IDX", "EDGE_PAR", "TET_IDX", "TET_SLOT", "TET_RV", "A
 HDR_FIELDS = ["magic", "version", "real_bytes", "n_sections", "V", "Vf", "Vf_pad", "Vstore", "F", "B",
               "VPT", "G", "n_chunks", "grasp_chunk", "slot_capacity", "n_att", "n_edge_items",
               "n_tet_items", "n_att_items", "bank_conflicts", "n_slots_total", "compact", "edge_gather",
-              "einc_bytes", "Vown", "cluster_k", "cluster_rank", "pad3"]
+              "einc_bytes", "Vown", "cluster_k", "cluster_rank", "boff"]
 
 
 class Program:
@@ -70,6 +70,9 @@ class Program:
             raw = self.sec("EINC", np.uint8, max(n, 1) * eb).reshape(-1, eb)
             word = raw[:, 0:4].copy().view(np.uint32)[:, 0]
             self.e_nbr = (word & 0x7FFFFFFF).astype(np.int32)
+            if H["boff"]:
+                assert np.all(self.e_nbr % 12 == 0)
+                self.e_nbr //= 12                               # fp32 records hold byte offsets
             self.e_nbr_pinned = (word >> 31).astype(bool)       # bit 31: neighbour pinned (w = 0)
             if eb == 8:
                 self.e_rest = raw[:, 4:8].copy().view(np.float32)[:, 0].astype(np.float64)
