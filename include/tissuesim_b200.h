@@ -93,8 +93,8 @@ typedef struct ts_layout_opts {
     int32_t schedule_banks;     /* 1 = bank-conflict-aware item schedule (default), -1 = off */
     int32_t smem_budget;        /* bytes of shared memory per CTA to aim for (0 = auto) */
     int32_t compact;            /* 16-bit item streams when possible (default), -1 = off */
-    int32_t edge_gather;        /* 1 = distance constraints gathered by the owner of each free vertex,
-                                   -1 = constraint-parallel phase 1 + slots, 0 = auto (fp32 gather) */
+    int32_t edge_gather;        /* distance constraints gathered by the owner of each free vertex
+                                   (default, 0/1), -1 = constraint-parallel phase 1 + slots */
     int32_t cluster_size;       /* CTAs per environment: 0 = auto (one CTA when the mesh fits, else the
                                    smallest thread-block cluster that holds it), 1 = one CTA, 2..16 */
 } ts_layout_opts;

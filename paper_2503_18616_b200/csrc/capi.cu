@@ -128,6 +128,7 @@ static void decode_part(const uint8_t *host, const uint8_t *b, TsDevProg &P) {
     P.send_off = reinterpret_cast<const int32_t *>(b + H->off[TS_SEC_SEND_OFF]);
     P.send = reinterpret_cast<const int32_t *>(b + H->off[TS_SEC_SEND]);
     P.face_own = reinterpret_cast<const int32_t *>(b + H->off[TS_SEC_FACE_OWN]);
+    P.wsplit = reinterpret_cast<const int32_t *>(b + H->off[TS_SEC_WSPLIT]);
 }
 
 static void fill_params(const ts_scene_desc &d, TsParams &S) {

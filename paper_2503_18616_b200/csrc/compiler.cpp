@@ -543,9 +543,9 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
 
     // edge_gather: distance constraints are gathered by the owner thread of each free vertex
     // (no phase-1 items, no slots); only attachments and tets go through slots
-    // (default for fp32; fp64 keeps slots: measured on B200, 4096 envs, reach_1170:
-    // fp32 0.867 vs 0.949 ms/step, fp64 4.47 vs 3.83 ms/step)
-    const bool eg = part || o.edge_gather > 0 || (o.edge_gather == 0 && o.precision == TS_F32);
+    // (the default; measured on B200, 4096 envs, reach_1170, with the gather done next to the
+    // phase-1 tets: fp32 0.677 vs 0.949 ms/step, fp64 3.58 vs 3.64 ms/step)
+    const bool eg = part || o.edge_gather >= 0;
 
     // ---- live constraints and per-vertex incidence counts ---------------
     std::vector<int> inc(V, 0), inc_e(V, 0);
@@ -1021,6 +1021,47 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
         }
     }
 
+    // ---- phase-1 work split across warps -------------------------------------
+    const int NW = B / 32;
+    std::vector<int32_t> wsplit((size_t)n_chunks * (NW + 1), 0);
+    {
+        const double CE = 1.0;   // owner-gathered edge incidence vs one tet item (tuned on B200, tools/tune.py)
+        double CT = 4.0;
+        if (const char *env = std::getenv("TS_SPLIT_CT")) CT = std::atof(env);
+        for (int c = 0; c < n_chunks; ++c) {
+            const int nt = chunk_rec[c].tet_count;
+            const int nb = (nt + 31) / 32;
+            std::vector<double> ce(NW, 0.0);
+            if (eg && c == 0)
+                for (int w = 0; w < NW; ++w)
+                    for (int lane = 0; lane < 32; ++lane) {
+                        int sum = 0;
+                        for (int r = 0; r < VPT; ++r) {
+                            const int p = r * B + 32 * w + lane;
+                            if (p < Vf) sum += evalence[p];
+                        }
+                        ce[w] = std::max(ce[w], CE * sum);
+                    }
+            // smallest level T with sum_w floor((T - ce_w) / CT) >= nb batches (32 items each)
+            double lo = 0.0, hi = 1e9;
+            auto fits = [&](double T) {
+                long tot = 0;
+                for (int w = 0; w < NW; ++w) tot += std::max(0L, (long)std::floor((T - ce[w]) / CT));
+                return tot >= nb;
+            };
+            for (int it = 0; it < 100; ++it) { const double mid = 0.5 * (lo + hi); (fits(mid) ? hi : lo) = mid; }
+            int left = nb, start = 0;
+            for (int w = 0; w < NW; ++w) {
+                int take = std::min(left, std::max(0, (int)std::floor((hi - ce[w]) / CT)));
+                if (w == NW - 1) take = left;
+                wsplit[(size_t)c * (NW + 1) + w] = std::min(start, nt);
+                start += 32 * take;
+                left -= take;
+            }
+            wsplit[(size_t)c * (NW + 1) + NW] = nt;
+        }
+    }
+
     // sizes (bytes) per section
     int64_t sz[TS_SEC_COUNT];
     sz[TS_SEC_CHUNK] = (int64_t)n_chunks * sizeof(TsChunk);
@@ -1052,6 +1093,7 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
     sz[TS_SEC_SEND_OFF] = 4LL * send_off.size();
     sz[TS_SEC_SEND] = 4LL * send.size();
     sz[TS_SEC_FACE_OWN] = 4LL * face_own.size();
+    sz[TS_SEC_WSPLIT] = 4LL * wsplit.size();
     TsProgHeader hdr{};
     hdr.compact = compact ? 1 : 0;
     hdr.w_free = w_free;
@@ -1092,6 +1134,7 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
     put(blob, hdr.off[TS_SEC_SEND_OFF], send_off);
     put(blob, hdr.off[TS_SEC_SEND], send);
     put(blob, hdr.off[TS_SEC_FACE_OWN], face_own);
+    put(blob, hdr.off[TS_SEC_WSPLIT], wsplit);
     auto put_real = [&](int sec, const std::vector<double> &v) {
         if (R == 8) put(blob, hdr.off[sec], v);
         else { std::vector<float> f(v.begin(), v.end()); put(blob, hdr.off[sec], f); }

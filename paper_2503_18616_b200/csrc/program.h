@@ -61,6 +61,11 @@ enum TsSection {
     TS_SEC_SEND_OFF,      // int32 [Vf_pad + 1] CSR offsets of the halo sends of owned free vertex p
     TS_SEC_SEND,          // int32 [n] (dest rank << 20) | dest storage position
     TS_SEC_FACE_OWN,      // int32 [F][3] (owner rank << 20) | owner position of a free face vertex, -1 pinned
+    // phase-1 work split: int32 [n_chunks][B/32 + 1] first tet item of each warp (relative to the
+    // chunk).  Contiguous ranges of 32-item batches, sized so that a warp's owner edge gather
+    // (done in phase 1 of chunk 0, it needs only the position snapshot) plus its tet items is
+    // about the same for every warp
+    TS_SEC_WSPLIT,
     TS_SEC_COUNT
 };
 

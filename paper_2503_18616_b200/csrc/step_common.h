@@ -80,6 +80,7 @@ struct TsDevProg {
     // cluster parts (cluster_k > 1): one CTA of an env's thread-block cluster
     int32_t Vown;             // end of the owned (written-back) storage positions
     int32_t boff;             // fp32 compact streams carry byte offsets (12 x index), padded
+    const int32_t *wsplit;    // [n_chunks][B/32 + 1] first tet item of each warp in a chunk
     int32_t cluster_k, cluster_rank;
     const int32_t *send_off;  // [Vf_pad + 1]
     const int32_t *send;      // (rank << 20) | storage position of a halo copy

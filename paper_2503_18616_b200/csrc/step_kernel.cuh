@@ -493,37 +493,38 @@ __device__ __forceinline__ void tet_item_b(const char *pb, char *sb, int *deg, u
 }
 
 template <typename Real>
-__device__ __forceinline__ void p1_tets(const TsDevProg &P, const Smem<Real> &m, int begin, int count, Real kv) {
+__device__ __forceinline__ void p1_tets(const TsDevProg &P, const Smem<Real> &m, int begin, int wb, int we, Real kv) {
+    // this warp's contiguous range [wb, we) of the chunk's items, lane l takes wb + l, wb + l + 32, ...
     const Real *rv = reinterpret_cast<const Real *>(P.tet_rv) + begin;
     const int vfp = P.Vf_pad;
-    const int stride = blockDim.x;
-    const int t = threadIdx.x;
+    const int lane = threadIdx.x & 31;
     if constexpr (sizeof(Real) == 4) {
         if (P.boff) {   // byte-offset stream, padded by a CTA's worth of items: unclamped prefetch
             const uint4 *it = P.tet_c + begin;
             const char *pb = reinterpret_cast<const char *>(m.pos);
             char *sb = reinterpret_cast<char *>(m.slot);   // == shared base + TS_SMEM_HEAD
-            uint4 nq = __ldg(it + t);
-            float nrv = __ldg(rv + t);
-            for (int i = t; i < count; i += stride) {
+            uint4 nq = __ldg(it + wb + lane);
+            float nrv = __ldg(rv + wb + lane);
+            for (int i = wb + lane; i < we; i += 32) {
                 const uint4 q = nq;
                 const float rvi = nrv;
-                nq = __ldg(it + i + stride);
-                nrv = __ldg(rv + i + stride);
+                nq = __ldg(it + i + 32);
+                nrv = __ldg(rv + i + 32);
                 tet_item_b(pb, sb, m.deg, q, rvi, kv, 12u * (unsigned)vfp);
             }
             return;
         }
     }
+    if (wb >= we) return;
     if (P.compact) {
         const uint4 *it = P.tet_c + begin;
         uint4 nq = make_uint4(0, 0, 0, 0);
         Real nrv = 0;
-        if (t < count) { nq = __ldg(it + t); nrv = rv[t]; }
-        for (int i = t; i < count; i += stride) {
+        if (wb + lane < we) { nq = __ldg(it + wb + lane); nrv = rv[wb + lane]; }
+        for (int i = wb + lane; i < we; i += 32) {
             const uint4 q = nq;
             const Real rvi = nrv;
-            { const int j = min(i + stride, count - 1); nq = __ldg(it + j); nrv = rv[j]; }
+            { const int j = min(i + 32, we - 1); nq = __ldg(it + j); nrv = rv[j]; }
             const int4 id = make_int4(q.x & 0xffff, q.x >> 16, q.y & 0xffff, q.y >> 16);
             const int4 sl = make_int4(q.z & 0xffff, q.z >> 16, q.w & 0xffff, q.w >> 16);
             tet_item<Real>(m, id, sl, rvi, kv, vfp);
@@ -534,13 +535,13 @@ __device__ __forceinline__ void p1_tets(const TsDevProg &P, const Smem<Real> &m,
     const int4 *slot = P.tet_slot + begin;
     int4 nid = make_int4(0, 0, 0, 0), nsl = make_int4(0, 0, 0, 0);
     Real nrv = 0;
-    if (t < count) { nid = __ldg(idx + t); nsl = __ldg(slot + t); nrv = rv[t]; }
-    for (int i = t; i < count; i += stride) {
+    if (wb + lane < we) { nid = __ldg(idx + wb + lane); nsl = __ldg(slot + wb + lane); nrv = rv[wb + lane]; }
+    for (int i = wb + lane; i < we; i += 32) {
         const int4 id = nid;
         const int4 sl = nsl;
         const Real rvi = nrv;
         {
-            const int j = min(i + stride, count - 1);
+            const int j = min(i + 32, we - 1);
             nid = __ldg(idx + j); nsl = __ldg(slot + j); nrv = rv[j];
         }
         tet_item<Real>(m, id, sl, rvi, kv, vfp);
@@ -1116,10 +1117,26 @@ __device__ __forceinline__ void step_env(const TsDevProg &P, const TsDevProg *pr
         for (int s = 0; s < S.substeps; ++s) {
             for (int c = 0; c < P.n_chunks; ++c) {
                 const TsChunk ch = P.chunks[c];
+                // owner-gathered edges need only the position snapshot: they run in phase 1 of the
+                // first chunk, next to this warp's share of the tets (the compiler sized the shares so
+                // that edges + tets take about the same time in every warp); they still come first in
+                // each vertex's sum, the reference order
+                if (P.edge_gather && c == 0) {
+#pragma unroll
+                    for (int r = 0; r < VPT; ++r) {
+                        const int p = r * B + t;
+                        if (p < P.Vf)
+                            owner_edges<Real>(P, m, p, lane, xr[r], yr[r], zr[r], ks, accx[r], accy[r], accz[r],
+                                              ndeg[r]);
+                    }
+                }
                 // phase 1: every kind of the chunk, no barrier in between (disjoint slots)
                 if (ch.edge_count) p1_edges<Real>(P, m, ch.edge_begin, ch.edge_count, ks);
                 if (ch.att_count) p1_atts<Real>(P, m, ch.att_begin, ch.att_count);
-                if (ch.tet_count) p1_tets<Real>(P, m, ch.tet_begin, ch.tet_count, kv);
+                if (ch.tet_count) {
+                    const int *ws = P.wsplit + c * (B / 32 + 1) + (t >> 5);
+                    p1_tets<Real>(P, m, ch.tet_begin, ws[0], ws[1], kv);
+                }
                 __syncthreads();
                 // phase 2: owner gathers its slots in reference order
                 const bool gchunk = c == P.grasp_chunk;
@@ -1131,8 +1148,6 @@ __device__ __forceinline__ void step_env(const TsDevProg &P, const TsDevProg *pr
                         const int val = P.valence[ch.val_off + p];
                         const int pre = gchunk ? P.gsplit[p] : val;
                         Real ax = accx[r], ay = accy[r], az = accz[r];
-                        if (P.edge_gather && c == 0)   // edges come first in the reference order
-                            owner_edges<Real>(P, m, p, lane, xr[r], yr[r], zr[r], ks, ax, ay, az, ndeg[r]);
 #pragma unroll 4
                         for (int k = 0; k < pre; ++k) {
                             const int sidx = base + 32 * k;

@@ -159,8 +159,7 @@ def layout_opts(precision="fp32", block_threads=0, max_chunk_slots=0, schedule_b
     o.max_chunk_slots = int(max_chunk_slots)
     o.schedule_banks = 1 if schedule_banks else -1
     o.compact = 1 if compact else -1
-    # None: the compiler's choice (owner gather for fp32; fp64 keeps constraint-parallel slots,
-    # where the per-incidence IEEE sqrt / div of the gather cost more than they save)
+    # None: the compiler's choice (owner gather); False: constraint-parallel edge slots
     o.edge_gather = 0 if edge_gather is None else (1 if edge_gather else -1)
     o.cluster_size = int(cluster_size)
     return o

@@ -16,7 +16,7 @@ import numpy as np
 SECTIONS = ["CHUNK", "EDGE_IDX", "EDGE_PAR", "TET_IDX", "TET_SLOT", "TET_RV", "ATT_IDX", "ATT_SLOT",
             "ATT_PAR", "ATT_ANCHOR", "REGION", "VALENCE", "STATIC_CNT", "S2O", "O2S", "W", "FACES",
             "FACES_ORIG", "REST", "GSPLIT", "EDGE_C", "TET_C", "EINC", "EREGION", "EVAL", "FACE_GID",
-            "SEND_OFF", "SEND", "FACE_OWN"]
+            "SEND_OFF", "SEND", "FACE_OWN", "WSPLIT"]
 HDR_FIELDS = ["magic", "version", "real_bytes", "n_sections", "V", "Vf", "Vf_pad", "Vstore", "F", "B",
               "VPT", "G", "n_chunks", "grasp_chunk", "slot_capacity", "n_att", "n_edge_items",
               "n_tet_items", "n_att_items", "bank_conflicts", "n_slots_total", "compact", "edge_gather",

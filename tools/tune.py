@@ -43,7 +43,10 @@ def main():
     chunks = [int(c) for c in os.environ.get("TS_CHUNKS", "0,4160,3000,2200,1600,1100").split(",")]
     blocks = [int(b) for b in os.environ.get("TS_BLOCKS", "0").split(",")]
     gathers = [int(g) for g in os.environ.get("TS_GATHER", "1").split(",")]
-    for prec, ch, bl, ga in itertools.product(precs, chunks, blocks, gathers):
+    cts = os.environ.get("TS_CTS", "").split(",") if os.environ.get("TS_CTS") else [None]
+    for prec, ch, bl, ga, ct in itertools.product(precs, chunks, blocks, gathers, cts):
+        if ct is not None:
+            os.environ["TS_SPLIT_CT"] = ct
         layout = {"edge_gather": bool(ga)}
         if ch:
             layout["max_chunk_slots"] = ch
@@ -51,7 +54,7 @@ def main():
             layout["block_threads"] = bl
         try:
             ms, info = time_layout(scene, n, prec, layout)
-            print(f"{prec} gather={ga} chunk={ch:5d} block={bl:4d}: {ms:.3f} ms/step  {n / ms * 1e3:12,.0f} env-steps/s  "
+            print(f"{prec} gather={ga} ct={ct} chunk={ch:5d} block={bl:4d}: {ms:.3f} ms/step  {n / ms * 1e3:12,.0f} env-steps/s  "
                   f"chunks={info['n_chunks']} slots={info['slot_capacity']} smem={info['smem_bytes']} "
                   f"conf={info['bank_conflicts_p1']}", flush=True)
         except Exception as exc:
