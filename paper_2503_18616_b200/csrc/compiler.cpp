@@ -49,6 +49,8 @@ inline int roundup(int x, int m) { return (x + m - 1) / m * m; }
 
 // effort of the bank-conflict searches (cluster parts compile K programs twice: a tenth)
 thread_local double g_search_effort = 1.0;
+// idle lanes allowed per 32-item tet batch (TS_TET_HOLES overrides; tuned on B200)
+int g_tet_holes = 0;
 
 template <typename T>
 void put(std::vector<uint8_t> &blob, int64_t off, const std::vector<T> &v) {
@@ -110,7 +112,7 @@ void local_search(std::vector<Item> &s, int bank_mod) {
 // order and the number of extra shared-memory wavefronts the residual
 // conflicts cost per pass over the chunk.
 std::vector<Item> schedule_items(std::vector<Item> items, int bank_mod, int batch, bool enable,
-                                 int *extra_wavefronts) {
+                                 int *extra_wavefronts, int max_holes = 0) {
     *extra_wavefronts = 0;
     if (!enable || items.size() <= 1) {
         // conflicts of the identity order, for reporting
@@ -163,13 +165,25 @@ std::vector<Item> schedule_items(std::vector<Item> items, int bank_mod, int batc
                 if ((int)pick.size() % bank_mod == 0) std::fill(used.begin(), used.end(), 0);
             }
         }
-        // fill the rest of the batch in index order
-        for (size_t i = first_free; i < items.size() && (int)pick.size() < batch; ++i) {
+        // lanes left without a conflict-free candidate: up to `max_holes` idle lanes (a dummy
+        // item the kernel skips: it costs issue slots but no shared-memory wavefronts, and the
+        // slack lets the banks of the remaining lanes stay distinct); the rest in index order
+        int holes = 0;
+        if (enable && done + pick.size() < items.size())
+            holes = std::min(max_holes, batch - (int)pick.size());
+        for (size_t i = first_free; i < items.size() && (int)pick.size() + holes < batch; ++i) {
             if (taken[i]) continue;
             pick.push_back((int)i);
             taken[i] = 1;
         }
         for (int i : pick) out.push_back(items[i]);
+        for (int hcount = 0; hcount < holes && (int)pick.size() + hcount < batch; ++hcount) {
+            Item dummy{};
+            dummy.kind = items.empty() ? TS_CHUNK_TET : items[0].kind;
+            dummy.index = -1;
+            dummy.nroles = 0;
+            out.push_back(dummy);
+        }
         done += pick.size();
     }
     if (enable && out.size() > (size_t)bank_mod) local_search(out, bank_mod);
@@ -299,8 +313,11 @@ void bank_refine(const std::vector<ListRef> &lists, std::vector<int> &o2s, std::
             if (sb_of[g1] == sb_of[g2]) continue;
             collect(sb_of[g1]); collect(sb_of[g2]);
         } else if (kind < 8) {                            // vertex swap inside a warp group / the pinned pool
-            u = item((int)(next() % n)).vid[next() % 2];
+            const Item &src = item((int)(next() % n));
+            if (src.nroles == 0) continue;   // idle lane of a batch
+            u = src.vid[next() % 2];
             const int pu = o2s[u];
+            if (pu < 0) continue;
             int pv;
             if (pu < Vf_pad) {
                 const int g = pu / 32;
@@ -519,6 +536,8 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
                     ts_layout_info &info, std::string &err, const PartSpec *part) {
     if (part && (int)part->own.size() != d.n_vert) { err = "part ownership mask size"; return TS_ERR_INVALID; }
     g_search_effort = part ? 0.1 : 1.0;
+    g_tet_holes = 0;   // measured: 2-8 idle lanes per batch cut conflicts but cost more issue (slower)
+    if (const char *env = std::getenv("TS_TET_HOLES")) g_tet_holes = std::atoi(env);
     const int V = d.n_vert, E = d.n_edge, T = d.n_tet, F = d.n_face, A = d.n_att;
     const int prec = o.precision;
     if (prec != TS_F32 && prec != TS_F64) { err = "precision must be TS_F32 or TS_F64"; return TS_ERR_INVALID; }
@@ -753,7 +772,10 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
             std::vector<Item> part;
             for (const Item &it : cb.items) if (it.kind == kind) { part.push_back(it); part.back().chunk = c; }
             int conf = 0;
-            std::vector<Item> s = schedule_items(part, bank_mod, 32, sched && kind != TS_CHUNK_ATT, &conf);
+            // tets may get idle lanes (TS_TET_HOLES per 32-item batch) where no conflict-free
+            // item is left; every tet still runs exactly once (off by default: slower on B200)
+            std::vector<Item> s = schedule_items(part, bank_mod, 32, sched && kind != TS_CHUNK_ATT, &conf,
+                                                 (kind == TS_CHUNK_TET && o.schedule_banks >= 0) ? g_tet_holes : 0);
             begin[k] = (int)all_items[k].size();
             count[k] = (int)s.size();
             all_items[k].insert(all_items[k].end(), s.begin(), s.end());
@@ -882,6 +904,11 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
     }
     for (int i = 0; i < nT; ++i) {
         const Item &it = all_items[2][i];
+        if (it.index < 0) {   // idle lane of a batch: slot -1 (compact: 0xffff) tells the kernel to skip it
+            for (int k = 0; k < 4; ++k) { tet_idx[4 * i + k] = 0; tet_slot[4 * i + k] = -1; }
+            tet_rv[i] = 0.0;
+            continue;
+        }
         for (int k = 0; k < 4; ++k) { tet_idx[4 * i + k] = it.pos[k]; tet_slot[4 * i + k] = it.slot[k]; }
         // fp32 build works with unscaled cross products G = 6 grad: it needs 6 V0
         tet_rv[i] = R == 8 ? d.rest_volume[it.index] : it.sign * 6.0 * d.rest_volume[it.index];
@@ -944,7 +971,8 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
         for (int i = 0; i < nT; ++i) {
             tet_c[4 * i + 0] = pk(scale_b * tet_idx[4 * i + 0], scale_b * tet_idx[4 * i + 1]);
             tet_c[4 * i + 1] = pk(scale_b * tet_idx[4 * i + 2], scale_b * tet_idx[4 * i + 3]);
-            tet_c[4 * i + 2] = pk(scale_b * tet_slot[4 * i + 0], scale_b * tet_slot[4 * i + 1]);
+            tet_c[4 * i + 2] = tet_slot[4 * i] < 0 ? 0xffffu   // idle lane (0xffff: never a slot offset)
+                                                   : pk(scale_b * tet_slot[4 * i + 0], scale_b * tet_slot[4 * i + 1]);
             tet_c[4 * i + 3] = pk(scale_b * tet_slot[4 * i + 2], scale_b * tet_slot[4 * i + 3]);
         }
     }

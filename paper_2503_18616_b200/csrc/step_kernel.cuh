@@ -510,7 +510,8 @@ __device__ __forceinline__ void p1_tets(const TsDevProg &P, const Smem<Real> &m,
                 const float rvi = nrv;
                 nq = __ldg(it + i + 32);
                 nrv = __ldg(rv + i + 32);
-                tet_item_b(pb, sb, m.deg, q, rvi, kv, 12u * (unsigned)vfp);
+                if ((q.z & 0xffffu) != 0xffffu)   // idle lane of the bank schedule
+                    tet_item_b(pb, sb, m.deg, q, rvi, kv, 12u * (unsigned)vfp);
             }
             return;
         }
@@ -527,7 +528,7 @@ __device__ __forceinline__ void p1_tets(const TsDevProg &P, const Smem<Real> &m,
             { const int j = min(i + 32, we - 1); nq = __ldg(it + j); nrv = rv[j]; }
             const int4 id = make_int4(q.x & 0xffff, q.x >> 16, q.y & 0xffff, q.y >> 16);
             const int4 sl = make_int4(q.z & 0xffff, q.z >> 16, q.w & 0xffff, q.w >> 16);
-            tet_item<Real>(m, id, sl, rvi, kv, vfp);
+            if (sl.x != 0xffff) tet_item<Real>(m, id, sl, rvi, kv, vfp);
         }
         return;
     }
@@ -544,7 +545,7 @@ __device__ __forceinline__ void p1_tets(const TsDevProg &P, const Smem<Real> &m,
             const int j = min(i + 32, we - 1);
             nid = __ldg(idx + j); nsl = __ldg(slot + j); nrv = rv[j];
         }
-        tet_item<Real>(m, id, sl, rvi, kv, vfp);
+        if (sl.x >= 0) tet_item<Real>(m, id, sl, rvi, kv, vfp);
     }
 }
 

@@ -172,9 +172,10 @@ class PartRun:
                     free = idx[:, pos] < H["Vf_pad"]
                     np.add.at(deg, idx[free & (m == 0), pos], 1)
             if tc:
-                idx = prog.tet_idx[tb:tb + tc]
-                sl = prog.tet_slot[tb:tb + tc]
-                rv = prog.tet_rv[tb:tb + tc]
+                live = prog.tet_slot[tb:tb + tc, 0] >= 0          # idle lanes of the bank schedule
+                idx = prog.tet_idx[tb:tb + tc][live]
+                sl = prog.tet_slot[tb:tb + tc][live]
+                rv = prog.tet_rv[tb:tb + tc][live]
                 pa = xs[idx[:, 0]]
                 ba, ca_, da = xs[idx[:, 1]] - pa, xs[idx[:, 2]] - pa, xs[idx[:, 3]] - pa
 

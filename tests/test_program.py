@@ -116,6 +116,10 @@ def test_slot_structure(reach_scene, gather):
                 continue
             sl = slots[b:b + n]
             idx = items[b:b + n, :roles]
+            if kind == 2:                       # idle lanes of the bank schedule (slot -1)
+                keep = sl[:, 0] >= 0
+                assert np.all(sl[~keep] == -1)
+                sl, idx = sl[keep], idx[keep]
             real = sl < padded
             assert np.all(real == (idx < H["Vf_pad"]))     # real slots exactly for free endpoints
             assert np.all(sl[~real] < padded + 32)          # pinned endpoints -> 32 trash slots
@@ -165,7 +169,8 @@ def test_schedule_is_permutation_and_reduces_conflicts(reach_scene):
     def constraints(p, idx, roles):
         vf = p.h["Vf_pad"]
         out = []
-        for row in idx[:, :roles]:
+        live = p.tet_slot[:, 0] >= 0 if roles == 4 else np.ones(len(idx), bool)
+        for row in idx[live][:, :roles]:
             if np.all(row >= vf):          # padding lane (pinned-only dummy edge)
                 continue
             out.append(tuple(sorted(int(p.s2o[q]) for q in row)))
@@ -204,9 +209,11 @@ def test_compact_streams_encode_the_full_program(reach_scene, precision):
     else:
         rl = p.edge_c[:, 2].copy().view(np.float32).astype(np.float64)
     assert np.array_equal(rl, p.edge_par[:, 0])
+    live = p.tet_slot[:, 0] >= 0
+    assert np.all(p.tet_c[~live, 2] == 0xFFFF)          # idle lanes: the kernel's skip sentinel
     for k in range(4):
-        assert np.array_equal((p.tet_c[:, k // 2] >> (16 * (k % 2))) & 0xFFFF, p.tet_idx[:, k])
-        assert np.array_equal((p.tet_c[:, 2 + k // 2] >> (16 * (k % 2))) & 0xFFFF, p.tet_slot[:, k])
+        assert np.array_equal(((p.tet_c[:, k // 2] >> (16 * (k % 2))) & 0xFFFF)[live], p.tet_idx[live, k])
+        assert np.array_equal(((p.tet_c[:, 2 + k // 2] >> (16 * (k % 2))) & 0xFFFF)[live], p.tet_slot[live, k])
 
 
 def test_nonuniform_mass_uses_full_streams(small_scene):

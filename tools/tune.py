@@ -44,9 +44,12 @@ def main():
     blocks = [int(b) for b in os.environ.get("TS_BLOCKS", "0").split(",")]
     gathers = [int(g) for g in os.environ.get("TS_GATHER", "1").split(",")]
     cts = os.environ.get("TS_CTS", "").split(",") if os.environ.get("TS_CTS") else [None]
-    for prec, ch, bl, ga, ct in itertools.product(precs, chunks, blocks, gathers, cts):
+    holes = os.environ.get("TS_HOLES", "").split(",") if os.environ.get("TS_HOLES") else [None]
+    for prec, ch, bl, ga, ct, ho in itertools.product(precs, chunks, blocks, gathers, cts, holes):
         if ct is not None:
             os.environ["TS_SPLIT_CT"] = ct
+        if ho is not None:
+            os.environ["TS_TET_HOLES"] = ho
         layout = {"edge_gather": bool(ga)}
         if ch:
             layout["max_chunk_slots"] = ch
@@ -54,7 +57,7 @@ def main():
             layout["block_threads"] = bl
         try:
             ms, info = time_layout(scene, n, prec, layout)
-            print(f"{prec} gather={ga} ct={ct} chunk={ch:5d} block={bl:4d}: {ms:.3f} ms/step  {n / ms * 1e3:12,.0f} env-steps/s  "
+            print(f"{prec} gather={ga} ct={ct} holes={ho} chunk={ch:5d} block={bl:4d}: {ms:.3f} ms/step  {n / ms * 1e3:12,.0f} env-steps/s  "
                   f"chunks={info['n_chunks']} slots={info['slot_capacity']} smem={info['smem_bytes']} "
                   f"conf={info['bank_conflicts_p1']}", flush=True)
         except Exception as exc:
