@@ -22,10 +22,10 @@ indexes the action stream so a shard reproduces the single-GPU envs.
 value  : device-timed throughput (inputs resident in HBM): CUDA events around
          each graph replay on the replaying stream, L2 flushed between timed
          steps (256 MiB write, untimed), max over ranks.
-e2e    : the same metric through the public API (EnvBatch.step) with HOST numpy
-         actions (H2D through pinned memory) and the step result read back to
-         the host (D2H of obs, reward, terminated, truncated) inside the timed
-         region.
+e2e    : the same metric through the public API with the reference's host
+         semantics (EnvBatch.step_numpy: numpy actions in through pinned memory,
+         numpy obs / reward / terminated / truncated / info out through one D2H
+         copy of the packed output block) inside the timed region.
 roofline: the binding roofline of this kernel is on-chip shared memory
          (SURVEY.md §8(d)); achieved = algorithmic bytes per env-step
          (substeps x (128 V + 88 E + 176 T) + 48 V + 64; 4,191,120 B for config 3)
@@ -297,17 +297,14 @@ def run_gpu(args, wl):
     rng = np.random.default_rng(1000 + rank)
     host_actions = [rng.uniform(-1.0, 1.0, (n, 3)) for _ in range(args.steps)]
     for i in range(min(2, args.warmup)):
-        o, r, te, tr, _ = env.step(host_actions[i])
-        o.cpu(), r.cpu(), te.cpu(), tr.cpu()
+        env.step_numpy(host_actions[i])
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize(dev)
     t0 = time.perf_counter()
-    d2h = 0
+    d2h = env._layout[1]            # the packed output block: obs, reward, flags, info arrays
     for i in range(args.steps):
-        o, r, te, tr, _ = env.step(host_actions[i])
-        res = (o.cpu(), r.cpu(), te.cpu(), tr.cpu())
-        d2h = sum(x.numel() * x.element_size() for x in res)
+        o, r, te, tr, _ = env.step_numpy(host_actions[i])   # numpy in / numpy out, reference semantics
     torch.cuda.synchronize(dev)
     e2e_s = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
     if world > 1:

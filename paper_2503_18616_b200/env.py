@@ -211,6 +211,7 @@ class EnvBatch:
     def _alloc_outputs(self):
         layout, total = self._layout
         buf = torch.empty(total, dtype=torch.uint8, device=self.device)
+        self._last_buf = buf
         return {name: buf[off:off + nb].view(dt).view(shape) for name, dt, shape, off, nb in layout}
 
     def _stage_actions(self, actions):
@@ -278,6 +279,35 @@ class EnvBatch:
             return out
         replay.graph = graph
         return replay
+
+    def step_numpy(self, actions):
+        """``step`` with the reference's host semantics (env.py:144-197): numpy actions in; numpy
+        obs / reward / terminated / truncated and an info dict of numpy arrays out
+        (``final_observation`` is None when no row is done, ``contacts`` an int).  One pinned H2D copy
+        of the actions and ONE D2H copy of the packed output block per call."""
+        self.step(actions)
+        layout, total = self._layout
+        if getattr(self, "_host_out", None) is None:
+            self._host_out = torch.empty(total, dtype=torch.uint8, pin_memory=True)
+            self._host_done = torch.cuda.Event()
+        with torch.cuda.device(self.device):
+            self._host_out.copy_(self._last_buf, non_blocking=True)
+            self._host_done.record()
+        self._host_done.synchronize()
+        raw = self._host_out.numpy()
+        out = {}
+        for name, dt, shape, off, nb in layout:
+            npdt = torch.empty(0, dtype=dt).numpy().dtype
+            out[name] = raw[off:off + nb].view(npdt).reshape(shape).copy()
+        done = out["done_mask"]
+        info = {
+            "distance": out["distance"], "success": out["success"], "diverged": out["diverged"],
+            "clipped": out["clipped"], "contacts": int(out["contacts"].sum()),
+            "contacts_per_env": out["contacts"], "episode_return": out["episode_return"],
+            "episode_length": out["episode_length"], "done_mask": done,
+            "final_observation": out["final_obs"] if done.any() else None,
+        }
+        return out["obs"], out["reward"], out["terminated"], out["truncated"], info
 
     def step(self, actions, validate=True, tool_override=None):
         """env.py:144-197 on the GPU.  Returns (obs, reward, terminated, truncated, info).
