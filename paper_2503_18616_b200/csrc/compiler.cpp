@@ -995,6 +995,45 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
             if (own_free(a)) lists[o2s[a]].push_back(e);
             if (own_free(b)) lists[o2s[b]].push_back(e);
         }
+        // fp32: the order of a vertex's edges is free (fp64 keeps edge-index order, the reference's
+        // summation order).  In round k the 32 lanes of a warp read their k-th neighbours: permute
+        // each lane's list so the neighbours of one round sit in distinct banks as far as possible
+        // (deterministic local search, sum over rounds of the largest bank multiplicity)
+        if (R == 4 && o.schedule_banks >= 0) {
+            uint64_t rs = 0x2545F4914F6CDD1Dull;
+            auto rnd = [&]() { rs ^= rs << 13; rs ^= rs >> 7; rs ^= rs << 17; return rs; };
+            auto other = [&](int p, int e) {
+                const int a = d.edges[2 * e], b = d.edges[2 * e + 1];
+                return o2s[a == s2o[p] ? b : a];
+            };
+            for (int g = 0; g < G; ++g) {
+                int kmax = 0;
+                for (int p = 32 * g; p < 32 * g + 32; ++p) kmax = std::max(kmax, (int)lists[p].size());
+                if (kmax < 2) continue;
+                std::vector<int> cnt((size_t)kmax * 32, 0);
+                auto bank = [&](int p, int k) { return other(p, lists[p][k]) % 32; };
+                for (int p = 32 * g; p < 32 * g + 32; ++p)
+                    for (int k = 0; k < (int)lists[p].size(); ++k) cnt[(size_t)k * 32 + bank(p, k)]++;
+                auto rmax = [&](int k) { int m = 0; for (int b = 0; b < 32; ++b) m = std::max(m, cnt[(size_t)k * 32 + b]); return m; };
+                const long iters = 4000L * kmax;
+                for (long it = 0; it < iters; ++it) {
+                    const int p = 32 * g + (int)(rnd() % 32);
+                    const int n = (int)lists[p].size();
+                    if (n < 2) continue;
+                    const int ka = (int)(rnd() % n), kb = (int)(rnd() % n);
+                    const int ba = bank(p, ka), bb = bank(p, kb);
+                    if (ka == kb || ba == bb) continue;
+                    const int before = rmax(ka) + rmax(kb);
+                    cnt[(size_t)ka * 32 + ba]--; cnt[(size_t)kb * 32 + ba]++;
+                    cnt[(size_t)kb * 32 + bb]--; cnt[(size_t)ka * 32 + bb]++;
+                    if (rmax(ka) + rmax(kb) <= before) std::swap(lists[p][ka], lists[p][kb]);
+                    else {
+                        cnt[(size_t)ka * 32 + ba]++; cnt[(size_t)kb * 32 + ba]--;
+                        cnt[(size_t)kb * 32 + bb]++; cnt[(size_t)ka * 32 + bb]--;
+                    }
+                }
+            }
+        }
         int base = 0;
         for (int g = 0; g < G; ++g) {
             int kmax = 0;
