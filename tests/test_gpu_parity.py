@@ -228,3 +228,30 @@ def test_contacts_detected_on_random_tissue_states(reach_scene):
                 assert np.array_equal(u, w)
             checked += len(a[0])
     assert checked > 1000
+
+
+def test_config1_single_env_1000_steps_bitwise(reach_scene):
+    """BASELINE config 1: one env, a 1000-step random-action rollout (ten 100-step episodes with
+    auto-resets) -- fp64 build with the oracle's tool poses: bitwise at every step."""
+    ref, gpu, out = run_pair(reach_scene, "fp64", 1, 1000, seed=21)
+    assert np.array_equal(gpu.sim.x.cpu().numpy(), ref.x) and np.array_equal(gpu.sim.v.cpu().numpy(), ref.v)
+    for rec in out:
+        ro, rr, rte, rtr, _ = rec["ref"]
+        go, gr, gte, gtr, _ = rec["gpu"]
+        assert np.array_equal(gr, rr) and np.array_equal(go, ro), rec["step"]
+        assert np.array_equal(gte, rte) and np.array_equal(gtr, rtr), rec["step"]
+    assert sum(int(rec["gpu"][2][0] or rec["gpu"][3][0]) for rec in out) >= 10   # >= 10 episodes ended
+
+
+def test_config2_distance_only_bitwise(reach_scene):
+    """BASELINE config 2: distance constraints only (tets emptied for the solver, as the reference's
+    tests do) -- the kernel's no-slot path (one barrier per substep), fp64 bitwise vs the oracle."""
+    import dataclasses
+    mesh, rest, cfg = reach_scene
+    scene = (dataclasses.replace(mesh, tets=np.zeros((0, 4), np.int32)),
+             dataclasses.replace(rest, rest_volume=np.zeros(0)), cfg)
+    ref, gpu, out = run_pair(scene, "fp64", 16, 60, seed=4)
+    assert gpu.sim.scene.info["n_chunks"] == 0
+    assert np.array_equal(gpu.sim.x.cpu().numpy(), ref.x) and np.array_equal(gpu.sim.v.cpu().numpy(), ref.v)
+    for rec in out:
+        assert np.array_equal(rec["gpu"][1], rec["ref"][1]), rec["step"]
