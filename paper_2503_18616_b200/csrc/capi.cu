@@ -129,6 +129,9 @@ static void decode_part(const uint8_t *host, const uint8_t *b, TsDevProg &P) {
     P.send = reinterpret_cast<const int32_t *>(b + H->off[TS_SEC_SEND]);
     P.face_own = reinterpret_cast<const int32_t *>(b + H->off[TS_SEC_FACE_OWN]);
     P.wsplit = reinterpret_cast<const int32_t *>(b + H->off[TS_SEC_WSPLIT]);
+    P.rvdict = H->rvdict;
+    P.rltab = reinterpret_cast<const float *>(b + H->off[TS_SEC_RLTAB]);
+    P.rvtab = reinterpret_cast<const float *>(b + H->off[TS_SEC_RVTAB]);
 }
 
 static void fill_params(const ts_scene_desc &d, TsParams &S) {

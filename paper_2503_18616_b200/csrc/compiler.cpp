@@ -958,6 +958,22 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
     // the streams are padded by one CTA's worth of zero items so prefetches need no clamp
     const bool boff = compact && eg && R == 4 && 12 * Vstore <= 65535 && 12 * slot_cap <= 65535;
     const int scale_b = boff ? 12 : 1;
+    // rest volumes as a dictionary index in the spare top bits of the four 16-bit position
+    // offsets (2 bits each; needs 12 Vstore < 16384) when few distinct 6 V0 values exist
+    std::vector<float> rv_tab;
+    std::vector<int> rv_idx(nT, 0);
+    if (boff && 12 * Vstore < 16384) {
+        std::vector<float> vals;
+        for (int i = 0; i < nT; ++i) if (all_items[2][i].index >= 0) vals.push_back((float)tet_rv[i]);
+        std::sort(vals.begin(), vals.end());
+        vals.erase(std::unique(vals.begin(), vals.end()), vals.end());
+        if (!vals.empty() && (int)vals.size() <= 256) {
+            rv_tab = vals;
+            for (int i = 0; i < nT; ++i)
+                if (all_items[2][i].index >= 0)
+                    rv_idx[i] = (int)(std::lower_bound(vals.begin(), vals.end(), (float)tet_rv[i]) - vals.begin());
+        }
+    }
     std::vector<uint32_t> edge_c(compact ? 4 * (size_t)nE : 0), tet_c(compact ? 4 * ((size_t)nT + B) : 0);
     if (compact) {
         auto pk = [](int lo, int hi) { return (uint32_t)(lo & 0xffff) | ((uint32_t)(hi & 0xffff) << 16); };
@@ -971,6 +987,11 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
         for (int i = 0; i < nT; ++i) {
             tet_c[4 * i + 0] = pk(scale_b * tet_idx[4 * i + 0], scale_b * tet_idx[4 * i + 1]);
             tet_c[4 * i + 1] = pk(scale_b * tet_idx[4 * i + 2], scale_b * tet_idx[4 * i + 3]);
+            if (!rv_tab.empty()) {   // index bits 2k, 2k+1 in bits 14-15 of 16-bit field k
+                const uint32_t r = (uint32_t)rv_idx[i];
+                tet_c[4 * i + 0] |= ((r & 3u) << 14) | (((r >> 2) & 3u) << 30);
+                tet_c[4 * i + 1] |= (((r >> 4) & 3u) << 14) | (((r >> 6) & 3u) << 30);
+            }
             tet_c[4 * i + 2] = tet_slot[4 * i] < 0 ? 0xffffu   // idle lane (0xffff: never a slot offset)
                                                    : pk(scale_b * tet_slot[4 * i + 0], scale_b * tet_slot[4 * i + 1]);
             tet_c[4 * i + 3] = pk(scale_b * tet_slot[4 * i + 2], scale_b * tet_slot[4 * i + 3]);
@@ -983,7 +1004,24 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
     //   -(w_p scale) (x_p - x_q),  scale = m ks (dist - rest) / (dist (w_a + w_b) + (1 - m)),
     // bitwise the reference's (-w_a scale) dx for p = a and (w_b scale) dx for p = b, since
     // x_b - x_a = -(x_a - x_b) exactly and the squares / weight sum are symmetric.
-    const int einc_bytes = eg ? ((R == 4 && compact) ? 8 : 16) : 0;
+    // fp32 byte-offset programs whose rest lengths take few distinct fp32 values (a structured
+    // slab has 2) use 4-byte records: {neighbour offset (16) | rest-length index (15) | pinned (1)}
+    // with the lengths in a small table -- half the L1 footprint of the edge stream
+    std::vector<float> rl_tab;
+    std::vector<int> rl_idx(E, -1);
+    if (eg && boff && 12 * Vstore <= 65535) {
+        std::vector<float> vals;
+        for (int e = 0; e < E; ++e) if (edge_live[e]) vals.push_back((float)d.rest_length[e]);
+        std::sort(vals.begin(), vals.end());
+        vals.erase(std::unique(vals.begin(), vals.end()), vals.end());
+        if ((int)vals.size() <= 256) {
+            rl_tab = vals;
+            for (int e = 0; e < E; ++e)
+                if (edge_live[e])
+                    rl_idx[e] = (int)(std::lower_bound(vals.begin(), vals.end(), (float)d.rest_length[e]) - vals.begin());
+        }
+    }
+    const int einc_bytes = eg ? (!rl_tab.empty() ? 4 : ((R == 4 && compact) ? 8 : 16)) : 0;
     std::vector<int32_t> eregion(eg ? G : 0, 0), evalence(eg ? Vf_pad : 0, 0);
     std::vector<uint8_t> einc;
     int n_einc = 0;
@@ -1055,8 +1093,14 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
                 // weight ratio (compact fp32 records), and halo neighbours of a cluster part are free
                 const int32_t nbr = (boff ? 12 * o2s[q] : o2s[q]) | (is_free(q) ? 0 : (int32_t)0x80000000u);
                 uint8_t *rec = einc.data() + (size_t)(eregion[p / 32] + 32 * k + p % 32) * einc_bytes;
-                std::memcpy(rec, &nbr, 4);
                 const double rl = d.rest_length[e];
+                if (einc_bytes == 4) {
+                    const uint32_t word = (uint32_t)(nbr & 0xffff) | ((uint32_t)rl_idx[e] << 16) |
+                                          ((uint32_t)nbr & 0x80000000u);
+                    std::memcpy(rec, &word, 4);
+                    continue;
+                }
+                std::memcpy(rec, &nbr, 4);
                 if (einc_bytes == 8) {
                     const float f = (float)rl;
                     std::memcpy(rec + 4, &f, 4);
@@ -1161,6 +1205,8 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
     sz[TS_SEC_SEND] = 4LL * send.size();
     sz[TS_SEC_FACE_OWN] = 4LL * face_own.size();
     sz[TS_SEC_WSPLIT] = 4LL * wsplit.size();
+    sz[TS_SEC_RLTAB] = 4LL * rl_tab.size();
+    sz[TS_SEC_RVTAB] = 4LL * rv_tab.size();
     TsProgHeader hdr{};
     hdr.compact = compact ? 1 : 0;
     hdr.w_free = w_free;
@@ -1169,6 +1215,7 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
     hdr.F = Floc; hdr.B = B; hdr.VPT = VPT; hdr.G = G;
     hdr.Vown = Vown; hdr.cluster_k = part ? part->K : 1; hdr.cluster_rank = part ? part->rank : 0;
     hdr.boff = boff ? 1 : 0;
+    hdr.rvdict = rv_tab.empty() ? 0 : 1;
     hdr.n_chunks = n_chunks; hdr.grasp_chunk = grasp_chunk; hdr.slot_capacity = slot_cap; hdr.n_att = nA;
     hdr.n_edge_items = nE; hdr.n_tet_items = nT; hdr.n_att_items = nA; hdr.bank_conflicts = total_conf;
     hdr.n_slots_total = n_slots_total;
@@ -1202,6 +1249,8 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
     put(blob, hdr.off[TS_SEC_SEND], send);
     put(blob, hdr.off[TS_SEC_FACE_OWN], face_own);
     put(blob, hdr.off[TS_SEC_WSPLIT], wsplit);
+    put(blob, hdr.off[TS_SEC_RLTAB], rl_tab);
+    put(blob, hdr.off[TS_SEC_RVTAB], rv_tab);
     auto put_real = [&](int sec, const std::vector<double> &v) {
         if (R == 8) put(blob, hdr.off[sec], v);
         else { std::vector<float> f(v.begin(), v.end()); put(blob, hdr.off[sec], f); }

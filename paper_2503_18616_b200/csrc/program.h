@@ -66,6 +66,8 @@ enum TsSection {
     // (done in phase 1 of chunk 0, it needs only the position snapshot) plus its tet items is
     // about the same for every warp
     TS_SEC_WSPLIT,
+    TS_SEC_RLTAB,         // float [] distinct rest lengths (4-byte edge records index it)
+    TS_SEC_RVTAB,         // float [] distinct 6 V0 values (rvdict programs: index in the tet stream)
     TS_SEC_COUNT
 };
 
@@ -112,6 +114,7 @@ struct TsProgHeader {
     int32_t n_slots_total, compact, edge_gather, einc_bytes;
     int32_t Vown, cluster_k, cluster_rank, boff;   // Vown: end of the owned (written-back) positions;
                                                    // boff: fp32 compact streams hold byte offsets
+    int32_t rvdict, pad4;                          // rvdict: tet rest volumes dictionary-coded
     double w_free;   // the common inverse mass of free vertices (compact programs)
     int64_t off[TS_SEC_COUNT];
     int64_t total_bytes;

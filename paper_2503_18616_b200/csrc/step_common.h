@@ -81,6 +81,9 @@ struct TsDevProg {
     int32_t Vown;             // end of the owned (written-back) storage positions
     int32_t boff;             // fp32 compact streams carry byte offsets (12 x index), padded
     const int32_t *wsplit;    // [n_chunks][B/32 + 1] first tet item of each warp in a chunk
+    int32_t rvdict;           // tet 6 V0 as a dictionary index in the stream's spare bits
+    const float *rltab;       // distinct rest lengths (4-byte edge records)
+    const float *rvtab;       // distinct 6 V0 values (rvdict)
     int32_t cluster_k, cluster_rank;
     const int32_t *send_off;  // [Vf_pad + 1]
     const int32_t *send;      // (rank << 20) | storage position of a halo copy

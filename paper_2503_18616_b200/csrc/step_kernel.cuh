@@ -448,8 +448,9 @@ __device__ __forceinline__ void tet_item(const Smem<Real> &m, int4 id, int4 sl, 
 // fp32 tet item on byte-offset streams (boff programs): q = {a | b << 16, c | d << 16, slot a | b << 16,
 // slot c | d << 16}, all byte offsets into the position / slot buffers (no index multiplies)
 __device__ __forceinline__ void tet_item_b(const char *pb, char *sb, int *deg, uint4 q, float rvi, float kv,
-                                           unsigned vfp_b) {
-    const unsigned oa = q.x & 0xffffu, ob = q.x >> 16, oc = q.y & 0xffffu, od = q.y >> 16;
+                                           unsigned vfp_b, unsigned pmask) {
+    // pmask = 0x3fff when the top two bits of each position field carry the 6 V0 dictionary index
+    const unsigned oa = q.x & pmask, ob = (q.x >> 16) & pmask, oc = q.y & pmask, od = (q.y >> 16) & pmask;
     auto ld = [&](unsigned o) { return *reinterpret_cast<const float *>(pb + o); };
     const float ax = ld(oa), ay = ld(oa + 4), az = ld(oa + 8);
     const float bax = ld(ob) - ax, bay = ld(ob + 4) - ay, baz = ld(ob + 8) - az;
@@ -504,6 +505,17 @@ __device__ __forceinline__ void p1_tets(const TsDevProg &P, const Smem<Real> &m,
             const char *pb = reinterpret_cast<const char *>(m.pos);
             char *sb = reinterpret_cast<char *>(m.slot);   // == shared base + TS_SMEM_HEAD
             uint4 nq = __ldg(it + wb + lane);
+            if (P.rvdict) {   // rest volume from the stream's spare bits + a tiny (L1-resident) table
+                for (int i = wb + lane; i < we; i += 32) {
+                    const uint4 q = nq;
+                    nq = __ldg(it + i + 32);
+                    const unsigned ri = ((q.x >> 14) & 3u) | ((q.x >> 28) & 12u) | ((q.y >> 10) & 48u) |
+                                        ((q.y >> 24) & 192u);
+                    if ((q.z & 0xffffu) != 0xffffu)   // idle lane of the bank schedule
+                        tet_item_b(pb, sb, m.deg, q, __ldg(P.rvtab + ri), kv, 12u * (unsigned)vfp, 0x3fffu);
+                }
+                return;
+            }
             float nrv = __ldg(rv + wb + lane);
             for (int i = wb + lane; i < we; i += 32) {
                 const uint4 q = nq;
@@ -511,7 +523,7 @@ __device__ __forceinline__ void p1_tets(const TsDevProg &P, const Smem<Real> &m,
                 nq = __ldg(it + i + 32);
                 nrv = __ldg(rv + i + 32);
                 if ((q.z & 0xffffu) != 0xffffu)   // idle lane of the bank schedule
-                    tet_item_b(pb, sb, m.deg, q, rvi, kv, 12u * (unsigned)vfp);
+                    tet_item_b(pb, sb, m.deg, q, rvi, kv, 12u * (unsigned)vfp, 0xffffu);
             }
             return;
         }
@@ -693,6 +705,25 @@ __device__ __forceinline__ void owner_edges(const TsDevProg &P, const Smem<Real>
             const double c = -(wp * scale);
             ax = ax + c * dx; ay = ay + c * dy; az = az + c * dz;
             ndeg += mm == 0.0;
+        }
+    } else if (P.einc_bytes == 4) {
+        // 4-byte records: {neighbour byte offset | rest-length index << 16 | pinned << 31}
+        const unsigned *rec = reinterpret_cast<const unsigned *>(P.einc) + rb;
+        const char *pb = reinterpret_cast<const char *>(m.pos);
+        const float hks = 0.5f * ks;
+        unsigned q = __ldg(rec);
+        for (int k = 0; k < ev; ++k) {
+            const unsigned cur = q;
+            q = __ldg(rec + 32 * (k + 1));
+            const float *nq = reinterpret_cast<const float *>(pb + (cur & 0xffffu));
+            const float rl = __ldg(P.rltab + ((cur >> 16) & 0x7fffu));
+            const float dx = px - nq[0], dy = py - nq[1], dz = pz - nq[2];
+            const float d2 = __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, dx * dx));
+            const bool degenerate = !(d2 >= 1e-24f);
+            const float f = degenerate ? 0.0f : __fmaf_rn(-rl, rsqrt_ftz(d2), 1.0f);
+            const float c = -((int)cur < 0 ? ks : hks) * f;
+            ax = __fmaf_rn(c, dx, ax); ay = __fmaf_rn(c, dy, ay); az = __fmaf_rn(c, dz, az);
+            ndeg += degenerate;
         }
     } else if (P.einc_bytes == 8 && P.boff) {
         // byte-offset records, padded by one row: the prefetch of record k + 1 needs no clamp

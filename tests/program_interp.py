@@ -16,11 +16,11 @@ import numpy as np
 SECTIONS = ["CHUNK", "EDGE_IDX", "EDGE_PAR", "TET_IDX", "TET_SLOT", "TET_RV", "ATT_IDX", "ATT_SLOT",
             "ATT_PAR", "ATT_ANCHOR", "REGION", "VALENCE", "STATIC_CNT", "S2O", "O2S", "W", "FACES",
             "FACES_ORIG", "REST", "GSPLIT", "EDGE_C", "TET_C", "EINC", "EREGION", "EVAL", "FACE_GID",
-            "SEND_OFF", "SEND", "FACE_OWN", "WSPLIT"]
+            "SEND_OFF", "SEND", "FACE_OWN", "WSPLIT", "RLTAB", "RVTAB"]
 HDR_FIELDS = ["magic", "version", "real_bytes", "n_sections", "V", "Vf", "Vf_pad", "Vstore", "F", "B",
               "VPT", "G", "n_chunks", "grasp_chunk", "slot_capacity", "n_att", "n_edge_items",
               "n_tet_items", "n_att_items", "bank_conflicts", "n_slots_total", "compact", "edge_gather",
-              "einc_bytes", "Vown", "cluster_k", "cluster_rank", "boff"]
+              "einc_bytes", "Vown", "cluster_k", "cluster_rank", "boff", "rvdict", "pad4"]
 
 
 class Program:
@@ -69,12 +69,20 @@ class Program:
             n = int(self.eregion[-1] + 32 * self.evalence[32 * (G - 1):32 * G].max()) if G else 0
             raw = self.sec("EINC", np.uint8, max(n, 1) * eb).reshape(-1, eb)
             word = raw[:, 0:4].copy().view(np.uint32)[:, 0]
+            if eb == 4:                                         # {offset | rest index << 16 | pinned << 31}
+                n_rl = int((self.off[SECTIONS.index("RVTAB")] - self.off[SECTIONS.index("RLTAB")]) // 4)
+                tab = self.sec("RLTAB", np.float32, n_rl).astype(np.float64)
+                self.e_rest = tab[(word >> 16) & 0x7FFF]
+                self.e_coef = None
+                word = (word & 0xFFFF) | (word & 0x80000000)
             self.e_nbr = (word & 0x7FFFFFFF).astype(np.int32)
             if H["boff"]:
                 assert np.all(self.e_nbr % 12 == 0)
                 self.e_nbr //= 12                               # fp32 records hold byte offsets
             self.e_nbr_pinned = (word >> 31).astype(bool)       # bit 31: neighbour pinned (w = 0)
-            if eb == 8:
+            if eb == 4:
+                pass
+            elif eb == 8:
                 self.e_rest = raw[:, 4:8].copy().view(np.float32)[:, 0].astype(np.float64)
                 self.e_coef = None
             elif H["real_bytes"] == 8:

@@ -148,7 +148,7 @@ def test_edge_gather_records(reach_scene, precision):
     blob, info = S.compile_program(_arrays(reach_scene), precision=precision, edge_gather=True)
     p = PI.Program(blob)
     w = rest.inverse_mass
-    assert p.h["einc_bytes"] == (8 if precision == "fp32" else 16)
+    assert p.h["einc_bytes"] == (4 if precision == "fp32" else 16)      # fp32: dictionary-coded rest lengths
     assert info["n_edge_items"] == 0            # no phase-1 edge items, no edge slots
     rt = np.float32 if precision == "fp32" else np.float64
     for pos in range(p.h["Vf"]):
@@ -317,3 +317,20 @@ def test_large_presets_compile_to_clusters():
     assert info["n_free"] == int((sc[1].inverse_mass > 0).sum())
     with pytest.raises(Exception, match="too large|shared memory"):
         S.compile_program(_arrays(sc), precision="fp32", cluster_size=1)
+
+
+def test_dictionary_coded_streams(reach_scene):
+    """fp32 byte-offset programs of a structured slab: rest lengths and 6 V0 take two fp32 values
+    each, so the edge records shrink to 4 bytes and the tet stream carries a 6 V0 index in the
+    spare top bits of its position offsets -- decoding them gives back exactly the full arrays."""
+    blob, info = S.compile_program(_arrays(reach_scene), precision="fp32")
+    p = PI.Program(blob)
+    assert p.h["einc_bytes"] == 4 and p.h["rvdict"] == 1
+    live = p.tet_slot[:, 0] >= 0
+    n_rv = len(np.unique(p.tet_rv[live].astype(np.float32)))
+    rvtab = p.sec("RVTAB", np.float32, n_rv)
+    q = p.tet_c[: len(p.tet_rv)]
+    ri = ((q[:, 0] >> 14) & 3) | ((q[:, 0] >> 28) & 12) | ((q[:, 1] >> 10) & 48) | ((q[:, 1] >> 24) & 192)
+    assert np.array_equal(rvtab[ri[live]].astype(np.float64), p.tet_rv[live])
+    offs = np.stack([q[:, 0] & 0x3FFF, (q[:, 0] >> 16) & 0x3FFF, q[:, 1] & 0x3FFF, (q[:, 1] >> 16) & 0x3FFF], 1)
+    assert np.array_equal(offs[live], 12 * p.tet_idx[live])
