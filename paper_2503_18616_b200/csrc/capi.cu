@@ -155,6 +155,10 @@ static void fill_params(const ts_scene_desc &d, TsParams &S) {
     S.w_l = d.w_distance; S.w_d = d.w_delta; S.w_s = d.w_success; S.reward_scale = d.reward_scale;
     S.max_steps = d.max_episode_steps; S.start_distance = d.start_distance;
     S.n_face = d.n_face;
+    // development ablation switch (results are wrong when set): 1 tets, 2 slot sums, 4 edge
+    // gather, 8 contacts, 16 grasp search, 64 the whole substep loop
+    S.ablate = 0;
+    if (const char *env = std::getenv("TS_ABLATE")) S.ablate = std::atoi(env);
     ts_finish_params(S);
 }
 

@@ -33,6 +33,7 @@ struct TsParams {
     int64_t max_steps;
     double start_distance, target_obs[3];
     int64_t n_face;           // surface faces of the whole mesh (detect_contacts row capacity 3F)
+    int32_t ablate, pad_a;    // development only (TS_ABLATE env var): skip phases to time them
     // fp32 copies of the solver constants (read straight from the constant bank by the fp32 build)
     float h_f, inv_h_f, damp_f, g_f[3], ks_f, hks_f, kv_f, pad_f;
 };

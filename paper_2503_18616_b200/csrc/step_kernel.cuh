@@ -1063,7 +1063,7 @@ __device__ __forceinline__ void step_env(const TsDevProg &P, const TsDevProg *pr
         __syncthreads();
     }
     // ---- B. grasp search: nearest free vertex (tool.py:380-389) ------
-    if (sc.need_search) {
+    if (sc.need_search && !(S.ablate & 16)) {
         double bk = INFINITY;
         int bi = 0x7fffffff;
         for (int p = t; p < P.Vf; p += B) {
@@ -1115,7 +1115,7 @@ __device__ __forceinline__ void step_env(const TsDevProg &P, const TsDevProg *pr
     const int gvs = sc.gv_orig >= 0 ? P.o2s[sc.gv_orig] : -1;
 
     // ---- C. substeps ---------------------------------------------------
-    if (mode & TS_M_SUBSTEPS) {
+    if ((mode & TS_M_SUBSTEPS) && !(S.ablate & 64)) {
         Real xr[VPT], yr[VPT], zr[VPT], accx[VPT], accy[VPT], accz[VPT];
         int ndeg[VPT], gcnt[VPT];
 #pragma unroll
@@ -1153,7 +1153,7 @@ __device__ __forceinline__ void step_env(const TsDevProg &P, const TsDevProg *pr
                 // first chunk, next to this warp's share of the tets (the compiler sized the shares so
                 // that edges + tets take about the same time in every warp); they still come first in
                 // each vertex's sum, the reference order
-                if (P.edge_gather && c == 0) {
+                if (P.edge_gather && c == 0 && !(S.ablate & 4)) {
 #pragma unroll
                     for (int r = 0; r < VPT; ++r) {
                         const int p = r * B + t;
@@ -1165,7 +1165,7 @@ __device__ __forceinline__ void step_env(const TsDevProg &P, const TsDevProg *pr
                 // phase 1: every kind of the chunk, no barrier in between (disjoint slots)
                 if (ch.edge_count) p1_edges<Real>(P, m, ch.edge_begin, ch.edge_count, ks);
                 if (ch.att_count) p1_atts<Real>(P, m, ch.att_begin, ch.att_count);
-                if (ch.tet_count) {
+                if (ch.tet_count && !(S.ablate & 1)) {
                     const int *ws = P.wsplit + c * (B / 32 + 1) + (t >> 5);
                     p1_tets<Real>(P, m, ch.tet_begin, ws[0], ws[1], kv);
                 }
@@ -1177,8 +1177,8 @@ __device__ __forceinline__ void step_env(const TsDevProg &P, const TsDevProg *pr
                     const int p = r * B + t;
                     if (p < P.Vf) {
                         const int base = P.region[ch.region_off + (p >> 5)] + lane;
-                        const int val = P.valence[ch.val_off + p];
-                        const int pre = gchunk ? P.gsplit[p] : val;
+                        const int val = (S.ablate & 2) ? 0 : P.valence[ch.val_off + p];
+                        const int pre = gchunk ? min(val, P.gsplit[p]) : val;
                         Real ax = accx[r], ay = accy[r], az = accz[r];
 #pragma unroll 4
                         for (int k = 0; k < pre; ++k) {
@@ -1256,7 +1256,7 @@ __device__ __forceinline__ void step_env(const TsDevProg &P, const TsDevProg *pr
     }
 
     // ---- D. contacts ---------------------------------------------------
-    if ((mode & (TS_M_CONTACTS | TS_M_DETECT_ONLY)) && (CL || P.F > 0)) {
+    if ((mode & (TS_M_CONTACTS | TS_M_DETECT_ONLY)) && (CL || P.F > 0) && !(S.ablate & 8)) {
         Cap<Real> *C = m.caps;   // built by threads 0..2 before the substeps
         Real *rec = m.slot;   // 3F records x 7 reals (the slot buffer is free now)
         for (int f = t; f < P.F; f += B) {
