@@ -93,11 +93,14 @@ def test_pinned_bitwise_constant(precision):
     assert not np_(sim.v)[0, mesh.pinned].any()
 
 
-def test_sim_with_attachments_matches_oracle_bitwise():
-    """Attachment constraints (vertex-anchor and vertex-face) run through the kernel bitwise vs the oracle."""
+@pytest.mark.parametrize("cluster", [0, 2], ids=["one-cta", "cluster2"])
+def test_sim_with_attachments_matches_oracle_bitwise(cluster):
+    """Attachment constraints (vertex-anchor and vertex-face) run through the kernel bitwise vs the
+    oracle -- also split over a 2-CTA cluster (attachment slots only for owned vertices)."""
     scene = build_slab_scene(3, 2, 2, damping=0.8, with_attachments=True)
     n = 2
-    sim = Simulation(*scene, num_instances=n, device="cuda:0", precision="fp64")
+    sim = Simulation(*scene, num_instances=n, device="cuda:0", precision="fp64",
+                     layout={"cluster_size": cluster} if cluster else None)
     ref = O.OracleEnv(O.scene_from_loaded(*scene), n)
     rng = np.random.default_rng(19)
     for _ in range(60):
