@@ -223,10 +223,17 @@ def run_gpu(args, wl):
     import torch.distributed as dist
 
     rank, world, local = env_info()
+    # TS_BENCH_DIST=gloo: a test mode that runs several ranks on one GPU (NCCL needs one GPU per rank)
+    backend = os.environ.get("TS_BENCH_DIST", "nccl")
+    local = local % max(1, torch.cuda.device_count()) if backend == "gloo" else local
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    rdev = dev if backend == "nccl" else torch.device("cpu")   # where the timing reductions run
 
     from paper_2503_18616_b200 import EnvBatch, _native as N
     from paper_2503_18616_b200.mesh import load_scene
@@ -283,7 +290,7 @@ def run_gpu(args, wl):
     assert sk_n.value == args.steps, (sk_n.value, args.steps)
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     total_ms = float(np.sum(step_ms))
-    t = torch.tensor([total_ms, sk_ms.value], dtype=torch.float64, device=dev)
+    t = torch.tensor([total_ms, sk_ms.value], dtype=torch.float64, device=rdev)
     if world > 1:
         dist.barrier()
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -306,7 +313,7 @@ def run_gpu(args, wl):
     for i in range(args.steps):
         o, r, te, tr, _ = env.step_numpy(host_actions[i])   # numpy in / numpy out, reference semantics
     torch.cuda.synchronize(dev)
-    e2e_s = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+    e2e_s = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=rdev)
     if world > 1:
         dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
     e2e_value = world * n * args.steps / float(e2e_s[0])
