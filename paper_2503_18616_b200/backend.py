@@ -10,7 +10,7 @@ protocol can call this module with the same numpy arguments:
   float32 -> the fp32 build);
 * ``detect_contacts(pos, faces, caps, iters)`` -> (face, cap, depth, dir, bary).
 
-Each call uploads, runs ONE kernel launch, and downloads; the compiled
+Each call uploads, runs the step kernels once, and downloads; the compiled
 topology program is cached per topology.  This is the validation boundary:
 production code calls ``EnvBatch`` / ``Simulation``, which keep state resident.
 Named "b200", never "cuda" (the reference's registry must keep rejecting

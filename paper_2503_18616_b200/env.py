@@ -12,9 +12,11 @@ behaviour; the return values are CUDA tensors:
   ``done_mask`` is false (the reference returns None when no row is done);
   ``contacts`` is evaluated lazily so a step never blocks the host.
 
-Every call to ``step`` is one launch of the fused sm_100a kernel
-(``csrc/step_kernel.cuh``), plus a one-block action check when the actions
-are already on the device and ``validate=True``.
+Every call to ``step`` is three stream-ordered launches -- the per-env command
+kernel, the fused sm_100a step kernel and the per-env epilogue
+(``csrc/step_kernel.cuh``) -- plus a one-block action check when the actions
+are already on the device and ``validate=True``; ``capture_step`` records them
+as one CUDA graph and ``step_numpy`` returns host arrays like the reference.
 """
 
 from __future__ import annotations

@@ -3,9 +3,11 @@
 ``Simulation`` keeps the reference's attribute names (``x``, ``v``, ``w``,
 ``grasped``, ``grasp_vertex``, ``tool``, ``mesh``, ``rest``, ``cfg``,
 ``params``, ``step_count``) but every per-instance array is a CUDA tensor
-that the sm_100a kernel updates in place.  One ``step`` is ONE kernel launch
-(tool command, grasp, substeps, contacts, divergence flags), see
-``csrc/step_kernel.cuh``.  Reference: solver.py:247-381.
+that the sm_100a kernels update in place.  One ``step`` is three stream-ordered
+launches -- the per-env command kernel (tool command, grasp release, capsule
+rows), the fused step kernel (grasp search, substeps, contacts, divergence
+flags; one CTA or one thread-block cluster per env) and the per-env epilogue --
+see ``csrc/step_kernel.cuh``.  Reference: solver.py:247-381.
 """
 
 from __future__ import annotations
