@@ -97,6 +97,8 @@ typedef struct ts_layout_opts {
                                    (default, 0/1), -1 = constraint-parallel phase 1 + slots */
     int32_t cluster_size;       /* CTAs per environment: 0 = auto (one CTA when the mesh fits, else the
                                    smallest thread-block cluster that holds it), 1 = one CTA, 2..16 */
+    int32_t refine_iters;       /* bank-schedule search iterations: 0 = thorough default (3000 per item,
+                                   at most 4 M; seconds), -1 = quick (150 per item), > 0 = explicit */
 } ts_layout_opts;
 
 typedef struct ts_layout_info {
@@ -160,6 +162,11 @@ int32_t ts_abi_version(void);
 
 int32_t ts_create(const ts_scene_desc *desc, const ts_layout_opts *opts, int32_t device,
                   ts_handle **out);
+/* ts_create from a program ts_compile_program made earlier (same library build, same scene):
+ * skips the compile (the bank-schedule search takes seconds).  `info` is what the compile
+ * reported.  Replaces the same reference step as ts_create. */
+int32_t ts_create_from_program(const ts_scene_desc *desc, const void *program, int64_t bytes,
+                               const ts_layout_info *info, int32_t device, ts_handle **out);
 int32_t ts_destroy(ts_handle *h);
 int32_t ts_query(const ts_handle *h, ts_layout_info *info);
 

@@ -48,7 +48,7 @@ class SceneDesc(ctypes.Structure):
 class LayoutOpts(ctypes.Structure):
     _fields_ = [("precision", _I32), ("block_threads", _I32), ("max_chunk_slots", _I32),
                 ("schedule_banks", _I32), ("smem_budget", _I32), ("compact", _I32),
-                ("edge_gather", _I32), ("cluster_size", _I32)]
+                ("edge_gather", _I32), ("cluster_size", _I32), ("refine_iters", _I32)]
 
 
 class LayoutInfo(ctypes.Structure):
@@ -87,6 +87,7 @@ _SIGNATURES = {
     "ts_abi_version": ([], _I32),
     "ts_launch_count": ([], _I64),
     "ts_create": ([_P, _P, _I32, _P], _I32),
+    "ts_create_from_program": ([_P, _P, _I64, _P, _I32, _P], _I32),
     "ts_destroy": ([_P], _I32),
     "ts_query": ([_P, _P], _I32),
     "ts_compile_program": ([_P, _P, _P, _P, _P], _I32),

@@ -162,6 +162,9 @@ static void fill_params(const ts_scene_desc &d, TsParams &S) {
     ts_finish_params(S);
 }
 
+static int32_t create_handle(const ts_scene_desc *desc, const ts_layout_opts &o, int32_t device, ts_handle *h,
+                             ts_handle **out);
+
 int32_t ts_create(const ts_scene_desc *desc, const ts_layout_opts *opts, int32_t device, ts_handle **out) {
     if (!desc || !out) return fail(TS_ERR_INVALID, "null argument");
     if (desc->substeps < 1) return fail(TS_ERR_INVALID, "substeps must be >= 1");
@@ -173,6 +176,39 @@ int32_t ts_create(const ts_scene_desc *desc, const ts_layout_opts *opts, int32_t
     std::string err;
     int rc = compile_any(*desc, o, h->host_blob, h->info, err);
     if (rc != TS_OK) { delete h; return fail(rc, err); }
+    return create_handle(desc, o, device, h, out);
+}
+
+int32_t ts_create_from_program(const ts_scene_desc *desc, const void *program, int64_t bytes,
+                               const ts_layout_info *info, int32_t device, ts_handle **out) {
+    if (!desc || !program || !info || !out) return fail(TS_ERR_INVALID, "null argument");
+    if (desc->substeps < 1) return fail(TS_ERR_INVALID, "substeps must be >= 1");
+    if (desc->dt <= 0.0) return fail(TS_ERR_INVALID, "dt must be positive");
+    if (bytes < (int64_t)sizeof(TsProgHeader)) return fail(TS_ERR_INVALID, "program too small");
+    const int32_t magic = *reinterpret_cast<const int32_t *>(program);
+    if (magic == TS_PROG_MAGIC) {
+        const TsProgHeader *H = reinterpret_cast<const TsProgHeader *>(program);
+        if (H->version != TS_PROG_VERSION || H->total_bytes != bytes || H->V != desc->n_vert)
+            return fail(TS_ERR_INVALID, "program does not match this library / scene");
+    } else if (magic == TS_CLUSTER_MAGIC) {
+        const TsClusterHeader *C = reinterpret_cast<const TsClusterHeader *>(program);
+        if (C->total_bytes != bytes || C->n_vert != desc->n_vert)
+            return fail(TS_ERR_INVALID, "program does not match this scene");
+    } else {
+        return fail(TS_ERR_INVALID, "not a compiled scene program");
+    }
+    ts_layout_opts o = default_opts();
+    o.precision = info->precision;
+    ts_handle *h = new ts_handle();
+    h->device = device;
+    h->precision = info->precision;
+    h->info = *info;
+    h->host_blob.assign(reinterpret_cast<const uint8_t *>(program), reinterpret_cast<const uint8_t *>(program) + bytes);
+    return create_handle(desc, o, device, h, out);
+}
+
+static int32_t create_handle(const ts_scene_desc *desc, const ts_layout_opts &o, int32_t device, ts_handle *h,
+                             ts_handle **out) {
     cudaError_t e = cudaSetDevice(device);
     if (e != cudaSuccess) { delete h; return cuda_fail(e, "cudaSetDevice"); }
     e = cudaMalloc(&h->dev_blob, h->host_blob.size());

@@ -49,6 +49,8 @@ inline int roundup(int x, int m) { return (x + m - 1) / m * m; }
 
 // effort of the bank-conflict searches (cluster parts compile K programs twice: a tenth)
 thread_local double g_search_effort = 1.0;
+// share of SA proposals that start from a conflicting sub-batch (TS_SA_FOCUS overrides)
+thread_local double g_focus = 0.7;
 // idle lanes allowed per 32-item tet batch (TS_TET_HOLES overrides; tuned on B200)
 int g_tet_holes = 0;
 
@@ -228,7 +230,7 @@ struct ListRef { std::vector<Item> *items; int begin, count; };
 // Deterministic (fixed-seed xorshift).  Slots are assigned afterwards from the
 // final positions, so the per-vertex summation order is untouched.
 void bank_refine(const std::vector<ListRef> &lists, std::vector<int> &o2s, std::vector<int> &s2o, int Vf,
-                 int Vf_pad, int Vown, int bank_mod, bool permute_tets) {
+                 int Vf_pad, int Vown, int bank_mod, bool permute_tets, int refine_iters) {
     struct Ref { int list, idx; };
     std::vector<Ref> items;                 // global item id -> (list, index)
     std::vector<int> sb_of, list_sb0;
@@ -282,7 +284,14 @@ void bank_refine(const std::vector<ListRef> &lists, std::vector<int> &o2s, std::
     const int n_halo = (int)std::count_if(s2o.begin() + Vown, s2o.end(), [](int v) { return v >= 0; });
     std::vector<int> touched;
     auto collect = [&](int sb) { if (std::find(touched.begin(), touched.end(), sb) == touched.end()) touched.push_back(sb); };
-    long iters = (long)(g_search_effort * std::min<long>(600000L, 150L * n));
+    // thorough by default (measured on B200, reach_1170 fp32: 175 k iterations -> 140 residual
+    // conflicts, 0.688 ms/step; 3 M -> 107, 0.674; 12 M -> 86, 0.670); programs are cached by
+    // the Python layer, so the seconds are paid once per scene and library build
+    long iters = refine_iters > 0 ? (long)refine_iters
+               : refine_iters < 0 ? std::min<long>(600000L, 150L * n) : std::min<long>(4000000L, 3000L * n);
+    iters = (long)(g_search_effort * iters);
+    g_focus = 0.7;
+    if (const char *env = std::getenv("TS_SA_FOCUS")) g_focus = std::atof(env);
     if (const char *env = std::getenv("TS_REFINE_ITERS")) iters = std::atol(env);
     const double T0 = 1.5, T1 = 0.05;
     // best state seen (the schedule lists, the vertex positions)
@@ -304,8 +313,19 @@ void bank_refine(const std::vector<ListRef> &lists, std::vector<int> &o2s, std::
         const int kind = (int)(next() % 10);
         // --- propose ---------------------------------------------------------
         int g1 = -1, g2 = -1, u = -1, v = -1, perm = -1;
+        // focus: most proposals start from an item of a sub-batch that still has a conflict
+        auto pick = [&]() {
+            int g = (int)(next() % n);
+            if (unif() < g_focus)
+                for (int tries = 0; tries < 8; ++tries) {
+                    const int q = sb_of[g] * 4;
+                    if (mx[q] > 1 || mx[q + 1] > 1 || mx[q + 2] > 1 || mx[q + 3] > 1) break;
+                    g = (int)(next() % n);
+                }
+            return g;
+        };
         if (kind < 5) {                                   // item swap inside a list
-            g1 = (int)(next() % n);
+            g1 = pick();
             const Ref r1 = items[g1];
             const int cnt_l = lists[r1.list].count;
             const int j = (int)(next() % cnt_l);
@@ -313,7 +333,7 @@ void bank_refine(const std::vector<ListRef> &lists, std::vector<int> &o2s, std::
             if (sb_of[g1] == sb_of[g2]) continue;
             collect(sb_of[g1]); collect(sb_of[g2]);
         } else if (kind < 8) {                            // vertex swap inside a warp group / the pinned pool
-            const Item &src = item((int)(next() % n));
+            const Item &src = item(pick());
             if (src.nroles == 0) continue;   // idle lane of a batch
             u = src.vid[next() % 2];
             const int pu = o2s[u];
@@ -793,7 +813,7 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
             if (chunk_rec[c].edge_count) lists.push_back({&all_items[0], chunk_rec[c].edge_begin, chunk_rec[c].edge_count});
             if (chunk_rec[c].tet_count) lists.push_back({&all_items[2], chunk_rec[c].tet_begin, chunk_rec[c].tet_count});
         }
-        bank_refine(lists, o2s, s2o, Vf, Vf_pad, Vown, bank_mod, /*permute_tets=*/R == 4);
+        bank_refine(lists, o2s, s2o, Vf, Vf_pad, Vown, bank_mod, /*permute_tets=*/R == 4, o.refine_iters);
         // edges: exact conflict-free batches by bipartite edge colouring (with the final positions)
         std::vector<Item> edges_out;
         for (int c = 0; c < n_chunks; ++c) {

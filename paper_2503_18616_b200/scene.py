@@ -13,6 +13,8 @@ the same host:
 from __future__ import annotations
 
 import ctypes
+import hashlib
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -152,7 +154,7 @@ class SceneArrays:
 
 
 def layout_opts(precision="fp32", block_threads=0, max_chunk_slots=0, schedule_banks=True, compact=True,
-                edge_gather=None, cluster_size=0):
+                edge_gather=None, cluster_size=0, refine_iters=0):
     o = N.LayoutOpts()
     o.precision = N.TS_F64 if precision in ("fp64", "float64", "f64", N.TS_F64) else N.TS_F32
     o.block_threads = int(block_threads)
@@ -162,14 +164,79 @@ def layout_opts(precision="fp32", block_threads=0, max_chunk_slots=0, schedule_b
     # None: the compiler's choice (owner gather); False: constraint-parallel edge slots
     o.edge_gather = 0 if edge_gather is None else (1 if edge_gather else -1)
     o.cluster_size = int(cluster_size)
+    o.refine_iters = int(refine_iters)
     return o
 
 
+# ---------------------------------------------------------------------------
+# compiled-program cache: the thorough bank-schedule search takes seconds, so a program is
+# compiled once per (scene, layout options, library build) -- memoised in the process and kept
+# under _native/programs/ (TS_PROGRAM_CACHE=0 disables the disk copy)
+# ---------------------------------------------------------------------------
+_MEMO: dict = {}
+_LIB_FP = None
+CACHE_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_native", "programs")
+
+
+def _lib_fingerprint():
+    global _LIB_FP
+    if _LIB_FP is None:
+        from .build import LIB
+        with open(LIB, "rb") as fh:
+            _LIB_FP = hashlib.sha1(fh.read()).hexdigest()
+    return _LIB_FP
+
+
+def _program_key(arrays: SceneArrays, o) -> str:
+    h = hashlib.sha1(_lib_fingerprint().encode())
+    for name in ("positions_rest", "inverse_mass", "edges", "rest_length", "tets", "rest_volume", "faces",
+                 "att_vertex", "att_faces", "att_is_face", "att_anchor", "att_rest", "att_k"):
+        a = np.ascontiguousarray(getattr(arrays, name))
+        h.update(f"{name}:{a.dtype}:{a.shape}".encode())
+        h.update(a.tobytes())
+    d = arrays.desc()
+    h.update(repr((d.k_s, d.k_v, d.k_contact, d.contact_iterations)).encode())
+    h.update(bytes(o))
+    return h.hexdigest()
+
+
 def compile_program(arrays: SceneArrays, **layout):
-    """Host copy of the compiled program (bytes, info dict) -- no GPU needed."""
+    """Host copy of the compiled program (bytes, info dict) -- no GPU needed.  Cached."""
+    blob, info = _compile_cached(arrays, layout_opts(**layout))
+    return blob.copy(), info.as_dict()
+
+
+def _compile_cached(arrays: SceneArrays, o):
+    key = _program_key(arrays, o)
+    hit = _MEMO.get(key)
+    if hit is not None:
+        return hit
+    path = os.path.join(CACHE_DIR, key + ".npz")
+    use_disk = os.environ.get("TS_PROGRAM_CACHE", "1") != "0"
+    if use_disk and os.path.exists(path):
+        try:
+            z = np.load(path)
+            info = N.LayoutInfo.from_buffer_copy(z["info"].tobytes())
+            _MEMO[key] = (z["blob"], info)
+            return _MEMO[key]
+        except Exception:   # a torn / stale file: recompile
+            pass
+    blob, info = _compile_raw(arrays, o)
+    _MEMO[key] = (blob, info)
+    if use_disk:
+        try:
+            os.makedirs(CACHE_DIR, exist_ok=True)
+            tmp = path + f".{os.getpid()}.tmp.npz"
+            np.savez(tmp, blob=blob, info=np.frombuffer(bytes(info), np.uint8))
+            os.replace(tmp, path)
+        except OSError:
+            pass
+    return blob, info
+
+
+def _compile_raw(arrays: SceneArrays, o):
     lib = N.load()
     d = arrays.desc()
-    o = layout_opts(**layout)
     info = N.LayoutInfo()
     # generous first guess so the (seconds-long, bank-refined) compile runs once
     guess = (1 << 20) + 512 * (len(arrays.edges) + len(arrays.tets) + len(arrays.att_vertex)) \
@@ -180,7 +247,7 @@ def compile_program(arrays: SceneArrays, **layout):
         rc = lib.ts_compile_program(ctypes.byref(d), ctypes.byref(o), N.ptr(buf), ctypes.byref(size),
                                     ctypes.byref(info))
         if rc == N.TS_OK:
-            return buf[:size.value].copy(), info.as_dict()
+            return buf[:size.value].copy(), info
         if size.value <= guess:
             N.check(rc, "ts_compile_program")
         guess = int(size.value)
@@ -196,9 +263,11 @@ class DeviceScene:
         self._desc = arrays.desc()
         self._opts = layout_opts(**layout)
         self.precision = "fp64" if self._opts.precision == N.TS_F64 else "fp32"
+        blob, pinfo = _compile_cached(arrays, self._opts)
         h = ctypes.c_void_p()
-        N.check(self.lib.ts_create(ctypes.byref(self._desc), ctypes.byref(self._opts), int(device_index),
-                                   ctypes.byref(h)), "ts_create")
+        N.check(self.lib.ts_create_from_program(ctypes.byref(self._desc), N.ptr(blob), int(blob.nbytes),
+                                                ctypes.byref(pinfo), int(device_index), ctypes.byref(h)),
+                "ts_create_from_program")
         self.handle = h
         info = N.LayoutInfo()
         N.check(self.lib.ts_query(h, ctypes.byref(info)), "ts_query")

@@ -46,9 +46,13 @@ def main():
     cts = os.environ.get("TS_CTS", "").split(",") if os.environ.get("TS_CTS") else [None]
     holes = os.environ.get("TS_HOLES", "").split(",") if os.environ.get("TS_HOLES") else [None]
     ablates = os.environ.get("TS_ABLATES", "").split(",") if os.environ.get("TS_ABLATES") else [None]
-    for prec, ch, bl, ga, ct, ho, ab in itertools.product(precs, chunks, blocks, gathers, cts, holes, ablates):
+    iters = os.environ.get("TS_ITERS", "").split(",") if os.environ.get("TS_ITERS") else [None]
+    for prec, ch, bl, ga, ct, ho, ab, itn in itertools.product(precs, chunks, blocks, gathers, cts, holes, ablates,
+                                                               iters):
         if ab is not None:
             os.environ["TS_ABLATE"] = ab
+        if itn is not None:
+            os.environ["TS_REFINE_ITERS"] = itn
         if ct is not None:
             os.environ["TS_SPLIT_CT"] = ct
         if ho is not None:
@@ -60,7 +64,7 @@ def main():
             layout["block_threads"] = bl
         try:
             ms, info = time_layout(scene, n, prec, layout)
-            print(f"{prec} gather={ga} ct={ct} holes={ho} ablate={ab} chunk={ch:5d} block={bl:4d}: {ms:.3f} ms/step  {n / ms * 1e3:12,.0f} env-steps/s  "
+            print(f"{prec} gather={ga} ct={ct} holes={ho} ablate={ab} iters={itn} chunk={ch:5d} block={bl:4d}: {ms:.3f} ms/step  {n / ms * 1e3:12,.0f} env-steps/s  "
                   f"chunks={info['n_chunks']} slots={info['slot_capacity']} smem={info['smem_bytes']} "
                   f"conf={info['bank_conflicts_p1']}", flush=True)
         except Exception as exc:
