@@ -870,15 +870,14 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
         int base = 0;
         for (int g = 0; g < G; ++g) { region[(size_t)c * G + g] = base; base += 32 * kmax[g]; }
         rec.slot_count = base;
-        // 32 "trash" slots after the regions: edge / tet endpoints that are pinned store there
-        // unconditionally (bank = p % 32, same as their position reads), nobody reads them back
-        const int trash = base;
-        slot_cap = std::max(slot_cap, base + 32);
+        // pinned endpoints get no slot (-1: the kernel predicates that store off; every store then
+        // has exactly one writer, so the step is clean under compute-sanitizer racecheck)
+        slot_cap = std::max(slot_cap, base);
         std::vector<int> k_next(Vf_pad, 0);
         for (Item *it : seqc) {
             for (int r = 0; r < it->nroles; ++r) {
                 const int p = it->pos[r];
-                if (p >= Vf_pad) { it->slot[r] = it->kind == TS_CHUNK_ATT ? -1 : trash + (p % 32); continue; }
+                if (p >= Vf_pad) { it->slot[r] = -1; continue; }
                 it->slot[r] = region[(size_t)c * G + p / 32] + 32 * k_next[p] + (p % 32);
                 k_next[p]++;
                 if (c == grasp_chunk && it->kind == TS_CHUNK_EDGE) gsplit[p] = k_next[p];
@@ -908,7 +907,7 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
         const int a = it.vid[0], b = it.vid[1];   // roles may be swapped by the bank refinement
         edge_idx[4 * i + 0] = it.pos[0]; edge_idx[4 * i + 1] = it.pos[1];
         edge_idx[4 * i + 2] = it.slot[0]; edge_idx[4 * i + 3] = it.slot[1];
-        if (it.index < 0) {   // padding lane of a colour class: pinned endpoints, trash slots only
+        if (it.index < 0) {   // padding lane of a colour class: pinned endpoints, no slot
             edge_par[4 * i + 0] = 0.0; edge_par[4 * i + 1] = 0.0; edge_par[4 * i + 2] = 0.0;
             edge_par[4 * i + 3] = 1.0;
             continue;
@@ -1012,9 +1011,11 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
                 tet_c[4 * i + 0] |= ((r & 3u) << 14) | (((r >> 2) & 3u) << 30);
                 tet_c[4 * i + 1] |= (((r >> 4) & 3u) << 14) | (((r >> 6) & 3u) << 30);
             }
-            tet_c[4 * i + 2] = tet_slot[4 * i] < 0 ? 0xffffu   // idle lane (0xffff: never a slot offset)
-                                                   : pk(scale_b * tet_slot[4 * i + 0], scale_b * tet_slot[4 * i + 1]);
-            tet_c[4 * i + 3] = pk(scale_b * tet_slot[4 * i + 2], scale_b * tet_slot[4 * i + 3]);
+            // slot fields: byte offsets (boff) or indices; 0xffff = no slot (pinned corner; all four:
+            // an idle lane of the bank schedule) -- never a multiple of 12 nor a valid index
+            auto so = [&](int s) { return s < 0 ? 0xffff : scale_b * s; };
+            tet_c[4 * i + 2] = pk(so(tet_slot[4 * i + 0]), so(tet_slot[4 * i + 1]));
+            tet_c[4 * i + 3] = pk(so(tet_slot[4 * i + 2]), so(tet_slot[4 * i + 3]));
         }
     }
 

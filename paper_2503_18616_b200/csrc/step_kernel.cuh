@@ -374,8 +374,8 @@ __device__ __forceinline__ void edge_item(const Smem<Real> &m, int pa, int pb, i
         ca = -wa * f;
         cb = wb * f;
     }
-    m.SX(sa) = ca * dx; m.SY(sa) = ca * dy; m.SZ(sa) = ca * dz;
-    m.SX(sb) = cb * dx; m.SY(sb) = cb * dy; m.SZ(sb) = cb * dz;   // pinned endpoints -> trash slots
+    if (sa >= 0) { m.SX(sa) = ca * dx; m.SY(sa) = ca * dy; m.SZ(sa) = ca * dz; }   // -1: pinned endpoint
+    if (sb >= 0) { m.SX(sb) = cb * dx; m.SY(sb) = cb * dy; m.SZ(sb) = cb * dz; }
     if (degenerate) {
         if (pa < vfp) atomicAdd(&m.deg[pa], 1);
         if (pb < vfp) atomicAdd(&m.deg[pb], 1);
@@ -397,7 +397,9 @@ __device__ __forceinline__ void p1_edges(const TsDevProg &P, const Smem<Real> &m
         for (int i = t; i < count; i += stride) {
             const uint4 q = nq;
             nq = __ldg(it + min(i + stride, count - 1));   // prefetch, branch-free
-            const int pa = q.x & 0xffff, pb = q.x >> 16, sa = q.y & 0xffff, sb = q.y >> 16;
+            const int pa = q.x & 0xffff, pb = q.x >> 16;
+            const int sa = (q.y & 0xffff) == 0xffff ? -1 : (int)(q.y & 0xffff);   // 0xffff: no slot
+            const int sb = (q.y >> 16) == 0xffff ? -1 : (int)(q.y >> 16);
             Real rl, wa, wb, wsum;
             if constexpr (sizeof(Real) == 8) {
                 rl = __hiloint2double((int)q.w, (int)q.z);
@@ -477,9 +479,14 @@ __device__ __forceinline__ void tet_item_b(const char *pb, char *sb, int *deg, u
     den = __fmaf_rn(Gdx, Gdx, den); den = __fmaf_rn(Gdy, Gdy, den); den = __fmaf_rn(Gdz, Gdz, den);
     const bool degenerate = !(den > 3.6e-17f);                  // sum|grad|^2 <= 1e-18
     const float sc = degenerate ? 0.0f : (-kv * c6) * rcp_ftz(den);
+    // 0xffff: a pinned corner has no slot -- a predicated store (no branch, no shared "trash" slot,
+    // so every shared word has one writer per phase)
+    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(sb);
     auto st3 = [&](unsigned o, float gx, float gy, float gz) {
-        float *d = reinterpret_cast<float *>(sb + o);
-        d[0] = sc * gx; d[1] = sc * gy; d[2] = sc * gz;
+        asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %0, 65535;\n\t"
+                     "@p st.shared.f32 [%1], %2;\n\t@p st.shared.f32 [%1+4], %3;\n\t"
+                     "@p st.shared.f32 [%1+8], %4;\n\t}"
+                     ::"r"(o), "r"(sbase + o), "f"(sc * gx), "f"(sc * gy), "f"(sc * gz) : "memory");
     };
     st3(q.z & 0xffffu, Gax, Gay, Gaz);
     st3(q.z >> 16, Gbx, Gby, Gbz);
@@ -511,7 +518,7 @@ __device__ __forceinline__ void p1_tets(const TsDevProg &P, const Smem<Real> &m,
                     nq = __ldg(it + i + 32);
                     const unsigned ri = ((q.x >> 14) & 3u) | ((q.x >> 28) & 12u) | ((q.y >> 10) & 48u) |
                                         ((q.y >> 24) & 192u);
-                    if ((q.z & 0xffffu) != 0xffffu)   // idle lane of the bank schedule
+                    if ((q.z & q.w) != 0xffffffffu)   // all four slots absent: idle lane of the bank schedule
                         tet_item_b(pb, sb, m.deg, q, __ldg(P.rvtab + ri), kv, 12u * (unsigned)vfp, 0x3fffu);
                 }
                 return;
@@ -522,7 +529,7 @@ __device__ __forceinline__ void p1_tets(const TsDevProg &P, const Smem<Real> &m,
                 const float rvi = nrv;
                 nq = __ldg(it + i + 32);
                 nrv = __ldg(rv + i + 32);
-                if ((q.z & 0xffffu) != 0xffffu)   // idle lane of the bank schedule
+                if ((q.z & q.w) != 0xffffffffu)   // idle lane of the bank schedule
                     tet_item_b(pb, sb, m.deg, q, rvi, kv, 12u * (unsigned)vfp, 0xffffu);
             }
             return;
@@ -539,8 +546,9 @@ __device__ __forceinline__ void p1_tets(const TsDevProg &P, const Smem<Real> &m,
             const Real rvi = nrv;
             { const int j = min(i + 32, we - 1); nq = __ldg(it + j); nrv = rv[j]; }
             const int4 id = make_int4(q.x & 0xffff, q.x >> 16, q.y & 0xffff, q.y >> 16);
-            const int4 sl = make_int4(q.z & 0xffff, q.z >> 16, q.w & 0xffff, q.w >> 16);
-            if (sl.x != 0xffff) tet_item<Real>(m, id, sl, rvi, kv, vfp);
+            auto s16 = [](unsigned v) { return v == 0xffffu ? -1 : (int)v; };   // 0xffff: no slot
+            const int4 sl = make_int4(s16(q.z & 0xffff), s16(q.z >> 16), s16(q.w & 0xffff), s16(q.w >> 16));
+            if ((q.z & q.w) != 0xffffffffu) tet_item<Real>(m, id, sl, rvi, kv, vfp);
         }
         return;
     }
@@ -557,7 +565,7 @@ __device__ __forceinline__ void p1_tets(const TsDevProg &P, const Smem<Real> &m,
             const int j = min(i + 32, we - 1);
             nid = __ldg(idx + j); nsl = __ldg(slot + j); nrv = rv[j];
         }
-        if (sl.x >= 0) tet_item<Real>(m, id, sl, rvi, kv, vfp);
+        if ((sl.x & sl.y & sl.z & sl.w) != -1) tet_item<Real>(m, id, sl, rvi, kv, vfp);   // all -1: idle lane
     }
 }
 
@@ -591,10 +599,10 @@ __device__ __forceinline__ void tet_item(const Smem<Real> &m, int4 id, int4 sl, 
                              + gdx * gdx + gdy * gdy + gdz * gdz;
             const Real mm = (Real)0.5 + copysign((Real)0.5, denom - (Real)1e-18);
             const Real sc = -mm * kv * cval / (denom + ((Real)1 - mm));
-            store_slot(m, sl.x, sc, gax, gay, gaz);
-            store_slot(m, sl.y, sc, gbx, gby, gbz);
-            store_slot(m, sl.z, sc, gcx, gcy, gcz);
-            store_slot(m, sl.w, sc, gdx, gdy, gdz);
+            put_slot(m, sl.x, sc, gax, gay, gaz);   // -1: pinned corner, no slot
+            put_slot(m, sl.y, sc, gbx, gby, gbz);
+            put_slot(m, sl.z, sc, gcx, gcy, gcz);
+            put_slot(m, sl.w, sc, gdx, gdy, gdz);
             degenerate = mm == (Real)0;
         } else {
             // fp32 build on unscaled cross products G = 6 grad (rv holds 6 V0):
@@ -619,10 +627,10 @@ __device__ __forceinline__ void tet_item(const Smem<Real> &m, int4 id, int4 sl, 
             den = __fmaf_rn(Gdx, Gdx, den); den = __fmaf_rn(Gdy, Gdy, den); den = __fmaf_rn(Gdz, Gdz, den);
             degenerate = !(den > 3.6e-17f);                  // sum|grad|^2 <= 1e-18
             const float sc = degenerate ? 0.0f : (-kv * c6) * rcp_ftz(den);
-            store_slot(m, sl.x, sc, Gax, Gay, Gaz);
-            store_slot(m, sl.y, sc, Gbx, Gby, Gbz);
-            store_slot(m, sl.z, sc, Gcx, Gcy, Gcz);
-            store_slot(m, sl.w, sc, Gdx, Gdy, Gdz);
+            put_slot(m, sl.x, sc, Gax, Gay, Gaz);
+            put_slot(m, sl.y, sc, Gbx, Gby, Gbz);
+            put_slot(m, sl.z, sc, Gcx, Gcy, Gcz);
+            put_slot(m, sl.w, sc, Gdx, Gdy, Gdz);
         }
         if (degenerate) {
             if (id.x < vfp) atomicAdd(&m.deg[id.x], 1);
@@ -828,6 +836,8 @@ static __device__ __forceinline__ void env_command(const TsDevProg &P, const TsP
     } else if (has_tool) {
         gv = L.grasp_vertex[env];
         for (int c = 0; c < 3; ++c) sc.drag[c] = S.rcm[c] + p.reach * p.ax[c];
+    } else {
+        for (int c = 0; c < 3; ++c) sc.drag[c] = 0.0;   // plugin detect_contacts: no tool, no drag
     }
     sc.need_search = 0;
     if (mode & TS_M_GRASP) {

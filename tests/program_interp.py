@@ -175,12 +175,13 @@ class PartRun:
                 ca = -par[:, 1] * scale
                 cb = par[:, 2] * scale
                 for col, coef, pos in ((2, ca, 0), (3, cb, 1)):
-                    sl = idx[:, col]          # pinned endpoints write to trash slots
-                    slots[sl] = coef[:, None] * d
+                    sl = idx[:, col]          # -1: pinned endpoint, no slot
+                    keep = sl >= 0
+                    slots[sl[keep]] = (coef[:, None] * d)[keep]
                     free = idx[:, pos] < H["Vf_pad"]
                     np.add.at(deg, idx[free & (m == 0), pos], 1)
             if tc:
-                live = prog.tet_slot[tb:tb + tc, 0] >= 0          # idle lanes of the bank schedule
+                live = (prog.tet_slot[tb:tb + tc] >= 0).any(axis=1)   # idle lanes of the bank schedule
                 idx = prog.tet_idx[tb:tb + tc][live]
                 sl = prog.tet_slot[tb:tb + tc][live]
                 rv = prog.tet_rv[tb:tb + tc][live]
@@ -200,7 +201,8 @@ class PartRun:
                 m = 0.5 + np.copysign(0.5, den - 1e-18)
                 scv = -m * kv * cval / (den + (1.0 - m))
                 for r, gg in enumerate((ga, gb, gc, gd)):
-                    slots[sl[:, r]] = scv[:, None] * gg
+                    keep = sl[:, r] >= 0                           # -1: pinned corner, no slot
+                    slots[sl[keep, r]] = (scv[:, None] * gg)[keep]
                     free = idx[:, r] < H["Vf_pad"]
                     np.add.at(deg, idx[free & (m == 0), r], 1)
             # phase 2: slots in order, the grasp spliced after the edge slots of the grasp chunk

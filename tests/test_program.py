@@ -116,17 +116,17 @@ def test_slot_structure(reach_scene, gather):
                 continue
             sl = slots[b:b + n]
             idx = items[b:b + n, :roles]
-            if kind == 2:                       # idle lanes of the bank schedule (slot -1)
-                keep = sl[:, 0] >= 0
+            if kind == 2:                       # idle lanes of the bank schedule (all four slots -1)
+                keep = (sl >= 0).any(axis=1)
                 assert np.all(sl[~keep] == -1)
                 sl, idx = sl[keep], idx[keep]
-            real = sl < padded
+            real = sl >= 0
             assert np.all(real == (idx < H["Vf_pad"]))     # real slots exactly for free endpoints
-            assert np.all(sl[~real] < padded + 32)          # pinned endpoints -> 32 trash slots
+            assert np.all(sl[real] < padded)                # pinned endpoints: no slot (-1)
             s = sl[real]
             assert len(np.unique(s)) == len(s)
-            # slot k of lane l sits at region + 32k + l: bank = owner lane (also for trash slots)
-            assert np.all(sl % 32 == idx % 32)
+            # slot k of lane l sits at region + 32k + l: bank = owner lane
+            assert np.all(sl[real] % 32 == idx[real] % 32)
             used.append(len(s))
         expected += sum(used)
     n_inc = info["n_edge_incidences"] if gather else 0
@@ -174,7 +174,7 @@ def test_schedule_is_permutation_and_reduces_conflicts(reach_scene):
     def constraints(p, idx, roles):
         vf = p.h["Vf_pad"]
         out = []
-        live = p.tet_slot[:, 0] >= 0 if roles == 4 else np.ones(len(idx), bool)
+        live = (p.tet_slot >= 0).any(axis=1) if roles == 4 else np.ones(len(idx), bool)
         for row in idx[live][:, :roles]:
             if np.all(row >= vf):          # padding lane (pinned-only dummy edge)
                 continue
@@ -201,8 +201,10 @@ def test_compact_streams_encode_the_full_program(reach_scene, precision):
     assert info["compact"] == 1 and p.h["compact"] == 1
     lo, hi = p.edge_c[:, 0] & 0xFFFF, p.edge_c[:, 0] >> 16
     assert np.array_equal(lo, p.edge_idx[:, 0]) and np.array_equal(hi, p.edge_idx[:, 1])
-    assert np.array_equal(p.edge_c[:, 1] & 0xFFFF, p.edge_idx[:, 2])
-    assert np.array_equal(p.edge_c[:, 1] >> 16, p.edge_idx[:, 3])
+    for col, half in ((2, p.edge_c[:, 1] & 0xFFFF), (3, p.edge_c[:, 1] >> 16)):
+        dec = half.astype(np.int64)
+        dec[dec == 0xFFFF] = -1                                  # pinned endpoint: no slot
+        assert np.array_equal(dec, p.edge_idx[:, col])
     if precision == "fp64":
         rl = p.edge_c[:, 2:4].copy().view(np.float64)[:, 0]
         vfp = p.h["Vf_pad"]
@@ -214,11 +216,14 @@ def test_compact_streams_encode_the_full_program(reach_scene, precision):
     else:
         rl = p.edge_c[:, 2].copy().view(np.float32).astype(np.float64)
     assert np.array_equal(rl, p.edge_par[:, 0])
-    live = p.tet_slot[:, 0] >= 0
-    assert np.all(p.tet_c[~live, 2] == 0xFFFF)          # idle lanes: the kernel's skip sentinel
+    live = (p.tet_slot >= 0).any(axis=1)
+    tc = p.tet_c[: len(p.tet_slot)]
+    assert np.all(tc[~live, 2] == 0xFFFFFFFF) and np.all(tc[~live, 3] == 0xFFFFFFFF)   # idle lanes
     for k in range(4):
-        assert np.array_equal(((p.tet_c[:, k // 2] >> (16 * (k % 2))) & 0xFFFF)[live], p.tet_idx[live, k])
-        assert np.array_equal(((p.tet_c[:, 2 + k // 2] >> (16 * (k % 2))) & 0xFFFF)[live], p.tet_slot[live, k])
+        assert np.array_equal(((tc[:, k // 2] >> (16 * (k % 2))) & 0xFFFF)[live], p.tet_idx[live, k])
+        sl = ((tc[:, 2 + k // 2] >> (16 * (k % 2))) & 0xFFFF).astype(np.int64)
+        sl[sl == 0xFFFF] = -1                                   # pinned corner: no slot
+        assert np.array_equal(sl[live], p.tet_slot[live, k])
 
 
 def test_nonuniform_mass_uses_full_streams(small_scene):
@@ -326,7 +331,7 @@ def test_dictionary_coded_streams(reach_scene):
     blob, info = S.compile_program(_arrays(reach_scene), precision="fp32")
     p = PI.Program(blob)
     assert p.h["einc_bytes"] == 4 and p.h["rvdict"] == 1
-    live = p.tet_slot[:, 0] >= 0
+    live = (p.tet_slot >= 0).any(axis=1)
     n_rv = len(np.unique(p.tet_rv[live].astype(np.float32)))
     rvtab = p.sec("RVTAB", np.float32, n_rv)
     q = p.tet_c[: len(p.tet_rv)]
