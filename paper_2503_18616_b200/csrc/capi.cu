@@ -156,7 +156,7 @@ static void fill_params(const ts_scene_desc &d, TsParams &S) {
     S.max_steps = d.max_episode_steps; S.start_distance = d.start_distance;
     S.n_face = d.n_face;
     // development ablation switch (results are wrong when set): 1 tets, 2 slot sums, 4 edge
-    // gather, 8 contacts, 16 grasp search, 64 the whole substep loop
+    // gather, 8 contacts, 16 grasp search, 64 the whole substep loop, 128 slot sums capped at 12
     S.ablate = 0;
     if (const char *env = std::getenv("TS_ABLATE")) S.ablate = std::atoi(env);
     ts_finish_params(S);

@@ -1187,7 +1187,8 @@ __device__ __forceinline__ void step_env(const TsDevProg &P, const TsDevProg *pr
                     const int p = r * B + t;
                     if (p < P.Vf) {
                         const int base = P.region[ch.region_off + (p >> 5)] + lane;
-                        const int val = (S.ablate & 2) ? 0 : P.valence[ch.val_off + p];
+                        const int val = (S.ablate & 2) ? 0 : ((S.ablate & 128) ? min(P.valence[ch.val_off + p], 12)
+                                                                                 : P.valence[ch.val_off + p]);
                         const int pre = gchunk ? min(val, P.gsplit[p]) : val;
                         Real ax = accx[r], ay = accy[r], az = accz[r];
 #pragma unroll 4

@@ -63,7 +63,7 @@ def main():
         if bl:
             layout["block_threads"] = bl
         try:
-            ms, info = time_layout(scene, n, prec, layout)
+            ms, info = time_layout(scene, n, prec, layout, grid=int(os.environ.get("TS_GRID", "0")))
             print(f"{prec} gather={ga} ct={ct} holes={ho} ablate={ab} iters={itn} chunk={ch:5d} block={bl:4d}: {ms:.3f} ms/step  {n / ms * 1e3:12,.0f} env-steps/s  "
                   f"chunks={info['n_chunks']} slots={info['slot_capacity']} smem={info['smem_bytes']} "
                   f"conf={info['bank_conflicts_p1']}", flush=True)
