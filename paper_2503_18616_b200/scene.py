@@ -211,7 +211,8 @@ def _compile_cached(arrays: SceneArrays, o):
     hit = _MEMO.get(key)
     if hit is not None:
         return hit
-    path = os.path.join(CACHE_DIR, key + ".npz")
+    prefix = _lib_fingerprint()[:12]
+    path = os.path.join(CACHE_DIR, f"{prefix}_{key}.npz")
     use_disk = os.environ.get("TS_PROGRAM_CACHE", "1") != "0"
     if use_disk and os.path.exists(path):
         try:
@@ -226,6 +227,9 @@ def _compile_cached(arrays: SceneArrays, o):
     if use_disk:
         try:
             os.makedirs(CACHE_DIR, exist_ok=True)
+            for old in os.listdir(CACHE_DIR):          # programs of other library builds are stale
+                if old.endswith(".npz") and not old.startswith(prefix):
+                    os.remove(os.path.join(CACHE_DIR, old))
             tmp = path + f".{os.getpid()}.tmp.npz"
             np.savez(tmp, blob=blob, info=np.frombuffer(bytes(info), np.uint8))
             os.replace(tmp, path)
