@@ -306,12 +306,10 @@ class EnvBatch:
             so.obs_f64 = int(self.obs_dtype == torch.float64)
             host = torch.empty(total, dtype=torch.uint8, pin_memory=True)
             raw = host.numpy()
-            hv = {}
-            for name, dt, shape, off, nb in layout:
-                npdt = torch.empty(0, dtype=dt).numpy().dtype
-                hv[name] = raw[off:off + nb].view(npdt).reshape(shape)
-            fx = self._np_fast = (dev_buf, so, host, hv, torch.cuda.Event())
-        dev_buf, so, host, hv, done_ev = fx
+            hv = [(name, torch.empty(0, dtype=dt).numpy().dtype, shape, off, nb)
+                  for name, dt, shape, off, nb in layout]
+            fx = self._np_fast = (dev_buf, so, host, raw, hv, torch.cuda.Event())
+        dev_buf, so, host, raw, hv, done_ev = fx
         st = self.sim.state_struct()
         with torch.cuda.device(self.device):
             stream = self.sim.stream_ptr()
@@ -321,7 +319,8 @@ class EnvBatch:
             done_ev.record()
         done_ev.synchronize()
         self.sim.step_count += 1
-        out = {name: v.copy() for name, v in hv.items()}
+        block = raw.copy()          # one host copy of the packed block; the arrays are views of it
+        out = {name: block[off:off + nb].view(dt).reshape(shape) for name, dt, shape, off, nb in hv}
         done = out["done_mask"]
         info = {
             "distance": out["distance"], "success": out["success"], "diverged": out["diverged"],

@@ -54,6 +54,27 @@ def _device(device):
     return dev
 
 
+# Latency policy for `layout=None` (measured, profiles/r01r/mesh_scaling.json): a thread-block
+# cluster costs ~90 us/step of DSMEM halo exchange and cluster barriers at any size, so it only
+# pays once one CTA needs more than that (about 768 vertices); it then pays while each CTA keeps
+# >= ~200 vertices and the envs x CTAs still fit on the SMs at once.
+CLUSTER_MIN_VERTICES = 768
+CLUSTER_MIN_VERTICES_PER_CTA = 200
+
+
+def latency_cluster_size(n_vert, num_instances, sms):
+    """CTAs per env for the auto layout: 0 (let the compiler pick the smallest layout that fits,
+    which maximises throughput) unless the GPU would otherwise be mostly idle."""
+    if n_vert < CLUSTER_MIN_VERTICES or num_instances < 1:
+        return 0
+    budget = min(16, sms // num_instances)
+    k = 0
+    for cand in (2, 4, 8, 16):
+        if cand <= budget and n_vert // cand >= CLUSTER_MIN_VERTICES_PER_CTA:
+            k = cand
+    return k
+
+
 def _as_device_f64(a, n, dev, name, width=3):
     if isinstance(a, torch.Tensor):
         t = a.to(device=dev, dtype=torch.float64)
@@ -95,9 +116,20 @@ class Simulation:
         self.dtype = torch.float64 if self.precision == "fp64" else torch.float32
         self.arrays = SceneArrays.from_loaded(mesh, rest, cfg, k_contact=k_contact,
                                               contact_iterations=contact_iterations)
+        layout = dict(layout or {})
+        auto_k = 0
+        if "cluster_size" not in layout:
+            sms = torch.cuda.get_device_properties(self.device).multi_processor_count
+            auto_k = latency_cluster_size(mesh.vertex_count, int(num_instances), sms)
         with torch.cuda.device(self.device):
-            self.scene = DeviceScene(self.arrays, self.device.index, precision=self.precision,
-                                     **(layout or {}))
+            try:
+                self.scene = DeviceScene(self.arrays, self.device.index, precision=self.precision,
+                                         **layout, **({"cluster_size": auto_k} if auto_k else {}))
+            except RuntimeError:
+                if not auto_k:
+                    raise
+                # the latency layout is smaller than the mesh needs: the compiler's own choice
+                self.scene = DeviceScene(self.arrays, self.device.index, precision=self.precision, **layout)
         self.backend = self.scene
         n, nv = int(num_instances), mesh.vertex_count
         self.num_instances = n

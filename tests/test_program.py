@@ -339,3 +339,13 @@ def test_dictionary_coded_streams(reach_scene):
     assert np.array_equal(rvtab[ri[live]].astype(np.float64), p.tet_rv[live])
     offs = np.stack([q[:, 0] & 0x3FFF, (q[:, 0] >> 16) & 0x3FFF, q[:, 1] & 0x3FFF, (q[:, 1] >> 16) & 0x3FFF], 1)
     assert np.array_equal(offs[live], 12 * p.tet_idx[live])
+
+
+def test_latency_cluster_policy():
+    """layout=None: clusters only for meshes past ~768 vertices and only while envs x CTAs fit the SMs
+    (measured crossover, profiles/r01r/mesh_scaling.json)."""
+    from paper_2503_18616_b200.solver import latency_cluster_size as k
+    assert k(392, 1, 148) == 0 and k(504, 1, 148) == 0        # one CTA beats any cluster
+    assert k(845, 1, 148) == 4 and k(2527, 1, 148) == 8 and k(12180, 1, 148) == 16
+    assert k(12180, 16, 148) == 8 and k(12180, 4096, 148) == 0   # throughput: the compiler's smallest fit
+    assert k(2527, 74, 148) == 2 and k(2527, 75, 148) == 0
