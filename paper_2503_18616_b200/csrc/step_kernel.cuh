@@ -50,6 +50,16 @@ __device__ __forceinline__ float rcp_ftz(float x) {
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
     return r;
 }
+// contact narrow phase arithmetic: IEEE in the fp64 (bitwise) build, single-MUFU in fp32
+template <typename Real> __device__ __forceinline__ Real cdiv(Real a, Real b);
+template <> __device__ __forceinline__ double cdiv<double>(double a, double b) { return a / b; }
+template <> __device__ __forceinline__ float cdiv<float>(float a, float b) { return a * rcp_ftz(b); }
+__device__ __forceinline__ double csqrt(double x) { return sqrt(x); }
+__device__ __forceinline__ float csqrt(float x) {
+    float r;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
 // solver constant in the build's precision (fp32 copies live in TsParams, no F2F in the loops)
 template <typename Real> __device__ __forceinline__ Real prm(double d, float f);
 template <> __device__ __forceinline__ double prm<double>(double d, float) { return d; }
@@ -190,15 +200,15 @@ __device__ void make_cap(const double *row, Cap<Real> &C) {
 
 template <typename Real>
 __device__ __forceinline__ Real cap_sd(const Cap<Real> &C, const Real *q, Real *grad) {
-    Real t = ((q[0] - C.p0[0]) * C.seg[0] + (q[1] - C.p0[1]) * C.seg[1] + (q[2] - C.p0[2]) * C.seg[2]) / C.dd;
+    Real t = cdiv<Real>((q[0] - C.p0[0]) * C.seg[0] + (q[1] - C.p0[1]) * C.seg[1] + (q[2] - C.p0[2]) * C.seg[2], C.dd);
     if (t < (Real)0) t = (Real)0;
     else if (t > (Real)1) t = (Real)1;
     const Real dx = q[0] - (C.p0[0] + t * C.seg[0]);
     const Real dy = q[1] - (C.p0[1] + t * C.seg[1]);
     const Real dz = q[2] - (C.p0[2] + t * C.seg[2]);
-    const Real nrm = sqrt(dx * dx + dy * dy + dz * dz);
+    const Real nrm = csqrt(dx * dx + dy * dy + dz * dz);
     if (grad) {
-        if (nrm > (Real)1e-12) { grad[0] = dx / nrm; grad[1] = dy / nrm; grad[2] = dz / nrm; }
+        if (nrm > (Real)1e-12) { grad[0] = cdiv<Real>(dx, nrm); grad[1] = cdiv<Real>(dy, nrm); grad[2] = cdiv<Real>(dz, nrm); }
         else { grad[0] = C.fb[0]; grad[1] = C.fb[1]; grad[2] = C.fb[2]; }
     }
     return nrm - C.radius;
@@ -210,7 +220,7 @@ __device__ __forceinline__ void simplex3(Real *b) {
     if (u0 < u1) { tmp = u0; u0 = u1; u1 = tmp; }
     if (u1 < u2) { tmp = u1; u1 = u2; u2 = tmp; }
     if (u0 < u1) { tmp = u0; u0 = u1; u1 = tmp; }
-    if (u2 - (u0 + u1 + u2 - (Real)1) / (Real)3 > (Real)0) theta = (u0 + u1 + u2 - (Real)1) / (Real)3;
+    if (u2 - cdiv<Real>(u0 + u1 + u2 - (Real)1, (Real)3) > (Real)0) theta = cdiv<Real>(u0 + u1 + u2 - (Real)1, (Real)3);
     else if (u1 - (u0 + u1 - (Real)1) / (Real)2 > (Real)0) theta = (u0 + u1 - (Real)1) / (Real)2;
     else theta = u0 - (Real)1;
     b[0] = cmax(b[0] - theta, (Real)0);
@@ -248,12 +258,12 @@ __device__ __noinline__ Real witness(const Cap<Real> &C, const Real *pa, const R
         gb[0] = g[0] * pa[0] + g[1] * pa[1] + g[2] * pa[2];
         gb[1] = g[0] * pb[0] + g[1] * pb[1] + g[2] * pb[2];
         gb[2] = g[0] * pc[0] + g[1] * pc[1] + g[2] * pc[2];
-        const Real mean_g = (gb[0] + gb[1] + gb[2]) / (Real)3;
+        const Real mean_g = cdiv<Real>(gb[0] + gb[1] + gb[2], (Real)3);
         gb[0] -= mean_g; gb[1] -= mean_g; gb[2] -= mean_g;
         const Real mag = cmax(cmax(fabs(gb[0]), fabs(gb[1])), fabs(gb[2]));
-        bary[0] -= step * gb[0] / (mag + (Real)1e-30);
-        bary[1] -= step * gb[1] / (mag + (Real)1e-30);
-        bary[2] -= step * gb[2] / (mag + (Real)1e-30);
+        bary[0] -= cdiv<Real>(step * gb[0], mag + (Real)1e-30);
+        bary[1] -= cdiv<Real>(step * gb[1], mag + (Real)1e-30);
+        bary[2] -= cdiv<Real>(step * gb[2], mag + (Real)1e-30);
         simplex3(bary);
         step *= (Real)0.7;
     }
@@ -1297,11 +1307,18 @@ __device__ __forceinline__ void step_env(const TsDevProg &P, const TsDevProg *pr
         }
         __syncthreads();
         if constexpr (!CL) {
-            if (t == 0) {
+            if (t < 32) {
+                // warp 0 finds the non-empty words (usually none); lane 0 walks them in order
                 int count = 0;
-                for (int wi = 0; wi < P.cbits_words; ++wi) {
-                    unsigned bits = m.cbits[wi];
-                    while (bits) {
+                for (int wb = 0; wb < P.cbits_words; wb += 32) {
+                  const unsigned word = wb + t < P.cbits_words ? m.cbits[wb + t] : 0u;
+                  unsigned nz = __ballot_sync(0xffffffffu, word != 0u);
+                  while (nz) {
+                    const int l = __ffs(nz) - 1;
+                    nz &= nz - 1;
+                    unsigned bits = __shfl_sync(0xffffffffu, word, l);
+                    const int wi = wb + l;
+                    if (t == 0) while (bits) {
                         const int b = __ffs(bits) - 1;
                         bits &= bits - 1;
                         const int key = wi * 32 + b;
@@ -1329,9 +1346,12 @@ __device__ __forceinline__ void step_env(const TsDevProg &P, const TsDevProg *pr
                         }
                         ++count;
                     }
+                  }
                 }
-                sc.n_contacts = count;
-                if (mode & TS_M_DETECT_ONLY) L.det_count[env] = count;
+                if (t == 0) {
+                    sc.n_contacts = count;
+                    if (mode & TS_M_DETECT_ONLY) L.det_count[env] = count;
+                }
             }
             __syncthreads();
         } else {
