@@ -238,8 +238,11 @@ __device__ __forceinline__ void bary_pt(const Real *b, const Real *pa, const Rea
 // Narrow phase of one (face, capsule) pair that passed the AABB test.
 // Returns sd; fills depth/dir/bary when sd < 0.
 template <typename Real>
-__device__ __noinline__ Real witness(const Cap<Real> &C, const Real *pa, const Real *pb, const Real *pc, int iters,
-                        Real *dir, Real *bary) {
+__device__ __noinline__ Real witness(const Cap<Real> &C, const Real *pa_, const Real *pb_, const Real *pc_, int iters,
+                        Real *dir, Real *bary_out) {
+    // register copies: the outputs live on the caller's stack and could alias the inputs
+    const Real pa[3] = {pa_[0], pa_[1], pa_[2]}, pb[3] = {pb_[0], pb_[1], pb_[2]}, pc[3] = {pc_[0], pc_[1], pc_[2]};
+    Real bary[3];
     const Real s0 = cap_sd<Real>(C, pa, nullptr);
     const Real s1 = cap_sd<Real>(C, pb, nullptr);
     const Real s2 = cap_sd<Real>(C, pc, nullptr);
@@ -277,6 +280,7 @@ __device__ __noinline__ Real witness(const Cap<Real> &C, const Real *pa, const R
         sd = cap_sd<Real>(C, pt, g);
     }
     dir[0] = g[0]; dir[1] = g[1]; dir[2] = g[2];
+    bary_out[0] = bary[0]; bary_out[1] = bary[1]; bary_out[2] = bary[2];
     return sd;
 }
 
@@ -1280,19 +1284,32 @@ __device__ __forceinline__ void step_env(const TsDevProg &P, const TsDevProg *pr
     if ((mode & (TS_M_CONTACTS | TS_M_DETECT_ONLY)) && (CL || P.F > 0) && !(S.ablate & 8)) {
         Cap<Real> *C = m.caps;   // built by threads 0..2 before the substeps
         Real *rec = m.slot;   // 3F records x 7 reals (the slot buffer is free now)
+        // union of the three capsule boxes: one test rejects almost every face
+        Real ulo[3], uhi[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            ulo[k] = cmin(cmin(C[0].lo[k], C[1].lo[k]), C[2].lo[k]);
+            uhi[k] = cmax(cmax(C[0].hi[k], C[1].hi[k]), C[2].hi[k]);
+        }
         for (int f = t; f < P.F; f += B) {
             const int ia = P.faces[3 * f], ib = P.faces[3 * f + 1], ic = P.faces[3 * f + 2];
             const Real pa[3] = {m.X(ia), m.Y(ia), m.Z(ia)};
             const Real pb[3] = {m.X(ib), m.Y(ib), m.Z(ib)};
             const Real pc[3] = {m.X(ic), m.Y(ic), m.Z(ic)};
+            Real tlo[3], thi[3];
+            bool any = true;
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                tlo[k] = cmin(cmin(pa[k], pb[k]), pc[k]);
+                thi[k] = cmax(cmax(pa[k], pb[k]), pc[k]);
+                any = any && !(thi[k] < ulo[k] || tlo[k] > uhi[k]);
+            }
+            if (!any) continue;
 #pragma unroll
             for (int ci = 0; ci < 3; ++ci) {
                 bool skip = false;
-                for (int k = 0; k < 3; ++k) {
-                    const Real tlo = cmin(cmin(pa[k], pb[k]), pc[k]);
-                    const Real thi = cmax(cmax(pa[k], pb[k]), pc[k]);
-                    if (thi < C[ci].lo[k] || tlo > C[ci].hi[k]) { skip = true; break; }
-                }
+                for (int k = 0; k < 3; ++k)
+                    if (thi[k] < C[ci].lo[k] || tlo[k] > C[ci].hi[k]) { skip = true; break; }
                 if (skip) continue;
                 Real dir[3], bary[3];
                 const Real sd = witness<Real>(C[ci], pa, pb, pc, S.contact_iters, dir, bary);
