@@ -119,6 +119,7 @@ static void decode_part(const uint8_t *host, const uint8_t *b, TsDevProg &P) {
     P.edge_c = reinterpret_cast<const uint4 *>(b + H->off[TS_SEC_EDGE_C]);
     P.tet_c = reinterpret_cast<const uint4 *>(b + H->off[TS_SEC_TET_C]);
     P.edge_gather = H->edge_gather;
+    P.narrow = H->narrow;
     P.einc_bytes = H->einc_bytes;
     P.einc = b + H->off[TS_SEC_EINC];
     P.eregion = reinterpret_cast<const int32_t *>(b + H->off[TS_SEC_EREGION]);

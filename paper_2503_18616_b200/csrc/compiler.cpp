@@ -1241,6 +1241,14 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
     hdr.n_edge_items = nE; hdr.n_tet_items = nT; hdr.n_att_items = nA; hdr.bank_conflicts = total_conf;
     hdr.n_slots_total = n_slots_total;
     hdr.edge_gather = eg ? 1 : 0; hdr.einc_bytes = einc_bytes;
+    {
+        // narrow layout (program.h): legal when nothing reads neighbour positions in phase 2 (the
+        // distance-only program gathers edges there) and no cluster peer reads the ping-pong copy
+        int maxval = 0;
+        for (int v : valence) maxval = std::max(maxval, v);
+        const char *nv = std::getenv("TS_NARROW");
+        hdr.narrow = (!part && (n_chunks >= 1 || !eg) && maxval <= 255 && !(nv && nv[0] == '0')) ? 1 : 0;
+    }
     int64_t off = roundup((int)sizeof(TsProgHeader), 256);
     for (int s = 0; s < TS_SEC_COUNT; ++s) { hdr.off[s] = off; off += ((sz[s] + 255) / 256) * 256; }
     hdr.total_bytes = off;

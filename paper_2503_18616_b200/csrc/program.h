@@ -19,7 +19,7 @@
 #include <stdint.h>
 
 #define TS_PROG_MAGIC 0x54534231  // "TSB1"
-#define TS_PROG_VERSION 2
+#define TS_PROG_VERSION 3
 
 enum TsChunkKind { TS_CHUNK_EDGE = 0, TS_CHUNK_ATT = 1, TS_CHUNK_TET = 2 };
 
@@ -79,16 +79,20 @@ struct TsChunk {
     int32_t val_off, conflicts, pad0, pad1;
 };
 
-#define TS_SMEM_HEAD 2048       // scalar block + capsule parameters, at the start of shared memory
+#define TS_SMEM_HEAD 1280       // scalar block + capsule parameters, at the start of shared memory
 
 // Shared memory one CTA needs for a program (the kernel's carve, step_kernel.cuh): positions
 // (x2 when ping-ponged), slot buffer / contact records, degenerate counters, contact bitmap,
 // scalar block.
-inline int ts_smem_layout_bytes(int Vstore, int slot_cap, int Vf_pad, int F, int real_bytes, int ping_pong) {
+// narrow programs (single CTA, >= 1 chunk, every chunk valence <= 255): phase 2 writes positions in
+// place (nothing reads a neighbour's position after the phase-1 barrier) and the degenerate-constraint
+// counters are bytes -- 6 KB less per CTA for reach_1170, which is what a 4th CTA per SM needs
+inline int ts_smem_layout_bytes(int Vstore, int slot_cap, int Vf_pad, int F, int real_bytes, int ping_pong,
+                                int narrow = 0) {
     size_t b = 0;
-    b += (size_t)3 * Vstore * real_bytes * (ping_pong ? 2 : 1);
+    b += (size_t)3 * Vstore * real_bytes * (ping_pong && !narrow ? 2 : 1);
     b += (size_t)3 * slot_cap * real_bytes;
-    b += (size_t)4 * Vf_pad;
+    b += (size_t)(narrow ? 1 : 4) * Vf_pad;
     b += (size_t)4 * ((3 * F + 31) / 32);
     b = (b + 15) / 16 * 16;
     b += TS_SMEM_HEAD;
@@ -114,7 +118,8 @@ struct TsProgHeader {
     int32_t n_slots_total, compact, edge_gather, einc_bytes;
     int32_t Vown, cluster_k, cluster_rank, boff;   // Vown: end of the owned (written-back) positions;
                                                    // boff: fp32 compact streams hold byte offsets
-    int32_t rvdict, pad4;                          // rvdict: tet rest volumes dictionary-coded
+    int32_t rvdict, narrow;                        // rvdict: tet rest volumes dictionary-coded;
+                                                   // narrow: one position buffer, 8-bit degenerate counters
     double w_free;   // the common inverse mass of free vertices (compact programs)
     int64_t off[TS_SEC_COUNT];
     int64_t total_bytes;

@@ -72,6 +72,7 @@ struct TsDevProg {
     double w_free;            // common inverse mass of free vertices (compact programs)
     const uint4 *edge_c;
     const uint4 *tet_c;
+    int32_t narrow;           // single position buffer + byte degenerate counters (program.h)
     int32_t edge_gather;      // 1: owner-gathered edges (records below), positions double-buffered
     int32_t einc_bytes;       // 8 or 16
     const void *einc;
@@ -148,7 +149,7 @@ struct TsLaunch {
 
 // Shared-memory layout sizes (bytes) for one CTA.
 inline int ts_smem_bytes(const TsDevProg &P, int real_bytes) {
-    return ts_smem_layout_bytes(P.Vstore, P.slot_cap, P.Vf_pad, P.F, real_bytes, P.edge_gather);
+    return ts_smem_layout_bytes(P.Vstore, P.slot_cap, P.Vf_pad, P.F, real_bytes, P.edge_gather, P.narrow);
 }
 
 // command kernel -> fused step kernel -> epilogue kernel, stream ordered

@@ -331,11 +331,28 @@ struct Smem {
     __device__ __forceinline__ Real &SX(int i) const { return slot[3 * i]; }
     __device__ __forceinline__ Real &SY(int i) const { return slot[3 * i + 1]; }
     __device__ __forceinline__ Real &SZ(int i) const { return slot[3 * i + 2]; }
-    int *deg;
+    int *deg;           // degenerate-constraint counters: int per vertex, or bytes when narrow
+    int narrow;
     unsigned *cbits;
     Scal *sc;
     Cap<Real> *caps;
 };
+
+__device__ __forceinline__ void deg_add(int narrow, int *deg, int i) {
+    if (narrow) atomicAdd(reinterpret_cast<unsigned *>(deg) + (i >> 2), 1u << ((i & 3) * 8));
+    else atomicAdd(&deg[i], 1);
+}
+__device__ __forceinline__ int deg_take(int narrow, int *deg, int i) {   // read and clear (phase 2)
+    if (narrow) {
+        unsigned char *b = reinterpret_cast<unsigned char *>(deg);
+        const int d = b[i];
+        if (d) b[i] = 0;
+        return d;
+    }
+    const int d = deg[i];
+    if (d) deg[i] = 0;
+    return d;
+}
 
 template <typename Real>
 __device__ __forceinline__ Smem<Real> carve(const TsDevProg &P, unsigned char *raw) {
@@ -352,9 +369,11 @@ __device__ __forceinline__ Smem<Real> carve(const TsDevProg &P, unsigned char *r
     Real *pos = slots + 3 * P.slot_cap;
     m.slot = slots;
     m.pos = pos;
-    m.alt = P.edge_gather ? pos + 3 * P.Vstore : pos;
-    m.deg = reinterpret_cast<int *>(pos + 3 * P.Vstore * (P.edge_gather ? 2 : 1));
-    m.cbits = reinterpret_cast<unsigned *>(m.deg + P.Vf_pad);
+    const bool pp = P.edge_gather && !P.narrow;   // ping-pong positions
+    m.alt = pp ? pos + 3 * P.Vstore : pos;
+    m.deg = reinterpret_cast<int *>(pos + 3 * P.Vstore * (pp ? 2 : 1));
+    m.narrow = P.narrow;
+    m.cbits = reinterpret_cast<unsigned *>(reinterpret_cast<unsigned char *>(m.deg) + (P.narrow ? 1 : 4) * P.Vf_pad);
     return m;
 }
 
@@ -391,8 +410,8 @@ __device__ __forceinline__ void edge_item(const Smem<Real> &m, int pa, int pb, i
     if (sa >= 0) { m.SX(sa) = ca * dx; m.SY(sa) = ca * dy; m.SZ(sa) = ca * dz; }   // -1: pinned endpoint
     if (sb >= 0) { m.SX(sb) = cb * dx; m.SY(sb) = cb * dy; m.SZ(sb) = cb * dz; }
     if (degenerate) {
-        if (pa < vfp) atomicAdd(&m.deg[pa], 1);
-        if (pb < vfp) atomicAdd(&m.deg[pb], 1);
+        if (pa < vfp) deg_add(m.narrow, m.deg, pa);
+        if (pb < vfp) deg_add(m.narrow, m.deg, pb);
     }
 }
 
@@ -463,7 +482,7 @@ __device__ __forceinline__ void tet_item(const Smem<Real> &m, int4 id, int4 sl, 
 
 // fp32 tet item on byte-offset streams (boff programs): q = {a | b << 16, c | d << 16, slot a | b << 16,
 // slot c | d << 16}, all byte offsets into the position / slot buffers (no index multiplies)
-__device__ __forceinline__ void tet_item_b(const char *pb, char *sb, int *deg, uint4 q, float rvi, float kv,
+__device__ __forceinline__ void tet_item_b(const char *pb, char *sb, int *deg, int narrow, uint4 q, float rvi, float kv,
                                            unsigned vfp_b, unsigned pmask) {
     // pmask = 0x3fff when the top two bits of each position field carry the 6 V0 dictionary index
     const unsigned oa = q.x & pmask, ob = (q.x >> 16) & pmask, oc = q.y & pmask, od = (q.y >> 16) & pmask;
@@ -507,10 +526,10 @@ __device__ __forceinline__ void tet_item_b(const char *pb, char *sb, int *deg, u
     st3(q.w & 0xffffu, Gcx, Gcy, Gcz);
     st3(q.w >> 16, Gdx, Gdy, Gdz);
     if (degenerate) {
-        if (oa < vfp_b) atomicAdd(&deg[oa / 12], 1);
-        if (ob < vfp_b) atomicAdd(&deg[ob / 12], 1);
-        if (oc < vfp_b) atomicAdd(&deg[oc / 12], 1);
-        if (od < vfp_b) atomicAdd(&deg[od / 12], 1);
+        if (oa < vfp_b) deg_add(narrow, deg, oa / 12);
+        if (ob < vfp_b) deg_add(narrow, deg, ob / 12);
+        if (oc < vfp_b) deg_add(narrow, deg, oc / 12);
+        if (od < vfp_b) deg_add(narrow, deg, od / 12);
     }
 }
 
@@ -533,7 +552,7 @@ __device__ __forceinline__ void p1_tets(const TsDevProg &P, const Smem<Real> &m,
                     const unsigned ri = ((q.x >> 14) & 3u) | ((q.x >> 28) & 12u) | ((q.y >> 10) & 48u) |
                                         ((q.y >> 24) & 192u);
                     if ((q.z & q.w) != 0xffffffffu)   // all four slots absent: idle lane of the bank schedule
-                        tet_item_b(pb, sb, m.deg, q, __ldg(P.rvtab + ri), kv, 12u * (unsigned)vfp, 0x3fffu);
+                        tet_item_b(pb, sb, m.deg, m.narrow, q, __ldg(P.rvtab + ri), kv, 12u * (unsigned)vfp, 0x3fffu);
                 }
                 return;
             }
@@ -544,7 +563,7 @@ __device__ __forceinline__ void p1_tets(const TsDevProg &P, const Smem<Real> &m,
                 nq = __ldg(it + i + 32);
                 nrv = __ldg(rv + i + 32);
                 if ((q.z & q.w) != 0xffffffffu)   // idle lane of the bank schedule
-                    tet_item_b(pb, sb, m.deg, q, rvi, kv, 12u * (unsigned)vfp, 0xffffu);
+                    tet_item_b(pb, sb, m.deg, m.narrow, q, rvi, kv, 12u * (unsigned)vfp, 0xffffu);
             }
             return;
         }
@@ -647,10 +666,10 @@ __device__ __forceinline__ void tet_item(const Smem<Real> &m, int4 id, int4 sl, 
             put_slot(m, sl.w, sc, Gdx, Gdy, Gdz);
         }
         if (degenerate) {
-            if (id.x < vfp) atomicAdd(&m.deg[id.x], 1);
-            if (id.y < vfp) atomicAdd(&m.deg[id.y], 1);
-            if (id.z < vfp) atomicAdd(&m.deg[id.z], 1);
-            if (id.w < vfp) atomicAdd(&m.deg[id.w], 1);
+            if (id.x < vfp) deg_add(m.narrow, m.deg, id.x);
+            if (id.y < vfp) deg_add(m.narrow, m.deg, id.y);
+            if (id.z < vfp) deg_add(m.narrow, m.deg, id.z);
+            if (id.w < vfp) deg_add(m.narrow, m.deg, id.w);
         }
     }
 }
@@ -688,11 +707,11 @@ __device__ void p1_atts(const TsDevProg &P, const Smem<Real> &m, int begin, int 
             put_slot(m, sl.w, cb, dx, dy, dz);
         }
         if (mm == (Real)0) {
-            if (sl.x >= 0) atomicAdd(&m.deg[id.x], 1);
+            if (sl.x >= 0) deg_add(m.narrow, m.deg, id.x);
             if (face) {
-                if (sl.y >= 0) atomicAdd(&m.deg[id.y], 1);
-                if (sl.z >= 0) atomicAdd(&m.deg[id.z], 1);
-                if (sl.w >= 0) atomicAdd(&m.deg[id.w], 1);
+                if (sl.y >= 0) deg_add(m.narrow, m.deg, id.y);
+                if (sl.z >= 0) deg_add(m.narrow, m.deg, id.z);
+                if (sl.w >= 0) deg_add(m.narrow, m.deg, id.w);
             }
         }
     }
@@ -1077,7 +1096,7 @@ __device__ __forceinline__ void step_env(const TsDevProg &P, const TsDevProg *pr
             vx[r] = vg[3 * o]; vy[r] = vg[3 * o + 1]; vz[r] = vg[3 * o + 2];
         }
     }
-    for (int p = t; p < P.Vf_pad; p += B) m.deg[p] = 0;
+    for (int p = t; p < (P.narrow ? P.Vf_pad / 4 : P.Vf_pad); p += B) m.deg[p] = 0;
     for (int i = t; i < P.cbits_words; i += B) m.cbits[i] = 0u;
     if constexpr (CL) cl::sync();   // every CTA holds its halo before anyone pushes into it
     else __syncthreads();
@@ -1220,8 +1239,7 @@ __device__ __forceinline__ void step_env(const TsDevProg &P, const TsDevProg *pr
                             }
                         }
                         accx[r] = ax; accy[r] = ay; accz[r] = az;
-                        const int dg = m.deg[p];
-                        if (dg) { ndeg[r] += dg; m.deg[p] = 0; }
+                        ndeg[r] += deg_take(m.narrow, m.deg, p);
                     }
                 }
                 if (c + 1 < P.n_chunks) __syncthreads();   // slots are reused by the next chunk
@@ -1263,7 +1281,8 @@ __device__ __forceinline__ void step_env(const TsDevProg &P, const TsDevProg *pr
                         vy[r] += h * gy; yr[r] += h * vy[r];
                         vz[r] += h * gz; zr[r] += h * vz[r];
                     }
-                    // edge_gather: other owners may still read this substep's snapshot -> ping-pong
+                    // ping-pong when other owners may still read this substep's snapshot (distance-only
+                    // gather in this phase, cluster halos); narrow programs write in place (alt == pos)
                     Real *dst = m.alt + 3 * p;
                     dst[0] = xr[r]; dst[1] = yr[r]; dst[2] = zr[r];
                     if constexpr (CL) halo_send<Real>(P, m.alt, p, xr[r], yr[r], zr[r]);

@@ -197,7 +197,12 @@ def _program_key(arrays: SceneArrays, o) -> str:
     d = arrays.desc()
     h.update(repr((d.k_s, d.k_v, d.k_contact, d.contact_iterations)).encode())
     h.update(bytes(o))
+    # the compiler's development knobs (environment) change the program too
+    h.update(repr([(k, os.environ.get(k)) for k in _COMPILER_ENV]).encode())
     return h.hexdigest()
+
+
+_COMPILER_ENV = ("TS_SA_FOCUS", "TS_REFINE_ITERS", "TS_TET_HOLES", "TS_SPLIT_CT", "TS_NARROW")
 
 
 def compile_program(arrays: SceneArrays, **layout):
