@@ -42,6 +42,7 @@ def build(force=False, verbose=False):
     os.makedirs(OUT_DIR, exist_ok=True)
     cmd = [nvcc_bin(), "-gencode", GENCODE, "-lineinfo", "-O3", "-fmad=false", "-std=c++17",
            "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v" if verbose else "-O3",
+           *os.environ.get("TS_NVCC_FLAGS", "").split(),   # development experiments only
            *[os.path.join(CSRC, s) for s in SOURCES], "-o", LIB + ".tmp"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:

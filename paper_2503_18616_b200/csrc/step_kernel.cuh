@@ -1522,7 +1522,13 @@ __device__ __forceinline__ void step_env(const TsDevProg &P, const TsDevProg *pr
 }
 
 template <typename Real, int VPT>
-__global__ void __launch_bounds__(512, sizeof(Real) == 4 ? 2 : 1) step_kernel(const __grid_constant__ TsDevProg P,
+#ifndef TS_STEP_MAXT
+#define TS_STEP_MAXT 512
+#endif
+#ifndef TS_STEP_MINB
+#define TS_STEP_MINB 2
+#endif
+__global__ void __launch_bounds__(TS_STEP_MAXT, sizeof(Real) == 4 ? TS_STEP_MINB : 1) step_kernel(const __grid_constant__ TsDevProg P,
                                                    const __grid_constant__ TsParams S,
                                                    const __grid_constant__ TsLaunch L) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
