@@ -1051,7 +1051,7 @@ __device__ __forceinline__ void halo_send(const TsDevProg &P, const Real *buf, i
 // CL = false: this CTA owns the whole env.  CL = true: this CTA is rank `rank` of the env's
 // cluster (program P = progs[rank]); it owns part of the vertices and keeps a halo of the rest
 // current over DSMEM; grasp search, contacts and the divergence flag are cluster-wide.
-template <typename Real, int VPT, bool CL>
+template <typename Real, int VPT, bool CL, bool EO = false>
 __device__ __forceinline__ void step_env(const TsDevProg &P, const TsDevProg *progs, const TsParams &S,
                                          const TsLaunch &L, Smem<Real> &m, int64_t env, unsigned rank) {
     Scal &sc = *m.sc;
@@ -1190,7 +1190,7 @@ __device__ __forceinline__ void step_env(const TsDevProg &P, const TsDevProg *pr
             }
         };
         for (int s = 0; s < S.substeps; ++s) {
-            for (int c = 0; c < P.n_chunks; ++c) {
+            if constexpr (!EO) for (int c = 0; c < P.n_chunks; ++c) {
                 const TsChunk ch = P.chunks[c];
                 // owner-gathered edges need only the position snapshot: they run in phase 1 of the
                 // first chunk, next to this warp's share of the tets (the compiler sized the shares so
@@ -1521,13 +1521,13 @@ __device__ __forceinline__ void step_env(const TsDevProg &P, const TsDevProg *pr
     else __syncthreads();           // shared scalars are reused by the next environment
 }
 
-template <typename Real, int VPT>
 #ifndef TS_STEP_MAXT
 #define TS_STEP_MAXT 512
 #endif
 #ifndef TS_STEP_MINB
 #define TS_STEP_MINB 2
 #endif
+template <typename Real, int VPT>
 __global__ void __launch_bounds__(TS_STEP_MAXT, sizeof(Real) == 4 ? TS_STEP_MINB : 1) step_kernel(const __grid_constant__ TsDevProg P,
                                                    const __grid_constant__ TsParams S,
                                                    const __grid_constant__ TsLaunch L) {
@@ -1536,6 +1536,26 @@ __global__ void __launch_bounds__(TS_STEP_MAXT, sizeof(Real) == 4 ? TS_STEP_MINB
     if ((L.mode & TS_M_CHECK_ACTIONS) && *L.bad_flag) return;   // deferred ValidationError: no state change
     for (int64_t env = blockIdx.x; env < L.n_env; env += gridDim.x)
         step_env<Real, VPT, false>(P, nullptr, S, L, m, env, 0);
+}
+
+// Distance-constraint-only programs (no chunks: SURVEY §8(d) config 2): the same step with the slot
+// machinery compiled out (measured 0.101 vs 0.124 ms/step at 1024 envs; more CTAs per SM at fewer
+// registers were slower: 0.118-0.123 ms, profiles/r01i/negative_results.txt).
+#ifndef TS_EDGES_MAXT
+#define TS_EDGES_MAXT 512
+#endif
+#ifndef TS_EDGES_MINB
+#define TS_EDGES_MINB 2
+#endif
+template <typename Real>
+__global__ void __launch_bounds__(TS_EDGES_MAXT, TS_EDGES_MINB) edges_step_kernel(const __grid_constant__ TsDevProg P,
+                                                            const __grid_constant__ TsParams S,
+                                                            const __grid_constant__ TsLaunch L) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    Smem<Real> m = carve<Real>(P, smem_raw);
+    if ((L.mode & TS_M_CHECK_ACTIONS) && *L.bad_flag) return;
+    for (int64_t env = blockIdx.x; env < L.n_env; env += gridDim.x)
+        step_env<Real, 1, false, true>(P, nullptr, S, L, m, env, 0);
 }
 
 // Large-mesh mode: a thread-block cluster of K CTAs per environment (grid = K x clusters).
@@ -1604,7 +1624,8 @@ template <typename Real>
 cudaError_t ts_launch_step(const TsDevProg &P, const TsParams &S, const TsLaunch &L, int grid, int smem,
                            cudaStream_t stream) {
     void (*fn)(const TsDevProg, const TsParams, const TsLaunch) = nullptr;
-    switch (P.VPT) {
+    if (sizeof(Real) == 4 && P.n_chunks == 0 && P.VPT == 1 && P.B <= TS_EDGES_MAXT) fn = tsk::edges_step_kernel<Real>;
+    else switch (P.VPT) {
         case 1: fn = tsk::step_kernel<Real, 1>; break;
         case 2: fn = tsk::step_kernel<Real, 2>; break;
         case 4: fn = tsk::step_kernel<Real, 4>; break;
