@@ -336,9 +336,9 @@ def run_gpu(args, wl):
         with open(prof) as fh:
             traffic = json.load(fh).get("dram_bytes_per_launch")
     hbm_achieved = hbm_bytes(V) * n / (kern_avg_ms * 1e-3) / 1e9
-    kname = (f"tsk::cluster_step_kernel<{'float' if args.precision == 'fp32' else 'double'}, "
-             f"{info['vertices_per_thread']}> x{info['cluster_size']} CTAs per env") if info["cluster_size"] > 1 \
-        else f"tsk::step_kernel<{'float' if args.precision == 'fp32' else 'double'}, {info['vertices_per_thread']}>"
+    kname = lib.ts_step_kernel_name(handle).decode()   # the instantiation the program selects
+    if info["cluster_size"] > 1:
+        kname += f" x{info['cluster_size']} CTAs per env"
 
     line = {
         "metric": wl["metric"], "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,

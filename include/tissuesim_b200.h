@@ -250,6 +250,10 @@ int64_t ts_launch_count(void);
 int32_t ts_kernel_timing(ts_handle *h, int32_t enable, int32_t max_launches);
 int32_t ts_kernel_time(ts_handle *h, double *total_ms, int64_t *launches);
 
+/* Name of the fused step kernel this handle launches (the layout-specialised instantiation the
+ * program selects), as ncu prints it -- for profiles and the bench's roofline line. */
+const char *ts_step_kernel_name(ts_handle *h);
+
 #ifdef __cplusplus
 }
 #endif

@@ -103,6 +103,7 @@ _SIGNATURES = {
     "ts_uniform_actions_dev": ([_P, _I64, _I64, ctypes.c_uint64, _P, _P], _I32),
     "ts_kernel_timing": ([_P, _I32, _I32], _I32),
     "ts_kernel_time": ([_P, _P, _P], _I32),
+    "ts_step_kernel_name": ([_P], ctypes.c_char_p),
 }
 
 _lib = None

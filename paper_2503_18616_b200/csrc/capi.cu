@@ -42,6 +42,23 @@ struct ts_handle {
     TsDevProg *dev_parts = nullptr;     // the same, on the device (cluster kernel argument)
 };
 
+static const char *ts_kernel_name_for(const TsDevProg &P, int real_bytes, int cluster_k, int ablate) {
+    static const char *names[] = {
+        "tsk::fast_step_kernel<float>", "tsk::edges_step_kernel<float>",
+        "tsk::step_kernel<float, 1>", "tsk::step_kernel<float, 2>", "tsk::step_kernel<float, 4>",
+        "tsk::step_kernel<float, 8>", "tsk::step_kernel<double, 1>", "tsk::step_kernel<double, 2>",
+        "tsk::step_kernel<double, 4>", "tsk::step_kernel<double, 8>",
+        "tsk::cluster_step_kernel<float, 1>", "tsk::cluster_step_kernel<float, 2>",
+        "tsk::cluster_step_kernel<float, 4>", "tsk::cluster_step_kernel<double, 1>",
+        "tsk::cluster_step_kernel<double, 2>", "tsk::cluster_step_kernel<double, 4>"};
+    const int d = real_bytes == 8;
+    if (cluster_k > 1) return names[10 + 3 * d + (P.VPT <= 1 ? 0 : P.VPT <= 2 ? 1 : 2)];
+    if (!d && ts_use_fast_kernel(P, ablate)) return names[0];
+    if (!d && ts_use_edges_kernel(P)) return names[1];
+    const int v = P.VPT <= 1 ? 0 : P.VPT == 2 ? 1 : P.VPT <= 4 ? 2 : 3;   // VPT 3 runs the 4 kernel
+    return names[2 + 4 * d + v];
+}
+
 extern "C" {
 
 const char *ts_last_error(void) { return g_err.c_str(); }
@@ -120,6 +137,9 @@ static void decode_part(const uint8_t *host, const uint8_t *b, TsDevProg &P) {
     P.tet_c = reinterpret_cast<const uint4 *>(b + H->off[TS_SEC_TET_C]);
     P.edge_gather = H->edge_gather;
     P.narrow = H->narrow;
+    P.fast = H->real_bytes == 4 && H->VPT == 1 && H->n_chunks == 1 && H->grasp_chunk == 0 && H->edge_gather &&
+             H->einc_bytes == 4 && H->boff && H->rvdict && H->narrow && H->n_att_items == 0 &&
+             H->n_edge_items == 0 && H->cluster_k == 1 && H->compact;
     P.einc_bytes = H->einc_bytes;
     P.einc = b + H->off[TS_SEC_EINC];
     P.eregion = reinterpret_cast<const int32_t *>(b + H->off[TS_SEC_EREGION]);
@@ -459,6 +479,11 @@ int32_t ts_kernel_timing(ts_handle *h, int32_t enable, int32_t max_launches) {
         if (e != cudaSuccess) return cuda_fail(e, "cudaEventCreate");
     }
     return TS_OK;
+}
+
+const char *ts_step_kernel_name(ts_handle *h) {
+    if (!h) { fail(TS_ERR_INVALID, "null handle"); return ""; }
+    return ts_kernel_name_for(h->prog, h->precision == TS_F64 ? 8 : 4, h->cluster_k, h->params.ablate);
 }
 
 int32_t ts_kernel_time(ts_handle *h, double *total_ms, int64_t *launches) {

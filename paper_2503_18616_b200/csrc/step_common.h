@@ -73,6 +73,7 @@ struct TsDevProg {
     const uint4 *edge_c;
     const uint4 *tet_c;
     int32_t narrow;           // single position buffer + byte degenerate counters (program.h)
+    int32_t fast;             // the reach-scene shape: fast_step_kernel (step_kernel.cuh)
     int32_t edge_gather;      // 1: owner-gathered edges (records below), positions double-buffered
     int32_t einc_bytes;       // 8 or 16
     const void *einc;
@@ -153,6 +154,26 @@ inline int ts_smem_bytes(const TsDevProg &P, int real_bytes) {
 }
 
 // command kernel -> fused step kernel -> epilogue kernel, stream ordered
+// step-kernel launch bounds (overridable with -D for experiments: build.py TS_NVCC_FLAGS)
+#ifndef TS_STEP_MAXT
+#define TS_STEP_MAXT 512
+#endif
+#ifndef TS_STEP_MINB
+#define TS_STEP_MINB 2
+#endif
+#ifndef TS_EDGES_MAXT
+#define TS_EDGES_MAXT 512
+#endif
+#ifndef TS_EDGES_MINB
+#define TS_EDGES_MINB 2
+#endif
+// fp32 shape-specialised kernels (step_kernel.cuh): the reach-scene shape, and distance-only programs
+inline bool ts_use_fast_kernel(const TsDevProg &P, int ablate) {
+    return P.fast && P.B <= TS_STEP_MAXT && !(ablate & 256);
+}
+inline bool ts_use_edges_kernel(const TsDevProg &P) {
+    return P.n_chunks == 0 && P.VPT == 1 && P.B <= TS_EDGES_MAXT;
+}
 template <typename Real>
 cudaError_t ts_launch_step(const TsDevProg &P, const TsParams &S, const TsLaunch &L, int grid,
                            int smem, cudaStream_t stream);

@@ -533,19 +533,19 @@ __device__ __forceinline__ void tet_item_b(const char *pb, char *sb, int *deg, i
     }
 }
 
-template <typename Real>
+template <typename Real, bool FAST = false>
 __device__ __forceinline__ void p1_tets(const TsDevProg &P, const Smem<Real> &m, int begin, int wb, int we, Real kv) {
     // this warp's contiguous range [wb, we) of the chunk's items, lane l takes wb + l, wb + l + 32, ...
     const Real *rv = reinterpret_cast<const Real *>(P.tet_rv) + begin;
     const int vfp = P.Vf_pad;
     const int lane = threadIdx.x & 31;
     if constexpr (sizeof(Real) == 4) {
-        if (P.boff) {   // byte-offset stream, padded by a CTA's worth of items: unclamped prefetch
+        if (FAST || P.boff) {   // byte-offset stream, padded by a CTA's worth of items: unclamped prefetch
             const uint4 *it = P.tet_c + begin;
             const char *pb = reinterpret_cast<const char *>(m.pos);
             char *sb = reinterpret_cast<char *>(m.slot);   // == shared base + TS_SMEM_HEAD
             uint4 nq = __ldg(it + wb + lane);
-            if (P.rvdict) {   // rest volume from the stream's spare bits + a tiny (L1-resident) table
+            if (FAST || P.rvdict) {   // rest volume from the stream's spare bits + a tiny (L1-resident) table
                 for (int i = wb + lane; i < we; i += 32) {
                     const uint4 q = nq;
                     nq = __ldg(it + i + 32);
@@ -725,7 +725,7 @@ __device__ void p1_atts(const TsDevProg &P, const Smem<Real> &m, int begin, int 
 // fp64: -(w_p scale) (x_p - x_q) with the reference's scale expression
 // (ts_lane_edges, _kernels.pyx:121-136) -- bitwise the reference's per-endpoint
 // term, see compiler.cpp; fp32: -coef (1 - rest / dist) (x_p - x_q) with FMAs.
-template <typename Real>
+template <typename Real, bool FAST = false>
 __device__ __forceinline__ void owner_edges(const TsDevProg &P, const Smem<Real> &m, int p, int lane, Real px,
                                             Real py, Real pz, Real ks, Real &ax, Real &ay, Real &az, int &ndeg) {
     const int ev = P.evalence[p];
@@ -747,7 +747,7 @@ __device__ __forceinline__ void owner_edges(const TsDevProg &P, const Smem<Real>
             ax = ax + c * dx; ay = ay + c * dy; az = az + c * dz;
             ndeg += mm == 0.0;
         }
-    } else if (P.einc_bytes == 4) {
+    } else if (FAST || P.einc_bytes == 4) {
         // 4-byte records: {neighbour byte offset | rest-length index << 16 | pinned << 31}
         const unsigned *rec = reinterpret_cast<const unsigned *>(P.einc) + rb;
         const char *pb = reinterpret_cast<const char *>(m.pos);
@@ -1051,7 +1051,7 @@ __device__ __forceinline__ void halo_send(const TsDevProg &P, const Real *buf, i
 // CL = false: this CTA owns the whole env.  CL = true: this CTA is rank `rank` of the env's
 // cluster (program P = progs[rank]); it owns part of the vertices and keeps a halo of the rest
 // current over DSMEM; grasp search, contacts and the divergence flag are cluster-wide.
-template <typename Real, int VPT, bool CL, bool EO = false>
+template <typename Real, int VPT, bool CL, bool EO = false, bool FAST = false>
 __device__ __forceinline__ void step_env(const TsDevProg &P, const TsDevProg *progs, const TsParams &S,
                                          const TsLaunch &L, Smem<Real> &m, int64_t env, unsigned rank) {
     Scal &sc = *m.sc;
@@ -1190,7 +1190,7 @@ __device__ __forceinline__ void step_env(const TsDevProg &P, const TsDevProg *pr
             }
         };
         for (int s = 0; s < S.substeps; ++s) {
-            if constexpr (!EO) for (int c = 0; c < P.n_chunks; ++c) {
+            if constexpr (!EO) for (int c = 0; c < (FAST ? 1 : P.n_chunks); ++c) {
                 const TsChunk ch = P.chunks[c];
                 // owner-gathered edges need only the position snapshot: they run in phase 1 of the
                 // first chunk, next to this warp's share of the tets (the compiler sized the shares so
@@ -1201,16 +1201,16 @@ __device__ __forceinline__ void step_env(const TsDevProg &P, const TsDevProg *pr
                     for (int r = 0; r < VPT; ++r) {
                         const int p = r * B + t;
                         if (p < P.Vf)
-                            owner_edges<Real>(P, m, p, lane, xr[r], yr[r], zr[r], ks, accx[r], accy[r], accz[r],
-                                              ndeg[r]);
+                            owner_edges<Real, FAST>(P, m, p, lane, xr[r], yr[r], zr[r], ks, accx[r], accy[r],
+                                                    accz[r], ndeg[r]);
                     }
                 }
                 // phase 1: every kind of the chunk, no barrier in between (disjoint slots)
-                if (ch.edge_count) p1_edges<Real>(P, m, ch.edge_begin, ch.edge_count, ks);
-                if (ch.att_count) p1_atts<Real>(P, m, ch.att_begin, ch.att_count);
+                if (!FAST && ch.edge_count) p1_edges<Real>(P, m, ch.edge_begin, ch.edge_count, ks);
+                if (!FAST && ch.att_count) p1_atts<Real>(P, m, ch.att_begin, ch.att_count);
                 if (ch.tet_count && !(S.ablate & 1)) {
                     const int *ws = P.wsplit + c * (B / 32 + 1) + (t >> 5);
-                    p1_tets<Real>(P, m, ch.tet_begin, ws[0], ws[1], kv);
+                    p1_tets<Real, FAST>(P, m, ch.tet_begin, ws[0], ws[1], kv);
                 }
                 __syncthreads();
                 // phase 2: owner gathers its slots in reference order
@@ -1239,12 +1239,12 @@ __device__ __forceinline__ void step_env(const TsDevProg &P, const TsDevProg *pr
                             }
                         }
                         accx[r] = ax; accy[r] = ay; accz[r] = az;
-                        ndeg[r] += deg_take(m.narrow, m.deg, p);
+                        ndeg[r] += deg_take(FAST ? 1 : m.narrow, m.deg, p);
                     }
                 }
-                if (c + 1 < P.n_chunks) __syncthreads();   // slots are reused by the next chunk
+                if (!FAST && c + 1 < P.n_chunks) __syncthreads();   // slots are reused by the next chunk
             }
-            if (P.grasp_chunk == P.n_chunks) {
+            if (!FAST && P.grasp_chunk == P.n_chunks) {
 #pragma unroll
                 for (int r = 0; r < VPT; ++r) {
                     const int p = r * B + t;
@@ -1291,7 +1291,7 @@ __device__ __forceinline__ void step_env(const TsDevProg &P, const TsDevProg *pr
             }
             if constexpr (CL) cl::sync();
             else __syncthreads();
-            if (P.edge_gather) {
+            if (!FAST && P.edge_gather) {
                 Real *cur = m.pos;
                 m.pos = m.alt;
                 m.alt = cur;
@@ -1521,12 +1521,6 @@ __device__ __forceinline__ void step_env(const TsDevProg &P, const TsDevProg *pr
     else __syncthreads();           // shared scalars are reused by the next environment
 }
 
-#ifndef TS_STEP_MAXT
-#define TS_STEP_MAXT 512
-#endif
-#ifndef TS_STEP_MINB
-#define TS_STEP_MINB 2
-#endif
 template <typename Real, int VPT>
 __global__ void __launch_bounds__(TS_STEP_MAXT, sizeof(Real) == 4 ? TS_STEP_MINB : 1) step_kernel(const __grid_constant__ TsDevProg P,
                                                    const __grid_constant__ TsParams S,
@@ -1538,15 +1532,23 @@ __global__ void __launch_bounds__(TS_STEP_MAXT, sizeof(Real) == 4 ? TS_STEP_MINB
         step_env<Real, VPT, false>(P, nullptr, S, L, m, env, 0);
 }
 
+// The reach-scene shape (fp32, one CTA, one chunk, owner-gathered edges in 4-byte records, byte-offset
+// tet stream with dictionary-coded volumes, no attachments, narrow layout): every layout test resolved
+// at compile time.  ts_fast_program() is the host-side test.
+template <typename Real>
+__global__ void __launch_bounds__(TS_STEP_MAXT, TS_STEP_MINB) fast_step_kernel(const __grid_constant__ TsDevProg P,
+                                                                              const __grid_constant__ TsParams S,
+                                                                              const __grid_constant__ TsLaunch L) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    Smem<Real> m = carve<Real>(P, smem_raw);
+    if ((L.mode & TS_M_CHECK_ACTIONS) && *L.bad_flag) return;
+    for (int64_t env = blockIdx.x; env < L.n_env; env += gridDim.x)
+        step_env<Real, 1, false, false, true>(P, nullptr, S, L, m, env, 0);
+}
+
 // Distance-constraint-only programs (no chunks: SURVEY §8(d) config 2): the same step with the slot
 // machinery compiled out (measured 0.101 vs 0.124 ms/step at 1024 envs; more CTAs per SM at fewer
 // registers were slower: 0.118-0.123 ms, profiles/r01i/negative_results.txt).
-#ifndef TS_EDGES_MAXT
-#define TS_EDGES_MAXT 512
-#endif
-#ifndef TS_EDGES_MINB
-#define TS_EDGES_MINB 2
-#endif
 template <typename Real>
 __global__ void __launch_bounds__(TS_EDGES_MAXT, TS_EDGES_MINB) edges_step_kernel(const __grid_constant__ TsDevProg P,
                                                             const __grid_constant__ TsParams S,
@@ -1624,8 +1626,11 @@ template <typename Real>
 cudaError_t ts_launch_step(const TsDevProg &P, const TsParams &S, const TsLaunch &L, int grid, int smem,
                            cudaStream_t stream) {
     void (*fn)(const TsDevProg, const TsParams, const TsLaunch) = nullptr;
-    if (sizeof(Real) == 4 && P.n_chunks == 0 && P.VPT == 1 && P.B <= TS_EDGES_MAXT) fn = tsk::edges_step_kernel<Real>;
-    else switch (P.VPT) {
+    if constexpr (sizeof(Real) == 4) {   // shape-specialised fp32 kernels
+        if (ts_use_fast_kernel(P, S.ablate)) fn = tsk::fast_step_kernel<Real>;
+        else if (ts_use_edges_kernel(P)) fn = tsk::edges_step_kernel<Real>;
+    }
+    if (!fn) switch (P.VPT) {
         case 1: fn = tsk::step_kernel<Real, 1>; break;
         case 2: fn = tsk::step_kernel<Real, 2>; break;
         case 4: fn = tsk::step_kernel<Real, 4>; break;
