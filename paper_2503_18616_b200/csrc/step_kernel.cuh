@@ -727,9 +727,10 @@ __device__ void p1_atts(const TsDevProg &P, const Smem<Real> &m, int begin, int 
 // term, see compiler.cpp; fp32: -coef (1 - rest / dist) (x_p - x_q) with FMAs.
 template <typename Real, bool FAST = false>
 __device__ __forceinline__ void owner_edges(const TsDevProg &P, const Smem<Real> &m, int p, int lane, Real px,
-                                            Real py, Real pz, Real ks, Real &ax, Real &ay, Real &az, int &ndeg) {
-    const int ev = P.evalence[p];
-    const int rb = P.eregion[p >> 5] + lane;
+                                            Real py, Real pz, Real ks, Real &ax, Real &ay, Real &az, int &ndeg,
+                                            int ev_h = 0, int rb_h = 0) {
+    const int ev = FAST ? ev_h : P.evalence[p];            // FAST: hoisted out of the substep loop
+    const int rb = FAST ? rb_h : P.eregion[p >> 5] + lane;
     if constexpr (sizeof(Real) == 8) {
         const int4 *rec = reinterpret_cast<const int4 *>(P.einc) + rb;
         const double *wst = reinterpret_cast<const double *>(P.w);
@@ -1177,6 +1178,21 @@ __device__ __forceinline__ void step_env(const TsDevProg &P, const TsDevProg *pr
         }
         if constexpr (CL) cl::sync();
         else __syncthreads();
+        // FAST (one chunk): the per-vertex program words are substep-invariant -> registers
+        int h_base[VPT], h_val[VPT], h_pre[VPT], h_cnt[VPT], h_ev[VPT], h_rb[VPT];
+        if constexpr (FAST) {
+            const TsChunk ch0 = P.chunks[0];
+#pragma unroll
+            for (int r = 0; r < VPT; ++r) {
+                const int p = max(0, min(r * B + t, P.Vf - 1));   // rows past Vf are never used
+                h_base[r] = P.region[ch0.region_off + (p >> 5)] + lane;
+                h_val[r] = P.valence[ch0.val_off + p];
+                h_pre[r] = min(h_val[r], P.gsplit[p]);
+                h_cnt[r] = P.static_cnt[p];
+                h_ev[r] = P.evalence[p];
+                h_rb[r] = P.eregion[p >> 5] + lane;
+            }
+        }
         const double d0 = sc.drag[0], d1 = sc.drag[1], d2 = sc.drag[2];
         // grasp contribution of owner slot r: after the vertex's edges (_kernels.pyx:283-298)
         auto add_grasp = [&](int r) {
@@ -1202,7 +1218,7 @@ __device__ __forceinline__ void step_env(const TsDevProg &P, const TsDevProg *pr
                         const int p = r * B + t;
                         if (p < P.Vf)
                             owner_edges<Real, FAST>(P, m, p, lane, xr[r], yr[r], zr[r], ks, accx[r], accy[r],
-                                                    accz[r], ndeg[r]);
+                                                    accz[r], ndeg[r], h_ev[r], h_rb[r]);
                     }
                 }
                 // phase 1: every kind of the chunk, no barrier in between (disjoint slots)
@@ -1214,15 +1230,15 @@ __device__ __forceinline__ void step_env(const TsDevProg &P, const TsDevProg *pr
                 }
                 __syncthreads();
                 // phase 2: owner gathers its slots in reference order
-                const bool gchunk = c == P.grasp_chunk;
+                const bool gchunk = FAST || c == P.grasp_chunk;
 #pragma unroll
                 for (int r = 0; r < VPT; ++r) {
                     const int p = r * B + t;
                     if (p < P.Vf) {
-                        const int base = P.region[ch.region_off + (p >> 5)] + lane;
-                        const int val = (S.ablate & 2) ? 0 : ((S.ablate & 128) ? min(P.valence[ch.val_off + p], 12)
-                                                                                 : P.valence[ch.val_off + p]);
-                        const int pre = gchunk ? min(val, P.gsplit[p]) : val;
+                        const int base = FAST ? h_base[r] : P.region[ch.region_off + (p >> 5)] + lane;
+                        const int val0 = FAST ? h_val[r] : P.valence[ch.val_off + p];
+                        const int val = (S.ablate & 2) ? 0 : ((S.ablate & 128) ? min(val0, 12) : val0);
+                        const int pre = FAST && !(S.ablate & 130) ? h_pre[r] : gchunk ? min(val, P.gsplit[p]) : val;
                         Real ax = accx[r], ay = accy[r], az = accz[r];
 #pragma unroll 4
                         for (int k = 0; k < pre; ++k) {
@@ -1259,7 +1275,7 @@ __device__ __forceinline__ void step_env(const TsDevProg &P, const TsDevProg *pr
             for (int r = 0; r < VPT; ++r) {
                 const int p = r * B + t;
                 if (p < P.Vf) {
-                    const int cnt = P.static_cnt[p] - ndeg[r] + gcnt[r];
+                    const int cnt = (FAST ? h_cnt[r] : P.static_cnt[p]) - ndeg[r] + gcnt[r];
                     if constexpr (sizeof(Real) == 8) {
                         const Real n = (Real)cnt;
                         const Real mm = (Real)0.5 + copysign((Real)0.5, n - (Real)0.5);
