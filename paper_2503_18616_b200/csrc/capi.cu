@@ -139,7 +139,8 @@ static void decode_part(const uint8_t *host, const uint8_t *b, TsDevProg &P) {
     P.narrow = H->narrow;
     P.fast = H->real_bytes == 4 && H->VPT == 1 && H->n_chunks == 1 && H->grasp_chunk == 0 && H->edge_gather &&
              H->einc_bytes == 4 && H->boff && H->rvdict && H->narrow && H->n_att_items == 0 &&
-             H->n_edge_items == 0 && H->cluster_k == 1 && H->compact;
+             H->n_edge_items == 0 && H->cluster_k == 1 && H->compact && H->n_rltab <= TS_TAB_CAP &&
+             H->n_rvtab <= TS_TAB_CAP;
     P.einc_bytes = H->einc_bytes;
     P.einc = b + H->off[TS_SEC_EINC];
     P.eregion = reinterpret_cast<const int32_t *>(b + H->off[TS_SEC_EREGION]);
@@ -153,6 +154,7 @@ static void decode_part(const uint8_t *host, const uint8_t *b, TsDevProg &P) {
     P.rvdict = H->rvdict;
     P.rltab = reinterpret_cast<const float *>(b + H->off[TS_SEC_RLTAB]);
     P.rvtab = reinterpret_cast<const float *>(b + H->off[TS_SEC_RVTAB]);
+    P.n_rltab = H->n_rltab; P.n_rvtab = H->n_rvtab;
 }
 
 static void fill_params(const ts_scene_desc &d, TsParams &S) {

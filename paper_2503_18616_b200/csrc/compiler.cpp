@@ -1237,6 +1237,7 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
     hdr.Vown = Vown; hdr.cluster_k = part ? part->K : 1; hdr.cluster_rank = part ? part->rank : 0;
     hdr.boff = boff ? 1 : 0;
     hdr.rvdict = rv_tab.empty() ? 0 : 1;
+    hdr.n_rltab = (int)rl_tab.size(); hdr.n_rvtab = (int)rv_tab.size();
     hdr.n_chunks = n_chunks; hdr.grasp_chunk = grasp_chunk; hdr.slot_capacity = slot_cap; hdr.n_att = nA;
     hdr.n_edge_items = nE; hdr.n_tet_items = nT; hdr.n_att_items = nA; hdr.bank_conflicts = total_conf;
     hdr.n_slots_total = n_slots_total;

@@ -19,7 +19,7 @@
 #include <stdint.h>
 
 #define TS_PROG_MAGIC 0x54534231  // "TSB1"
-#define TS_PROG_VERSION 3
+#define TS_PROG_VERSION 4
 
 enum TsChunkKind { TS_CHUNK_EDGE = 0, TS_CHUNK_ATT = 1, TS_CHUNK_TET = 2 };
 
@@ -79,7 +79,9 @@ struct TsChunk {
     int32_t val_off, conflicts, pad0, pad1;
 };
 
-#define TS_SMEM_HEAD 1280       // scalar block + capsule parameters, at the start of shared memory
+#define TS_SMEM_HEAD 1792       // [scalars + capsules: 1280 | rest-length table | 6V0 table]
+#define TS_TAB_OFF 1280         // the two dictionary tables of fast programs, TS_TAB_CAP floats each
+#define TS_TAB_CAP 64       // scalar block + capsule parameters, at the start of shared memory
 
 // Shared memory one CTA needs for a program (the kernel's carve, step_kernel.cuh): positions
 // (x2 when ping-ponged), slot buffer / contact records, degenerate counters, contact bitmap,
@@ -120,6 +122,7 @@ struct TsProgHeader {
                                                    // boff: fp32 compact streams hold byte offsets
     int32_t rvdict, narrow;                        // rvdict: tet rest volumes dictionary-coded;
                                                    // narrow: one position buffer, 8-bit degenerate counters
+    int32_t n_rltab, n_rvtab;                      // dictionary sizes (RLTAB / RVTAB entries)
     double w_free;   // the common inverse mass of free vertices (compact programs)
     int64_t off[TS_SEC_COUNT];
     int64_t total_bytes;

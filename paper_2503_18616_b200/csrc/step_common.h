@@ -87,6 +87,7 @@ struct TsDevProg {
     int32_t rvdict;           // tet 6 V0 as a dictionary index in the stream's spare bits
     const float *rltab;       // distinct rest lengths (4-byte edge records)
     const float *rvtab;       // distinct 6 V0 values (rvdict)
+    int32_t n_rltab, n_rvtab; // their sizes (fast programs keep both in shared memory: TS_TAB_OFF)
     int32_t cluster_k, cluster_rank;
     const int32_t *send_off;  // [Vf_pad + 1]
     const int32_t *send;      // (rank << 20) | storage position of a halo copy

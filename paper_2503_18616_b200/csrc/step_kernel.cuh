@@ -338,6 +338,12 @@ struct Smem {
     Cap<Real> *caps;
 };
 
+// fast programs' dictionary tables at a fixed shared-memory offset (no base pointer to keep live)
+__device__ __forceinline__ const float *smem_tab(int byte_off) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    return reinterpret_cast<const float *>(smem_raw + byte_off);
+}
+
 __device__ __forceinline__ void deg_add(int narrow, int *deg, int i) {
     if (narrow) atomicAdd(reinterpret_cast<unsigned *>(deg) + (i >> 2), 1u << ((i & 3) * 8));
     else atomicAdd(&deg[i], 1);
@@ -361,7 +367,7 @@ __device__ __forceinline__ Smem<Real> carve(const TsDevProg &P, unsigned char *r
     //  arithmetic in phase 1), and everything a cluster peer addresses over DSMEM (scalars,
     //  slots / contact records, positions, the contact key list in the counters) sits at the same
     //  offset in every CTA of the cluster (parts share Vstore and the slot capacity)
-    static_assert(((sizeof(Scal) + 15) / 16) * 16 + 3 * sizeof(Cap<Real>) <= TS_SMEM_HEAD, "scalar block");
+    static_assert(((sizeof(Scal) + 15) / 16) * 16 + 3 * sizeof(Cap<Real>) <= TS_TAB_OFF, "scalar block");
     Smem<Real> m;
     m.sc = reinterpret_cast<Scal *>(raw);
     m.caps = reinterpret_cast<Cap<Real> *>(raw + ((sizeof(Scal) + 15) / 16) * 16);
@@ -552,7 +558,9 @@ __device__ __forceinline__ void p1_tets(const TsDevProg &P, const Smem<Real> &m,
                     const unsigned ri = ((q.x >> 14) & 3u) | ((q.x >> 28) & 12u) | ((q.y >> 10) & 48u) |
                                         ((q.y >> 24) & 192u);
                     if ((q.z & q.w) != 0xffffffffu)   // all four slots absent: idle lane of the bank schedule
-                        tet_item_b(pb, sb, m.deg, m.narrow, q, __ldg(P.rvtab + ri), kv, 12u * (unsigned)vfp, 0x3fffu);
+                        tet_item_b(pb, sb, m.deg, m.narrow, q,
+                                   FAST ? smem_tab(TS_TAB_OFF + 4 * TS_TAB_CAP)[ri] : __ldg(P.rvtab + ri), kv,
+                                   12u * (unsigned)vfp, 0x3fffu);
                 }
                 return;
             }
@@ -758,7 +766,7 @@ __device__ __forceinline__ void owner_edges(const TsDevProg &P, const Smem<Real>
             const unsigned cur = q;
             q = __ldg(rec + 32 * (k + 1));
             const float *nq = reinterpret_cast<const float *>(pb + (cur & 0xffffu));
-            const float rl = __ldg(P.rltab + ((cur >> 16) & 0x7fffu));
+            const float rl = FAST ? smem_tab(TS_TAB_OFF)[(cur >> 16) & 0x7fffu] : __ldg(P.rltab + ((cur >> 16) & 0x7fffu));
             const float dx = px - nq[0], dy = py - nq[1], dz = pz - nq[2];
             const float d2 = __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, dx * dx));
             const bool degenerate = !(d2 >= 1e-24f);
@@ -1098,6 +1106,13 @@ __device__ __forceinline__ void step_env(const TsDevProg &P, const TsDevProg *pr
         }
     }
     for (int p = t; p < (P.narrow ? P.Vf_pad / 4 : P.Vf_pad); p += B) m.deg[p] = 0;
+    if constexpr (FAST) {   // dictionary tables -> shared memory (read by every tet / edge of every substep)
+        float *tab = const_cast<float *>(smem_tab(TS_TAB_OFF));
+        for (int i = t; i < 2 * TS_TAB_CAP; i += B) {
+            const int j = i - TS_TAB_CAP;
+            tab[i] = i < TS_TAB_CAP ? (i < P.n_rltab ? __ldg(P.rltab + i) : 0.0f) : (j < P.n_rvtab ? __ldg(P.rvtab + j) : 0.0f);
+        }
+    }
     for (int i = t; i < P.cbits_words; i += B) m.cbits[i] = 0u;
     if constexpr (CL) cl::sync();   // every CTA holds its halo before anyone pushes into it
     else __syncthreads();

@@ -20,7 +20,7 @@ SECTIONS = ["CHUNK", "EDGE_IDX", "EDGE_PAR", "TET_IDX", "TET_SLOT", "TET_RV", "A
 HDR_FIELDS = ["magic", "version", "real_bytes", "n_sections", "V", "Vf", "Vf_pad", "Vstore", "F", "B",
               "VPT", "G", "n_chunks", "grasp_chunk", "slot_capacity", "n_att", "n_edge_items",
               "n_tet_items", "n_att_items", "bank_conflicts", "n_slots_total", "compact", "edge_gather",
-              "einc_bytes", "Vown", "cluster_k", "cluster_rank", "boff", "rvdict", "narrow"]
+              "einc_bytes", "Vown", "cluster_k", "cluster_rank", "boff", "rvdict", "narrow", "n_rltab", "n_rvtab"]
 
 
 class Program:
