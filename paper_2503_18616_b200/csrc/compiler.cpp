@@ -977,6 +977,19 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
     // the streams are padded by one CTA's worth of zero items so prefetches need no clamp
     const bool boff = compact && eg && R == 4 && 12 * Vstore <= 65535 && 12 * slot_cap <= 65535;
     const int scale_b = boff ? 12 : 1;
+    // narrow layout (program.h): legal when nothing reads neighbour positions in phase 2 (the
+    // distance-only program gathers edges there) and no cluster peer reads the ping-pong copy.
+    // Narrow programs put the positions first, so byte-offset streams address positions and
+    // slots from ONE base (slot offsets carry + 12 Vstore) -- which must fit the 16-bit fields
+    bool narrow = false;
+    {
+        int maxval = 0;
+        for (int v : valence) maxval = std::max(maxval, v);
+        const char *nv = std::getenv("TS_NARROW");
+        narrow = !part && (n_chunks >= 1 || !eg) && maxval <= 255 && !(nv && nv[0] == '0') &&
+                 (!boff || 12 * (Vstore + slot_cap) < 65535);
+    }
+    const int slot_b0 = (narrow && boff) ? 12 * Vstore : 0;
     // rest volumes as a dictionary index in the spare top bits of the four 16-bit position
     // offsets (2 bits each; needs 12 Vstore < 16384) when few distinct 6 V0 values exist
     std::vector<float> rv_tab;
@@ -1013,7 +1026,7 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
             }
             // slot fields: byte offsets (boff) or indices; 0xffff = no slot (pinned corner; all four:
             // an idle lane of the bank schedule) -- never a multiple of 12 nor a valid index
-            auto so = [&](int s) { return s < 0 ? 0xffff : scale_b * s; };
+            auto so = [&](int s) { return s < 0 ? 0xffff : slot_b0 + scale_b * s; };
             tet_c[4 * i + 2] = pk(so(tet_slot[4 * i + 0]), so(tet_slot[4 * i + 1]));
             tet_c[4 * i + 3] = pk(so(tet_slot[4 * i + 2]), so(tet_slot[4 * i + 3]));
         }
@@ -1242,14 +1255,7 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
     hdr.n_edge_items = nE; hdr.n_tet_items = nT; hdr.n_att_items = nA; hdr.bank_conflicts = total_conf;
     hdr.n_slots_total = n_slots_total;
     hdr.edge_gather = eg ? 1 : 0; hdr.einc_bytes = einc_bytes;
-    {
-        // narrow layout (program.h): legal when nothing reads neighbour positions in phase 2 (the
-        // distance-only program gathers edges there) and no cluster peer reads the ping-pong copy
-        int maxval = 0;
-        for (int v : valence) maxval = std::max(maxval, v);
-        const char *nv = std::getenv("TS_NARROW");
-        hdr.narrow = (!part && (n_chunks >= 1 || !eg) && maxval <= 255 && !(nv && nv[0] == '0')) ? 1 : 0;
-    }
+    hdr.narrow = narrow ? 1 : 0;
     int64_t off = roundup((int)sizeof(TsProgHeader), 256);
     for (int s = 0; s < TS_SEC_COUNT; ++s) { hdr.off[s] = off; off += ((sz[s] + 255) / 256) * 256; }
     hdr.total_bytes = off;

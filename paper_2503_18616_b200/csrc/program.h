@@ -88,7 +88,10 @@ struct TsChunk {
 // scalar block.
 // narrow programs (single CTA, >= 1 chunk, every chunk valence <= 255): phase 2 writes positions in
 // place (nothing reads a neighbour's position after the phase-1 barrier) and the degenerate-constraint
-// counters are bytes -- 6 KB less per CTA for reach_1170, which is what a 4th CTA per SM needs
+// counters are bytes -- 6 KB less per CTA for reach_1170.  Layout order: narrow [head | positions |
+// slots | counters | bitmap] (one base for both, byte-offset slot fields carry + 12 Vstore); wide
+// [head | slots | positions | ping-pong | counters | bitmap] (slots at a constant offset in every
+// CTA of a cluster)
 inline int ts_smem_layout_bytes(int Vstore, int slot_cap, int Vf_pad, int F, int real_bytes, int ping_pong,
                                 int narrow = 0) {
     size_t b = 0;

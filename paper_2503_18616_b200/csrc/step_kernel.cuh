@@ -338,6 +338,11 @@ struct Smem {
     Cap<Real> *caps;
 };
 
+// narrow programs' positions (and byte-offset slot fields) start at this constant address
+__device__ __forceinline__ char *smem_base() {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    return reinterpret_cast<char *>(smem_raw + TS_SMEM_HEAD);
+}
 // fast programs' dictionary tables at a fixed shared-memory offset (no base pointer to keep live)
 __device__ __forceinline__ const float *smem_tab(int byte_off) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -371,14 +376,19 @@ __device__ __forceinline__ Smem<Real> carve(const TsDevProg &P, unsigned char *r
     Smem<Real> m;
     m.sc = reinterpret_cast<Scal *>(raw);
     m.caps = reinterpret_cast<Cap<Real> *>(raw + ((sizeof(Scal) + 15) / 16) * 16);
-    Real *slots = reinterpret_cast<Real *>(raw + TS_SMEM_HEAD);
-    Real *pos = slots + 3 * P.slot_cap;
-    m.slot = slots;
-    m.pos = pos;
-    const bool pp = P.edge_gather && !P.narrow;   // ping-pong positions
-    m.alt = pp ? pos + 3 * P.Vstore : pos;
-    m.deg = reinterpret_cast<int *>(pos + 3 * P.Vstore * (pp ? 2 : 1));
+    Real *base = reinterpret_cast<Real *>(raw + TS_SMEM_HEAD);
     m.narrow = P.narrow;
+    if (P.narrow) {   // [positions | slots | counters]
+        m.pos = m.alt = base;
+        m.slot = base + 3 * P.Vstore;
+        m.deg = reinterpret_cast<int *>(m.slot + 3 * P.slot_cap);
+    } else {          // [slots | positions | ping-pong | counters]
+        const bool pp = P.edge_gather;
+        m.slot = base;
+        m.pos = base + 3 * P.slot_cap;
+        m.alt = pp ? m.pos + 3 * P.Vstore : m.pos;
+        m.deg = reinterpret_cast<int *>(m.pos + 3 * P.Vstore * (pp ? 2 : 1));
+    }
     m.cbits = reinterpret_cast<unsigned *>(reinterpret_cast<unsigned char *>(m.deg) + (P.narrow ? 1 : 4) * P.Vf_pad);
     return m;
 }
@@ -548,8 +558,9 @@ __device__ __forceinline__ void p1_tets(const TsDevProg &P, const Smem<Real> &m,
     if constexpr (sizeof(Real) == 4) {
         if (FAST || P.boff) {   // byte-offset stream, padded by a CTA's worth of items: unclamped prefetch
             const uint4 *it = P.tet_c + begin;
-            const char *pb = reinterpret_cast<const char *>(m.pos);
-            char *sb = reinterpret_cast<char *>(m.slot);   // == shared base + TS_SMEM_HEAD
+            // narrow: slot fields are offsets from the position base too (FAST: a constant address)
+            const char *pb = FAST ? smem_base() : reinterpret_cast<const char *>(m.pos);
+            char *sb = FAST ? smem_base() : reinterpret_cast<char *>(P.narrow ? m.pos : m.slot);
             uint4 nq = __ldg(it + wb + lane);
             if (FAST || P.rvdict) {   // rest volume from the stream's spare bits + a tiny (L1-resident) table
                 for (int i = wb + lane; i < we; i += 32) {
@@ -759,7 +770,7 @@ __device__ __forceinline__ void owner_edges(const TsDevProg &P, const Smem<Real>
     } else if (FAST || P.einc_bytes == 4) {
         // 4-byte records: {neighbour byte offset | rest-length index << 16 | pinned << 31}
         const unsigned *rec = reinterpret_cast<const unsigned *>(P.einc) + rb;
-        const char *pb = reinterpret_cast<const char *>(m.pos);
+        const char *pb = FAST ? smem_base() : reinterpret_cast<const char *>(m.pos);
         const float hks = 0.5f * ks;
         unsigned q = __ldg(rec);
         for (int k = 0; k < ev; ++k) {
@@ -1200,7 +1211,7 @@ __device__ __forceinline__ void step_env(const TsDevProg &P, const TsDevProg *pr
 #pragma unroll
             for (int r = 0; r < VPT; ++r) {
                 const int p = max(0, min(r * B + t, P.Vf - 1));   // rows past Vf are never used
-                h_base[r] = P.region[ch0.region_off + (p >> 5)] + lane;
+                h_base[r] = 12 * (P.Vstore + P.region[ch0.region_off + (p >> 5)] + lane);   // bytes from smem_base
                 h_val[r] = P.valence[ch0.val_off + p];
                 h_pre[r] = min(h_val[r], P.gsplit[p]);
                 h_cnt[r] = P.static_cnt[p];
@@ -1250,24 +1261,28 @@ __device__ __forceinline__ void step_env(const TsDevProg &P, const TsDevProg *pr
                 for (int r = 0; r < VPT; ++r) {
                     const int p = r * B + t;
                     if (p < P.Vf) {
-                        const int base = FAST ? h_base[r] : P.region[ch.region_off + (p >> 5)] + lane;
+                        const int base = FAST ? 0 : P.region[ch.region_off + (p >> 5)] + lane;
                         const int val0 = FAST ? h_val[r] : P.valence[ch.val_off + p];
                         const int val = (S.ablate & 2) ? 0 : ((S.ablate & 128) ? min(val0, 12) : val0);
                         const int pre = FAST && !(S.ablate & 130) ? h_pre[r] : gchunk ? min(val, P.gsplit[p]) : val;
                         Real ax = accx[r], ay = accy[r], az = accz[r];
+                        // slot k of this vertex (FAST: a byte offset from the constant shared base)
+                        auto add_slot = [&](int k) {
+                            if constexpr (FAST) {
+                                const float *q = reinterpret_cast<const float *>(smem_base() + h_base[r] + 384 * k);
+                                ax += q[0]; ay += q[1]; az += q[2];
+                            } else {
+                                const int sidx = base + 32 * k;
+                                ax += m.SX(sidx); ay += m.SY(sidx); az += m.SZ(sidx);
+                            }
+                        };
 #pragma unroll 4
-                        for (int k = 0; k < pre; ++k) {
-                            const int sidx = base + 32 * k;
-                            ax += m.SX(sidx); ay += m.SY(sidx); az += m.SZ(sidx);
-                        }
+                        for (int k = 0; k < pre; ++k) add_slot(k);
                         if (gchunk) {
                             accx[r] = ax; accy[r] = ay; accz[r] = az;
                             add_grasp(r);
                             ax = accx[r]; ay = accy[r]; az = accz[r];
-                            for (int k = pre; k < val; ++k) {
-                                const int sidx = base + 32 * k;
-                                ax += m.SX(sidx); ay += m.SY(sidx); az += m.SZ(sidx);
-                            }
+                            for (int k = pre; k < val; ++k) add_slot(k);
                         }
                         accx[r] = ax; accy[r] = ay; accz[r] = az;
                         ndeg[r] += deg_take(FAST ? 1 : m.narrow, m.deg, p);

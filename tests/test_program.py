@@ -339,6 +339,11 @@ def test_dictionary_coded_streams(reach_scene):
     assert np.array_equal(rvtab[ri[live]].astype(np.float64), p.tet_rv[live])
     offs = np.stack([q[:, 0] & 0x3FFF, (q[:, 0] >> 16) & 0x3FFF, q[:, 1] & 0x3FFF, (q[:, 1] >> 16) & 0x3FFF], 1)
     assert np.array_equal(offs[live], 12 * p.tet_idx[live])
+    # narrow layout: positions first, slot fields are byte offsets from the same base (+ 12 Vstore)
+    assert p.h["narrow"] == 1
+    sl = np.stack([q[:, 2] & 0xFFFF, q[:, 2] >> 16, q[:, 3] & 0xFFFF, q[:, 3] >> 16], 1).astype(np.int64)
+    want = np.where(p.tet_slot >= 0, 12 * (p.h["Vstore"] + p.tet_slot), 0xFFFF)
+    assert np.array_equal(sl[live], want[live])
 
 
 def test_latency_cluster_policy():
