@@ -160,11 +160,11 @@ class Simulation:
         keys = (self.x, self.v, self.tool.axis, self.tool.jaw_dir, self.tool.reach,
                 self.tool.clamp_angle, self.grasp_vertex, self.grasped, self._steps, self._l_prev,
                 self._return)
-        for t in keys:
-            if not t.is_contiguous() or t.device != self.device:
-                raise ValidationError("simulation state tensors must stay contiguous on the engine device")
         sig = tuple(t.data_ptr() for t in keys)
-        if self._state is None or self._state[0] != sig:
+        if self._state is None or self._state[0] != sig:   # a tensor was replaced: check it
+            for t in keys:
+                if not t.is_contiguous() or t.device != self.device:
+                    raise ValidationError("simulation state tensors must stay contiguous on the engine device")
             st = N.EnvState()
             (st.x, st.v, st.tool_axis, st.tool_jaw, st.tool_reach, st.tool_clamp, st.grasp_vertex,
              st.grasped, st.steps, st.l_prev, st.ep_return) = sig
