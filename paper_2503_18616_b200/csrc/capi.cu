@@ -257,6 +257,8 @@ static int32_t create_handle(const ts_scene_desc *desc, const ts_layout_opts &o,
         decode_part(hb, db, h->prog);
         h->smem = ts_smem_bytes(h->prog, R);
     }
+    h->prog.pf_base = h->dev_blob;
+    h->prog.pf_bytes = (int64_t)h->host_blob.size() / 16 * 16;
     fill_params(*desc, h->params);
     int max_smem = 0;
     cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);

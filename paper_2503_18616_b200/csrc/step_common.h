@@ -74,6 +74,8 @@ struct TsDevProg {
     const uint4 *tet_c;
     int32_t narrow;           // single position buffer + byte degenerate counters (program.h)
     int32_t fast;             // the reach-scene shape: fast_step_kernel (step_kernel.cuh)
+    const void *pf_base;      // the handle's whole device program (all parts): cmd_kernel prefetches
+    int64_t pf_bytes;         //   it into L2 so the step kernel's first program reads do not go to HBM
     int32_t edge_gather;      // 1: owner-gathered edges (records below), positions double-buffered
     int32_t einc_bytes;       // 8 or 16
     const void *einc;

@@ -983,6 +983,16 @@ static __global__ void __launch_bounds__(128) cmd_kernel(const __grid_constant__
                                                   const __grid_constant__ TsParams S,
                                                   const __grid_constant__ TsLaunch L) {
     if ((L.mode & TS_M_CHECK_ACTIONS) && *L.bad_flag) return;   // deferred ValidationError
+    if (blockIdx.x == 0 && P.pf_base && !(S.ablate & 512)) {
+        // the step kernel that follows reads the whole program every substep: start its L2 fill
+        // now (bulk prefetch, 16 KB per request, fire and forget) -- after an L2 flush the
+        // first substep of a small batch otherwise waits on HBM for every program line
+        const char *b = reinterpret_cast<const char *>(P.pf_base);
+        for (int64_t off = 16384 * (int64_t)threadIdx.x; off < P.pf_bytes; off += 16384 * (int64_t)blockDim.x) {
+            const unsigned n = (unsigned)min((int64_t)16384, P.pf_bytes - off);
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(b + off), "r"(n) : "memory");
+        }
+    }
     for (int64_t env = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; env < L.n_env;
          env += (int64_t)gridDim.x * blockDim.x)
         env_command(P, S, L, env, L.cmd[env]);
