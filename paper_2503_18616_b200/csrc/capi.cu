@@ -315,6 +315,9 @@ static int launch(ts_handle *h, const TsLaunch &L_in, cudaStream_t s) {
     cudaError_t e = ts_launch_cmd(h->prog, h->params, L, s);
     if (e != cudaSuccess) return cuda_fail(e, "command kernel launch");
     const bool timed = 2 * h->tev_used + 1 < (int64_t)h->tev.size();
+    // programmatic dependent launch of step and epilogue (each overlaps its predecessor's tail);
+    // off while the step kernel is being timed, so its events bracket exactly its own execution
+    const bool pdl = !timed && !(h->params.ablate & 1024);
     if (timed) cudaEventRecord(h->tev[2 * h->tev_used], s);
     if (h->cluster_k > 1)
         e = h->precision == TS_F64
@@ -323,11 +326,11 @@ static int launch(ts_handle *h, const TsLaunch &L_in, cudaStream_t s) {
                 : ts_launch_cluster_step<float>(h->dev_parts, h->prog.VPT, h->cluster_k, h->prog.B, h->params, L,
                                                 grid, h->smem, s);
     else
-        e = h->precision == TS_F64 ? ts_launch_step<double>(h->prog, h->params, L, grid, h->smem, s)
-                                   : ts_launch_step<float>(h->prog, h->params, L, grid, h->smem, s);
+        e = h->precision == TS_F64 ? ts_launch_step<double>(h->prog, h->params, L, grid, h->smem, s, pdl)
+                                   : ts_launch_step<float>(h->prog, h->params, L, grid, h->smem, s, pdl);
     if (e != cudaSuccess) return cuda_fail(e, "step kernel launch");
     if (timed) cudaEventRecord(h->tev[2 * h->tev_used++ + 1], s);
-    e = ts_launch_epilogue(h->prog, h->params, L, s);
+    e = ts_launch_epilogue(h->prog, h->params, L, s, pdl);
     if (e != cudaSuccess) return cuda_fail(e, "epilogue kernel launch");
     g_launches.fetch_add(3);
     return TS_OK;

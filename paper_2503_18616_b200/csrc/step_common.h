@@ -179,13 +179,17 @@ inline bool ts_use_edges_kernel(const TsDevProg &P) {
 }
 template <typename Real>
 cudaError_t ts_launch_step(const TsDevProg &P, const TsParams &S, const TsLaunch &L, int grid,
-                           int smem, cudaStream_t stream);
+                           int smem, cudaStream_t stream, bool pdl = false);
 // large meshes: `n_clusters` clusters of K CTAs (part programs `parts`, device array)
 template <typename Real>
 cudaError_t ts_launch_cluster_step(const TsDevProg *parts, int VPT, int K, int B, const TsParams &S,
                                    const TsLaunch &L, int n_clusters, int smem, cudaStream_t stream);
 cudaError_t ts_launch_cmd(const TsDevProg &P, const TsParams &S, const TsLaunch &L, cudaStream_t stream);
-cudaError_t ts_launch_epilogue(const TsDevProg &P, const TsParams &S, const TsLaunch &L, cudaStream_t stream);
+// pdl: programmatic dependent launch -- the kernel may start while the previous kernel of the
+// stream (this library's own command / step kernel) runs, and waits (griddepcontrol.wait) before it
+// reads that kernel's results
+cudaError_t ts_launch_epilogue(const TsDevProg &P, const TsParams &S, const TsLaunch &L, cudaStream_t stream,
+                               bool pdl = false);
 template <typename Real>
 cudaError_t ts_launch_reset(const TsDevProg &P, const TsParams &S, const TsLaunch &L,
                             const uint8_t *mask, int observe_only, cudaStream_t stream);

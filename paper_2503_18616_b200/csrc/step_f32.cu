@@ -4,7 +4,7 @@
 #include "step_kernel.cuh"
 
 template cudaError_t ts_launch_step<float>(const TsDevProg &, const TsParams &, const TsLaunch &, int, int,
-                                           cudaStream_t);
+                                           cudaStream_t, bool);
 template cudaError_t ts_launch_reset<float>(const TsDevProg &, const TsParams &, const TsLaunch &,
                                             const uint8_t *, int, cudaStream_t);
 template cudaError_t ts_launch_cluster_step<float>(const TsDevProg *, int, int, int, const TsParams &, const TsLaunch &,

@@ -338,6 +338,10 @@ struct Smem {
     Cap<Real> *caps;
 };
 
+// programmatic dependent launch (sm_90+): no-ops when the kernel was launched normally
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 // narrow programs' positions (and byte-offset slot fields) start at this constant address
 __device__ __forceinline__ char *smem_base() {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -982,6 +986,7 @@ static __device__ __forceinline__ void env_epilogue(const TsParams &S, const TsL
 static __global__ void __launch_bounds__(128) cmd_kernel(const __grid_constant__ TsDevProg P,
                                                   const __grid_constant__ TsParams S,
                                                   const __grid_constant__ TsLaunch L) {
+    pdl_trigger();   // the step kernel may launch now: it only reads the state before pdl_wait
     if ((L.mode & TS_M_CHECK_ACTIONS) && *L.bad_flag) return;   // deferred ValidationError
     if (blockIdx.x == 0 && P.pf_base && !(S.ablate & 512)) {
         // the step kernel that follows reads the whole program every substep: start its L2 fill
@@ -1001,6 +1006,7 @@ static __global__ void __launch_bounds__(128) cmd_kernel(const __grid_constant__
 static __global__ void __launch_bounds__(128) epilogue_kernel(const __grid_constant__ TsDevProg P,
                                                        const __grid_constant__ TsParams S,
                                                        const __grid_constant__ TsLaunch L) {
+    pdl_wait();      // every step-kernel result of this step is visible after this
     if ((L.mode & TS_M_CHECK_ACTIONS) && *L.bad_flag) return;
     for (int64_t env = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; env < L.n_env;
          env += (int64_t)gridDim.x * blockDim.x)
@@ -1100,15 +1106,9 @@ __device__ __forceinline__ void step_env(const TsDevProg &P, const TsDevProg *pr
     Real *xg = reinterpret_cast<Real *>(L.x) + env * (int64_t)P.V * 3;
     Real *vg = reinterpret_cast<Real *>(L.v) + env * (int64_t)P.V * 3;
 
-    // ---- A. the env's command block (cmd_kernel) + the state load ------
-    TsCmd &cmd = L.cmd[env];
-    if (t < 24) {
-        const double *src = t < 21 ? &cmd.caps[0][0] + t : cmd.drag + (t - 21);
-        (&sc.caps[0][0])[t] = *src;            // caps[21] and drag[3] are contiguous in Scal too
-    } else if (t == 24) {
-        sc.gv_orig = cmd.gv; sc.need_search = cmd.need_search; sc.n_contacts = 0;
-    }
-    // state -> shared (storage order) / registers
+    // ---- A. the state load, then the env's command block (cmd_kernel) ---
+    // state -> shared (storage order) / registers: the command kernel does not write x / v, so
+    // under programmatic dependent launch this overlaps the command kernel's tail
     for (int p = t; p < P.Vstore; p += B) {
         const int o = P.s2o[p];
         Real a = 0, b = 0, c = 0;
@@ -1135,6 +1135,14 @@ __device__ __forceinline__ void step_env(const TsDevProg &P, const TsDevProg *pr
         }
     }
     for (int i = t; i < P.cbits_words; i += B) m.cbits[i] = 0u;
+    pdl_wait();   // the command blocks (and the grasp flags the command kernel released) are ready
+    TsCmd &cmd = L.cmd[env];
+    if (t < 24) {
+        const double *src = t < 21 ? &cmd.caps[0][0] + t : cmd.drag + (t - 21);
+        (&sc.caps[0][0])[t] = *src;            // caps[21] and drag[3] are contiguous in Scal too
+    } else if (t == 24) {
+        sc.gv_orig = cmd.gv; sc.need_search = cmd.need_search; sc.n_contacts = 0;
+    }
     if constexpr (CL) cl::sync();   // every CTA holds its halo before anyone pushes into it
     else __syncthreads();
 
@@ -1581,6 +1589,7 @@ template <typename Real, int VPT>
 __global__ void __launch_bounds__(TS_STEP_MAXT, sizeof(Real) == 4 ? TS_STEP_MINB : 1) step_kernel(const __grid_constant__ TsDevProg P,
                                                    const __grid_constant__ TsParams S,
                                                    const __grid_constant__ TsLaunch L) {
+    pdl_trigger();   // the epilogue may launch early; it waits for this grid before reading
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem<Real> m = carve<Real>(P, smem_raw);
     if ((L.mode & TS_M_CHECK_ACTIONS) && *L.bad_flag) return;   // deferred ValidationError: no state change
@@ -1595,6 +1604,7 @@ template <typename Real>
 __global__ void __launch_bounds__(TS_STEP_MAXT, TS_STEP_MINB) fast_step_kernel(const __grid_constant__ TsDevProg P,
                                                                               const __grid_constant__ TsParams S,
                                                                               const __grid_constant__ TsLaunch L) {
+    pdl_trigger();   // the epilogue may launch early; it waits for this grid before reading
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem<Real> m = carve<Real>(P, smem_raw);
     if ((L.mode & TS_M_CHECK_ACTIONS) && *L.bad_flag) return;
@@ -1609,6 +1619,7 @@ template <typename Real>
 __global__ void __launch_bounds__(TS_EDGES_MAXT, TS_EDGES_MINB) edges_step_kernel(const __grid_constant__ TsDevProg P,
                                                             const __grid_constant__ TsParams S,
                                                             const __grid_constant__ TsLaunch L) {
+    pdl_trigger();   // the epilogue may launch early; it waits for this grid before reading
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem<Real> m = carve<Real>(P, smem_raw);
     if ((L.mode & TS_M_CHECK_ACTIONS) && *L.bad_flag) return;
@@ -1675,12 +1686,30 @@ __global__ void reset_kernel(const TsDevProg P, const TsParams S, const TsLaunch
 
 }  // namespace tsk
 
+// launch `fn` normally, or with programmatic stream serialization (PDL) so that it may start while
+// the stream's previous kernel finishes (the kernel calls pdl_wait before consuming its results)
+template <typename... Args>
+static cudaError_t ts_launch_pdl(void (*fn)(Args...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
+                                 bool pdl, const TsDevProg &P, const TsParams &S, const TsLaunch &L) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = pdl ? attr : nullptr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, fn, P, S, L);
+}
+
 // ---------------------------------------------------------------------------
 // launchers (instantiated per precision in step_f32.cu / step_f64.cu)
 // ---------------------------------------------------------------------------
 template <typename Real>
 cudaError_t ts_launch_step(const TsDevProg &P, const TsParams &S, const TsLaunch &L, int grid, int smem,
-                           cudaStream_t stream) {
+                           cudaStream_t stream, bool pdl) {
     void (*fn)(const TsDevProg, const TsParams, const TsLaunch) = nullptr;
     if constexpr (sizeof(Real) == 4) {   // shape-specialised fp32 kernels
         if (ts_use_fast_kernel(P, S.ablate)) fn = tsk::fast_step_kernel<Real>;
@@ -1698,8 +1727,7 @@ cudaError_t ts_launch_step(const TsDevProg &P, const TsParams &S, const TsLaunch
     }
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    fn<<<grid, P.B, smem, stream>>>(P, S, L);
-    return cudaGetLastError();
+    return ts_launch_pdl(fn, dim3((unsigned)grid), dim3((unsigned)P.B), (size_t)smem, stream, pdl, P, S, L);
 }
 
 template <typename Real>
@@ -1755,8 +1783,9 @@ cudaError_t ts_launch_cmd(const TsDevProg &P, const TsParams &S, const TsLaunch 
     return cudaGetLastError();
 }
 
-cudaError_t ts_launch_epilogue(const TsDevProg &P, const TsParams &S, const TsLaunch &L, cudaStream_t stream) {
-    tsk::epilogue_kernel<<<scalar_grid(L.n_env), 128, 0, stream>>>(P, S, L);
-    return cudaGetLastError();
+cudaError_t ts_launch_epilogue(const TsDevProg &P, const TsParams &S, const TsLaunch &L, cudaStream_t stream,
+                               bool pdl) {
+    return ts_launch_pdl(tsk::epilogue_kernel, dim3((unsigned)scalar_grid(L.n_env)), dim3(128), 0, stream, pdl,
+                         P, S, L);
 }
 #endif
