@@ -258,6 +258,12 @@ def run_gpu(args, wl):
         N.check(lib.ts_uniform_actions_dev(N.ptr(acts), n, first_env, 12345, N.ptr(counter), stream_ptr()),
                 "ts_uniform_actions_dev")
 
+    # our kernels per step (action draw + command + step + epilogue), counted by the library on an
+    # eager step; the graph replays below launch exactly these
+    n0 = lib.ts_launch_count()
+    draw()
+    env.step(acts, validate=False)
+    per_step_launches = lib.ts_launch_count() - n0
     # ---- device-timed: the graph-captured step (W warm-up steps run inside capture_step) ------
     replay = env.capture_step(acts, pre=draw, warmup=args.warmup)
     for _ in range(2):
@@ -297,8 +303,8 @@ def run_gpu(args, wl):
     total_ms, kern_total_ms = float(t[0]), float(t[1])
     value = world * n * args.steps / (total_ms * 1e-3)
     kern_avg_ms = kern_total_ms / args.steps
-    # our kernels inside the timed graph replays: action draw + counter bump + command + step + epilogue
-    launches = 5 * args.steps
+    # our kernels inside the timed graph replays
+    launches = per_step_launches * args.steps
 
     # ---- end to end through the public API with host buffers -------------
     rng = np.random.default_rng(1000 + rank)

@@ -517,7 +517,7 @@ int32_t ts_uniform_actions_dev(double *actions, int64_t num_envs, int64_t first_
     cudaError_t e = ts_launch_uniform_dev(actions, 3 * num_envs, 3 * first_env, seed, counter,
                                           reinterpret_cast<cudaStream_t>(stream));
     if (e != cudaSuccess) return cuda_fail(e, "uniform kernel launch");
-    g_launches.fetch_add(2);
+    g_launches.fetch_add(3 * num_envs <= 65536 ? 1 : 2);
     return TS_OK;
 }
 
@@ -580,8 +580,24 @@ cudaError_t ts_launch_uniform(double *out, int64_t n, int64_t first, uint64_t se
 
 __global__ void counter_kernel(uint64_t *c) { *c += 1; }
 
+// small draws: one block reads the device counter, draws, and bumps it itself (one launch)
+__global__ void __launch_bounds__(1024) uniform_bump_kernel(double *out, int64_t n, int64_t first, uint64_t seed,
+                                                            uint64_t *dev_counter) {
+    const uint64_t counter = *dev_counter;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+        const uint64_t r = splitmix64(seed ^ splitmix64(counter * 0x100000001B3ull + (uint64_t)(i + first)));
+        out[i] = 2.0 * ((double)(r >> 11) * (1.0 / 9007199254740992.0)) - 1.0;
+    }
+    __syncthreads();   // every thread has read the counter
+    if (threadIdx.x == 0) *dev_counter = counter + 1;
+}
+
 cudaError_t ts_launch_uniform_dev(double *out, int64_t n, int64_t first, uint64_t seed, uint64_t *counter,
                                   cudaStream_t stream) {
+    if (n <= 65536) {   // <= 21845 envs: one block (a few microseconds), one launch
+        uniform_bump_kernel<<<1, 1024, 0, stream>>>(out, n, first, seed, counter);
+        return cudaGetLastError();
+    }
     int grid = (int)((n + 255) / 256);
     if (grid > 4096) grid = 4096;
     uniform_kernel<<<grid, 256, 0, stream>>>(out, n, first, seed, 0, counter);
