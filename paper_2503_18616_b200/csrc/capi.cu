@@ -257,8 +257,12 @@ static int32_t create_handle(const ts_scene_desc *desc, const ts_layout_opts &o,
         decode_part(hb, db, h->prog);
         h->smem = ts_smem_bytes(h->prog, R);
     }
-    h->prog.pf_base = h->dev_blob;
-    h->prog.pf_bytes = (int64_t)h->host_blob.size() / 16 * 16;
+    // L2 prefetch of the program by the command kernel: small programs only -- a multi-MB cluster
+    // program's bulk prefetches keep the command kernel alive longer than they save (52,359-tet
+    // slab, one env: 155.6 -> 187 us/step with it)
+    const int64_t pf = (int64_t)h->host_blob.size() / 16 * 16;
+    h->prog.pf_base = pf <= (512 << 10) ? h->dev_blob : nullptr;
+    h->prog.pf_bytes = pf <= (512 << 10) ? pf : 0;
     fill_params(*desc, h->params);
     int max_smem = 0;
     cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
