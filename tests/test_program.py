@@ -354,3 +354,12 @@ def test_latency_cluster_policy():
     assert k(845, 1, 148) == 4 and k(2527, 1, 148) == 8 and k(12180, 1, 148) == 16
     assert k(12180, 16, 148) == 8 and k(12180, 4096, 148) == 0   # throughput: the compiler's smallest fit
     assert k(2527, 74, 148) == 2 and k(2527, 75, 148) == 0
+
+
+def test_latency_block_policy():
+    """Small fp32 batches (<= one env per SM) get ~1.3 threads per free vertex; large batches, fp64
+    and already-wide meshes keep the compiler's default."""
+    from paper_2503_18616_b200.solver import latency_block_threads as b
+    assert b(294, 1, 148, "fp32") == 384 and b(294, 148, 148, "fp32") == 384
+    assert b(294, 149, 148, "fp32") == 0 and b(294, 1, 148, "fp64") == 0
+    assert b(500, 1, 148, "fp32") == 0           # 512 cap: no wider than the default 512
