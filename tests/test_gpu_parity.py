@@ -255,3 +255,37 @@ def test_config2_distance_only_bitwise(reach_scene):
     assert np.array_equal(gpu.sim.x.cpu().numpy(), ref.x) and np.array_equal(gpu.sim.v.cpu().numpy(), ref.v)
     for rec in out:
         assert np.array_equal(rec["gpu"][1], rec["ref"][1]), rec["step"]
+
+
+def test_p4_rcm_invariance_device_tool_state(reach_scene):
+    """Acceptance P4 (pkg/tests/test_acceptance.py, test_tool.py:rcm_invariance_random_walk) on the
+    device command kernel: over a 150-step random walk (auto-resets included) the tool axis stays a
+    unit vector through the RCM, the jaw stays orthonormal to it, the clamp angle stays in range, the
+    drag point stays in the workspace box -- and the pose equals the numpy oracle's within 1e-9
+    (the reference pins its own tool kinematics to 1e-9..1e-12, test_tool.py:35-44)."""
+    import torch
+    n = 64
+    mesh, rest, cfg = reach_scene
+    ref = O.OracleEnv(O.scene_from_loaded(*reach_scene), n)
+    ref.reset()
+    gpu = EnvBatch(reach_scene, num_envs=n, device="cuda:0", precision="fp64")
+    gpu.reset()
+    rng = np.random.default_rng(4)
+    rcm = np.asarray(cfg.rcm)
+    lo, hi = np.asarray(cfg.workspace_low), np.asarray(cfg.workspace_high)
+    for _ in range(150):
+        a = rng.uniform(-1.0, 1.0, (n, 3))
+        ref.step(a)
+        gpu.step(a)
+        t = gpu.sim.tool
+        ax, jw = t.axis.cpu().numpy(), t.jaw_dir.cpu().numpy()
+        reach, clamp = t.reach.cpu().numpy(), t.clamp_angle.cpu().numpy()
+        assert np.abs(np.linalg.norm(ax, axis=1) - 1.0).max() <= 1e-12
+        assert np.abs(np.linalg.norm(jw, axis=1) - 1.0).max() <= 1e-12
+        assert np.abs(np.einsum("ij,ij->i", ax, jw)).max() <= 1e-12
+        assert np.all(clamp > 0.0) and np.all(clamp < 30.0)
+        drag = rcm + reach[:, None] * ax
+        assert np.all(drag >= lo - 1e-12) and np.all(drag <= hi + 1e-12)
+        assert np.abs(ax - ref.axis).max() <= 1e-9 and np.abs(jw - ref.jaw).max() <= 1e-9
+        assert np.abs(reach - ref.reach).max() <= 1e-9 and np.abs(clamp - ref.clamp).max() <= 1e-9
+    torch.cuda.synchronize()
