@@ -170,3 +170,45 @@ def test_kinetic_energy_matches_definition(small_scene):
     v = np_(sim.v)
     ke = 0.5 * np.einsum("nvq,nvq->nv", v, v) @ small_scene[0].vertex_mass
     assert np.allclose(np_(sim.kinetic_energy()), ke, rtol=1e-12)
+
+
+@pytest.mark.gpu
+def test_tool_command_edge_cases_match_oracle(reach_scene):
+    """test_tool.py's command cases on the device command kernel (Simulation.step(targets, angles)):
+    identity command, pure advance along the axis, lateral reach, workspace clip, the trocar
+    singularity (target at the RCM: rejected, pose held), a sub-threshold rotation (reach changes,
+    axis kept) and a quarter turn -- flags exact, pose within 1e-12 of the numpy oracle."""
+    import oracle as O
+    from paper_2503_18616_b200 import EnvBatch
+    import dataclasses
+    mesh, rest, cfg = reach_scene
+    # the workspace box of the reach scene excludes the RCM; widen it so the singularity is reachable
+    cfg = dataclasses.replace(cfg, workspace_high=np.array([0.11, 0.10, 0.055]))
+    scene = (mesh, rest, cfg)
+    env = EnvBatch(scene, num_envs=7, device="cuda:0", precision="fp64")
+    env.reset()
+    ref = O.OracleEnv(O.scene_from_loaded(*scene), 7)
+    ref.reset()
+    rcm = np.asarray(cfg.rcm, np.float64)
+    drag = ref.drag_points().copy()
+    ax0 = ref.axis[0].copy()
+    side = np.cross(ax0, [0.0, 0.0, 1.0])
+    side /= np.linalg.norm(side)
+    targets = np.stack([
+        drag[0],                                   # identity
+        drag[1] + 0.005 * ax0,                     # pure advance
+        drag[2] + 0.004 * side,                    # lateral reach
+        np.array([0.5, -0.5, 0.2]),                # far outside the workspace: clipped
+        rcm,                                       # trocar singularity: rejected
+        drag[5] + 1e-13 * side,                    # rotation below MIN_ROTATION
+        rcm + np.linalg.norm(drag[6] - rcm) * side,  # quarter turn
+    ])
+    angles = np.array([2.0, 2.0, 5.0, 2.0, 7.0, 2.0, 1.0])
+    info = env.sim.step(targets=targets, angles=angles)
+    r_clipped, r_rejected = ref.apply_commands(targets, angles)
+    assert np.array_equal(info["clipped"].cpu().numpy(), r_clipped)
+    assert np.array_equal(info["rejected"].cpu().numpy(), r_rejected)
+    assert r_rejected[4] and not r_rejected[:4].any() and r_clipped[3]
+    t = env.sim.tool
+    for got, want in ((t.axis, ref.axis), (t.jaw_dir, ref.jaw), (t.reach, ref.reach), (t.clamp_angle, ref.clamp)):
+        assert np.abs(got.cpu().numpy() - want).max() <= 1e-12
