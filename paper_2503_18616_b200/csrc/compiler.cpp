@@ -1017,8 +1017,12 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
             else { const float f = (float)rl; std::memcpy(&edge_c[4 * i + 2], &f, 4); edge_c[4 * i + 3] = 0; }
         }
         for (int i = 0; i < nT; ++i) {
-            tet_c[4 * i + 0] = pk(scale_b * tet_idx[4 * i + 0], scale_b * tet_idx[4 * i + 1]);
-            tet_c[4 * i + 1] = pk(scale_b * tet_idx[4 * i + 2], scale_b * tet_idx[4 * i + 3]);
+            // an idle lane (dummy item) reads the corner "Vf_pad" -- never a free vertex, so even if it
+            // is executed it touches no degenerate counter; its slot fields are all absent
+            const bool idle = all_items[2][i].index < 0 && boff;
+            auto po = [&](int k) { return idle ? scale_b * Vf_pad : scale_b * tet_idx[4 * i + k]; };
+            tet_c[4 * i + 0] = pk(po(0), po(1));
+            tet_c[4 * i + 1] = pk(po(2), po(3));
             if (!rv_tab.empty()) {   // index bits 2k, 2k+1 in bits 14-15 of 16-bit field k
                 const uint32_t r = (uint32_t)rv_idx[i];
                 tet_c[4 * i + 0] |= ((r & 3u) << 14) | (((r >> 2) & 3u) << 30);

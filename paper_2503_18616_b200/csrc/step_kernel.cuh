@@ -572,7 +572,10 @@ __device__ __forceinline__ void p1_tets(const TsDevProg &P, const Smem<Real> &m,
                     nq = __ldg(it + i + 32);
                     const unsigned ri = ((q.x >> 14) & 3u) | ((q.x >> 28) & 12u) | ((q.y >> 10) & 48u) |
                                         ((q.y >> 24) & 192u);
-                    if ((q.z & q.w) != 0xffffffffu)   // all four slots absent: idle lane of the bank schedule
+                    // all four slots absent: an idle lane of the bank schedule (or four pinned corners);
+                    // the fast kernel runs it anyway: its stores are predicated off and its corners
+                    // are not free vertices (the compiler points idle lanes past Vf_pad)
+                    if (FAST || (q.z & q.w) != 0xffffffffu)
                         tet_item_b(pb, sb, m.deg, m.narrow, q,
                                    FAST ? smem_tab(TS_TAB_OFF + 4 * TS_TAB_CAP)[ri] : __ldg(P.rvtab + ri), kv,
                                    12u * (unsigned)vfp, 0x3fffu);
