@@ -200,7 +200,9 @@ def reference_env(num_envs, seed=0, dist_only=False, threads=REF_THREADS):
         return env, "port", 1
 
 
-def time_reference(num_envs, steps, warmup, seed=0, dist_only=False):
+def time_reference(num_envs, steps, warmup, seed=0, dist_only=False, min_seconds=0.0, max_steps=None):
+    """Env-steps/s of the reference on this host: `steps` timed batches, or -- with min_seconds --
+    as many as it takes to reach that much CPU time (at most max_steps).  Returns the steps run."""
     threads = min(REF_THREADS, max(1, num_envs))
     env, kind, cores = reference_env(num_envs, seed, dist_only, threads)
     env.reset(seed=seed) if kind == "reference" else env.reset()
@@ -208,10 +210,13 @@ def time_reference(num_envs, steps, warmup, seed=0, dist_only=False):
     for _ in range(warmup):
         env.step(rng.uniform(-1.0, 1.0, (num_envs, 3)))
     t0 = time.perf_counter()
-    for _ in range(steps):
+    done = 0
+    while done < steps or (min_seconds and time.perf_counter() - t0 < min_seconds
+                           and (max_steps is None or done < max_steps)):
         env.step(rng.uniform(-1.0, 1.0, (num_envs, 3)))
+        done += 1
     el = time.perf_counter() - t0
-    return num_envs * steps / el, el, kind, cores
+    return num_envs * done / el, el, kind, cores, done
 
 
 # ---------------------------------------------------------------------------
@@ -369,9 +374,9 @@ def run_gpu(args, wl):
         "clocks": clocks.summary(),
     }
     if world == 1 and not args.no_cpu_baseline:
-        # a bounded sample: ~10-30 s of CPU work
-        cpu_steps = max(2, args.cpu_steps if n >= 1024 else min(2000, args.cpu_steps * max(1, 4096 // n) // 4))
-        val, el, kind, cores = time_reference(n, cpu_steps, 1, dist_only=wl["distance_only"])
+        # a bounded sample: at least --cpu-steps batches and at least 12 s of CPU work (~10-30 s)
+        val, el, kind, cores, cpu_steps = time_reference(n, args.cpu_steps, 1, dist_only=wl["distance_only"],
+                                                         min_seconds=12.0, max_steps=200000)
         line["cpu_baseline"] = {"value": val, "unit": UNIT, "cores": cores, "kind": kind,
                                 "sample": f"{cpu_steps} env steps x {n} envs after 1 warm-up step "
                                           f"({el:.1f} s), reach_1170{' distance-only' if wl['distance_only'] else ''}, "
@@ -422,7 +427,7 @@ def main():
     ap.add_argument("--envs", type=int, default=0, help="envs per GPU (0: the config's)")
     ap.add_argument("--cluster", type=int, default=0, help="CTAs per env (0: automatic)")
     ap.add_argument("--precision", choices=("fp32", "fp64"), default="fp32")
-    ap.add_argument("--cpu-steps", type=int, default=25)
+    ap.add_argument("--cpu-steps", type=int, default=2, help="minimum timed CPU-baseline batches (and >= 12 s)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
