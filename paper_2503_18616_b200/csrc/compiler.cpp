@@ -451,7 +451,7 @@ void bank_refine(const std::vector<ListRef> &lists, std::vector<int> &o2s, std::
 // oriented to balance every bank's in/out degree (swapping roles is bit-exact),
 // then Koenig's theorem gives a colouring with max-degree colours; each colour
 // becomes one batch, padded with dummy edges between pinned vertices (they
-// write only trash slots and touch no counter).  Returns false (list untouched)
+// have no slots -- their stores are predicated off -- and touch no counter).  Returns false (list untouched)
 // when there are no pinned vertices to build dummies from.
 bool edge_coloring_schedule(std::vector<Item> &list, const std::vector<int> &o2s, const std::vector<int> &s2o,
                             int Vf_pad, int bank_mod) {
@@ -719,7 +719,7 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
     int budget = o.max_chunk_slots > 0 ? o.max_chunk_slots : (1 << 30);
     if (o.max_chunk_slots <= 0) {
         const int fixed = ts_smem_layout_bytes(Vstore, 0, Vf_pad, Floc, R, eg ? 1 : 0);
-        const int avail = (TS_SMEM_LIMIT - fixed) / (3 * R) - 32;    // minus the 32 trash slots
+        const int avail = (TS_SMEM_LIMIT - fixed) / (3 * R) - 32;    // minus a margin of 32 slots
         if (avail < 7 * Floc || avail < 64) {
             err = "mesh too large for one CTA per environment (shared memory); use a cluster program";
             return TS_ERR_UNSUPPORTED;
