@@ -1115,7 +1115,8 @@ __device__ __forceinline__ void step_env(const TsDevProg &P, const TsDevProg *pr
     for (int p = t; p < P.Vstore; p += B) {
         const int o = P.s2o[p];
         Real a = 0, b = 0, c = 0;
-        if (o >= 0) { a = xg[3 * o]; b = xg[3 * o + 1]; c = xg[3 * o + 2]; }
+        // state is read once per env-step: streaming loads keep L1 for the program streams
+        if (o >= 0) { a = __ldcs(xg + 3 * o); b = __ldcs(xg + 3 * o + 1); c = __ldcs(xg + 3 * o + 2); }
         m.X(p) = a; m.Y(p) = b; m.Z(p) = c;
         m.alt[3 * p] = a; m.alt[3 * p + 1] = b; m.alt[3 * p + 2] = c;   // pinned rows of the ping-pong
     }
@@ -1126,7 +1127,7 @@ __device__ __forceinline__ void step_env(const TsDevProg &P, const TsDevProg *pr
         vx[r] = vy[r] = vz[r] = 0;
         if (p < P.Vf) {
             const int o = P.s2o[p];
-            vx[r] = vg[3 * o]; vy[r] = vg[3 * o + 1]; vz[r] = vg[3 * o + 2];
+            vx[r] = __ldcs(vg + 3 * o); vy[r] = __ldcs(vg + 3 * o + 1); vz[r] = __ldcs(vg + 3 * o + 2);
         }
     }
     for (int p = t; p < (P.narrow ? P.Vf_pad / 4 : P.Vf_pad); p += B) m.deg[p] = 0;
