@@ -1228,8 +1228,12 @@ __device__ __forceinline__ void step_env(const TsDevProg &P, const TsDevProg *pr
         else __syncthreads();
         // FAST (one chunk): the per-vertex program words are substep-invariant -> registers
         int h_base[VPT], h_val[VPT], h_pre[VPT], h_cnt[VPT], h_ev[VPT], h_rb[VPT];
+        int h_tb = 0, h_wb = 0, h_we = 0;   // FAST: the chunk's tet base and this warp's range
         if constexpr (FAST) {
             const TsChunk ch0 = P.chunks[0];
+            h_tb = ch0.tet_begin;
+            h_wb = P.wsplit[t >> 5];
+            h_we = P.wsplit[(t >> 5) + 1];
 #pragma unroll
             for (int r = 0; r < VPT; ++r) {
                 const int p = max(0, min(r * B + t, P.Vf - 1));   // rows past Vf are never used
@@ -1272,9 +1276,13 @@ __device__ __forceinline__ void step_env(const TsDevProg &P, const TsDevProg *pr
                 // phase 1: every kind of the chunk, no barrier in between (disjoint slots)
                 if (!FAST && ch.edge_count) p1_edges<Real>(P, m, ch.edge_begin, ch.edge_count, ks);
                 if (!FAST && ch.att_count) p1_atts<Real>(P, m, ch.att_begin, ch.att_count);
-                if (ch.tet_count && !(S.ablate & 1)) {
-                    const int *ws = P.wsplit + c * (B / 32 + 1) + (t >> 5);
-                    p1_tets<Real, FAST>(P, m, ch.tet_begin, ws[0], ws[1], kv);
+                if ((FAST || ch.tet_count) && !(S.ablate & 1)) {
+                    if constexpr (FAST) {
+                        p1_tets<Real, FAST>(P, m, h_tb, h_wb, h_we, kv);
+                    } else {
+                        const int *ws = P.wsplit + c * (B / 32 + 1) + (t >> 5);
+                        p1_tets<Real, FAST>(P, m, ch.tet_begin, ws[0], ws[1], kv);
+                    }
                 }
                 __syncthreads();
                 // phase 2: owner gathers its slots in reference order
