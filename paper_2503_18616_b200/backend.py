@@ -114,8 +114,14 @@ def run_substeps(x, v, w, edges, rest_len, ks, tets, rest_vol, kv,
 
 
 def detect_contacts(pos, faces, caps, iters=8, *, layout=None):
-    """Contacts of one position set (V, 3) against capsule rows (C, 7), capsule-major order."""
-    pos = np.ascontiguousarray(pos, np.float64)
+    """Contacts of one position set (V, 3) against capsule rows (C, 7), capsule-major order.
+
+    float64 positions run the fp64 build (bitwise equal to _kernels.detect_contacts); float32
+    positions run the fp32 build's narrow phase -- the production kernel's arithmetic -- like
+    ``run_substeps`` dispatches on the dtype of x.  Rows come back as float64 either way."""
+    pos = np.asarray(pos)
+    precision = "fp32" if pos.dtype == np.float32 else "fp64"
+    pos = np.ascontiguousarray(pos, np.float32 if precision == "fp32" else np.float64)
     faces = np.ascontiguousarray(faces, np.int32).reshape(-1, 3)
     caps = np.ascontiguousarray(caps, np.float64).reshape(-1, 7)
     nf, nc = len(faces), len(caps)
@@ -132,7 +138,7 @@ def detect_contacts(pos, faces, caps, iters=8, *, layout=None):
     rows[:nc] = caps
     sc = _scene_for(np.ones(nv), np.zeros((0, 2), np.int32), np.zeros(0), 1.0, np.zeros((0, 4), np.int32),
                     np.zeros(0), 1.0, np.zeros(0, np.int32), np.zeros((0, 3), np.int32), np.zeros(0, np.uint8),
-                    np.zeros((0, 3)), np.zeros(0), np.zeros(0), "fp64", faces=faces, iters=iters, layout=layout)
+                    np.zeros((0, 3)), np.zeros(0), np.zeros(0), precision, faces=faces, iters=iters, layout=layout)
     dev = torch.device("cuda", torch.cuda.current_device())
     x = torch.as_tensor(pos[None], device=dev)
     c = torch.as_tensor(rows[None], device=dev)

@@ -129,6 +129,8 @@ class EnvBatch:
         self._pinned_actions = None
         self._dev_actions = None
         self._layout = self._out_layout()
+        self._numpy_layout = self._out_layout(torch.float64)
+        self.numpy_block_bytes = self._numpy_layout[1]   # D2H bytes per step_numpy call
 
     # -- reference-named state (views of the device state) ------------------
     @property
@@ -198,12 +200,12 @@ class EnvBatch:
         self._ready = True
         return obs if idx is None else obs[torch.as_tensor(idx, device=self.device)]
 
-    def _out_layout(self):
+    def _out_layout(self, obs_dtype=None):
         n = self.num_envs
         off = 0
         layout = []
         for name, dt, shape in _OUTS:
-            dt = self.obs_dtype if dt is None else dt
+            dt = (obs_dtype or self.obs_dtype) if dt is None else dt
             numel = n * int(np.prod(shape)) if shape else n
             nbytes = numel * torch.tensor([], dtype=dt).element_size()
             layout.append((name, dt, (n, *shape), off, nbytes))
@@ -284,7 +286,8 @@ class EnvBatch:
 
     def step_numpy(self, actions):
         """``step`` with the reference's host semantics (env.py:144-197): numpy actions in; numpy
-        obs / reward / terminated / truncated and an info dict of numpy arrays out
+        float64 obs (whatever the build precision, like the reference's ``_observe_rows``),
+        reward / terminated / truncated and an info dict of numpy arrays out
         (``final_observation`` is None when no row is done, ``contacts`` an int).
 
         The first call runs eagerly and then records the device side of a step -- the H2D copy of
@@ -302,14 +305,14 @@ class EnvBatch:
             raise ValidationError(f"actions must have shape {(n, ACTION_SIZE)}, got {a.shape}")
         fx = getattr(self, "_np_fast", None)
         if fx is None:
-            layout, total = self._layout
+            layout, total = self._numpy_layout
             dev_buf = torch.empty(total, dtype=torch.uint8, device=self.device)
             views = {name: dev_buf[off:off + nb].view(dt).view(shape) for name, dt, shape, off, nb in layout}
             so = N.StepOut()
             for name in ("obs", "reward", "terminated", "truncated", "distance", "success", "diverged",
                          "clipped", "contacts", "episode_return", "episode_length", "done_mask", "final_obs"):
                 setattr(so, name, N.ptr(views[name]))
-            so.obs_f64 = int(self.obs_dtype == torch.float64)
+            so.obs_f64 = 1                          # float64 observations, as the reference returns
             host = torch.empty(total, dtype=torch.uint8, pin_memory=True)
             hv = [(name, torch.empty(0, dtype=dt).numpy().dtype, shape, off, nb) for name, dt, shape, off, nb in layout]
             pin_a = torch.empty((n, ACTION_SIZE), dtype=torch.float64, pin_memory=True)

@@ -273,6 +273,7 @@ class DeviceScene:
         self._opts = layout_opts(**layout)
         self.precision = "fp64" if self._opts.precision == N.TS_F64 else "fp32"
         blob, pinfo = _compile_cached(arrays, self._opts)
+        self.program_key = _program_key(arrays, self._opts)   # equal keys = the same compiled program
         h = ctypes.c_void_p()
         N.check(self.lib.ts_create_from_program(ctypes.byref(self._desc), N.ptr(blob), int(blob.nbytes),
                                                 ctypes.byref(pinfo), int(device_index), ctypes.byref(h)),

@@ -150,3 +150,34 @@ def test_ppo_gradient_allreduce_two_ranks():
     w1, r1 = out[1]
     assert np.array_equal(w0, w1)
     assert np.allclose(r0, r1, equal_nan=True)
+
+
+@pytest.mark.timeout(300)
+def test_bench_gpus_two_launches_two_ranks():
+    """`bench.py --gpus 2` outside torchrun re-launches itself as 2 ranks (the driver's command form
+    at N > 1); --dry-run exercises the rank / shard / max-over-ranks plumbing on CPU with gloo."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, TS_BENCH_DIST="gloo")
+    env.pop("WORLD_SIZE", None)
+    res = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--steps", "3",
+                          "--warmup", "3", "--dry-run"], capture_output=True, text=True, env=env, timeout=240)
+    assert res.returncode == 0, res.stderr[-2000:]
+    lines = [ln for ln in res.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, res.stdout           # rank 0 alone prints
+    line = json.loads(lines[0])
+    assert line["n_gpus"] == 2
+    assert line["shards"] == [[0, 4096], [4096, 8192]]   # weak scaling: 4096 envs per rank
+    assert line["job_time"] == 0.002                    # max over ranks
+
+
+def test_bench_rejects_world_mismatch():
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    import bench
+    bench.check_world(2, 2)
+    with pytest.raises(SystemExit):
+        bench.check_world(1, 2)
