@@ -34,11 +34,40 @@
 
 #include <stdint.h>
 
+/* DLPack (https://github.com/dmlc/dlpack, ABI v1): the typed tensor descriptor of the *_dl
+ * entries.  The subset below is layout-identical to dlpack.h; include dlpack.h first to use it. */
+#ifndef DLPACK_MAJOR_VERSION
+#ifdef __cplusplus
+extern "C" {
+#endif
+typedef enum { kDLCPU = 1, kDLCUDA = 2, kDLCUDAHost = 3, kDLCUDAManaged = 13 } DLDeviceType;
+typedef enum { kDLInt = 0, kDLUInt = 1, kDLFloat = 2, kDLBool = 6 } DLDataTypeCode;
+typedef struct { DLDeviceType device_type; int32_t device_id; } DLDevice;
+typedef struct { uint8_t code; uint8_t bits; uint16_t lanes; } DLDataType;
+typedef struct {
+    void *data;
+    DLDevice device;
+    int32_t ndim;
+    DLDataType dtype;
+    int64_t *shape;
+    int64_t *strides;        /* in elements; NULL = compact row-major */
+    uint64_t byte_offset;
+} DLTensor;
+typedef struct DLManagedTensor {
+    DLTensor dl_tensor;
+    void *manager_ctx;
+    void (*deleter)(struct DLManagedTensor *self);
+} DLManagedTensor;
+#ifdef __cplusplus
+}
+#endif
+#endif
+
 #ifdef __cplusplus
 extern "C" {
 #endif
 
-#define TS_ABI_VERSION 2
+#define TS_ABI_VERSION 3
 
 enum ts_status {
     TS_OK = 0,
@@ -223,6 +252,74 @@ int32_t ts_run_substeps(ts_handle *h, void *x, void *v, int64_t num_envs,
 int32_t ts_detect_contacts(ts_handle *h, const void *x, int64_t num_envs, const double *caps,
                            int32_t *count, int32_t *face, int32_t *cap, double *depth,
                            double *dir, double *bary, void *stream);
+
+/* ---- Typed (DLPack) entries: the product boundary ------------------------------------------
+ * The same calls as above with every array passed as a DLTensor (what torch.utils.dlpack /
+ * __dlpack__ hand over, zero-copy).  Each tensor is checked before anything is launched:
+ * device (kDLCUDA / kDLCUDAManaged on the handle's device), dtype (code, bits, lanes = 1),
+ * ndim, shape (N from x's leading dimension, V from the scene) and compact row-major strides;
+ * byte_offset is honoured.  Any mismatch returns TS_ERR_INVALID naming the tensor, the way the
+ * reference's typed memoryviews reject a wrong buffer at entry (_kernels.pyx:577-585).
+ * Dtypes: x, v Real = float32 (TS_F32 handle) / float64 (TS_F64); tool_* float64;
+ * grasp_vertex, steps int64; grasped uint8 or bool; l_prev, ep_return float64. */
+typedef struct ts_env_tensors {
+    const DLTensor *x, *v;                                   /* (N,V,3) Real */
+    const DLTensor *tool_axis, *tool_jaw;                    /* (N,3) f64 */
+    const DLTensor *tool_reach, *tool_clamp;                 /* (N,) f64 */
+    const DLTensor *grasp_vertex;                            /* (N,) i64 */
+    const DLTensor *grasped;                                 /* (N,V) u8/bool */
+    const DLTensor *steps;                                   /* (N,) i64 */
+    const DLTensor *l_prev, *ep_return;                      /* (N,) f64 */
+} ts_env_tensors;
+
+/* Outputs (any may be NULL): obs / final_obs (N,6) float32 or float64 (both the same dtype),
+ * reward / distance / episode_return (N,) f64, flags (N,) bool/u8, contacts (N,) i32,
+ * episode_length (N,) i64. */
+typedef struct ts_step_out_tensors {
+    const DLTensor *obs, *reward, *terminated, *truncated, *distance, *success, *diverged, *clipped;
+    const DLTensor *contacts, *episode_return, *episode_length, *done_mask, *final_obs;
+} ts_step_out_tensors;
+
+/* Tool-pose injection, typed: axis, jaw (N,3) f64; reach, clamp (N,) f64; clipped (N,) u8/bool
+ * or NULL. */
+typedef struct ts_tool_override_tensors {
+    const DLTensor *axis, *jaw, *reach, *clamp, *clipped;
+} ts_tool_override_tensors;
+
+/* EnvBatch.step (env.py:144-197): actions (N,3) float32/float64 on the device (or NULL with an
+ * override); bad_action_flag (1,) int32 or NULL, as ts_env_step. */
+int32_t ts_env_step_dl(ts_handle *h, const ts_env_tensors *st, const DLTensor *actions,
+                       const ts_step_out_tensors *out, const ts_tool_override_tensors *ovr,
+                       const DLTensor *bad_action_flag, void *stream);
+
+/* EnvBatch.reset (env.py:123-142): mask (N,) u8/bool or NULL (all rows); obs (N,6) f32/f64 or
+ * NULL. */
+int32_t ts_env_reset_dl(ts_handle *h, const ts_env_tensors *st, const DLTensor *mask,
+                        const DLTensor *obs, void *stream);
+
+/* EnvBatch._observe_rows (env.py:99-115): obs (N,6) f32/f64 of all rows. */
+int32_t ts_env_observe_dl(ts_handle *h, const ts_env_tensors *st, const DLTensor *obs, void *stream);
+
+/* Simulation.step (solver.py:322-366): targets (N,3) f64 or NULL, angles (N,) f64 or NULL;
+ * outputs clipped / rejected / diverged (N,) bool/u8, contacts (N,) i32, each optional. */
+int32_t ts_sim_step_dl(ts_handle *h, const ts_env_tensors *st, const DLTensor *targets,
+                       const DLTensor *angles, const ts_tool_override_tensors *ovr,
+                       const DLTensor *clipped, const DLTensor *rejected, const DLTensor *diverged,
+                       const DLTensor *contacts, void *stream);
+
+/* backend.run_substeps (_kernels.pyx:577-592): x, v (N,V,3) Real, grasp_vertex (N,) i64,
+ * drag_points (N,3) f64; gravity host (3) doubles. */
+int32_t ts_run_substeps_dl(ts_handle *h, const DLTensor *x, const DLTensor *v,
+                           const DLTensor *grasp_vertex, const DLTensor *drag_points,
+                           const double *gravity, double hstep, int32_t substeps, double damping,
+                           void *stream);
+
+/* backend.detect_contacts (_kernels.pyx:797-947): x (N,V,3) Real, caps (N,3,7) f64; count (N,)
+ * i32, face / cap (N,3F) i32, depth (N,3F) f64, dir / bary (N,3F,3) f64. */
+int32_t ts_detect_contacts_dl(ts_handle *h, const DLTensor *x, const DLTensor *caps,
+                              const DLTensor *count, const DLTensor *face, const DLTensor *cap,
+                              const DLTensor *depth, const DLTensor *dir, const DLTensor *bary,
+                              void *stream);
 
 /* Uniform(-1,1) actions (N,3) float64 on device from a counter-based hash of
  * (seed, counter, global env index first_env + i): a multi-GPU shard draws

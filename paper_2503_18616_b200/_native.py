@@ -81,6 +81,69 @@ class ToolOverride(ctypes.Structure):
     _fields_ = [("axis", _P), ("jaw", _P), ("reach", _P), ("clamp", _P), ("clipped", _P)]
 
 
+# ---- typed (DLPack) boundary -------------------------------------------------------------------
+ENV_TENSORS = ("x", "v", "tool_axis", "tool_jaw", "tool_reach", "tool_clamp", "grasp_vertex", "grasped",
+               "steps", "l_prev", "ep_return")
+STEP_OUTS = ("obs", "reward", "terminated", "truncated", "distance", "success", "diverged", "clipped",
+             "contacts", "episode_return", "episode_length", "done_mask", "final_obs")
+OVERRIDE_TENSORS = ("axis", "jaw", "reach", "clamp", "clipped")
+
+
+class EnvTensors(ctypes.Structure):
+    _fields_ = [(k, _P) for k in ENV_TENSORS]
+
+
+class StepOutTensors(ctypes.Structure):
+    _fields_ = [(k, _P) for k in STEP_OUTS]
+
+
+class ToolOverrideTensors(ctypes.Structure):
+    _fields_ = [(k, _P) for k in OVERRIDE_TENSORS]
+
+
+_capsule_ptr = ctypes.pythonapi.PyCapsule_GetPointer
+_capsule_ptr.restype = ctypes.c_void_p
+_capsule_ptr.argtypes = [ctypes.py_object, ctypes.c_char_p]
+
+
+class DL:
+    """A zero-copy DLPack view of a torch tensor (``torch.utils.dlpack.to_dlpack``): ``.ptr`` is the
+    ``DLManagedTensor*`` (its first member is the ``DLTensor`` the *_dl entries read).  The capsule
+    is kept alive with this object and frees the managed tensor when collected (it is never
+    consumed: the library only borrows the view for the call)."""
+
+    __slots__ = ("capsule", "ptr", "tensor")
+
+    def __init__(self, t):
+        from torch.utils.dlpack import to_dlpack
+        self.tensor = t
+        self.capsule = to_dlpack(t)
+        self.ptr = _capsule_ptr(self.capsule, b"dltensor")
+
+
+def dl(t):
+    """DL view of `t` (None -> None)."""
+    return None if t is None else DL(t)
+
+
+def dlp(d):
+    """DLTensor* of a DL view (None -> NULL).  The caller keeps `d` alive across the C call: a
+    collected capsule frees the DLManagedTensor the pointer refers to (never ``dlp(dl(t))``)."""
+    return None if d is None else d.ptr
+
+
+def dl_struct(cls, names, tensors):
+    """A ctypes struct of DLTensor* from {name: tensor or None}; keeps the DL views on the struct."""
+    s = cls()
+    keep = []
+    for name in names:
+        d = dl(tensors.get(name))
+        keep.append(d)
+        setattr(s, name, dlp(d))
+    s._keep = keep
+    return s
+
+
 # exported symbols (checked by tests/test_abi.py against include/tissuesim_b200.h)
 _SIGNATURES = {
     "ts_last_error": ([], ctypes.c_char_p),
@@ -104,6 +167,12 @@ _SIGNATURES = {
     "ts_kernel_timing": ([_P, _I32, _I32], _I32),
     "ts_kernel_time": ([_P, _P, _P], _I32),
     "ts_step_kernel_name": ([_P], ctypes.c_char_p),
+    "ts_env_step_dl": ([_P, _P, _P, _P, _P, _P, _P], _I32),
+    "ts_env_reset_dl": ([_P, _P, _P, _P, _P], _I32),
+    "ts_env_observe_dl": ([_P, _P, _P, _P], _I32),
+    "ts_sim_step_dl": ([_P, _P, _P, _P, _P, _P, _P, _P, _P, _P], _I32),
+    "ts_run_substeps_dl": ([_P, _P, _P, _P, _P, _P, _D, _I32, _D, _P], _I32),
+    "ts_detect_contacts_dl": ([_P, _P, _P, _P, _P, _P, _P, _P, _P, _P], _I32),
 }
 
 _lib = None

@@ -106,8 +106,9 @@ def run_substeps(x, v, w, edges, rest_len, ks, tets, rest_vol, kv,
     drag = torch.as_tensor(np.ascontiguousarray(drag_points, np.float64).reshape(n_env, 3), device=dev)
     grav = (ctypes.c_double * 3)(*[float(a) for a in np.asarray(g, np.float64)])
     stream = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
-    N.check(sc.lib.ts_run_substeps(sc.handle, N.ptr(xt), N.ptr(vt), n_env, N.ptr(gv), N.ptr(drag), grav,
-                                   float(h), int(substeps), float(damping), stream), "ts_run_substeps")
+    views = [N.dl(t) for t in (xt, vt, gv, drag)]
+    N.check(sc.lib.ts_run_substeps_dl(sc.handle, *(d.ptr for d in views), grav, float(h), int(substeps),
+                                      float(damping), stream), "ts_run_substeps")
     x_np[...] = xt.cpu().numpy()
     v_np[...] = vt.cpu().numpy()
     return None
@@ -150,8 +151,8 @@ def detect_contacts(pos, faces, caps, iters=8, *, layout=None):
     direc = torch.zeros((cap_n, 3), dtype=torch.float64, device=dev)
     bary = torch.zeros((cap_n, 3), dtype=torch.float64, device=dev)
     stream = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
-    N.check(sc.lib.ts_detect_contacts(sc.handle, N.ptr(x), 1, N.ptr(c), N.ptr(count), N.ptr(face), N.ptr(capi),
-                                      N.ptr(depth), N.ptr(direc), N.ptr(bary), stream), "ts_detect_contacts")
+    views = [N.dl(t) for t in (x, c, count, face[None], capi[None], depth[None], direc[None], bary[None])]
+    N.check(sc.lib.ts_detect_contacts_dl(sc.handle, *(d.ptr for d in views), stream), "ts_detect_contacts")
     k = int(count.item())
     return (face[:k].cpu().numpy(), capi[:k].cpu().numpy(), depth[:k].cpu().numpy(),
             direc[:k].cpu().numpy(), bary[:k].cpu().numpy())

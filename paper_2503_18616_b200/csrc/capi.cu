@@ -40,6 +40,7 @@ struct ts_handle {
     int cluster_k = 1;                  // > 1: thread-block cluster program (large meshes)
     std::vector<TsDevProg> parts;       // decoded part programs (host copies)
     TsDevProg *dev_parts = nullptr;     // the same, on the device (cluster kernel argument)
+    int64_t n_vert = 0;                 // scene vertex count (typed-entry shape checks)
 };
 
 static const char *ts_kernel_name_for(const TsDevProg &P, int real_bytes, int cluster_k, int ablate) {
@@ -264,6 +265,7 @@ static int32_t create_handle(const ts_scene_desc *desc, const ts_layout_opts &o,
     h->prog.pf_base = pf <= (512 << 10) ? h->dev_blob : nullptr;
     h->prog.pf_bytes = pf <= (512 << 10) ? pf : 0;
     fill_params(*desc, h->params);
+    h->n_vert = desc->n_vert;
     int max_smem = 0;
     cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
     if (h->smem > max_smem) {
@@ -529,6 +531,236 @@ int32_t ts_set_max_grid(ts_handle *h, int32_t max_grid) {
     if (!h) return fail(TS_ERR_INVALID, "null argument");
     h->max_grid = max_grid;
     return TS_OK;
+}
+
+}  // extern "C"
+
+// ---- typed (DLPack) entries ----------------------------------------------------------------
+namespace {
+enum Kind { K_REAL, K_F64, K_F32_OR_F64, K_I64, K_I32, K_U8 };
+
+// Checks one DLTensor against (kind, shape) and returns its data address in *out.  Shape entries
+// of -1 are free.  NULL tensors are accepted only when `optional`.
+int check_dl(const ts_handle *h, const DLTensor *t, const char *name, Kind kind, int ndim, const int64_t *shape,
+             bool optional, void **out, int *is_f64 = nullptr) {
+    *out = nullptr;
+    if (!t) {
+        if (optional) return TS_OK;
+        return fail(TS_ERR_INVALID, std::string(name) + ": tensor required");
+    }
+    char buf[320];
+    if (t->device.device_type != kDLCUDA && t->device.device_type != kDLCUDAManaged) {
+        std::snprintf(buf, sizeof(buf), "%s: expected a CUDA tensor, got DLPack device type %d", name,
+                      (int)t->device.device_type);
+        return fail(TS_ERR_INVALID, buf);
+    }
+    if (t->device.device_id != h->device) {
+        std::snprintf(buf, sizeof(buf), "%s: tensor is on cuda:%d, the handle on cuda:%d", name,
+                      (int)t->device.device_id, h->device);
+        return fail(TS_ERR_INVALID, buf);
+    }
+    const DLDataType d = t->dtype;
+    bool ok = d.lanes == 1;
+    bool f64 = false;
+    switch (kind) {
+        case K_REAL: f64 = h->precision == TS_F64; ok = ok && d.code == kDLFloat && d.bits == (f64 ? 64 : 32); break;
+        case K_F64: f64 = true; ok = ok && d.code == kDLFloat && d.bits == 64; break;
+        case K_F32_OR_F64: f64 = d.bits == 64; ok = ok && d.code == kDLFloat && (d.bits == 32 || d.bits == 64); break;
+        case K_I64: ok = ok && d.code == kDLInt && d.bits == 64; break;
+        case K_I32: ok = ok && d.code == kDLInt && d.bits == 32; break;
+        case K_U8: ok = ok && (d.code == kDLUInt || d.code == kDLBool) && d.bits == 8; break;
+    }
+    if (!ok) {
+        static const char *want[] = {"", "float64", "float32 or float64", "int64", "int32", "uint8 or bool"};
+        std::snprintf(buf, sizeof(buf), "%s: dtype (code %d, %d bits, %d lanes) is not %s", name, (int)d.code,
+                      (int)d.bits, (int)d.lanes,
+                      kind == K_REAL ? (h->precision == TS_F64 ? "float64 (fp64 handle)" : "float32 (fp32 handle)")
+                                     : want[kind]);
+        return fail(TS_ERR_INVALID, buf);
+    }
+    if (is_f64) *is_f64 = f64;
+    bool shape_ok = t->ndim == ndim && (ndim == 0 || t->shape);
+    for (int i = 0; shape_ok && i < ndim; ++i) shape_ok = shape[i] < 0 || t->shape[i] == shape[i];
+    if (!shape_ok) {
+        std::string got = "(";
+        for (int i = 0; i < t->ndim && t->shape; ++i) got += std::to_string(t->shape[i]) + (i + 1 < t->ndim ? "," : "");
+        std::string exp = "(";
+        for (int i = 0; i < ndim; ++i) exp += (shape[i] < 0 ? std::string("*") : std::to_string(shape[i])) + (i + 1 < ndim ? "," : "");
+        return fail(TS_ERR_INVALID, std::string(name) + ": shape " + got + ") where " + exp + ") is required");
+    }
+    if (t->strides) {   // compact row-major (dimensions of extent 1 may carry any stride)
+        int64_t expect = 1;
+        for (int i = ndim - 1; i >= 0; --i) {
+            if (t->shape[i] != 1 && t->strides[i] != expect)
+                return fail(TS_ERR_INVALID, std::string(name) + ": tensor is not contiguous (row-major)");
+            expect *= t->shape[i];
+        }
+    }
+    if (!t->data) {
+        int64_t numel = 1;
+        for (int i = 0; i < ndim; ++i) numel *= t->shape[i];
+        if (numel) return fail(TS_ERR_INVALID, std::string(name) + ": null data");
+    }
+    *out = t->data ? reinterpret_cast<char *>(t->data) + t->byte_offset : nullptr;
+    return TS_OK;
+}
+
+#define TS_CHECK(expr) do { int rc_ = (expr); if (rc_ != TS_OK) return rc_; } while (0)
+
+int env_state_dl(const ts_handle *h, const ts_env_tensors *st, ts_env_state &o, int64_t &n) {
+    if (!st || !st->x) return fail(TS_ERR_INVALID, "state: x required");
+    if (st->x->ndim != 3 || !st->x->shape) return fail(TS_ERR_INVALID, "x: shape (N,V,3) required");
+    n = st->x->shape[0];
+    const int64_t V = h->n_vert;
+    const int64_t nv3[3] = {n, V, 3}, n3[2] = {n, 3}, n1[1] = {n}, nv[2] = {n, V};
+    void *p;
+    TS_CHECK(check_dl(h, st->x, "x", K_REAL, 3, nv3, false, &o.x));
+    TS_CHECK(check_dl(h, st->v, "v", K_REAL, 3, nv3, false, &o.v));
+    TS_CHECK(check_dl(h, st->tool_axis, "tool_axis", K_F64, 2, n3, false, &p)); o.tool_axis = (double *)p;
+    TS_CHECK(check_dl(h, st->tool_jaw, "tool_jaw", K_F64, 2, n3, false, &p)); o.tool_jaw = (double *)p;
+    TS_CHECK(check_dl(h, st->tool_reach, "tool_reach", K_F64, 1, n1, false, &p)); o.tool_reach = (double *)p;
+    TS_CHECK(check_dl(h, st->tool_clamp, "tool_clamp", K_F64, 1, n1, false, &p)); o.tool_clamp = (double *)p;
+    TS_CHECK(check_dl(h, st->grasp_vertex, "grasp_vertex", K_I64, 1, n1, false, &p)); o.grasp_vertex = (int64_t *)p;
+    TS_CHECK(check_dl(h, st->grasped, "grasped", K_U8, 2, nv, false, &p)); o.grasped = (uint8_t *)p;
+    TS_CHECK(check_dl(h, st->steps, "steps", K_I64, 1, n1, false, &p)); o.steps = (int64_t *)p;
+    TS_CHECK(check_dl(h, st->l_prev, "l_prev", K_F64, 1, n1, false, &p)); o.l_prev = (double *)p;
+    TS_CHECK(check_dl(h, st->ep_return, "ep_return", K_F64, 1, n1, false, &p)); o.ep_return = (double *)p;
+    return TS_OK;
+}
+
+int override_dl(const ts_handle *h, const ts_tool_override_tensors *t, int64_t n, ts_tool_override &o) {
+    const int64_t n3[2] = {n, 3}, n1[1] = {n};
+    void *p;
+    TS_CHECK(check_dl(h, t->axis, "override axis", K_F64, 2, n3, false, &p)); o.axis = (const double *)p;
+    TS_CHECK(check_dl(h, t->jaw, "override jaw", K_F64, 2, n3, false, &p)); o.jaw = (const double *)p;
+    TS_CHECK(check_dl(h, t->reach, "override reach", K_F64, 1, n1, false, &p)); o.reach = (const double *)p;
+    TS_CHECK(check_dl(h, t->clamp, "override clamp", K_F64, 1, n1, false, &p)); o.clamp = (const double *)p;
+    TS_CHECK(check_dl(h, t->clipped, "override clipped", K_U8, 1, n1, true, &p)); o.clipped = (const uint8_t *)p;
+    return TS_OK;
+}
+}  // namespace
+
+extern "C" {
+
+int32_t ts_env_step_dl(ts_handle *h, const ts_env_tensors *st, const DLTensor *actions,
+                       const ts_step_out_tensors *out, const ts_tool_override_tensors *ovr,
+                       const DLTensor *bad_action_flag, void *stream) {
+    if (!h || !st || !out) return fail(TS_ERR_INVALID, "null argument");
+    ts_env_state s;
+    int64_t n;
+    TS_CHECK(env_state_dl(h, st, s, n));
+    const int64_t n3[2] = {n, 3}, n1[1] = {n}, n6[2] = {n, 6}, one[1] = {1};
+    void *a = nullptr, *p;
+    int a64 = 1;
+    TS_CHECK(check_dl(h, actions, "actions", K_F32_OR_F64, 2, n3, ovr != nullptr, &a, &a64));
+    ts_tool_override o{};
+    if (ovr) TS_CHECK(override_dl(h, ovr, n, o));
+    ts_step_out so{};
+    int obs64 = 1, fin64 = -1;
+    TS_CHECK(check_dl(h, out->obs, "obs", K_F32_OR_F64, 2, n6, true, &so.obs, &obs64));
+    TS_CHECK(check_dl(h, out->final_obs, "final_obs", K_F32_OR_F64, 2, n6, true, &so.final_obs, &fin64));
+    if (out->obs && out->final_obs && obs64 != fin64)
+        return fail(TS_ERR_INVALID, "final_obs: dtype must equal obs's");
+    so.obs_f64 = out->obs ? obs64 : (out->final_obs ? fin64 : 1);
+    TS_CHECK(check_dl(h, out->reward, "reward", K_F64, 1, n1, true, &p)); so.reward = (double *)p;
+    TS_CHECK(check_dl(h, out->distance, "distance", K_F64, 1, n1, true, &p)); so.distance = (double *)p;
+    TS_CHECK(check_dl(h, out->episode_return, "episode_return", K_F64, 1, n1, true, &p)); so.episode_return = (double *)p;
+    TS_CHECK(check_dl(h, out->episode_length, "episode_length", K_I64, 1, n1, true, &p)); so.episode_length = (int64_t *)p;
+    TS_CHECK(check_dl(h, out->contacts, "contacts", K_I32, 1, n1, true, &p)); so.contacts = (int32_t *)p;
+    TS_CHECK(check_dl(h, out->terminated, "terminated", K_U8, 1, n1, true, &p)); so.terminated = (uint8_t *)p;
+    TS_CHECK(check_dl(h, out->truncated, "truncated", K_U8, 1, n1, true, &p)); so.truncated = (uint8_t *)p;
+    TS_CHECK(check_dl(h, out->success, "success", K_U8, 1, n1, true, &p)); so.success = (uint8_t *)p;
+    TS_CHECK(check_dl(h, out->diverged, "diverged", K_U8, 1, n1, true, &p)); so.diverged = (uint8_t *)p;
+    TS_CHECK(check_dl(h, out->clipped, "clipped", K_U8, 1, n1, true, &p)); so.clipped = (uint8_t *)p;
+    TS_CHECK(check_dl(h, out->done_mask, "done_mask", K_U8, 1, n1, true, &p)); so.done_mask = (uint8_t *)p;
+    void *flag = nullptr;
+    TS_CHECK(check_dl(h, bad_action_flag, "bad_action_flag", K_I32, 1, one, true, &flag));
+    return ts_env_step(h, &s, n, a, a ? !a64 : 0, &so, ovr ? &o : nullptr, (int32_t *)flag, stream);
+}
+
+int32_t ts_env_reset_dl(ts_handle *h, const ts_env_tensors *st, const DLTensor *mask, const DLTensor *obs,
+                        void *stream) {
+    if (!h || !st) return fail(TS_ERR_INVALID, "null argument");
+    ts_env_state s;
+    int64_t n;
+    TS_CHECK(env_state_dl(h, st, s, n));
+    const int64_t n1[1] = {n}, n6[2] = {n, 6};
+    void *m, *o;
+    int o64 = 1;
+    TS_CHECK(check_dl(h, mask, "mask", K_U8, 1, n1, true, &m));
+    TS_CHECK(check_dl(h, obs, "obs", K_F32_OR_F64, 2, n6, true, &o, &o64));
+    return ts_env_reset(h, &s, n, (const uint8_t *)m, o, o64, stream);
+}
+
+int32_t ts_env_observe_dl(ts_handle *h, const ts_env_tensors *st, const DLTensor *obs, void *stream) {
+    if (!h || !st) return fail(TS_ERR_INVALID, "null argument");
+    ts_env_state s;
+    int64_t n;
+    TS_CHECK(env_state_dl(h, st, s, n));
+    const int64_t n6[2] = {n, 6};
+    void *o;
+    int o64 = 1;
+    TS_CHECK(check_dl(h, obs, "obs", K_F32_OR_F64, 2, n6, false, &o, &o64));
+    return ts_env_observe(h, &s, n, o, o64, stream);
+}
+
+int32_t ts_sim_step_dl(ts_handle *h, const ts_env_tensors *st, const DLTensor *targets, const DLTensor *angles,
+                       const ts_tool_override_tensors *ovr, const DLTensor *clipped, const DLTensor *rejected,
+                       const DLTensor *diverged, const DLTensor *contacts, void *stream) {
+    if (!h || !st) return fail(TS_ERR_INVALID, "null argument");
+    ts_env_state s;
+    int64_t n;
+    TS_CHECK(env_state_dl(h, st, s, n));
+    const int64_t n3[2] = {n, 3}, n1[1] = {n};
+    void *t, *a, *c, *r, *d, *k;
+    TS_CHECK(check_dl(h, targets, "targets", K_F64, 2, n3, true, &t));
+    TS_CHECK(check_dl(h, angles, "angles", K_F64, 1, n1, true, &a));
+    ts_tool_override o{};
+    if (ovr) TS_CHECK(override_dl(h, ovr, n, o));
+    TS_CHECK(check_dl(h, clipped, "clipped", K_U8, 1, n1, true, &c));
+    TS_CHECK(check_dl(h, rejected, "rejected", K_U8, 1, n1, true, &r));
+    TS_CHECK(check_dl(h, diverged, "diverged", K_U8, 1, n1, true, &d));
+    TS_CHECK(check_dl(h, contacts, "contacts", K_I32, 1, n1, true, &k));
+    return ts_sim_step(h, &s, n, (const double *)t, (const double *)a, ovr ? &o : nullptr, (uint8_t *)c,
+                       (uint8_t *)r, (uint8_t *)d, (int32_t *)k, stream);
+}
+
+int32_t ts_run_substeps_dl(ts_handle *h, const DLTensor *x, const DLTensor *v, const DLTensor *grasp_vertex,
+                           const DLTensor *drag_points, const double *gravity, double hstep, int32_t substeps,
+                           double damping, void *stream) {
+    if (!h || !x) return fail(TS_ERR_INVALID, "null argument");
+    if (x->ndim != 3 || !x->shape) return fail(TS_ERR_INVALID, "x: shape (N,V,3) required");
+    const int64_t n = x->shape[0];
+    const int64_t nv3[3] = {n, h->n_vert, 3}, n3[2] = {n, 3}, n1[1] = {n};
+    void *px, *pv, *pg, *pd;
+    TS_CHECK(check_dl(h, x, "x", K_REAL, 3, nv3, false, &px));
+    TS_CHECK(check_dl(h, v, "v", K_REAL, 3, nv3, false, &pv));
+    TS_CHECK(check_dl(h, grasp_vertex, "grasp_vertex", K_I64, 1, n1, false, &pg));
+    TS_CHECK(check_dl(h, drag_points, "drag_points", K_F64, 2, n3, false, &pd));
+    if (n == 0) return TS_OK;
+    return ts_run_substeps(h, px, pv, n, (const int64_t *)pg, (const double *)pd, gravity, hstep, substeps,
+                           damping, stream);
+}
+
+int32_t ts_detect_contacts_dl(ts_handle *h, const DLTensor *x, const DLTensor *caps, const DLTensor *count,
+                              const DLTensor *face, const DLTensor *cap, const DLTensor *depth, const DLTensor *dir,
+                              const DLTensor *bary, void *stream) {
+    if (!h || !x) return fail(TS_ERR_INVALID, "null argument");
+    if (x->ndim != 3 || !x->shape) return fail(TS_ERR_INVALID, "x: shape (N,V,3) required");
+    const int64_t n = x->shape[0], F3 = 3 * (int64_t)h->params.n_face;
+    const int64_t nv3[3] = {n, h->n_vert, 3}, c37[3] = {n, 3, 7}, n1[1] = {n}, nf[2] = {n, F3}, nf3[3] = {n, F3, 3};
+    void *px, *pc, *pn, *pf, *pk, *pd, *pr, *pb;
+    TS_CHECK(check_dl(h, x, "x", K_REAL, 3, nv3, false, &px));
+    TS_CHECK(check_dl(h, caps, "caps", K_F64, 3, c37, false, &pc));
+    TS_CHECK(check_dl(h, count, "count", K_I32, 1, n1, false, &pn));
+    TS_CHECK(check_dl(h, face, "face", K_I32, 2, nf, false, &pf));
+    TS_CHECK(check_dl(h, cap, "cap", K_I32, 2, nf, false, &pk));
+    TS_CHECK(check_dl(h, depth, "depth", K_F64, 2, nf, false, &pd));
+    TS_CHECK(check_dl(h, dir, "dir", K_F64, 3, nf3, false, &pr));
+    TS_CHECK(check_dl(h, bary, "bary", K_F64, 3, nf3, false, &pb));
+    if (n == 0) return TS_OK;
+    return ts_detect_contacts(h, px, n, (const double *)pc, (int32_t *)pn, (int32_t *)pf, (int32_t *)pk,
+                              (double *)pd, (double *)pr, (double *)pb, stream);
 }
 
 }  // extern "C"

@@ -126,6 +126,7 @@ class EnvBatch:
         self.seed_value = seed
         self._rng = None
         self._bad_flag = torch.zeros(1, dtype=torch.int32, device=self.device)
+        self._bad_flag_dl = N.dl(self._bad_flag)
         self._pinned_actions = None
         self._dev_actions = None
         self._layout = self._out_layout()
@@ -163,10 +164,10 @@ class EnvBatch:
     def _observe_all(self):
         obs = torch.empty((self.num_envs, OBSERVATION_SIZE), dtype=self.obs_dtype, device=self.device)
         st = self.sim.state_struct()
+        obs_dl = N.dl(obs)            # the view must outlive the call
         with torch.cuda.device(self.device):
-            N.check(self.sim.scene.lib.ts_env_observe(self.sim.scene.handle, ctypes.byref(st), self.num_envs,
-                                                      N.ptr(obs), int(self.obs_dtype == torch.float64),
-                                                      self.sim.stream_ptr()), "ts_env_observe")
+            N.check(self.sim.scene.lib.ts_env_observe_dl(self.sim.scene.handle, ctypes.byref(st),
+                                                         obs_dl.ptr, self.sim.stream_ptr()), "ts_env_observe")
         return obs
 
     def _observe_rows(self, idx):
@@ -193,10 +194,10 @@ class EnvBatch:
             mask = torch.as_tensor(m, device=self.device)
         obs = torch.empty((n, OBSERVATION_SIZE), dtype=self.obs_dtype, device=self.device)
         st = self.sim.state_struct()
+        mask_dl, obs_dl = N.dl(mask), N.dl(obs)   # the views must outlive the call
         with torch.cuda.device(self.device):
-            N.check(self.sim.scene.lib.ts_env_reset(self.sim.scene.handle, ctypes.byref(st), n, N.ptr(mask),
-                                                    N.ptr(obs), int(self.obs_dtype == torch.float64),
-                                                    self.sim.stream_ptr()), "ts_env_reset")
+            N.check(self.sim.scene.lib.ts_env_reset_dl(self.sim.scene.handle, ctypes.byref(st), N.dlp(mask_dl),
+                                                       obs_dl.ptr, self.sim.stream_ptr()), "ts_env_reset")
         self._ready = True
         return obs if idx is None else obs[torch.as_tensor(idx, device=self.device)]
 
@@ -308,17 +309,14 @@ class EnvBatch:
             layout, total = self._numpy_layout
             dev_buf = torch.empty(total, dtype=torch.uint8, device=self.device)
             views = {name: dev_buf[off:off + nb].view(dt).view(shape) for name, dt, shape, off, nb in layout}
-            so = N.StepOut()
-            for name in ("obs", "reward", "terminated", "truncated", "distance", "success", "diverged",
-                         "clipped", "contacts", "episode_return", "episode_length", "done_mask", "final_obs"):
-                setattr(so, name, N.ptr(views[name]))
-            so.obs_f64 = 1                          # float64 observations, as the reference returns
+            # float64 observations, as the reference returns: the obs views are float64 (_numpy_layout)
+            so = N.dl_struct(N.StepOutTensors, N.STEP_OUTS, views)
             host = torch.empty(total, dtype=torch.uint8, pin_memory=True)
             hv = [(name, torch.empty(0, dtype=dt).numpy().dtype, shape, off, nb) for name, dt, shape, off, nb in layout]
             pin_a = torch.empty((n, ACTION_SIZE), dtype=torch.float64, pin_memory=True)
             dev_a = torch.empty((n, ACTION_SIZE), dtype=torch.float64, device=self.device)
             fx = self._np_fast = {"dev_buf": dev_buf, "so": so, "host": host, "raw": host.numpy(), "hv": hv,
-                                  "pin_a": pin_a, "pin_np": pin_a.numpy(), "dev_a": dev_a,
+                                  "pin_a": pin_a, "pin_np": pin_a.numpy(), "dev_a": dev_a, "dl_a": N.dl(dev_a),
                                   "done": torch.cuda.Event(), "graph": None, "sig": None}
         pin = fx["pin_np"]
         np.copyto(pin, a, casting="unsafe")
@@ -329,8 +327,8 @@ class EnvBatch:
 
         def device_side():
             fx["dev_a"].copy_(fx["pin_a"], non_blocking=True)
-            N.check(self.sim.scene.lib.ts_env_step(self.sim.scene.handle, ctypes.byref(st), n, N.ptr(fx["dev_a"]),
-                                                   0, ctypes.byref(fx["so"]), None, None, self.sim.stream_ptr()),
+            N.check(self.sim.scene.lib.ts_env_step_dl(self.sim.scene.handle, ctypes.byref(st), fx["dl_a"].ptr,
+                                                      ctypes.byref(fx["so"]), None, None, self.sim.stream_ptr()),
                     "ts_env_step")
             fx["host"].copy_(fx["dev_buf"], non_blocking=True)
 
@@ -372,21 +370,18 @@ class EnvBatch:
         n = self.num_envs
         a, is_f32, on_device = self._stage_actions(actions)
         out = self._alloc_outputs()
-        so = N.StepOut()
-        for name in ("obs", "reward", "terminated", "truncated", "distance", "success", "diverged",
-                     "clipped", "contacts", "episode_return", "episode_length", "done_mask", "final_obs"):
-            setattr(so, name, N.ptr(out[name]))
-        so.obs_f64 = int(self.obs_dtype == torch.float64)
+        so = N.dl_struct(N.StepOutTensors, N.STEP_OUTS, out)
         ovr = None
         if tool_override is not None:
             ovr, _keep = _override_struct(tool_override, n, self.device)
         check = on_device and validate
         st = self.sim.state_struct()
+        a_dl = N.dl(a)
         with torch.cuda.device(self.device):
-            N.check(self.sim.scene.lib.ts_env_step(
-                self.sim.scene.handle, ctypes.byref(st), n, N.ptr(a), int(is_f32), ctypes.byref(so),
+            N.check(self.sim.scene.lib.ts_env_step_dl(
+                self.sim.scene.handle, ctypes.byref(st), a_dl.ptr, ctypes.byref(so),
                 ctypes.byref(ovr) if ovr is not None else None,
-                N.ptr(self._bad_flag) if check else None, self.sim.stream_ptr()), "ts_env_step")
+                self._bad_flag_dl.ptr if check else None, self.sim.stream_ptr()), "ts_env_step")
         if check and int(self._bad_flag.item()) != 0:
             raise ValidationError("actions must be finite")
         self.sim.step_count += 1

@@ -179,11 +179,18 @@ CACHE_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_native", 
 
 
 def _lib_fingerprint():
+    """Hash of what decides a program's bytes: the scene compiler's sources (compiler.cpp, its
+    header and the blob format in program.h) -- kernel-only rebuilds keep the cache.  Falls back to
+    the library itself when the sources are absent."""
     global _LIB_FP
     if _LIB_FP is None:
-        from .build import LIB
-        with open(LIB, "rb") as fh:
-            _LIB_FP = hashlib.sha1(fh.read()).hexdigest()
+        from .build import CSRC, LIB
+        h = hashlib.sha1()
+        srcs = [os.path.join(CSRC, f) for f in ("compiler.cpp", "compiler.h", "program.h")]
+        for f in (srcs if all(os.path.exists(f) for f in srcs) else [LIB]):
+            with open(f, "rb") as fh:
+                h.update(fh.read())
+        _LIB_FP = h.hexdigest()
     return _LIB_FP
 
 

@@ -172,19 +172,14 @@ class Simulation:
 
     # -- C-ABI plumbing -----------------------------------------------------
     def state_struct(self):
-        """ts_env_state pointing at the live tensors (rebuilt if a tensor was replaced)."""
+        """ts_env_tensors: DLPack views of the live state tensors (rebuilt when a tensor was
+        replaced; the library checks every view's dtype / shape / device / strides per call)."""
         keys = (self.x, self.v, self.tool.axis, self.tool.jaw_dir, self.tool.reach,
                 self.tool.clamp_angle, self.grasp_vertex, self.grasped, self._steps, self._l_prev,
                 self._return)
-        sig = tuple(t.data_ptr() for t in keys)
-        if self._state is None or self._state[0] != sig:   # a tensor was replaced: check it
-            for t in keys:
-                if not t.is_contiguous() or t.device != self.device:
-                    raise ValidationError("simulation state tensors must stay contiguous on the engine device")
-            st = N.EnvState()
-            (st.x, st.v, st.tool_axis, st.tool_jaw, st.tool_reach, st.tool_clamp, st.grasp_vertex,
-             st.grasped, st.steps, st.l_prev, st.ep_return) = sig
-            self._state = (sig, st)
+        sig = tuple((t.data_ptr(), t.dtype, tuple(t.shape), t.stride()) for t in keys)
+        if self._state is None or self._state[0] != sig:
+            self._state = (sig, N.dl_struct(N.EnvTensors, N.ENV_TENSORS, dict(zip(N.ENV_TENSORS, keys))))
         return self._state[1]
 
     def stream_ptr(self):
@@ -201,9 +196,10 @@ class Simulation:
             m[sel] = 1
             mask = torch.as_tensor(m, device=self.device)
         st = self.state_struct()
+        mask_dl = N.dl(mask)          # the view must outlive the call
         with torch.cuda.device(self.device):
-            N.check(self.scene.lib.ts_env_reset(self.scene.handle, ctypes.byref(st), n, N.ptr(mask), None, 0,
-                                                self.stream_ptr()), "ts_env_reset")
+            N.check(self.scene.lib.ts_env_reset_dl(self.scene.handle, ctypes.byref(st), N.dlp(mask_dl), None,
+                                                   self.stream_ptr()), "ts_env_reset")
 
     def step(self, targets=None, angles=None, raise_on_divergence=True, tool_override=None):
         """One outer step (solver.py:322-366).  Returns an info dict of device tensors."""
@@ -223,12 +219,12 @@ class Simulation:
         if tool_override is not None:
             ovr, keep = _override_struct(tool_override, n, dev)
         st = self.state_struct()
+        views = [N.dl(x) for x in (t, a, clipped, rejected, diverged, contacts)]
         with torch.cuda.device(dev):
-            N.check(self.scene.lib.ts_sim_step(
-                self.scene.handle, ctypes.byref(st), n, N.ptr(t), N.ptr(a),
+            N.check(self.scene.lib.ts_sim_step_dl(
+                self.scene.handle, ctypes.byref(st), N.dlp(views[0]), N.dlp(views[1]),
                 ctypes.byref(ovr) if ovr is not None else None,
-                N.ptr(clipped), N.ptr(rejected), N.ptr(diverged), N.ptr(contacts),
-                self.stream_ptr()), "ts_sim_step")
+                *(N.dlp(v) for v in views[2:]), self.stream_ptr()), "ts_sim_step")
         self.step_count += 1
         if targets is not None or tool_override is not None:
             info["clipped"], info["rejected"] = clipped, rejected
@@ -286,7 +282,7 @@ class LazyInt:
 
 
 def _override_struct(ovr, n, dev):
-    """ts_tool_override from a dict of post-command poses (validation injection)."""
+    """ts_tool_override_tensors from a dict of post-command poses (validation injection)."""
     def t(name, width):
         return _as_device_f64(ovr[name], n, dev, name, width)
     keep = {"axis": t("axis", 3), "jaw": t("jaw", 3), "reach": t("reach", 1), "clamp": t("clamp", 1)}
@@ -294,8 +290,4 @@ def _override_struct(ovr, n, dev):
     if clipped is not None:
         keep["clipped"] = torch.as_tensor(np.asarray(clipped, np.uint8) if not isinstance(clipped, torch.Tensor)
                                           else clipped.to(torch.uint8), device=dev).contiguous()
-    s = N.ToolOverride()
-    s.axis, s.jaw, s.reach, s.clamp = (N.ptr(keep[k]) for k in ("axis", "jaw", "reach", "clamp"))
-    s.clipped = N.ptr(keep.get("clipped"))
-    s._keep = keep
-    return s, keep
+    return N.dl_struct(N.ToolOverrideTensors, N.OVERRIDE_TENSORS, keep), keep

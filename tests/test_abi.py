@@ -38,7 +38,7 @@ def test_nm_exports():
 
 def test_abi_version_and_errors():
     lib = N.load()
-    assert lib.ts_abi_version() == 2
+    assert lib.ts_abi_version() == 3
     h = ctypes.c_void_p()
     rc = lib.ts_create(None, None, 0, ctypes.byref(h))
     assert rc == N.TS_ERR_INVALID

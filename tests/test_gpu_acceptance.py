@@ -1,0 +1,175 @@
+"""Acceptance criteria P1, P2, P6 and P9 restated against the sm_100a kernels.
+
+The reference checks them on its scalar numpy ops and CPU backends
+(`/root/reference/pkg/tests/test_acceptance.py:34-83, 152-168, 203-221`); here every
+projection, detection and push-out runs in the device kernels (plugin `run_substeps`, the
+production `Simulation.step`), in both builds.  P3, P4, P5, P7 and P10 live in
+test_gpu_solver.py / test_gpu_parity.py / test_gpu_env.py.
+"""
+
+import tempfile
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from conftest import build_slab_scene
+from paper_2503_18616_b200 import Simulation
+from paper_2503_18616_b200 import backend as B
+
+pytestmark = pytest.mark.gpu
+
+_NO_ATT = (np.zeros(0, np.int32), np.zeros((0, 3), np.int32), np.zeros(0, np.uint8), np.zeros((0, 3)),
+           np.zeros(0), np.zeros(0))
+
+
+def report(criterion, detail):
+    print(f"\nPASS {criterion}: {detail}")
+
+
+def _one_substep(pos, edges, rest_len, ks, tets, rest_vol, kv, dtype):
+    """One substep of the device solver from rest velocity, no gravity: x + averaged corrections."""
+    x = np.array(pos[None], dtype=dtype, copy=True)
+    v = np.zeros_like(x)
+    B.run_substeps(x, v, np.ones(len(pos)), edges, rest_len, ks, tets, rest_vol, kv, *_NO_ATT,
+                   np.array([-1]), np.zeros((1, 3)), np.zeros(3), 1e-3, 1, 0.0)
+    return x[0].astype(np.float64)
+
+
+@pytest.mark.parametrize("precision,tol", [("fp64", 1e-9), ("fp32", 2e-5)])
+def test_p1_distance_projection_exactness(precision, tol):
+    """test_acceptance.py:34-50: 1000 random pairs (rest 0.05..2, unit-normal endpoints), one
+    projection each -> the pair sits at its rest length.  All 1000 pairs are disjoint edges of one
+    device scene, so one kernel launch projects them all."""
+    rng = np.random.default_rng(100)
+    pos, rest = [], []
+    while len(rest) < 1000:
+        x = rng.normal(0.0, 1.0, (2, 3))
+        r = rng.uniform(0.05, 2.0)
+        if np.linalg.norm(x[0] - x[1]) < 1e-6:
+            continue
+        pos.append(x)
+        rest.append(r)
+    pos = np.concatenate(pos)
+    if precision == "fp32":
+        pos = pos.astype(np.float32).astype(np.float64)       # the fp32 build's inputs, exactly
+    edges = np.arange(2000, dtype=np.int32).reshape(1000, 2)
+    rest = np.asarray(rest)
+    x2 = _one_substep(pos, edges, rest, 1.0, np.zeros((0, 4), np.int32), np.zeros(0), 1.0,
+                      np.float64 if precision == "fp64" else np.float32)
+    err = np.abs(np.linalg.norm(x2[0::2] - x2[1::2], axis=1) - rest) / rest
+    assert err.max() < tol, err.max()
+    report("P1", f"{precision}: 1000 pairs on device, worst relative length error {err.max():.2e}")
+
+
+def _tet_volume(p):
+    return float(np.dot(np.cross(p[1] - p[0], p[2] - p[0]), p[3] - p[0]) / 6.0)
+
+
+@pytest.mark.parametrize("precision,tol", [("fp64", 1e-5), ("fp32", 1e-4)])
+def test_p2_volume_gradient_finite_differences(precision, tol):
+    """test_acceptance.py:53-80: the volume gradient against central finite differences, through
+    the device: a tet projection moves corner i by -(V - V0) / sum|grad|^2 * grad_i (k_v = 1, all
+    inverse masses 1, one constraint per vertex), so the kernel's displacement of 100 random
+    disjoint tets must equal that expression built from the finite-difference gradient."""
+    rng = np.random.default_rng(101)
+    step = 1e-6
+    pts, vols, fds = [], [], []
+    while len(pts) < 100:
+        p = rng.normal(size=(4, 3))
+        if precision == "fp32":
+            p = p.astype(np.float32).astype(np.float64)
+        vol = _tet_volume(p)
+        if abs(vol) < 1e-3:
+            continue
+        fd = np.zeros((4, 3))
+        for i in range(4):
+            for c in range(3):
+                plus, minus = p.copy(), p.copy()
+                plus[i, c] += step
+                minus[i, c] -= step
+                fd[i, c] = (_tet_volume(plus) - _tet_volume(minus)) / (2 * step)
+        pts.append(p)
+        vols.append(vol)
+        fds.append(fd)
+    pos = np.concatenate(pts)
+    tets = np.arange(400, dtype=np.int32).reshape(100, 4)
+    rest_vol = 0.5 * np.asarray(vols)                    # every constraint active: C = V / 2
+    x2 = _one_substep(pos, np.zeros((0, 2), np.int32), np.zeros(0), 1.0, tets, rest_vol, 1.0,
+                      np.float64 if precision == "fp64" else np.float32)
+    worst = 0.0
+    for t in range(100):
+        fd = fds[t]
+        expect = -(vols[t] - rest_vol[t]) / float(np.sum(fd * fd)) * fd
+        got = x2[4 * t:4 * t + 4] - pos[4 * t:4 * t + 4]
+        worst = max(worst, float(np.abs(got - expect).max() / np.abs(expect).max()))
+    assert worst < tol, worst
+    report("P2", f"{precision}: 100 random tets on device, worst relative error vs finite differences {worst:.2e}")
+
+
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+def test_p6_contact_resolution(precision):
+    """test_acceptance.py:152-168: a static tool capsule penetrating the tissue is pushed out to a
+    residual depth < 1e-4 m within 50 steps.  Production step kernel (contact detection + the
+    sequential push-out of collision.py:55-73), constraints and gravity off so only contacts move
+    vertices; the residual is measured by the device detect_contacts plugin entry."""
+    mesh, rest, cfg = build_slab_scene(3, 2, 2, pin="x0", k_s=0.0, k_v=0.0, gravity=np.zeros(3), damping=0.0)
+    sim = Simulation(mesh, rest, cfg, device="cuda:0", precision=precision)
+    ref = O.OracleEnv(O.scene_from_loaded(mesh, rest, cfg), 1)
+    top = float(mesh.positions_rest[:, 1].max())
+    rcm = np.asarray(cfg.rcm, np.float64)
+    ref.axis[:] = [0.0, -1.0, 0.0]
+    ref.jaw[:] = [1.0, 0.0, 0.0]
+    ref.reach[:] = rcm[1] - top + 0.002                  # drag point 2 mm inside the top surface
+    ref.clamp[:] = 20.0                                  # open jaws: no grasp
+    pose = {"axis": ref.axis.copy(), "jaw": ref.jaw.copy(), "reach": ref.reach.copy(), "clamp": ref.clamp.copy()}
+    caps = ref.capsule_rows()[0]
+    faces = mesh.surface_faces
+
+    def residual():
+        x = sim.x[0].cpu().numpy()
+        found = B.detect_contacts(x, faces, caps, 8)
+        return float(found[2].max()) if len(found[0]) else 0.0
+
+    depth0 = residual()
+    assert depth0 > 1e-3                                 # the capsule starts well inside
+    touched = 0
+    for step in range(50):
+        info = sim.step(tool_override=pose)
+        touched += int(info["contacts_per_env"][0])
+        depth = residual()
+        if depth < 1e-4:
+            break
+    assert depth < 1e-4, depth
+    assert touched > 0
+    report("P6", f"{precision}: initial depth {depth0:.2e} m, residual {depth:.2e} m after {step + 1} device steps")
+
+
+@pytest.fixture(scope="module")
+def scenes_p9():
+    from paper_2503_18616_b200.mesh import make_slab_scene
+    with tempfile.TemporaryDirectory() as d:
+        small = make_slab_scene(d, tets=1170, name="p9s")
+        big = make_slab_scene(d, tets=9729, name="p9b")
+        from paper_2503_18616_b200.mesh import load_scene
+        yield load_scene(small), load_scene(big)
+
+
+def test_p9_throughput_scaling(scenes_p9):
+    """test_acceptance.py:203-221 through the reference's own benchmark protocol (cli.run_benchmark,
+    EnvBatch.step with host numpy actions): 8 envs >= 2x the single-env throughput, and the
+    9729-tet slab slower than the 1170-tet one."""
+    from paper_2503_18616_b200.cli import run_benchmark
+    small, big = scenes_p9
+    seeds = [0, 1, 2]
+    rep = run_benchmark("sim", [1, 8], small, steps=600, seeds=seeds, warmup=30)
+    single, batched = rep.rows
+    ratio = batched.mean_sps / single.mean_sps
+    assert ratio >= 2.0, ratio
+    rep_big = run_benchmark("sim", [1], big, steps=120, seeds=seeds, warmup=10)
+    bigrow = rep_big.rows[0]
+    assert bigrow.tets == 9720
+    assert bigrow.mean_sps < single.mean_sps
+    report("P9", f"8 envs {ratio:.2f}x single env ({batched.mean_sps:.0f} vs {single.mean_sps:.0f} steps/s); "
+                 f"{bigrow.tets} tets {bigrow.mean_sps:.0f} < {single.tets} tets {single.mean_sps:.0f}")
