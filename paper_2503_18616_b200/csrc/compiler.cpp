@@ -43,6 +43,29 @@ struct Item {
     int vid[4];        // original vertex ids of the roles
     int chunk;
     int sign = 1;      // fp32 tets: -1 after an odd corner permutation (signed volume flips)
+    int copy[4] = {0, 0, 0, 0};   // pinned corner: which shared-memory copy of the vertex it reads
+    int idle_pos = 0;  // idle lane whose pos[] holds the four (pinned) positions it reads
+};
+
+// Pinned vertices never move, so fp32 fast programs keep several shared-memory copies of them
+// (copy j of the pinned vertex at primary position p sits in bank (p + j * 32 / n_copies) mod 32):
+// a pinned corner of a tet (or a pinned edge neighbour) reads whichever copy keeps its batch
+// conflict-free.  Copy 0 is the primary (written back, divergence-checked); copies 1.. sit after
+// Vown, where the kernel treats them like halo positions (loaded with the state, never written).
+struct PinCopies {
+    int n = 1, Vf_pad = 0, Vown = 0, Np_pad = 0;
+    // copy j sits j * shift() banks from the primary: 9 (not 32 / n) so the bank sets of different
+    // vertices overlap and a pinned corner's load can move between any two banks through chains
+    int shift() const {
+        if (const char *env = std::getenv("TS_PIN_SHIFT")) return std::atoi(env);
+        return n > 1 ? 9 : 0;
+    }
+    bool pinned(int p) const { return p >= Vf_pad && p < Vown; }
+    // storage position of copy j of the vertex whose primary position is p
+    int pos(int p, int j) const {
+        if (j == 0 || !pinned(p)) return p;
+        return Vown + (j - 1) * Np_pad + (p - Vf_pad + j * shift()) % Np_pad;
+    }
 };
 
 inline int roundup(int x, int m) { return (x + m - 1) / m * m; }
@@ -230,7 +253,8 @@ struct ListRef { std::vector<Item> *items; int begin, count; };
 // Deterministic (fixed-seed xorshift).  Slots are assigned afterwards from the
 // final positions, so the per-vertex summation order is untouched.
 void bank_refine(const std::vector<ListRef> &lists, std::vector<int> &o2s, std::vector<int> &s2o, int Vf,
-                 int Vf_pad, int Vown, int bank_mod, bool permute_tets, int refine_iters) {
+                 int Vf_pad, int Vown, int bank_mod, bool permute_tets, int refine_iters,
+                 const PinCopies &pc = PinCopies()) {
     struct Ref { int list, idx; };
     std::vector<Ref> items;                 // global item id -> (list, index)
     std::vector<int> sb_of, list_sb0;
@@ -259,8 +283,10 @@ void bank_refine(const std::vector<ListRef> &lists, std::vector<int> &o2s, std::
         while (mx[q] > 0 && hist[(size_t)q * 33 + mx[q]] == 0) mx[q]--;
     };
     auto bank = [&](int v) { return o2s[v] % bank_mod; };
+    // bank of role r of item x: its vertex's position, or the copy it reads (pinned corners)
+    auto ibank = [&](const Item &x, int r) { return pc.pos(o2s[x.vid[r]], x.copy[r]) % bank_mod; };
     for (int g = 0; g < n; ++g)
-        for (int r = 0; r < item(g).nroles; ++r) add(sb_of[g], r, bank(item(g).vid[r]), +1);
+        for (int r = 0; r < item(g).nroles; ++r) add(sb_of[g], r, ibank(item(g), r), +1);
     // objective: 4 x (extra wavefronts = max bank load - 1) + (items sharing a bank): the
     // second term is a smooth surrogate that lets the search cross the plateaus of the first
     auto sb_cost = [&](int sb) {
@@ -310,9 +336,9 @@ void bank_refine(const std::vector<ListRef> &lists, std::vector<int> &o2s, std::
         if (total < best && it - last_snap > 2000) { best = total; snapshot(); last_snap = it; }
         const double T = T0 * std::pow(T1 / T0, (double)it / iters);
         touched.clear();
-        const int kind = (int)(next() % 10);
+        const int kind = (int)(next() % (pc.n > 1 ? 12 : 10));
         // --- propose ---------------------------------------------------------
-        int g1 = -1, g2 = -1, u = -1, v = -1, perm = -1;
+        int g1 = -1, g2 = -1, u = -1, v = -1, perm = -1, rc = -1, old_copy = 0;
         // focus: most proposals start from an item of a sub-batch that still has a conflict
         auto pick = [&]() {
             int g = (int)(next() % n);
@@ -354,6 +380,15 @@ void bank_refine(const std::vector<ListRef> &lists, std::vector<int> &o2s, std::
             if (v < 0 || v == u || bank(u) == bank(v)) continue;
             for (auto &e : inc[u]) collect(sb_of[e.first]);
             for (auto &e : inc[v]) collect(sb_of[e.first]);
+        } else if (kind >= 10) {                          // another copy for a pinned corner
+            g1 = pick();
+            Item &x = item(g1);
+            if (x.nroles == 0) continue;
+            const int r = (int)(next() % x.nroles);
+            if (!pc.pinned(o2s[x.vid[r]])) continue;
+            rc = r;
+            old_copy = x.copy[r];
+            collect(sb_of[g1]);
         } else {                                          // role permutation of one item
             g1 = (int)(next() % n);
             Item &x = item(g1);
@@ -365,26 +400,33 @@ void bank_refine(const std::vector<ListRef> &lists, std::vector<int> &o2s, std::
         long before = 0;
         for (int sb : touched) before += sb_cost(sb);
         // --- apply (as a reversible function) -----------------------------------
-        auto remove_item = [&](int g) { Item &x = item(g); for (int r = 0; r < x.nroles; ++r) add(sb_of[g], r, bank(x.vid[r]), -1); };
-        auto insert_item = [&](int g) { Item &x = item(g); for (int r = 0; r < x.nroles; ++r) add(sb_of[g], r, bank(x.vid[r]), +1); };
+        auto remove_item = [&](int g) { Item &x = item(g); for (int r = 0; r < x.nroles; ++r) add(sb_of[g], r, ibank(x, r), -1); };
+        auto insert_item = [&](int g) { Item &x = item(g); for (int r = 0; r < x.nroles; ++r) add(sb_of[g], r, ibank(x, r), +1); };
         auto permute = [&](Item &x, int p) {
             // edges: (a b) -> (b a); tets: the three double transpositions (orientation kept)
-            if (p == 0) std::swap(x.vid[0], x.vid[1]);
+            if (p == 0) { std::swap(x.vid[0], x.vid[1]); std::swap(x.copy[0], x.copy[1]); }
             else {
                 // tets (fp32 build): one transposition of two corners; the signed volume flips, so
                 // the constraint is rewritten with -V0 (C' = -C, grad C' = -grad C: same correction)
                 static const int tr[6][2] = {{0, 1}, {0, 2}, {0, 3}, {1, 2}, {1, 3}, {2, 3}};
                 std::swap(x.vid[tr[p - 1][0]], x.vid[tr[p - 1][1]]);
+                std::swap(x.copy[tr[p - 1][0]], x.copy[tr[p - 1][1]]);
                 x.sign = -x.sign;
             }
         };
         auto swap_vertices = [&]() {
-            for (auto &e : inc[u]) add(sb_of[e.first], e.second, bank(u), -1);
-            for (auto &e : inc[v]) add(sb_of[e.first], e.second, bank(v), -1);
+            for (auto &e : inc[u]) add(sb_of[e.first], e.second, ibank(item(e.first), e.second), -1);
+            for (auto &e : inc[v]) add(sb_of[e.first], e.second, ibank(item(e.first), e.second), -1);
             std::swap(o2s[u], o2s[v]);
             s2o[o2s[u]] = u; s2o[o2s[v]] = v;
-            for (auto &e : inc[u]) add(sb_of[e.first], e.second, bank(u), +1);
-            for (auto &e : inc[v]) add(sb_of[e.first], e.second, bank(v), +1);
+            for (auto &e : inc[u]) add(sb_of[e.first], e.second, ibank(item(e.first), e.second), +1);
+            for (auto &e : inc[v]) add(sb_of[e.first], e.second, ibank(item(e.first), e.second), +1);
+        };
+        auto recopy = [&](int c) {
+            Item &x = item(g1);
+            remove_item(g1);
+            x.copy[rc] = c;
+            insert_item(g1);
         };
         auto swap_items = [&]() {
             remove_item(g1); remove_item(g2);
@@ -416,6 +458,7 @@ void bank_refine(const std::vector<ListRef> &lists, std::vector<int> &o2s, std::
         };
         if (g2 >= 0) { swap_items(); fix_inc_after_swap(); }
         else if (u >= 0) swap_vertices();
+        else if (rc >= 0) recopy((old_copy + 1 + (int)(next() % (pc.n - 1))) % pc.n);
         else permute_item(perm);
         long after = 0;
         for (int sb : touched) after += sb_cost(sb);
@@ -427,6 +470,7 @@ void bank_refine(const std::vector<ListRef> &lists, std::vector<int> &o2s, std::
         // --- revert ----------------------------------------------------------------
         if (g2 >= 0) { swap_items(); fix_inc_after_swap(); }
         else if (u >= 0) swap_vertices();
+        else if (rc >= 0) recopy(old_copy);
         else {
             // inverse permutations: every move above is an involution
             permute_item(perm);
@@ -550,6 +594,278 @@ bool edge_coloring_schedule(std::vector<Item> &list, const std::vector<int> &o2s
 template <typename Real>
 struct Real4T { Real x, y, z, w; };
 
+uint64_t xorshift(uint64_t &s) { s ^= s << 13; s ^= s >> 7; s ^= s << 17; return s; }
+double unit(uint64_t &s) { return (double)(xorshift(s) >> 11) * (1.0 / 9007199254740992.0); }
+
+// ---- fp32 gather programs: lanes for the owner edge gather ------------------------------------
+// In round k of the owner gather the 32 lanes of warp w read their k-th neighbours; the round is
+// conflict-free only if those sit in distinct banks, so the rounds a warp needs are at least the
+// largest number of its neighbour reads that fall in one bank (its "bank load").  Free vertex
+// banks are their lanes; lanes inside a warp group are free to permute (the group keeps its
+// vertices, so phase-2 balance is unchanged).  Simulated annealing over lane swaps minimises, per
+// warp, the bank load above the warp's longest list (the rounds it runs anyway), with a quadratic
+// term that spreads the rest; pinned neighbours are left out (they read whichever copy fits).
+// The tet corners' per-bank totals stay under the tet batches' capacity (penalty).
+void balance_lanes(const std::vector<std::vector<int>> &nbrs, const std::vector<int> &tetval, std::vector<int> &o2s,
+                   std::vector<int> &s2o, int Vf, int tet_cap_per_bank) {
+    const int G = (Vf + 31) / 32;
+    std::vector<int> kmax(G, 0);
+    for (int p = 0; p < Vf; ++p) kmax[p / 32] = std::max(kmax[p / 32], (int)nbrs[s2o[p]].size());
+    // rev[u]: free vertices that read u (u's bank lands in their warps' loads)
+    const int V = (int)o2s.size();
+    std::vector<std::vector<int>> rev(V);
+    for (int p = 0; p < Vf; ++p)
+        for (int u : nbrs[s2o[p]]) if (o2s[u] >= 0 && o2s[u] < Vf) rev[u].push_back(s2o[p]);
+    std::vector<int> L((size_t)G * 32, 0), T(32, 0);
+    auto warp = [&](int v) { return o2s[v] / 32; };
+    auto bank = [&](int v) { return o2s[v] % 32; };
+    for (int p = 0; p < Vf; ++p) {
+        const int v = s2o[p];
+        for (int u : nbrs[v]) if (o2s[u] >= 0 && o2s[u] < Vf) L[(size_t)warp(v) * 32 + bank(u)]++;
+        T[p % 32] += tetval[v];
+    }
+    auto lcost = [&](int w, int l) { const int e = std::max(0, l - kmax[w]); return 64L * e + (long)l * l; };
+    auto tcost = [&](int t) { return 256L * std::max(0, t - tet_cap_per_bank); };
+    uint64_t rng = 0x9E3779B97F4A7C15ull;
+    const long iters = std::min<long>(3000000L, 4000L * Vf);
+    const double T0 = 8.0, T1 = 0.05;
+    std::vector<std::pair<size_t, int>> delta;   // (L index, change)
+    auto report = [&](const char *when) {
+        if (!std::getenv("TS_DEBUG_REFINE")) return;
+        for (int w = 0; w < G; ++w) {
+            int mx = 0;
+            for (int b = 0; b < 32; ++b) mx = std::max(mx, L[(size_t)w * 32 + b]);
+            std::fprintf(stderr, "%s warp %d kmax %d free-neighbour bank load %d\n", when, w, kmax[w], mx);
+        }
+        int tm = 0; for (int b = 0; b < 32; ++b) tm = std::max(tm, T[b]);
+        std::fprintf(stderr, "%s tet bank max %d (cap %d)\n", when, tm, tet_cap_per_bank);
+    };
+    report("before");
+    for (long it = 0; it < iters; ++it) {
+        const int pa = (int)(xorshift(rng) % Vf);
+        const int g = pa / 32, hi = std::min(Vf, 32 * g + 32);
+        const int pb = 32 * g + (int)(xorshift(rng) % (hi - 32 * g));
+        if (pa == pb) continue;
+        const int a = s2o[pa], b = s2o[pb];
+        const int ba = pa % 32, bb = pb % 32;
+        delta.clear();
+        for (int v : rev[a]) { delta.push_back({(size_t)warp(v) * 32 + ba, -1}); delta.push_back({(size_t)warp(v) * 32 + bb, +1}); }
+        for (int v : rev[b]) { delta.push_back({(size_t)warp(v) * 32 + bb, -1}); delta.push_back({(size_t)warp(v) * 32 + ba, +1}); }
+        long before = tcost(T[ba]) + tcost(T[bb]), after;
+        std::vector<size_t> cells;   // costs are evaluated on the touched cells
+
+        for (auto &d : delta) cells.push_back(d.first);
+        std::sort(cells.begin(), cells.end());
+        cells.erase(std::unique(cells.begin(), cells.end()), cells.end());
+        for (size_t c : cells) before += lcost((int)(c / 32), L[c]);
+        for (auto &d : delta) L[d.first] += d.second;
+        T[ba] += tetval[b] - tetval[a]; T[bb] += tetval[a] - tetval[b];
+        after = tcost(T[ba]) + tcost(T[bb]);
+        for (size_t c : cells) after += lcost((int)(c / 32), L[c]);
+        const double temp = T0 * std::pow(T1 / T0, (double)it / iters);
+        if (after <= before || unit(rng) < std::exp(-(double)(after - before) / temp)) {
+            std::swap(o2s[a], o2s[b]);
+            s2o[pa] = b; s2o[pb] = a;
+        } else {
+            for (auto &d : delta) L[d.first] -= d.second;
+            T[ba] -= tetval[b] - tetval[a]; T[bb] -= tetval[a] - tetval[b];
+        }
+    }
+    report("after");
+}
+
+// ---- fp32 gather programs: conflict-free tet batches ------------------------------------------
+// A batch of 32 tets is conflict-free when, for each role, its 32 corners sit in distinct banks.
+// With free corner order (fp32: any permutation, the rest volume's sign follows the parity) that
+// holds iff every bank carries at most 4 of the batch's 128 corners: the batch is then a bipartite
+// multigraph (tets x banks) of maximum degree 4, which Koenig's theorem colours with 4 colours =
+// roles.  So: (1) simulated annealing packs the tets into batches under a per-bank capacity of 4
+// (moves: swap two tets, move a tet into a batch's spare lane, re-pick the copy a pinned corner
+// reads); (2) each batch's roles come from an exact bipartite edge colouring; (3) spare lanes get
+// idle items whose four role positions are pinned positions on banks the batch leaves unused.
+// Returns the residual extra wavefronts per pass (0 when every batch fits).
+int pack_tet_batches(std::vector<Item> &items, const std::vector<int> &o2s, const std::vector<int> &s2o,
+                     const PinCopies &pc, int Vstore) {
+    const int n = (int)items.size();
+    if (n == 0) return 0;
+    int extra_batches = 0;
+    if (const char *env = std::getenv("TS_TET_EXTRA_BATCHES")) extra_batches = std::atoi(env);
+    const int NB = (n + 31) / 32 + extra_batches;
+    auto tok_bank = [&](const Item &x, int r) { return pc.pos(o2s[x.vid[r]], x.copy[r]) % 32; };
+    std::vector<int> batch(n), size(NB, 0), cnt((size_t)NB * 32, 0);
+    std::vector<std::vector<int>> members(NB);
+    // greedy start: each tet into the batch (with room) where it adds the least excess
+    for (int t = 0; t < n; ++t) {
+        int best = -1, bexc = 1 << 30;
+        for (int j = 0; j < NB; ++j) {
+            if (size[j] >= 32) continue;
+            int exc = 0;
+            for (int r = 0; r < 4; ++r) exc += cnt[(size_t)j * 32 + tok_bank(items[t], r)] >= 4;
+            if (exc < bexc) { bexc = exc; best = j; if (!exc) break; }
+        }
+        batch[t] = best; size[best]++;
+        for (int r = 0; r < 4; ++r) cnt[(size_t)best * 32 + tok_bank(items[t], r)]++;
+    }
+    auto cell = [&](int j, int b) -> int & { return cnt[(size_t)j * 32 + b]; };
+    long total = 0;
+    for (int j = 0; j < NB; ++j) for (int b = 0; b < 32; ++b) total += std::max(0, cell(j, b) - 4);
+    std::vector<std::vector<int>> pinned_roles(n);
+    for (int t = 0; t < n; ++t)
+        for (int r = 0; r < 4; ++r) if (pc.pinned(o2s[items[t].vid[r]])) pinned_roles[t].push_back(r);
+    uint64_t rng = 0x2545F4914F6CDD1Dull;
+    const long iters = std::min<long>(30000000L, 10000L * n);
+    const double T0 = 3.0, T1 = 0.05;
+    auto exc = [&](int v) { return std::max(0, v - 4); };
+    // objective per (batch, bank) cell: the excess over 4 (extra wavefronts) plus a quadratic term
+    // that keeps the search moving on the plateaus of the excess
+    auto cc = [&](int v) { return 16L * exc(v) + (long)v * v; };
+    long obj = 0;
+    for (int j = 0; j < NB; ++j) for (int b = 0; b < 32; ++b) obj += cc(cell(j, b));
+    const long total0 = total;
+    long n_acc = 0, n_it = 0;
+    auto bad_item = [&](int t) {
+        for (int r = 0; r < 4; ++r) if (cell(batch[t], tok_bank(items[t], r)) > 4) return true;
+        return false;
+    };
+    for (long it = 0; it < iters && total > 0; ++it) {
+        const double temp = T0 * std::pow(T1 / T0, (double)it / iters);
+        ++n_it;
+        const int kind = (int)(xorshift(rng) % 8);
+        int t = (int)(xorshift(rng) % n);
+        for (int tries = 0; tries < 16 && !bad_item(t); ++tries) t = (int)(xorshift(rng) % n);   // focus
+        long dobj = 0, dexc = 0;
+        auto bump = [&](int j, int b, int sgn) {
+            int &c = cell(j, b);
+            dobj -= cc(c); dexc -= exc(c);
+            c += sgn;
+            dobj += cc(c); dexc += exc(c);
+        };
+        auto shift = [&](int x, int from, int to) {
+            for (int r = 0; r < 4; ++r) { const int b = tok_bank(items[x], r); bump(from, b, -1); bump(to, b, +1); }
+        };
+        if (kind < 5) {                                   // swap two tets between batches / move to a spare lane
+            const int u = (int)(xorshift(rng) % n);
+            const int ja = batch[t], jb = batch[u];
+            if (ja == jb) continue;
+            const bool move = kind == 4 && size[jb] < 32;
+            shift(t, ja, jb);
+            if (!move) shift(u, jb, ja);
+            if (dobj <= 0 || unit(rng) < std::exp(-(double)dobj / temp)) {
+                total += dexc; obj += dobj; ++n_acc;
+                batch[t] = jb;
+                if (move) { size[ja]--; size[jb]++; }
+                else batch[u] = ja;
+            } else {
+                if (!move) shift(u, ja, jb);
+                shift(t, jb, ja);
+            }
+        } else {                                          // re-pick a pinned corner's copy
+            if (pc.n < 2 || pinned_roles[t].empty()) continue;
+            const int r = pinned_roles[t][xorshift(rng) % pinned_roles[t].size()];
+            const int j = batch[t];
+            const int c0 = items[t].copy[r];
+            const int b0 = tok_bank(items[t], r);
+            items[t].copy[r] = (c0 + 1 + (int)(xorshift(rng) % (pc.n - 1))) % pc.n;
+            const int b1 = tok_bank(items[t], r);
+            bump(j, b0, -1); bump(j, b1, +1);
+            if (dobj <= 0 || unit(rng) < std::exp(-(double)dobj / temp)) {
+                total += dexc; obj += dobj;
+            } else {
+                bump(j, b1, -1); bump(j, b0, +1);
+                items[t].copy[r] = c0;
+            }
+        }
+    }
+    if (std::getenv("TS_DEBUG_REFINE")) {
+        long chk = 0;
+        for (int j = 0; j < NB; ++j) for (int b = 0; b < 32; ++b) chk += std::max(0, cell(j, b) - 4);
+        std::fprintf(stderr, "pack: %d tets, %d batches, excess %ld -> %ld (check %ld), %ld iterations, %ld swaps accepted\n",
+                     n, NB, total0, total, chk, n_it, n_acc);
+    }
+    // pinned storage positions by bank (for the idle lanes)
+    std::vector<int> pin_by_bank(32, -1);
+    for (int p = pc.Vf_pad; p < Vstore; ++p)
+        if (s2o[p] >= 0 && pin_by_bank[p % 32] < 0) pin_by_bank[p % 32] = p;
+    // per batch: roles by bipartite edge colouring (tets x banks, 4 colours)
+    std::vector<Item> out;
+    out.reserve((size_t)NB * 32);
+    for (int j = 0; j < NB; ++j) members[j].clear();
+    for (int t = 0; t < n; ++t) members[batch[t]].push_back(t);
+    int residual = 0;
+    for (int j = 0; j < NB; ++j) {
+        const std::vector<int> &mb = members[j];
+        const int m = (int)mb.size();
+        // colour[i][k]: role of corner k of member i; at_t[i][c] / at_b[b][c]: corner holding colour c
+        const int NC = std::max(4, [&] { int mx = 0; for (int b = 0; b < 32; ++b) mx = std::max(mx, cell(j, b)); return mx; }());
+        std::vector<int> col((size_t)m * 4, -1), at_t((size_t)m * NC, -1), at_b((size_t)32 * NC, -1);
+        auto bk = [&](int i, int k) { return tok_bank(items[mb[i]], k); };
+        for (int i = 0; i < m; ++i)
+            for (int k = 0; k < 4; ++k) {
+                const int b = bk(i, k);
+                int ca = -1, cb = -1;
+                for (int c = 0; c < NC && ca < 0; ++c) if (at_t[(size_t)i * NC + c] < 0) ca = c;
+                for (int c = 0; c < NC && cb < 0; ++c) if (at_b[(size_t)b * NC + c] < 0) cb = c;
+                if (at_b[(size_t)b * NC + ca] >= 0) {
+                    // flip the (ca, cb) alternating path that starts at bank b
+                    std::vector<int> path;   // corners (i * 4 + k) along the path
+                    int node = b, side = 1, c_want = ca;
+                    while (true) {
+                        const int e = side ? at_b[(size_t)node * NC + c_want] : at_t[(size_t)node * NC + c_want];
+                        if (e < 0) break;
+                        path.push_back(e);
+                        node = side ? e / 4 : bk(e / 4, e % 4);
+                        side ^= 1;
+                        c_want = c_want == ca ? cb : ca;
+                    }
+                    for (int e : path) {   // clear, then recolour swapped
+                        at_t[(size_t)(e / 4) * NC + col[e]] = -1;
+                        at_b[(size_t)bk(e / 4, e % 4) * NC + col[e]] = -1;
+                    }
+                    for (int e : path) {
+                        col[e] = col[e] == ca ? cb : ca;
+                        at_t[(size_t)(e / 4) * NC + col[e]] = e;
+                        at_b[(size_t)bk(e / 4, e % 4) * NC + col[e]] = e;
+                    }
+                }
+                col[(size_t)i * 4 + k] = ca;
+                at_t[(size_t)i * NC + ca] = i * 4 + k;
+                at_b[(size_t)b * NC + ca] = i * 4 + k;
+            }
+        // members: corners with colour >= 4 (over-full banks only) go to the free role of their tet
+        std::vector<std::vector<char>> used(4, std::vector<char>(32, 0));
+        for (int i = 0; i < m; ++i) {
+            Item x = items[mb[i]];
+            int role_of[4], taken = 0;
+            for (int k = 0; k < 4; ++k) { role_of[k] = col[(size_t)i * 4 + k] < 4 ? col[(size_t)i * 4 + k] : -1; if (role_of[k] >= 0) taken |= 1 << role_of[k]; }
+            for (int k = 0; k < 4; ++k)
+                if (role_of[k] < 0) { int r = 0; while (taken >> r & 1) ++r; role_of[k] = r; taken |= 1 << r; }
+            Item y = x;
+            int perm[4];
+            for (int k = 0; k < 4; ++k) { y.vid[role_of[k]] = x.vid[k]; y.copy[role_of[k]] = x.copy[k]; perm[k] = role_of[k]; }
+            int inv = 0;
+            for (int a = 0; a < 4; ++a) for (int b2 = a + 1; b2 < 4; ++b2) inv += perm[a] > perm[b2];
+            if (inv & 1) y.sign = -y.sign;
+            for (int r = 0; r < 4; ++r) used[r][tok_bank(y, r)]++;
+            out.push_back(y);
+        }
+        for (int r = 0; r < 4; ++r) for (int b = 0; b < 32; ++b) residual += std::max(0, (int)used[r][b] - 1);
+        // idle lanes: one position per role on a bank that role leaves unused (all idle lanes of the
+        // batch read the same four addresses: a broadcast)
+        if (m < 32) {
+            Item dmy{};
+            dmy.kind = TS_CHUNK_TET; dmy.index = -1; dmy.nroles = 0; dmy.idle_pos = 1;
+            for (int r = 0; r < 4; ++r) {
+                int p = pc.Vf_pad;
+                for (int b = 0; b < 32; ++b) if (!used[r][b] && pin_by_bank[b] >= 0) { p = pin_by_bank[b]; break; }
+                dmy.pos[r] = p;
+            }
+            for (int i = m; i < 32; ++i) out.push_back(dmy);
+        }
+    }
+    items.swap(out);
+    return residual;
+}
+
 }  // namespace
 
 int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector<uint8_t> &blob,
@@ -663,7 +979,16 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
     const int Vf = (int)free_v.size();
     const int Vf_pad = roundup(Vf, 32);
     const int Vown = Vf_pad + roundup((int)pinned_v.size(), 32);
-    int Vstore = Vown + roundup((int)halo_v.size(), 32);
+    // pinned copies (PinCopies): fp32 single-CTA gather programs with a bank schedule (TS_PIN_COPIES
+    // overrides: 1, 2, 4 or 8)
+    PinCopies pc;
+    pc.Vf_pad = Vf_pad; pc.Vown = Vown; pc.Np_pad = Vown - Vf_pad;
+    if (prec == TS_F32 && !part && eg && o.schedule_banks >= 0 && pc.Np_pad > 0) pc.n = 4;
+    if (const char *env = std::getenv("TS_PIN_COPIES")) {
+        const int c = std::atoi(env);
+        if (c == 1 || ((c == 2 || c == 4 || c == 8) && prec == TS_F32 && !part && pc.Np_pad > 0)) pc.n = c;
+    }
+    int Vstore = Vown + roundup((int)halo_v.size(), 32) + (pc.n - 1) * pc.Np_pad;
     if (part && part->force_Vstore) {
         if (part->force_Vstore < Vstore) { err = "forced Vstore too small"; return TS_ERR_INVALID; }
         Vstore = part->force_Vstore;
@@ -672,6 +997,11 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
     for (int i = 0; i < Vf; ++i) { s2o[i] = free_v[i]; o2s[free_v[i]] = i; }
     for (size_t i = 0; i < pinned_v.size(); ++i) { s2o[Vf_pad + i] = pinned_v[i]; o2s[pinned_v[i]] = Vf_pad + (int)i; }
     for (size_t i = 0; i < halo_v.size(); ++i) { s2o[Vown + i] = halo_v[i]; o2s[halo_v[i]] = Vown + (int)i; }
+    auto place_copies = [&]() {   // s2o of the pinned copies from the primaries' (final) positions
+        for (int p = Vf_pad; p < Vown; ++p)
+            for (int j = 1; j < pc.n; ++j) s2o[pc.pos(p, j)] = s2o[p];
+    };
+    place_copies();
 
     // fp32: one thread per free vertex (3 CTAs/SM fit); fp64 runs 1 CTA/SM (shared memory), so it
     // takes 1.5x the threads to widen phase 1 (measured on B200: 3.81 vs 4.30 ms at 4096 envs)
@@ -806,14 +1136,51 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
         r.region_off = c * G;
         r.val_off = c * Vf_pad;
     }
+    // fp32 gather programs with pinned copies: lanes balanced for the owner edge gather, then tets
+    // packed into conflict-free batches (balance_lanes, pack_tet_batches)
+    const bool packed = sched && o.schedule_banks != 2 && pc.n > 1 && std::getenv("TS_PACK_TETS") == nullptr
+                        ? true : (std::getenv("TS_PACK_TETS") && std::atoi(std::getenv("TS_PACK_TETS")) && pc.n > 1);
+    if (packed) {
+        std::vector<std::vector<int>> nbrs(V);
+        std::vector<int> tetval(V, 0);
+        for (int e = 0; e < E; ++e) {
+            if (!local_edge(e)) continue;
+            const int a = d.edges[2 * e], b = d.edges[2 * e + 1];
+            if (own_free(a)) nbrs[a].push_back(b);
+            if (own_free(b)) nbrs[b].push_back(a);
+        }
+        for (const Item &it : kinds[2]) for (int r = 0; r < 4; ++r) if (is_free(it.vid[r])) tetval[it.vid[r]]++;
+        int nb_tot = 0;
+        for (int c = 0; c < n_chunks; ++c) nb_tot = std::max(nb_tot, (chunk_rec[c].tet_count + 31) / 32);
+        balance_lanes(nbrs, tetval, o2s, s2o, Vf, 4 * nb_tot - 8);
+        place_copies();
+        std::vector<Item> tets_out;
+        int resid = 0;
+        for (int c = 0; c < n_chunks; ++c) {
+            std::vector<Item> part;
+            for (int i = 0; i < chunk_rec[c].tet_count; ++i) {
+                const Item &it = all_items[2][chunk_rec[c].tet_begin + i];
+                if (it.index >= 0) { part.push_back(it); part.back().sign = 1; for (int r = 0; r < 4; ++r) part.back().copy[r] = 0; }
+            }
+            std::sort(part.begin(), part.end(), [](const Item &x, const Item &y) { return x.index < y.index; });
+            for (Item &it : part) for (int r = 0; r < 4; ++r) it.vid[r] = d.tets[4 * it.index + r];   // reference corner order
+            resid += pack_tet_batches(part, o2s, s2o, pc, Vstore);
+            chunk_rec[c].tet_begin = (int)tets_out.size();
+            chunk_rec[c].tet_count = (int)part.size();
+            tets_out.insert(tets_out.end(), part.begin(), part.end());
+        }
+        all_items[2].swap(tets_out);
+        if (std::getenv("TS_DEBUG_REFINE")) std::fprintf(stderr, "pack_tet_batches: residual %d\n", resid);
+    }
     // joint refinement: item order, vertex lanes inside each warp, role order (see bank_refine)
-    if (sched && o.schedule_banks != 2) {
+    if (sched && o.schedule_banks != 2 && !packed) {
         std::vector<ListRef> lists;
         for (int c = 0; c < n_chunks; ++c) {
             if (chunk_rec[c].edge_count) lists.push_back({&all_items[0], chunk_rec[c].edge_begin, chunk_rec[c].edge_count});
             if (chunk_rec[c].tet_count) lists.push_back({&all_items[2], chunk_rec[c].tet_begin, chunk_rec[c].tet_count});
         }
-        bank_refine(lists, o2s, s2o, Vf, Vf_pad, Vown, bank_mod, /*permute_tets=*/R == 4, o.refine_iters);
+        bank_refine(lists, o2s, s2o, Vf, Vf_pad, Vown, bank_mod, /*permute_tets=*/R == 4, o.refine_iters, pc);
+        place_copies();
         // edges: exact conflict-free batches by bipartite edge colouring (with the final positions)
         std::vector<Item> edges_out;
         for (int c = 0; c < n_chunks; ++c) {
@@ -833,10 +1200,10 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
         }
         all_items[0].swap(edges_out);
     }
-    // final positions of every role
+    // final positions of every role (pinned corners: the copy they read)
     for (int k = 0; k < 3; ++k)
         for (Item &it : all_items[k])
-            for (int r = 0; r < it.nroles; ++r) it.pos[r] = o2s[it.vid[r]];
+            for (int r = 0; r < it.nroles; ++r) it.pos[r] = pc.pos(o2s[it.vid[r]], it.copy[r]);
     int total_conf = 0;
     for (int c = 0; c < n_chunks; ++c) {
         TsChunk &r = chunk_rec[c];
@@ -1019,8 +1386,9 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
         for (int i = 0; i < nT; ++i) {
             // an idle lane (dummy item) reads the corner "Vf_pad" -- never a free vertex, so even if it
             // is executed it touches no degenerate counter; its slot fields are all absent
-            const bool idle = all_items[2][i].index < 0 && boff;
-            auto po = [&](int k) { return idle ? scale_b * Vf_pad : scale_b * tet_idx[4 * i + k]; };
+            const Item &ti = all_items[2][i];
+            const bool idle = ti.index < 0 && boff;
+            auto po = [&](int k) { return idle ? scale_b * (ti.idle_pos ? ti.pos[k] : Vf_pad) : scale_b * tet_idx[4 * i + k]; };
             tet_c[4 * i + 0] = pk(po(0), po(1));
             tet_c[4 * i + 1] = pk(po(2), po(3));
             if (!rv_tab.empty()) {   // index bits 2k, 2k+1 in bits 14-15 of 16-bit field k
@@ -1075,26 +1443,119 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
         // summation order).  In round k the 32 lanes of a warp read their k-th neighbours: permute
         // each lane's list so the neighbours of one round sit in distinct banks as far as possible
         // (deterministic local search, sum over rounds of the largest bank multiplicity)
-        if (R == 4 && o.schedule_banks >= 0) {
+        // a pinned neighbour may be read from any of its copies (PinCopies): a second move kind
+        std::vector<std::vector<int>> ecopy(Vf_pad);
+        for (int p = 0; p < Vf_pad; ++p) ecopy[p].assign(lists[p].size(), 0);
+        auto other = [&](int p, int e) {
+            const int a = d.edges[2 * e], b = d.edges[2 * e + 1];
+            return o2s[a == s2o[p] ? b : a];
+        };
+        auto nbr_pos = [&](int p, int k) { return pc.pos(other(p, lists[p][k]), ecopy[p][k]); };
+        if (packed && einc_bytes == 4) {
+            // Conflict-free rounds by bipartite edge colouring (lanes x banks): a pinned neighbour
+            // reads the copy on the least-loaded bank, then Koenig's theorem colours the warp's reads
+            // with K colours = rounds, K = max(longest list, largest bank load) -- no round has two
+            // reads on one bank.  A lane's gaps become null records (offset 0xffff): the kernel
+            // loads nothing for them and the degenerate guard zeroes the term (static_cnt adds the
+            // nulls back, like the count of a coincident edge).
+            for (int g = 0; g < G; ++g) {
+                const int p0 = 32 * g, p1 = std::min(Vf, 32 * g + 32);
+                if (p1 <= p0) continue;
+                struct Tok { int p, e, copy, bank; };
+                std::vector<Tok> toks;
+                std::vector<int> deg(32, 0), lane_deg(32, 0), pinned_tok;
+                for (int p = p0; p < p1; ++p)
+                    for (int e : lists[p]) {
+                        const int q = other(p, e);
+                        lane_deg[p % 32]++;
+                        if (pc.pinned(q)) { pinned_tok.push_back((int)toks.size()); toks.push_back({p, e, 0, -1}); }
+                        else { toks.push_back({p, e, 0, q % 32}); deg[q % 32]++; }
+                    }
+                for (int ti : pinned_tok) {   // least-loaded copy
+                    Tok &t = toks[ti];
+                    const int q = other(t.p, t.e);
+                    int bc = 0, bb = pc.pos(q, 0) % 32;
+                    for (int j = 1; j < pc.n; ++j) {
+                        const int b = pc.pos(q, j) % 32;
+                        if (deg[b] < deg[bb]) { bb = b; bc = j; }
+                    }
+                    t.copy = bc; t.bank = bb; deg[bb]++;
+                }
+                const int NC = std::max(*std::max_element(deg.begin(), deg.end()),
+                                        *std::max_element(lane_deg.begin(), lane_deg.end()));
+                if (NC == 0) continue;
+                std::vector<int> col(toks.size(), -1), at_l((size_t)32 * NC, -1), at_b((size_t)32 * NC, -1);
+                for (int ti = 0; ti < (int)toks.size(); ++ti) {
+                    const int l = toks[ti].p % 32, b = toks[ti].bank;
+                    int ca = -1, cb = -1;
+                    for (int c = 0; c < NC && ca < 0; ++c) if (at_l[(size_t)l * NC + c] < 0) ca = c;
+                    for (int c = 0; c < NC && cb < 0; ++c) if (at_b[(size_t)b * NC + c] < 0) cb = c;
+                    if (at_b[(size_t)b * NC + ca] >= 0) {   // flip the (ca, cb) path from bank b
+                        std::vector<int> path;
+                        int node = b, side = 1, cw = ca;
+                        while (true) {
+                            const int e = side ? at_b[(size_t)node * NC + cw] : at_l[(size_t)node * NC + cw];
+                            if (e < 0) break;
+                            path.push_back(e);
+                            node = side ? toks[e].p % 32 : toks[e].bank;
+                            side ^= 1;
+                            cw = cw == ca ? cb : ca;
+                        }
+                        for (int e : path) { at_l[(size_t)(toks[e].p % 32) * NC + col[e]] = -1; at_b[(size_t)toks[e].bank * NC + col[e]] = -1; }
+                        for (int e : path) {
+                            col[e] = col[e] == ca ? cb : ca;
+                            at_l[(size_t)(toks[e].p % 32) * NC + col[e]] = e;
+                            at_b[(size_t)toks[e].bank * NC + col[e]] = e;
+                        }
+                    }
+                    col[ti] = ca;
+                    at_l[(size_t)l * NC + ca] = ti;
+                    at_b[(size_t)b * NC + ca] = ti;
+                }
+                // rounds -> lists: up to the lane's last coloured round, gaps as nulls (-1)
+                for (int p = p0; p < p1; ++p) {
+                    int last = -1;
+                    for (int c = 0; c < NC; ++c) if (at_l[(size_t)(p % 32) * NC + c] >= 0) last = c;
+                    std::vector<int> nl(last + 1, -1), nc(last + 1, 0);
+                    for (int c = 0; c <= last; ++c) {
+                        const int ti = at_l[(size_t)(p % 32) * NC + c];
+                        if (ti >= 0) { nl[c] = toks[ti].e; nc[c] = toks[ti].copy; }
+                    }
+                    lists[p] = nl;
+                    ecopy[p] = nc;
+                }
+            }
+        } else if (R == 4 && o.schedule_banks >= 0) {
             uint64_t rs = 0x2545F4914F6CDD1Dull;
             auto rnd = [&]() { rs ^= rs << 13; rs ^= rs >> 7; rs ^= rs << 17; return rs; };
-            auto other = [&](int p, int e) {
-                const int a = d.edges[2 * e], b = d.edges[2 * e + 1];
-                return o2s[a == s2o[p] ? b : a];
-            };
             for (int g = 0; g < G; ++g) {
                 int kmax = 0;
                 for (int p = 32 * g; p < 32 * g + 32; ++p) kmax = std::max(kmax, (int)lists[p].size());
-                if (kmax < 2) continue;
+                if (kmax < 1) continue;
                 std::vector<int> cnt((size_t)kmax * 32, 0);
-                auto bank = [&](int p, int k) { return other(p, lists[p][k]) % 32; };
+                auto bank = [&](int p, int k) { return nbr_pos(p, k) % 32; };
                 for (int p = 32 * g; p < 32 * g + 32; ++p)
                     for (int k = 0; k < (int)lists[p].size(); ++k) cnt[(size_t)k * 32 + bank(p, k)]++;
                 auto rmax = [&](int k) { int m = 0; for (int b = 0; b < 32; ++b) m = std::max(m, cnt[(size_t)k * 32 + b]); return m; };
-                const long iters = 4000L * kmax;
+                const long iters = 6000L * kmax;
                 for (long it = 0; it < iters; ++it) {
                     const int p = 32 * g + (int)(rnd() % 32);
                     const int n = (int)lists[p].size();
+                    if (n < 1) continue;
+                    if (pc.n > 1 && (rnd() & 1)) {          // another copy of a pinned neighbour
+                        const int k = (int)(rnd() % n);
+                        if (!pc.pinned(other(p, lists[p][k]))) continue;
+                        const int b0 = bank(p, k), c0 = ecopy[p][k];
+                        const int before = rmax(k);
+                        ecopy[p][k] = (c0 + 1 + (int)(rnd() % (pc.n - 1))) % pc.n;
+                        const int b1 = bank(p, k);
+                        cnt[(size_t)k * 32 + b0]--; cnt[(size_t)k * 32 + b1]++;
+                        if (rmax(k) > before) {
+                            cnt[(size_t)k * 32 + b1]--; cnt[(size_t)k * 32 + b0]++;
+                            ecopy[p][k] = c0;
+                        }
+                        continue;
+                    }
                     if (n < 2) continue;
                     const int ka = (int)(rnd() % n), kb = (int)(rnd() % n);
                     const int ba = bank(p, ka), bb = bank(p, kb);
@@ -1102,8 +1563,10 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
                     const int before = rmax(ka) + rmax(kb);
                     cnt[(size_t)ka * 32 + ba]--; cnt[(size_t)kb * 32 + ba]++;
                     cnt[(size_t)kb * 32 + bb]--; cnt[(size_t)ka * 32 + bb]++;
-                    if (rmax(ka) + rmax(kb) <= before) std::swap(lists[p][ka], lists[p][kb]);
-                    else {
+                    if (rmax(ka) + rmax(kb) <= before) {
+                        std::swap(lists[p][ka], lists[p][kb]);
+                        std::swap(ecopy[p][ka], ecopy[p][kb]);
+                    } else {
                         cnt[(size_t)ka * 32 + ba]++; cnt[(size_t)kb * 32 + ba]--;
                         cnt[(size_t)kb * 32 + bb]++; cnt[(size_t)ka * 32 + bb]--;
                     }
@@ -1121,15 +1584,22 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
         for (int p = 0; p < Vf; ++p) {
             const int self = s2o[p];
             evalence[p] = (int)lists[p].size();
-            static_cnt[p] += evalence[p];
-            n_einc += evalence[p];
+            static_cnt[p] += evalence[p];      // null records (packed programs) count as degenerate edges
             for (int k = 0; k < evalence[p]; ++k) {
                 const int e = lists[p][k];
+                if (e < 0) {   // null record (packed 4-byte records only): no load, zero term, counted degenerate
+                    uint8_t *rec = einc.data() + (size_t)(eregion[p / 32] + 32 * k + p % 32) * einc_bytes;
+                    const uint32_t word = 0xffffu;
+                    std::memcpy(rec, &word, 4);
+                    continue;
+                }
+                ++n_einc;
                 const int a = d.edges[2 * e], b = d.edges[2 * e + 1];
                 const int q = a == self ? b : a;
+                const int qpos = nbr_pos(p, k);
                 // bit 31: the neighbour is pinned (w = 0); with uniform free mass that fixes the
                 // weight ratio (compact fp32 records), and halo neighbours of a cluster part are free
-                const int32_t nbr = (boff ? 12 * o2s[q] : o2s[q]) | (is_free(q) ? 0 : (int32_t)0x80000000u);
+                const int32_t nbr = (boff ? 12 * qpos : qpos) | (is_free(q) ? 0 : (int32_t)0x80000000u);
                 uint8_t *rec = einc.data() + (size_t)(eregion[p / 32] + 32 * k + p % 32) * einc_bytes;
                 const double rl = d.rest_length[e];
                 if (einc_bytes == 4) {

@@ -783,9 +783,16 @@ __device__ __forceinline__ void owner_edges(const TsDevProg &P, const Smem<Real>
         for (int k = 0; k < ev; ++k) {
             const unsigned cur = q;
             q = __ldg(rec + 32 * (k + 1));
-            const float *nq = reinterpret_cast<const float *>(pb + (cur & 0xffffu));
+            const unsigned off = cur & 0xffffu;
             const float rl = FAST ? smem_tab(TS_TAB_OFF)[(cur >> 16) & 0x7fffu] : __ldg(P.rltab + ((cur >> 16) & 0x7fffu));
-            const float dx = px - nq[0], dy = py - nq[1], dz = pz - nq[2];
+            // null record (0xffff, a gap of the compiler's conflict-free rounds): no load, dx = 0, so
+            // the degenerate guard zeroes the term and counts it (static_cnt holds the nulls)
+            float qx = px, qy = py, qz = pz;
+            if (off != 0xffffu) {
+                const float *nq = reinterpret_cast<const float *>(pb + off);
+                qx = nq[0]; qy = nq[1]; qz = nq[2];
+            }
+            const float dx = px - qx, dy = py - qy, dz = pz - qz;
             const float d2 = __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, dx * dx));
             const bool degenerate = !(d2 >= 1e-24f);
             const float f = degenerate ? 0.0f : __fmaf_rn(-rl, rsqrt_ftz(d2), 1.0f);

@@ -76,9 +76,12 @@ class Program:
                 self.e_coef = None
                 word = (word & 0xFFFF) | (word & 0x80000000)
             self.e_nbr = (word & 0x7FFFFFFF).astype(np.int32)
+            # null records (offset 0xffff, gaps of the conflict-free rounds): no neighbour, a zero
+            # term counted as degenerate
+            self.e_null = self.e_nbr == 0xFFFF
             if H["boff"]:
-                assert np.all(self.e_nbr % 12 == 0)
-                self.e_nbr //= 12                               # fp32 records hold byte offsets
+                assert np.all((self.e_nbr % 12 == 0) | self.e_null)
+                self.e_nbr = np.where(self.e_null, -1, self.e_nbr // 12)   # fp32 records hold byte offsets
             self.e_nbr_pinned = (word >> 31).astype(bool)       # bit 31: neighbour pinned (w = 0)
             if eb == 4:
                 pass
@@ -93,10 +96,20 @@ class Program:
                 self.e_rest = raw[:, 8:12].copy().view(np.float32)[:, 0].astype(np.float64)
 
     def edge_records(self, p):
-        """(neighbour storage positions, rest lengths) of free position p, in gather order."""
+        """(neighbour storage positions, rest lengths) of free position p, in gather order (null
+        records skipped)."""
         k = np.arange(int(self.evalence[p]))
         r = self.eregion[p // 32] + 32 * k + p % 32
+        if hasattr(self, "e_null"):
+            r = r[~self.e_null[r]]
         return self.e_nbr[r], self.e_rest[r]
+
+    def edge_nulls(self, p):
+        """Null records of free position p (each counts as one degenerate edge)."""
+        if not hasattr(self, "e_null"):
+            return 0
+        k = np.arange(int(self.evalence[p]))
+        return int(self.e_null[self.eregion[p // 32] + 32 * k + p % 32].sum())
 
     def sec(self, name, dtype, count):
         o = int(self.off[SECTIONS.index(name)])
@@ -139,6 +152,7 @@ class PartRun:
             # owner-gathered distance constraints (step_kernel.cuh owner_edges, fp64 form)
             for p in range(Vf):
                 nb, rl = prog.edge_records(p)
+                cnt_adj[p] -= prog.edge_nulls(p)
                 if len(nb) == 0:
                     continue
                 d = xs[p][None, :] - xs[nb]

@@ -98,11 +98,25 @@ def test_slot_structure(reach_scene, gather):
     assert H["edge_gather"] == info["edge_gather"] == int(gather)
     # storage order: free first (sorted by gather cost, descending), then pinned
     assert np.all(w[p.s2o[:Vf]] > 0) and np.all(w[p.s2o[H["Vf_pad"]:][p.s2o[H["Vf_pad"]:] >= 0]] == 0)
-    assert np.array_equal(np.sort(p.s2o[p.s2o >= 0]), np.arange(mesh.vertex_count))
+    own = p.s2o[:H["Vown"]]
+    assert np.array_equal(np.sort(own[own >= 0]), np.arange(mesh.vertex_count))
+    # after Vown (fp32 gather programs): extra shared copies of the pinned vertices only, each pinned
+    # vertex the same number of times, every copy of a vertex in a different bank
+    copies = p.s2o[H["Vown"]:]
+    pinned = np.flatnonzero(w == 0)
+    if gather:
+        assert len(copies) > 0 and np.all(w[copies[copies >= 0]] == 0)
+        reps = np.bincount(copies[copies >= 0], minlength=mesh.vertex_count)[pinned]
+        assert np.all(reps == reps[0]) and reps[0] >= 1
+        for v in pinned:
+            assert len(set(np.flatnonzero(p.s2o == v) % 32)) == reps[0] + 1
+    else:
+        assert np.all(copies < 0)
     # warps own vertices of similar cost: the groups of 32 are the cost-sorted order
     # (lanes inside a group may be permuted by the bank refinement); an owner-gathered edge
     # weighs three slots
-    sc = p.static_cnt[:Vf] + (2 * p.evalence[:Vf] if gather else 0)
+    nulls = np.array([p.edge_nulls(q) for q in range(H["Vf_pad"])]) if gather else np.zeros(H["Vf_pad"], int)
+    sc = p.static_cnt[:Vf] - nulls[:Vf] + (2 * (p.evalence[:Vf] - nulls[:Vf]) if gather else 0)
     ref = np.sort(sc)[::-1]
     for g in range(0, Vf, 32):
         assert sorted(sc[g:g + 32]) == sorted(ref[g:g + 32])
@@ -130,14 +144,16 @@ def test_slot_structure(reach_scene, gather):
             used.append(len(s))
         expected += sum(used)
     n_inc = info["n_edge_incidences"] if gather else 0
-    assert expected == info["n_slots_total"] == p.static_cnt.sum() - n_inc
+    assert expected == info["n_slots_total"] == p.static_cnt.sum() - n_inc - nulls.sum()
     # per-vertex incidence count equals the reference's count of live constraints touching it
     inc = _edge_incidence(mesh, w)
     if gather:
-        assert np.array_equal(p.evalence[:Vf], inc[p.s2o[:Vf]]) and n_inc == inc.sum()
+        assert np.array_equal(p.evalence[:Vf] - nulls[:Vf], inc[p.s2o[:Vf]]) and n_inc == inc.sum()
     for t in mesh.tets:
         inc[t] += w[t] > 0
-    assert np.array_equal(p.static_cnt[:Vf], inc[p.s2o[:Vf]])
+    # static counts: live incidences, plus the null records of the gather rounds (each counted
+    # degenerate every substep, so the applied count is unchanged)
+    assert np.array_equal(p.static_cnt[:Vf] - nulls[:Vf], inc[p.s2o[:Vf]])
 
 
 @pytest.mark.parametrize("precision", ["fp32", "fp64"])
