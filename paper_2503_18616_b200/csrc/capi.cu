@@ -140,7 +140,7 @@ static void decode_part(const uint8_t *host, const uint8_t *b, TsDevProg &P) {
     P.narrow = H->narrow;
     P.fast = H->real_bytes == 4 && H->VPT == 1 && H->n_chunks == 1 && H->grasp_chunk == 0 && H->edge_gather &&
              H->einc_bytes == 4 && H->boff && H->rvdict && H->narrow && H->n_att_items == 0 &&
-             H->n_edge_items == 0 && H->cluster_k == 1 && H->compact && H->n_rltab <= TS_TAB_CAP &&
+             H->n_edge_items == 0 && H->cluster_k == 1 && H->compact && 2 * H->n_rltab <= TS_TAB_CAP &&
              H->n_rvtab <= TS_TAB_CAP;
     P.einc_bytes = H->einc_bytes;
     P.einc = b + H->off[TS_SEC_EINC];
@@ -257,6 +257,7 @@ static int32_t create_handle(const ts_scene_desc *desc, const ts_layout_opts &o,
     } else {
         decode_part(hb, db, h->prog);
         h->smem = ts_smem_bytes(h->prog, R);
+        if (h->prog.fast && ts_smem_window(device) != TS_SMEM_WINDOW) h->prog.fast = 0;   // generic kernel
     }
     // L2 prefetch of the program by the command kernel: small programs only -- a multi-MB cluster
     // program's bulk prefetches keep the command kernel alive longer than they save (52,359-tet
@@ -866,6 +867,29 @@ __global__ void __launch_bounds__(1024) smem_probe_kernel(int iters, float *sink
         idx = (idx + 32) & (n4 - 1);
     }
     if (acc.x + acc.y + acc.z + acc.w == 1.2345f) sink[threadIdx.x] = acc.x;
+}
+
+// The .shared address of the first dynamic shared-memory byte of a non-cluster launch (once per
+// device): the fast step kernel's constant shared addresses assume TS_SMEM_WINDOW.
+static __global__ void smem_window_kernel(uint32_t *out) {
+    extern __shared__ __align__(16) unsigned char raw[];
+    if (threadIdx.x == 0) *out = (uint32_t)__cvta_generic_to_shared(raw);
+}
+
+uint32_t ts_smem_window(int device) {
+    static uint32_t cached[64];
+    static bool have[64];
+    if (device < 0 || device >= 64) return 0;
+    if (have[device]) return cached[device];
+    uint32_t *d = nullptr, v = 0;
+    if (cudaMalloc(&d, sizeof(uint32_t)) == cudaSuccess) {
+        smem_window_kernel<<<1, 32, 1024>>>(d);
+        if (cudaMemcpy(&v, d, sizeof(uint32_t), cudaMemcpyDeviceToHost) != cudaSuccess) v = 0;
+        cudaFree(d);
+    }
+    cached[device] = v;
+    have[device] = true;
+    return v;
 }
 
 extern "C" int32_t ts_smem_probe(int32_t device, int32_t iters, double *gbs_out) {

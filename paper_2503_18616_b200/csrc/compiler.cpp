@@ -630,6 +630,7 @@ void balance_lanes(const std::vector<std::vector<int>> &nbrs, const std::vector<
     const long iters = std::min<long>(3000000L, 4000L * Vf);
     const double T0 = 8.0, T1 = 0.05;
     std::vector<std::pair<size_t, int>> delta;   // (L index, change)
+    std::vector<size_t> cells;                   // touched cells (costs are evaluated on them)
     auto report = [&](const char *when) {
         if (!std::getenv("TS_DEBUG_REFINE")) return;
         for (int w = 0; w < G; ++w) {
@@ -652,7 +653,7 @@ void balance_lanes(const std::vector<std::vector<int>> &nbrs, const std::vector<
         for (int v : rev[a]) { delta.push_back({(size_t)warp(v) * 32 + ba, -1}); delta.push_back({(size_t)warp(v) * 32 + bb, +1}); }
         for (int v : rev[b]) { delta.push_back({(size_t)warp(v) * 32 + bb, -1}); delta.push_back({(size_t)warp(v) * 32 + ba, +1}); }
         long before = tcost(T[ba]) + tcost(T[bb]), after;
-        std::vector<size_t> cells;   // costs are evaluated on the touched cells
+        cells.clear();
 
         for (auto &d : delta) cells.push_back(d.first);
         std::sort(cells.begin(), cells.end());
@@ -713,7 +714,8 @@ int pack_tet_batches(std::vector<Item> &items, const std::vector<int> &o2s, cons
     for (int t = 0; t < n; ++t)
         for (int r = 0; r < 4; ++r) if (pc.pinned(o2s[items[t].vid[r]])) pinned_roles[t].push_back(r);
     uint64_t rng = 0x2545F4914F6CDD1Dull;
-    const long iters = std::min<long>(30000000L, 10000L * n);
+    long iters = std::min<long>(12000000L, 3000L * n);   // reach_1170: ~3.5 M, a few seconds
+    if (const char *env = std::getenv("TS_PACK_ITERS")) iters = std::atol(env);
     const double T0 = 3.0, T1 = 0.05;
     auto exc = [&](int v) { return std::max(0, v - 4); };
     // objective per (batch, bank) cell: the excess over 4 (extra wavefronts) plus a quadratic term
@@ -727,8 +729,10 @@ int pack_tet_batches(std::vector<Item> &items, const std::vector<int> &o2s, cons
         for (int r = 0; r < 4; ++r) if (cell(batch[t], tok_bank(items[t], r)) > 4) return true;
         return false;
     };
+    // annealing passes (the later ones reheated less) until the packing is conflict-free
+    for (int pass = 0; pass < 4 && total > 0; ++pass)
     for (long it = 0; it < iters && total > 0; ++it) {
-        const double temp = T0 * std::pow(T1 / T0, (double)it / iters);
+        const double temp = (T0 / (1 + pass)) * std::pow(T1 / (T0 / (1 + pass)), (double)it / iters);
         ++n_it;
         const int kind = (int)(xorshift(rng) % 8);
         int t = (int)(xorshift(rng) % n);
@@ -1411,8 +1415,11 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
     // bitwise the reference's (-w_a scale) dx for p = a and (w_b scale) dx for p = b, since
     // x_b - x_a = -(x_a - x_b) exactly and the squares / weight sum are symmetric.
     // fp32 byte-offset programs whose rest lengths take few distinct fp32 values (a structured
-    // slab has 2) use 4-byte records: {neighbour offset (16) | rest-length index (15) | pinned (1)}
-    // with the lengths in a small table -- half the L1 footprint of the edge stream
+    // slab has 2) use 4-byte records: {neighbour offset (16) | pair index (16)} with a small table
+    // of (rest length, coefficient) pairs -- coefficient = -k_s w_p / (w_p + w_q), i.e. -k_s / 2,
+    // or -k_s for a pinned neighbour (uniform free mass) -- half the L1 footprint of the edge
+    // stream and one shared load for both operands.  Pair 0 is the null record {0, 0} (a gap of
+    // the conflict-free rounds): its term is exactly zero.
     std::vector<float> rl_tab;
     std::vector<int> rl_idx(E, -1);
     if (eg && boff && 12 * Vstore <= 65535) {
@@ -1428,6 +1435,20 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
         }
     }
     const int einc_bytes = eg ? (!rl_tab.empty() ? 4 : ((R == 4 && compact) ? 8 : 16)) : 0;
+    std::vector<float> pair_tab;                      // RLTAB section of 4-byte programs: {rl, coef} pairs
+    auto pair_index = [&](int e, bool pinned_nbr) {   // 1 + 2 * rest-length index + pinned
+        return 1 + 2 * rl_idx[e] + (pinned_nbr ? 1 : 0);
+    };
+    if (einc_bytes == 4) {
+        pair_tab.assign(2 * (1 + 2 * rl_tab.size()), 0.0f);
+        const float ks_f = (float)d.k_s;
+        for (size_t i = 0; i < rl_tab.size(); ++i)
+            for (int pin = 0; pin < 2; ++pin) {
+                const int k = 1 + 2 * (int)i + pin;
+                pair_tab[2 * k] = rl_tab[i];
+                pair_tab[2 * k + 1] = -(pin ? ks_f : 0.5f * ks_f);
+            }
+    }
     std::vector<int32_t> eregion(eg ? G : 0, 0), evalence(eg ? Vf_pad : 0, 0);
     std::vector<uint8_t> einc;
     int n_einc = 0;
@@ -1581,19 +1602,40 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
             base += 32 * kmax;
         }
         einc.assign(((size_t)base + 32) * einc_bytes, 0);   // + one padding row: unclamped prefetch
+        // null records read a pinned position on a bank their round leaves free (no conflict; a
+        // pinned neighbour is never within 1e-12 of a free vertex, so the null is not degenerate),
+        // or -- when no such position exists -- their own position (dx = 0: degenerate, counted in
+        // static_cnt so the applied count is unchanged)
+        std::vector<int> pin_at_bank(32, -1);
+        for (int q = Vf_pad; q < Vstore; ++q)
+            if (s2o[q] >= 0 && !is_free(s2o[q]) && pin_at_bank[q % 32] < 0) pin_at_bank[q % 32] = q;
+        std::vector<int> null_pos((size_t)G * 64, -2);   // per (warp, round): chosen position (-1: own)
+        auto null_for = [&](int g, int k) {
+            int &np = null_pos[(size_t)g * 64 + std::min(k, 63)];
+            if (np != -2 && k < 64) return np;
+            std::vector<char> used(32, 0);
+            for (int q = 32 * g; q < std::min(Vf, 32 * g + 32); ++q)
+                if (k < (int)lists[q].size() && lists[q][k] >= 0) used[nbr_pos(q, k) % 32] = 1;
+            int pos = -1;
+            for (int b = 0; b < 32 && pos < 0; ++b) if (!used[b] && pin_at_bank[b] >= 0) pos = pin_at_bank[b];
+            if (k < 64) np = pos;
+            return pos;
+        };
         for (int p = 0; p < Vf; ++p) {
             const int self = s2o[p];
             evalence[p] = (int)lists[p].size();
-            static_cnt[p] += evalence[p];      // null records (packed programs) count as degenerate edges
             for (int k = 0; k < evalence[p]; ++k) {
                 const int e = lists[p][k];
-                if (e < 0) {   // null record (packed 4-byte records only): no load, zero term, counted degenerate
+                if (e < 0) {   // null record (4-byte programs): pair 0, a zero term
                     uint8_t *rec = einc.data() + (size_t)(eregion[p / 32] + 32 * k + p % 32) * einc_bytes;
-                    const uint32_t word = 0xffffu;
+                    const int np = null_for(p / 32, k);
+                    const uint32_t word = (uint32_t)(12 * (np >= 0 ? np : p)) & 0xffffu;
+                    if (np < 0) static_cnt[p] += 1;   // own position: counted degenerate every substep
                     std::memcpy(rec, &word, 4);
                     continue;
                 }
                 ++n_einc;
+                static_cnt[p] += 1;
                 const int a = d.edges[2 * e], b = d.edges[2 * e + 1];
                 const int q = a == self ? b : a;
                 const int qpos = nbr_pos(p, k);
@@ -1603,8 +1645,7 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
                 uint8_t *rec = einc.data() + (size_t)(eregion[p / 32] + 32 * k + p % 32) * einc_bytes;
                 const double rl = d.rest_length[e];
                 if (einc_bytes == 4) {
-                    const uint32_t word = (uint32_t)(nbr & 0xffff) | ((uint32_t)rl_idx[e] << 16) |
-                                          ((uint32_t)nbr & 0x80000000u);
+                    const uint32_t word = (uint32_t)(nbr & 0xffff) | ((uint32_t)pair_index(e, !is_free(q)) << 16);
                     std::memcpy(rec, &word, 4);
                     continue;
                 }
@@ -1713,7 +1754,7 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
     sz[TS_SEC_SEND] = 4LL * send.size();
     sz[TS_SEC_FACE_OWN] = 4LL * face_own.size();
     sz[TS_SEC_WSPLIT] = 4LL * wsplit.size();
-    sz[TS_SEC_RLTAB] = 4LL * rl_tab.size();
+    sz[TS_SEC_RLTAB] = 4LL * pair_tab.size();
     sz[TS_SEC_RVTAB] = 4LL * rv_tab.size();
     TsProgHeader hdr{};
     hdr.compact = compact ? 1 : 0;
@@ -1724,7 +1765,7 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
     hdr.Vown = Vown; hdr.cluster_k = part ? part->K : 1; hdr.cluster_rank = part ? part->rank : 0;
     hdr.boff = boff ? 1 : 0;
     hdr.rvdict = rv_tab.empty() ? 0 : 1;
-    hdr.n_rltab = (int)rl_tab.size(); hdr.n_rvtab = (int)rv_tab.size();
+    hdr.n_rltab = (int)pair_tab.size() / 2; hdr.n_rvtab = (int)rv_tab.size();
     hdr.n_chunks = n_chunks; hdr.grasp_chunk = grasp_chunk; hdr.slot_capacity = slot_cap; hdr.n_att = nA;
     hdr.n_edge_items = nE; hdr.n_tet_items = nT; hdr.n_att_items = nA; hdr.bank_conflicts = total_conf;
     hdr.n_slots_total = n_slots_total;
@@ -1759,7 +1800,7 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
     put(blob, hdr.off[TS_SEC_SEND], send);
     put(blob, hdr.off[TS_SEC_FACE_OWN], face_own);
     put(blob, hdr.off[TS_SEC_WSPLIT], wsplit);
-    put(blob, hdr.off[TS_SEC_RLTAB], rl_tab);
+    put(blob, hdr.off[TS_SEC_RLTAB], pair_tab);
     put(blob, hdr.off[TS_SEC_RVTAB], rv_tab);
     auto put_real = [&](int sec, const std::vector<double> &v) {
         if (R == 8) put(blob, hdr.off[sec], v);

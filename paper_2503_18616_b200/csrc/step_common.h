@@ -171,6 +171,12 @@ inline int ts_smem_bytes(const TsDevProg &P, int real_bytes) {
 #define TS_EDGES_MINB 2
 #endif
 // fp32 shape-specialised kernels (step_kernel.cuh): the reach-scene shape, and distance-only programs
+// .shared address of the first byte of dynamic shared memory in a non-cluster launch on sm_100
+// (the fast kernel's constant addressing, step_kernel.cuh lds3c); probed by the library at handle
+// creation (ts_smem_window), which keeps the fast kernel off if the device reports another value
+#define TS_SMEM_WINDOW 0x400u
+uint32_t ts_smem_window(int device);
+
 inline bool ts_use_fast_kernel(const TsDevProg &P, int ablate) {
     return P.fast && P.B <= TS_STEP_MAXT && !(ablate & 256);
 }

@@ -352,6 +352,33 @@ __device__ __forceinline__ const float *smem_tab(int byte_off) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     return reinterpret_cast<const float *>(smem_raw + byte_off);
 }
+// 32-bit .shared address of byte `byte_off` of the dynamic shared memory.
+__device__ __forceinline__ uint32_t smem_u32(int byte_off) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    return (uint32_t)__cvta_generic_to_shared(smem_raw + byte_off);
+}
+// The fast kernel addresses shared memory with ld/st.shared at CONSTANT addresses: offset
+// register + immediate (TS_SMEM_WINDOW + the byte offset in the dynamic block).  A generic pointer,
+// or a base kept in a register, costs the CTA's shared-window computation (S2UR SR_CgaCtaId, ULEA)
+// or an add in every loop iteration.  TS_SMEM_WINDOW is the .shared address of the first dynamic
+// byte of a non-cluster launch; the library probes it once (ts_smem_window_probe) and selects the
+// fast kernel only when it matches, and the kernel traps if launched otherwise.
+#define TS_SB (TS_SMEM_WINDOW + TS_SMEM_HEAD)   // .shared address of smem_base()
+__device__ __forceinline__ float lds1c(uint32_t off) {          // [off + TS_SMEM_WINDOW]
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1+%2];" : "=f"(v) : "r"(off), "n"(TS_SMEM_WINDOW));
+    return v;
+}
+__device__ __forceinline__ float2 lds2c(uint32_t off) {
+    float2 v;
+    asm volatile("ld.shared.v2.f32 {%0, %1}, [%2+%3];" : "=f"(v.x), "=f"(v.y) : "r"(off), "n"(TS_SMEM_WINDOW));
+    return v;
+}
+// one AoS vertex / slot at byte `off` from smem_base()
+__device__ __forceinline__ void lds3c(uint32_t off, float &x, float &y, float &z) {
+    asm volatile("ld.shared.f32 %0, [%3+%4];\n\tld.shared.f32 %1, [%3+%5];\n\tld.shared.f32 %2, [%3+%6];"
+                 : "=f"(x), "=f"(y), "=f"(z) : "r"(off), "n"(TS_SB), "n"(TS_SB + 4), "n"(TS_SB + 8));
+}
 
 __device__ __forceinline__ void deg_add(int narrow, int *deg, int i) {
     if (narrow) atomicAdd(reinterpret_cast<unsigned *>(deg) + (i >> 2), 1u << ((i & 3) * 8));
@@ -550,6 +577,76 @@ __device__ __forceinline__ void tet_item_b(const char *pb, char *sb, int *deg, i
         if (ob < vfp_b) deg_add(narrow, deg, ob / 12);
         if (oc < vfp_b) deg_add(narrow, deg, oc / 12);
         if (od < vfp_b) deg_add(narrow, deg, od / 12);
+    }
+}
+
+// The fast kernel's tet item: byte offsets from the 32-bit shared base sb (positions and slots share
+// it: narrow layout), rest volume 6 V0 given; same arithmetic as tet_item_b.
+__device__ __forceinline__ void tet_item_fast(int *deg, uint4 q, float rvi, float kv, unsigned vfp_b) {
+    const unsigned oa = q.x & 0x3fffu, ob = (q.x >> 16) & 0x3fffu, oc = q.y & 0x3fffu, od = (q.y >> 16) & 0x3fffu;
+    float ax, ay, az, bx, by, bz, cx, cy, cz, dx, dy, dz;
+    lds3c(oa, ax, ay, az);
+    lds3c(ob, bx, by, bz);
+    lds3c(oc, cx, cy, cz);
+    lds3c(od, dx, dy, dz);
+    const float bax = bx - ax, bay = by - ay, baz = bz - az;
+    const float cax = cx - ax, cay = cy - ay, caz = cz - az;
+    const float dax = dx - ax, day = dy - ay, daz = dz - az;
+    const float Gbx = __fmaf_rn(cay, daz, -caz * day);
+    const float Gby = __fmaf_rn(caz, dax, -cax * daz);
+    const float Gbz = __fmaf_rn(cax, day, -cay * dax);
+    const float Gcx = __fmaf_rn(day, baz, -daz * bay);
+    const float Gcy = __fmaf_rn(daz, bax, -dax * baz);
+    const float Gcz = __fmaf_rn(dax, bay, -day * bax);
+    const float Gdx = __fmaf_rn(bay, caz, -baz * cay);
+    const float Gdy = __fmaf_rn(baz, cax, -bax * caz);
+    const float Gdz = __fmaf_rn(bax, cay, -bay * cax);
+    const float Gax = -(Gbx + Gcx + Gdx);
+    const float Gay = -(Gby + Gcy + Gdy);
+    const float Gaz = -(Gbz + Gcz + Gdz);
+    const float c6 = __fmaf_rn(Gdz, daz, __fmaf_rn(Gdy, day, Gdx * dax)) - rvi;
+    float den = Gax * Gax;
+    den = __fmaf_rn(Gay, Gay, den); den = __fmaf_rn(Gaz, Gaz, den);
+    den = __fmaf_rn(Gbx, Gbx, den); den = __fmaf_rn(Gby, Gby, den); den = __fmaf_rn(Gbz, Gbz, den);
+    den = __fmaf_rn(Gcx, Gcx, den); den = __fmaf_rn(Gcy, Gcy, den); den = __fmaf_rn(Gcz, Gcz, den);
+    den = __fmaf_rn(Gdx, Gdx, den); den = __fmaf_rn(Gdy, Gdy, den); den = __fmaf_rn(Gdz, Gdz, den);
+    const bool degenerate = !(den > 3.6e-17f);                  // sum|grad|^2 <= 1e-18
+    const float sc = degenerate ? 0.0f : (-kv * c6) * rcp_ftz(den);
+    auto st3 = [&](unsigned o, float gx, float gy, float gz) {   // 0xffff: pinned corner, store predicated off
+        asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %0, 65535;\n\t"
+                     "@p st.shared.f32 [%0+%4], %1;\n\t@p st.shared.f32 [%0+%5], %2;\n\t"
+                     "@p st.shared.f32 [%0+%6], %3;\n\t}"
+                     ::"r"(o), "f"(sc * gx), "f"(sc * gy), "f"(sc * gz), "n"(TS_SB), "n"(TS_SB + 4), "n"(TS_SB + 8)
+                     : "memory");
+    };
+    st3(q.z & 0xffffu, Gax, Gay, Gaz);
+    st3(q.z >> 16, Gbx, Gby, Gbz);
+    st3(q.w & 0xffffu, Gcx, Gcy, Gcz);
+    st3(q.w >> 16, Gdx, Gdy, Gdz);
+    if (degenerate) {
+        if (oa < vfp_b) deg_add(1, deg, oa / 12);
+        if (ob < vfp_b) deg_add(1, deg, ob / 12);
+        if (oc < vfp_b) deg_add(1, deg, oc / 12);
+        if (od < vfp_b) deg_add(1, deg, od / 12);
+    }
+}
+
+// The fast kernel's share of one warp's tet items [wb, wb + 32 j) (the stream is padded by a CTA's
+// worth of items: the prefetch needs no clamp).  RV4: at most 4 distinct 6 V0 values, whose
+// dictionary index sits in bits 14-15 of the first position field alone.
+template <bool RV4>
+__device__ __forceinline__ void p1_tets_fast(const TsDevProg &P, int *deg, int begin, int wb, int we, float kv) {
+    const int lane = threadIdx.x & 31;
+    const unsigned vfp_b = 12u * (unsigned)P.Vf_pad;
+    const uint4 *ip = P.tet_c + begin + wb + lane;
+    uint4 nq = __ldg(ip);
+    for (int i = wb + lane; i < we; i += 32) {
+        const uint4 q = nq;
+        ip += 32;
+        nq = __ldg(ip);
+        const unsigned ri = RV4 ? ((q.x >> 14) & 3u)
+                                : (((q.x >> 14) & 3u) | ((q.x >> 28) & 12u) | ((q.y >> 10) & 48u) | ((q.y >> 24) & 192u));
+        tet_item_fast(deg, q, lds1c(TS_TAB_OFF + 4 * TS_TAB_CAP + 4 * ri), kv, vfp_b);
     }
 }
 
@@ -775,28 +872,29 @@ __device__ __forceinline__ void owner_edges(const TsDevProg &P, const Smem<Real>
             ndeg += mm == 0.0;
         }
     } else if (FAST || P.einc_bytes == 4) {
-        // 4-byte records: {neighbour byte offset | rest-length index << 16 | pinned << 31}
+        // 4-byte records: {neighbour byte offset | pair index << 16}, pair = {rest length, -k_s w_p /
+        // (w_p + w_q)} (pair 0 = {0, 0}: a null record of the compiler's conflict-free rounds, whose
+        // term is exactly zero)
         const unsigned *rec = reinterpret_cast<const unsigned *>(P.einc) + rb;
-        const char *pb = FAST ? smem_base() : reinterpret_cast<const char *>(m.pos);
-        const float hks = 0.5f * ks;
         unsigned q = __ldg(rec);
         for (int k = 0; k < ev; ++k) {
             const unsigned cur = q;
             q = __ldg(rec + 32 * (k + 1));
-            const unsigned off = cur & 0xffffu;
-            const float rl = FAST ? smem_tab(TS_TAB_OFF)[(cur >> 16) & 0x7fffu] : __ldg(P.rltab + ((cur >> 16) & 0x7fffu));
-            // null record (0xffff, a gap of the compiler's conflict-free rounds): no load, dx = 0, so
-            // the degenerate guard zeroes the term and counts it (static_cnt holds the nulls)
-            float qx = px, qy = py, qz = pz;
-            if (off != 0xffffu) {
-                const float *nq = reinterpret_cast<const float *>(pb + off);
+            float qx, qy, qz;
+            float2 rc;
+            if constexpr (FAST) {
+                rc = lds2c(TS_TAB_OFF + 8 * (cur >> 16));
+                lds3c(cur & 0xffffu, qx, qy, qz);
+            } else {
+                rc = __ldg(reinterpret_cast<const float2 *>(P.rltab) + (cur >> 16));
+                const float *nq = reinterpret_cast<const float *>(reinterpret_cast<const char *>(m.pos) + (cur & 0xffffu));
                 qx = nq[0]; qy = nq[1]; qz = nq[2];
             }
             const float dx = px - qx, dy = py - qy, dz = pz - qz;
             const float d2 = __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, dx * dx));
             const bool degenerate = !(d2 >= 1e-24f);
-            const float f = degenerate ? 0.0f : __fmaf_rn(-rl, rsqrt_ftz(d2), 1.0f);
-            const float c = -((int)cur < 0 ? ks : hks) * f;
+            const float f = degenerate ? 0.0f : __fmaf_rn(-rc.x, rsqrt_ftz(d2), 1.0f);
+            const float c = rc.y * f;
             ax = __fmaf_rn(c, dx, ax); ay = __fmaf_rn(c, dy, ay); az = __fmaf_rn(c, dz, az);
             ndeg += degenerate;
         }
@@ -1142,7 +1240,8 @@ __device__ __forceinline__ void step_env(const TsDevProg &P, const TsDevProg *pr
         float *tab = const_cast<float *>(smem_tab(TS_TAB_OFF));
         for (int i = t; i < 2 * TS_TAB_CAP; i += B) {
             const int j = i - TS_TAB_CAP;
-            tab[i] = i < TS_TAB_CAP ? (i < P.n_rltab ? __ldg(P.rltab + i) : 0.0f) : (j < P.n_rvtab ? __ldg(P.rvtab + j) : 0.0f);
+            // [edge pairs {rest, coef} | 6 V0 values]
+            tab[i] = i < TS_TAB_CAP ? (i < 2 * P.n_rltab ? __ldg(P.rltab + i) : 0.0f) : (j < P.n_rvtab ? __ldg(P.rvtab + j) : 0.0f);
         }
     }
     for (int i = t; i < P.cbits_words; i += B) m.cbits[i] = 0u;
@@ -1285,7 +1384,8 @@ __device__ __forceinline__ void step_env(const TsDevProg &P, const TsDevProg *pr
                 if (!FAST && ch.att_count) p1_atts<Real>(P, m, ch.att_begin, ch.att_count);
                 if ((FAST || ch.tet_count) && !(S.ablate & 1)) {
                     if constexpr (FAST) {
-                        p1_tets<Real, FAST>(P, m, h_tb, h_wb, h_we, kv);
+                        if (P.n_rvtab <= 4) p1_tets_fast<true>(P, m.deg, h_tb, h_wb, h_we, kv);
+                        else p1_tets_fast<false>(P, m.deg, h_tb, h_wb, h_we, kv);
                     } else {
                         const int *ws = P.wsplit + c * (B / 32 + 1) + (t >> 5);
                         p1_tets<Real, FAST>(P, m, ch.tet_begin, ws[0], ws[1], kv);
@@ -1306,8 +1406,9 @@ __device__ __forceinline__ void step_env(const TsDevProg &P, const TsDevProg *pr
                         // slot k of this vertex (FAST: a byte offset from the constant shared base)
                         auto add_slot = [&](int k) {
                             if constexpr (FAST) {
-                                const float *q = reinterpret_cast<const float *>(smem_base() + h_base[r] + 384 * k);
-                                ax += q[0]; ay += q[1]; az += q[2];
+                                float qx, qy, qz;
+                                lds3c(h_base[r] + 384 * k, qx, qy, qz);
+                                ax += qx; ay += qy; az += qz;
                             } else {
                                 const int sidx = base + 32 * k;
                                 ax += m.SX(sidx); ay += m.SY(sidx); az += m.SZ(sidx);
@@ -1625,6 +1726,7 @@ __global__ void __launch_bounds__(TS_STEP_MAXT, TS_STEP_MINB) fast_step_kernel(c
                                                                               const __grid_constant__ TsLaunch L) {
     pdl_trigger();   // the epilogue may launch early; it waits for this grid before reading
     extern __shared__ __align__(16) unsigned char smem_raw[];
+    if (smem_u32(0) != TS_SMEM_WINDOW) __trap();   // constant shared addresses (lds3c): never silently wrong
     Smem<Real> m = carve<Real>(P, smem_raw);
     if ((L.mode & TS_M_CHECK_ACTIONS) && *L.bad_flag) return;
     for (int64_t env = blockIdx.x; env < L.n_env; env += gridDim.x)

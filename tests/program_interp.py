@@ -69,19 +69,20 @@ class Program:
             n = int(self.eregion[-1] + 32 * self.evalence[32 * (G - 1):32 * G].max()) if G else 0
             raw = self.sec("EINC", np.uint8, max(n, 1) * eb).reshape(-1, eb)
             word = raw[:, 0:4].copy().view(np.uint32)[:, 0]
-            if eb == 4:                                         # {offset | rest index << 16 | pinned << 31}
-                n_rl = int((self.off[SECTIONS.index("RVTAB")] - self.off[SECTIONS.index("RLTAB")]) // 4)
-                tab = self.sec("RLTAB", np.float32, n_rl).astype(np.float64)
-                self.e_rest = tab[(word >> 16) & 0x7FFF]
+            self.e_null = np.zeros(len(word), bool)
+            if eb == 4:           # {offset | pair index << 16}; pairs {rest, -k_s w_p / (w_p + w_q)}
+                tab = self.sec("RLTAB", np.float32, 2 * H["n_rltab"]).reshape(-1, 2).astype(np.float64)
+                idx = word >> 16
+                self.e_rest = tab[idx, 0]
+                self.e_pair_coef = tab[idx, 1]
                 self.e_coef = None
-                word = (word & 0xFFFF) | (word & 0x80000000)
+                # pair 0 = {0, 0}: a null record (a gap of the conflict-free rounds), whose term is 0
+                self.e_null = idx == 0
+                word = word & 0xFFFF
             self.e_nbr = (word & 0x7FFFFFFF).astype(np.int32)
-            # null records (offset 0xffff, gaps of the conflict-free rounds): no neighbour, a zero
-            # term counted as degenerate
-            self.e_null = self.e_nbr == 0xFFFF
             if H["boff"]:
-                assert np.all((self.e_nbr % 12 == 0) | self.e_null)
-                self.e_nbr = np.where(self.e_null, -1, self.e_nbr // 12)   # fp32 records hold byte offsets
+                assert np.all(self.e_nbr % 12 == 0)
+                self.e_nbr //= 12                               # fp32 records hold byte offsets
             self.e_nbr_pinned = (word >> 31).astype(bool)       # bit 31: neighbour pinned (w = 0)
             if eb == 4:
                 pass
@@ -105,7 +106,17 @@ class Program:
         return self.e_nbr[r], self.e_rest[r]
 
     def edge_nulls(self, p):
-        """Null records of free position p (each counts as one degenerate edge)."""
+        """Null records of free position p that read p's own position: dx = 0, so the kernel counts
+        each as a degenerate edge (the compiler adds them to static_cnt).  Nulls reading a pinned
+        position are not degenerate and not counted."""
+        if not hasattr(self, "e_null"):
+            return 0
+        k = np.arange(int(self.evalence[p]))
+        r = self.eregion[p // 32] + 32 * k + p % 32
+        return int((self.e_null[r] & (self.e_nbr[r] == p)).sum())
+
+    def edge_null_count(self, p):
+        """All null records of free position p."""
         if not hasattr(self, "e_null"):
             return 0
         k = np.arange(int(self.evalence[p]))

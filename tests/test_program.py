@@ -116,7 +116,8 @@ def test_slot_structure(reach_scene, gather):
     # (lanes inside a group may be permuted by the bank refinement); an owner-gathered edge
     # weighs three slots
     nulls = np.array([p.edge_nulls(q) for q in range(H["Vf_pad"])]) if gather else np.zeros(H["Vf_pad"], int)
-    sc = p.static_cnt[:Vf] - nulls[:Vf] + (2 * (p.evalence[:Vf] - nulls[:Vf]) if gather else 0)
+    alln = np.array([p.edge_null_count(q) for q in range(H["Vf_pad"])]) if gather else np.zeros(H["Vf_pad"], int)
+    sc = p.static_cnt[:Vf] - nulls[:Vf] + (2 * (p.evalence[:Vf] - alln[:Vf]) if gather else 0)
     ref = np.sort(sc)[::-1]
     for g in range(0, Vf, 32):
         assert sorted(sc[g:g + 32]) == sorted(ref[g:g + 32])
@@ -148,7 +149,7 @@ def test_slot_structure(reach_scene, gather):
     # per-vertex incidence count equals the reference's count of live constraints touching it
     inc = _edge_incidence(mesh, w)
     if gather:
-        assert np.array_equal(p.evalence[:Vf] - nulls[:Vf], inc[p.s2o[:Vf]]) and n_inc == inc.sum()
+        assert np.array_equal(p.evalence[:Vf] - alln[:Vf], inc[p.s2o[:Vf]]) and n_inc == inc.sum()
     for t in mesh.tets:
         inc[t] += w[t] > 0
     # static counts: live incidences, plus the null records of the gather rounds (each counted

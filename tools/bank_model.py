@@ -80,10 +80,9 @@ def model(prog: Program):
             act = [p for p in ps if k < ev[p]]
             rec = raw[prog.eregion[w] + 32 * k + np.asarray(act) % 32]
             nb = (rec & 0xFFFF).astype(np.int64)
-            nb = nb[nb != 0xFFFF]                   # null records load nothing
             for c in range(3):
                 acc("edge_load", HEAD + nb + 4 * c)
-            acc("edge_rl", TAB + 4 * ((rec >> 16) & 0x7FFF).astype(np.int64))
+            acc("edge_rl", TAB + 8 * (rec >> 16).astype(np.int64))     # {rest, coef} pair (one 64-bit load)
         pitch = H.get("slot_pitch", 32) or 32
         for k in range(int(max(val[p] for p in ps))):
             act = np.asarray([p for p in ps if k < val[p]])
