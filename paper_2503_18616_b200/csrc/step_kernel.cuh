@@ -527,6 +527,17 @@ __device__ __forceinline__ void store_slot(const Smem<Real> &m, int s, Real c, R
 template <typename Real>
 __device__ __forceinline__ void tet_item(const Smem<Real> &m, int4 id, int4 sl, Real rvi, Real kv, int vfp);
 
+// fp32 builds: sum |G|^2 of a tet's four (unscaled) gradients as three independent 4-term FMA chains
+// -- a shorter dependency chain than one 12-term sum; every fp32 tet path uses this one order
+__device__ __forceinline__ float tet_den(float Gax, float Gay, float Gaz, float Gbx, float Gby, float Gbz, float Gcx,
+                                         float Gcy, float Gcz, float Gdx, float Gdy, float Gdz) {
+    float d0 = Gax * Gax, d1 = Gbx * Gbx, d2 = Gcx * Gcx;
+    d0 = __fmaf_rn(Gay, Gay, d0); d1 = __fmaf_rn(Gby, Gby, d1); d2 = __fmaf_rn(Gcy, Gcy, d2);
+    d0 = __fmaf_rn(Gaz, Gaz, d0); d1 = __fmaf_rn(Gbz, Gbz, d1); d2 = __fmaf_rn(Gcz, Gcz, d2);
+    d0 = __fmaf_rn(Gdx, Gdx, d0); d1 = __fmaf_rn(Gdy, Gdy, d1); d2 = __fmaf_rn(Gdz, Gdz, d2);
+    return (d0 + d1) + d2;
+}
+
 // fp32 tet item on byte-offset streams (boff programs): q = {a | b << 16, c | d << 16, slot a | b << 16,
 // slot c | d << 16}, all byte offsets into the position / slot buffers (no index multiplies)
 __device__ __forceinline__ void tet_item_b(const char *pb, char *sb, int *deg, int narrow, uint4 q, float rvi, float kv,
@@ -552,11 +563,7 @@ __device__ __forceinline__ void tet_item_b(const char *pb, char *sb, int *deg, i
     const float Gay = -(Gby + Gcy + Gdy);
     const float Gaz = -(Gbz + Gcz + Gdz);
     const float c6 = __fmaf_rn(Gdz, daz, __fmaf_rn(Gdy, day, Gdx * dax)) - rvi;
-    float den = Gax * Gax;
-    den = __fmaf_rn(Gay, Gay, den); den = __fmaf_rn(Gaz, Gaz, den);
-    den = __fmaf_rn(Gbx, Gbx, den); den = __fmaf_rn(Gby, Gby, den); den = __fmaf_rn(Gbz, Gbz, den);
-    den = __fmaf_rn(Gcx, Gcx, den); den = __fmaf_rn(Gcy, Gcy, den); den = __fmaf_rn(Gcz, Gcz, den);
-    den = __fmaf_rn(Gdx, Gdx, den); den = __fmaf_rn(Gdy, Gdy, den); den = __fmaf_rn(Gdz, Gdz, den);
+    const float den = tet_den(Gax, Gay, Gaz, Gbx, Gby, Gbz, Gcx, Gcy, Gcz, Gdx, Gdy, Gdz);
     const bool degenerate = !(den > 3.6e-17f);                  // sum|grad|^2 <= 1e-18
     const float sc = degenerate ? 0.0f : (-kv * c6) * rcp_ftz(den);
     // 0xffff: a pinned corner has no slot -- a predicated store (no branch, no shared "trash" slot,
@@ -605,11 +612,7 @@ __device__ __forceinline__ void tet_item_fast(int *deg, uint4 q, float rvi, floa
     const float Gay = -(Gby + Gcy + Gdy);
     const float Gaz = -(Gbz + Gcz + Gdz);
     const float c6 = __fmaf_rn(Gdz, daz, __fmaf_rn(Gdy, day, Gdx * dax)) - rvi;
-    float den = Gax * Gax;
-    den = __fmaf_rn(Gay, Gay, den); den = __fmaf_rn(Gaz, Gaz, den);
-    den = __fmaf_rn(Gbx, Gbx, den); den = __fmaf_rn(Gby, Gby, den); den = __fmaf_rn(Gbz, Gbz, den);
-    den = __fmaf_rn(Gcx, Gcx, den); den = __fmaf_rn(Gcy, Gcy, den); den = __fmaf_rn(Gcz, Gcz, den);
-    den = __fmaf_rn(Gdx, Gdx, den); den = __fmaf_rn(Gdy, Gdy, den); den = __fmaf_rn(Gdz, Gdz, den);
+    const float den = tet_den(Gax, Gay, Gaz, Gbx, Gby, Gbz, Gcx, Gcy, Gcz, Gdx, Gdy, Gdz);
     const bool degenerate = !(den > 3.6e-17f);                  // sum|grad|^2 <= 1e-18
     const float sc = degenerate ? 0.0f : (-kv * c6) * rcp_ftz(den);
     auto st3 = [&](unsigned o, float gx, float gy, float gz) {   // 0xffff: pinned corner, store predicated off
@@ -640,6 +643,7 @@ __device__ __forceinline__ void p1_tets_fast(const TsDevProg &P, int *deg, int b
     const unsigned vfp_b = 12u * (unsigned)P.Vf_pad;
     const uint4 *ip = P.tet_c + begin + wb + lane;
     uint4 nq = __ldg(ip);
+#pragma unroll 2
     for (int i = wb + lane; i < we; i += 32) {
         const uint4 q = nq;
         ip += 32;
@@ -776,11 +780,7 @@ __device__ __forceinline__ void tet_item(const Smem<Real> &m, int4 id, int4 sl, 
             const float Gay = -(Gby + Gcy + Gdy);
             const float Gaz = -(Gbz + Gcz + Gdz);
             const float c6 = __fmaf_rn(Gdz, daz, __fmaf_rn(Gdy, day, Gdx * dax)) - rvi;
-            float den = Gax * Gax;
-            den = __fmaf_rn(Gay, Gay, den); den = __fmaf_rn(Gaz, Gaz, den);
-            den = __fmaf_rn(Gbx, Gbx, den); den = __fmaf_rn(Gby, Gby, den); den = __fmaf_rn(Gbz, Gbz, den);
-            den = __fmaf_rn(Gcx, Gcx, den); den = __fmaf_rn(Gcy, Gcy, den); den = __fmaf_rn(Gcz, Gcz, den);
-            den = __fmaf_rn(Gdx, Gdx, den); den = __fmaf_rn(Gdy, Gdy, den); den = __fmaf_rn(Gdz, Gdz, den);
+            const float den = tet_den(Gax, Gay, Gaz, Gbx, Gby, Gbz, Gcx, Gcy, Gcz, Gdx, Gdy, Gdz);
             degenerate = !(den > 3.6e-17f);                  // sum|grad|^2 <= 1e-18
             const float sc = degenerate ? 0.0f : (-kv * c6) * rcp_ftz(den);
             put_slot(m, sl.x, sc, Gax, Gay, Gaz);

@@ -20,7 +20,14 @@ def main():
         layout["max_chunk_slots"] = int(os.environ["TS_CHUNK"])
     if os.environ.get("TS_BLOCK"):
         layout["block_threads"] = int(os.environ["TS_BLOCK"])
-    env = EnvBatch(load_scene(default_scene_path()), num_envs=n, device="cuda:0", precision=prec, layout=layout)
+    scene = load_scene(default_scene_path())
+    if os.environ.get("TS_DIST_ONLY"):   # config 2: tets emptied (bench.distance_only)
+        import dataclasses
+        import numpy as np
+        mesh, rest, cfg = scene
+        scene = (dataclasses.replace(mesh, tets=np.zeros((0, 4), np.int32)),
+                 dataclasses.replace(rest, rest_volume=np.zeros(0)), cfg)
+    env = EnvBatch(scene, num_envs=n, device="cuda:0", precision=prec, layout=layout)
     env.reset()
     acts = torch.empty((n, 3), dtype=torch.float64, device="cuda:0")
     lib = N.load()
