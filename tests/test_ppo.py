@@ -211,3 +211,24 @@ class TestTrainGPU:
         assert 0.0 <= res["success_rate"] <= 1.0 and res["mean_length"] <= 5.0
         with pytest.raises(ValidationError):
             evaluate(env, ActorCritic(6, 3).to("cuda:0"), episodes=0)
+
+
+@pytest.mark.gpu
+def test_p8_reach_task_convergence_on_gpu():
+    """Acceptance P8 (`/root/reference/pkg/tests/test_acceptance.py:186-200`) at the config-4 size:
+    on-GPU PPO on 4096 reach_1170 envs crosses a trailing mean episode reward of 80 (the reference's
+    stop rule: trailing-`stop_window`-episode mean held for `stop_patience` updates,
+    ppo.py:405-413) within 120 updates (~2 M env steps, a few seconds on one B200), and the greedy
+    policy then succeeds on >= 90% of 200 episodes, the reference's P8 bar."""
+    from paper_2503_18616_b200 import EnvBatch
+    from paper_2503_18616_b200.mesh import default_scene_path, load_scene
+    env = EnvBatch(load_scene(default_scene_path()), num_envs=4096, seed=0, device="cuda:0")
+    cfg = PPOConfig.for_num_envs(4096, stop_at_reward=80.0, stop_window=100, seed=0)
+    cfg.total_steps = 120 * cfg.steps_before_update
+    stats = train(env, cfg)
+    assert stats.reward_crossed_at is not None, stats.rows[-3:]
+    assert stats.reward_crossed_at <= 120 * cfg.steps_before_update
+    res = evaluate(env, stats.model, episodes=200, seed=1)
+    assert res["success_rate"] >= 0.90, res
+    print(f"\nPASS P8 (GPU): reward > 80 at {stats.reward_crossed_at} env steps "
+          f"({stats.reward_crossed_wall:.1f} s); greedy success {res['success_rate']:.2f}")

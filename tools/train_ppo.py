@@ -61,7 +61,7 @@ def main():
     ev = evaluate(env, stats.model, episodes=500, seed=123) if rank == 0 else None
     if rank == 0:
         print(json.dumps({
-            "metric": "wall-clock to trailing-100 mean reward > 80 (on-GPU PPO, tissue reach)",
+            "metric": f"wall-clock to trailing-{cfg.stop_window}-episode mean reward > 80 (on-GPU PPO, tissue reach)",
             "reward_crossed_at_env_steps": stats.reward_crossed_at, "reward_crossed_wall_s": stats.reward_crossed_wall,
             "stopped_early_at": stats.stopped_early_at, "wall_s": wall, "updates": len(stats.rows),
             "n_gpus": world, "envs_per_gpu": args.envs, "stop_window": cfg.stop_window,
