@@ -1009,8 +1009,9 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
 
     // fp32: one thread per free vertex (3 CTAs/SM fit); fp64 runs 1 CTA/SM (shared memory), so it
     // takes 1.5x the threads to widen phase 1 (measured on B200: 3.81 vs 4.30 ms at 4096 envs)
+    // cluster parts: 1.5x too -- one env's CTAs run a few warps each and are latency-bound
     int B = o.block_threads > 0 ? o.block_threads
-                                : std::min(512, std::max(64, R == 8 ? roundup(Vf_pad * 3 / 2, 32) : Vf_pad));
+                                : std::min(512, std::max(64, (R == 8 || part) ? roundup(Vf_pad * 3 / 2, 32) : Vf_pad));
     if (part && part->force_B) B = part->force_B;
     if (B % 32 != 0 || B < 32 || B > 512) { err = "block_threads must be a multiple of 32 in [32, 512]"; return TS_ERR_INVALID; }
     const int VPT = std::max(1, (Vf_pad + B - 1) / B);
@@ -1357,6 +1358,8 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
         int maxval = 0;
         for (int v : valence) maxval = std::max(maxval, v);
         const char *nv = std::getenv("TS_NARROW");
+        // (distance-only gather programs stay wide: a narrow one needs a second barrier between the
+        // gather and the in-place apply, measured slower even at 4 CTAs / SM, profiles/r02j)
         narrow = !part && (n_chunks >= 1 || !eg) && maxval <= 255 && !(nv && nv[0] == '0') &&
                  (!boff || 12 * (Vstore + slot_cap) < 65535);
     }

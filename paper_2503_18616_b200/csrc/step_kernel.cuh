@@ -848,12 +848,12 @@ __device__ void p1_atts(const TsDevProg &P, const Smem<Real> &m, int begin, int 
 // fp64: -(w_p scale) (x_p - x_q) with the reference's scale expression
 // (ts_lane_edges, _kernels.pyx:121-136) -- bitwise the reference's per-endpoint
 // term, see compiler.cpp; fp32: -coef (1 - rest / dist) (x_p - x_q) with FMAs.
-template <typename Real, bool FAST = false>
+template <typename Real, bool FAST = false, bool HOIST = FAST>
 __device__ __forceinline__ void owner_edges(const TsDevProg &P, const Smem<Real> &m, int p, int lane, Real px,
                                             Real py, Real pz, Real ks, Real &ax, Real &ay, Real &az, int &ndeg,
                                             int ev_h = 0, int rb_h = 0) {
-    const int ev = FAST ? ev_h : P.evalence[p];            // FAST: hoisted out of the substep loop
-    const int rb = FAST ? rb_h : P.eregion[p >> 5] + lane;
+    const int ev = HOIST ? ev_h : P.evalence[p];            // HOIST: read once, before the substep loop
+    const int rb = HOIST ? rb_h : P.eregion[p >> 5] + lane;
     if constexpr (sizeof(Real) == 8) {
         const int4 *rec = reinterpret_cast<const int4 *>(P.einc) + rb;
         const double *wst = reinterpret_cast<const double *>(P.w);
@@ -886,7 +886,8 @@ __device__ __forceinline__ void owner_edges(const TsDevProg &P, const Smem<Real>
                 rc = lds2c(TS_TAB_OFF + 8 * (cur >> 16));
                 lds3c(cur & 0xffffu, qx, qy, qz);
             } else {
-                rc = __ldg(reinterpret_cast<const float2 *>(P.rltab) + (cur >> 16));
+                rc = 2 * P.n_rltab <= TS_TAB_CAP ? reinterpret_cast<const float2 *>(smem_tab(TS_TAB_OFF))[cur >> 16]
+                                                 : __ldg(reinterpret_cast<const float2 *>(P.rltab) + (cur >> 16));
                 const float *nq = reinterpret_cast<const float *>(reinterpret_cast<const char *>(m.pos) + (cur & 0xffffu));
                 qx = nq[0]; qy = nq[1]; qz = nq[2];
             }
@@ -1236,7 +1237,8 @@ __device__ __forceinline__ void step_env(const TsDevProg &P, const TsDevProg *pr
         }
     }
     for (int p = t; p < (P.narrow ? P.Vf_pad / 4 : P.Vf_pad); p += B) m.deg[p] = 0;
-    if constexpr (FAST) {   // dictionary tables -> shared memory (read by every tet / edge of every substep)
+    if (FAST || (sizeof(Real) == 4 && P.einc_bytes == 4 && 2 * P.n_rltab <= TS_TAB_CAP)) {
+        // dictionary tables -> shared memory (read by every tet / edge of every substep)
         float *tab = const_cast<float *>(smem_tab(TS_TAB_OFF));
         for (int i = t; i < 2 * TS_TAB_CAP; i += B) {
             const int j = i - TS_TAB_CAP;
@@ -1335,6 +1337,23 @@ __device__ __forceinline__ void step_env(const TsDevProg &P, const TsDevProg *pr
         // FAST (one chunk): the per-vertex program words are substep-invariant -> registers
         int h_base[VPT], h_val[VPT], h_pre[VPT], h_cnt[VPT], h_ev[VPT], h_rb[VPT];
         int h_tb = 0, h_wb = 0, h_we = 0;   // FAST: the chunk's tet base and this warp's range
+        // cluster parts (a few warps per CTA, latency-bound): the substep-invariant per-vertex words
+        // in registers too -- counts and edge rows always, chunk 0's slot rows when it is the only one
+        constexpr bool HC = CL && sizeof(Real) == 4;   // (the fp64 cluster kernels are out of registers already)
+        const bool hc1 = HC && P.n_chunks == 1;
+        if constexpr (HC) {
+            const TsChunk ch0 = P.chunks[0];
+#pragma unroll
+            for (int r = 0; r < VPT; ++r) {
+                const int p = max(0, min(r * B + t, P.Vf - 1));
+                h_cnt[r] = P.static_cnt[p];
+                h_ev[r] = P.edge_gather ? P.evalence[p] : 0;
+                h_rb[r] = P.edge_gather ? P.eregion[p >> 5] + lane : 0;
+                h_base[r] = hc1 ? P.region[ch0.region_off + (p >> 5)] + lane : 0;
+                h_val[r] = hc1 ? P.valence[ch0.val_off + p] : 0;
+                h_pre[r] = hc1 ? min(h_val[r], P.gsplit[p]) : 0;
+            }
+        }
         if constexpr (FAST) {
             const TsChunk ch0 = P.chunks[0];
             h_tb = ch0.tet_begin;
@@ -1375,8 +1394,8 @@ __device__ __forceinline__ void step_env(const TsDevProg &P, const TsDevProg *pr
                     for (int r = 0; r < VPT; ++r) {
                         const int p = r * B + t;
                         if (p < P.Vf)
-                            owner_edges<Real, FAST>(P, m, p, lane, xr[r], yr[r], zr[r], ks, accx[r], accy[r],
-                                                    accz[r], ndeg[r], h_ev[r], h_rb[r]);
+                            owner_edges<Real, FAST, FAST || HC>(P, m, p, lane, xr[r], yr[r], zr[r], ks, accx[r],
+                                                                accy[r], accz[r], ndeg[r], h_ev[r], h_rb[r]);
                     }
                 }
                 // phase 1: every kind of the chunk, no barrier in between (disjoint slots)
@@ -1398,10 +1417,11 @@ __device__ __forceinline__ void step_env(const TsDevProg &P, const TsDevProg *pr
                 for (int r = 0; r < VPT; ++r) {
                     const int p = r * B + t;
                     if (p < P.Vf) {
-                        const int base = FAST ? 0 : P.region[ch.region_off + (p >> 5)] + lane;
-                        const int val0 = FAST ? h_val[r] : P.valence[ch.val_off + p];
+                        const int base = FAST ? 0 : hc1 ? h_base[r] : P.region[ch.region_off + (p >> 5)] + lane;
+                        const int val0 = FAST || hc1 ? h_val[r] : P.valence[ch.val_off + p];
                         const int val = (S.ablate & 2) ? 0 : ((S.ablate & 128) ? min(val0, 12) : val0);
-                        const int pre = FAST && !(S.ablate & 130) ? h_pre[r] : gchunk ? min(val, P.gsplit[p]) : val;
+                        const int pre = (FAST || hc1) && !(S.ablate & 130) ? h_pre[r]
+                                        : gchunk ? min(val, P.gsplit[p]) : val;
                         Real ax = accx[r], ay = accy[r], az = accz[r];
                         // slot k of this vertex (FAST: a byte offset from the constant shared base)
                         auto add_slot = [&](int k) {
@@ -1443,7 +1463,7 @@ __device__ __forceinline__ void step_env(const TsDevProg &P, const TsDevProg *pr
             for (int r = 0; r < VPT; ++r) {
                 const int p = r * B + t;
                 if (p < P.Vf) {
-                    const int cnt = (FAST ? h_cnt[r] : P.static_cnt[p]) - ndeg[r] + gcnt[r];
+                    const int cnt = (FAST || HC ? h_cnt[r] : P.static_cnt[p]) - ndeg[r] + gcnt[r];
                     if constexpr (sizeof(Real) == 8) {
                         const Real n = (Real)cnt;
                         const Real mm = (Real)0.5 + copysign((Real)0.5, n - (Real)0.5);

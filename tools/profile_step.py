@@ -20,6 +20,8 @@ def main():
         layout["max_chunk_slots"] = int(os.environ["TS_CHUNK"])
     if os.environ.get("TS_BLOCK"):
         layout["block_threads"] = int(os.environ["TS_BLOCK"])
+    if os.environ.get("TS_CLUSTER"):
+        layout["cluster_size"] = int(os.environ["TS_CLUSTER"])
     scene = load_scene(default_scene_path())
     if os.environ.get("TS_DIST_ONLY"):   # config 2: tets emptied (bench.distance_only)
         import dataclasses
