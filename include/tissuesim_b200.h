@@ -261,7 +261,11 @@ int32_t ts_detect_contacts(ts_handle *h, const void *x, int64_t num_envs, const 
  * byte_offset is honoured.  Any mismatch returns TS_ERR_INVALID naming the tensor, the way the
  * reference's typed memoryviews reject a wrong buffer at entry (_kernels.pyx:577-585).
  * Dtypes: x, v Real = float32 (TS_F32 handle) / float64 (TS_F64); tool_* float64;
- * grasp_vertex, steps int64; grasped uint8 or bool; l_prev, ep_return float64. */
+ * grasp_vertex, steps int64; grasped uint8 or bool; l_prev, ep_return float64.
+ * ts_env_step_dl also takes its actions and step outputs in pinned host memory (kDLCUDAHost, or
+ * kDLCPU at a page-locked address, as torch exports torch.empty(..., pin_memory=True)): the
+ * command kernel reads the actions and the epilogue writes the outputs in place over the bus
+ * (zero-copy; EnvBatch.step_numpy does this).  Pageable host memory is rejected. */
 typedef struct ts_env_tensors {
     const DLTensor *x, *v;                                   /* (N,V,3) Real */
     const DLTensor *tool_axis, *tool_jaw;                    /* (N,3) f64 */

@@ -542,20 +542,34 @@ enum Kind { K_REAL, K_F64, K_F32_OR_F64, K_I64, K_I32, K_U8 };
 
 // Checks one DLTensor against (kind, shape) and returns its data address in *out.  Shape entries
 // of -1 are free.  NULL tensors are accepted only when `optional`.
+// host_ok: pinned host memory (kDLCUDAHost) is accepted too -- the kernels read / write it in place
+// through the unified address space (zero-copy actions and step outputs)
 int check_dl(const ts_handle *h, const DLTensor *t, const char *name, Kind kind, int ndim, const int64_t *shape,
-             bool optional, void **out, int *is_f64 = nullptr) {
+             bool optional, void **out, int *is_f64 = nullptr, bool host_ok = false) {
     *out = nullptr;
     if (!t) {
         if (optional) return TS_OK;
         return fail(TS_ERR_INVALID, std::string(name) + ": tensor required");
     }
     char buf[320];
-    if (t->device.device_type != kDLCUDA && t->device.device_type != kDLCUDAManaged) {
-        std::snprintf(buf, sizeof(buf), "%s: expected a CUDA tensor, got DLPack device type %d", name,
-                      (int)t->device.device_type);
+    // pinned host memory: kDLCUDAHost, or kDLCPU whose address the CUDA runtime knows as page-locked
+    // (torch exports pinned tensors as kDLCPU); the kernels then use its device alias
+    void *host_alias = nullptr;
+    if (host_ok && (t->device.device_type == kDLCUDAHost || t->device.device_type == kDLCPU) && t->data) {
+        cudaPointerAttributes attr;
+        if (cudaPointerGetAttributes(&attr, t->data) == cudaSuccess && attr.type == cudaMemoryTypeHost &&
+            attr.devicePointer)
+            host_alias = attr.devicePointer;
+        else
+            cudaGetLastError();   // clear the lookup error of a pageable pointer
+    }
+    const bool pinned_host = host_alias != nullptr;
+    if (t->device.device_type != kDLCUDA && t->device.device_type != kDLCUDAManaged && !pinned_host) {
+        std::snprintf(buf, sizeof(buf), "%s: expected a CUDA tensor%s, got DLPack device type %d", name,
+                      host_ok ? " or pinned host memory" : "", (int)t->device.device_type);
         return fail(TS_ERR_INVALID, buf);
     }
-    if (t->device.device_id != h->device) {
+    if (!pinned_host && t->device.device_id != h->device) {
         std::snprintf(buf, sizeof(buf), "%s: tensor is on cuda:%d, the handle on cuda:%d", name,
                       (int)t->device.device_id, h->device);
         return fail(TS_ERR_INVALID, buf);
@@ -602,7 +616,8 @@ int check_dl(const ts_handle *h, const DLTensor *t, const char *name, Kind kind,
         for (int i = 0; i < ndim; ++i) numel *= t->shape[i];
         if (numel) return fail(TS_ERR_INVALID, std::string(name) + ": null data");
     }
-    *out = t->data ? reinterpret_cast<char *>(t->data) + t->byte_offset : nullptr;
+    void *base = pinned_host ? host_alias : t->data;
+    *out = base ? reinterpret_cast<char *>(base) + t->byte_offset : nullptr;
     return TS_OK;
 }
 
@@ -653,27 +668,27 @@ int32_t ts_env_step_dl(ts_handle *h, const ts_env_tensors *st, const DLTensor *a
     const int64_t n3[2] = {n, 3}, n1[1] = {n}, n6[2] = {n, 6}, one[1] = {1};
     void *a = nullptr, *p;
     int a64 = 1;
-    TS_CHECK(check_dl(h, actions, "actions", K_F32_OR_F64, 2, n3, ovr != nullptr, &a, &a64));
+    TS_CHECK(check_dl(h, actions, "actions", K_F32_OR_F64, 2, n3, ovr != nullptr, &a, &a64, true));
     ts_tool_override o{};
     if (ovr) TS_CHECK(override_dl(h, ovr, n, o));
     ts_step_out so{};
     int obs64 = 1, fin64 = -1;
-    TS_CHECK(check_dl(h, out->obs, "obs", K_F32_OR_F64, 2, n6, true, &so.obs, &obs64));
-    TS_CHECK(check_dl(h, out->final_obs, "final_obs", K_F32_OR_F64, 2, n6, true, &so.final_obs, &fin64));
+    TS_CHECK(check_dl(h, out->obs, "obs", K_F32_OR_F64, 2, n6, true, &so.obs, &obs64, true));
+    TS_CHECK(check_dl(h, out->final_obs, "final_obs", K_F32_OR_F64, 2, n6, true, &so.final_obs, &fin64, true));
     if (out->obs && out->final_obs && obs64 != fin64)
         return fail(TS_ERR_INVALID, "final_obs: dtype must equal obs's");
     so.obs_f64 = out->obs ? obs64 : (out->final_obs ? fin64 : 1);
-    TS_CHECK(check_dl(h, out->reward, "reward", K_F64, 1, n1, true, &p)); so.reward = (double *)p;
-    TS_CHECK(check_dl(h, out->distance, "distance", K_F64, 1, n1, true, &p)); so.distance = (double *)p;
-    TS_CHECK(check_dl(h, out->episode_return, "episode_return", K_F64, 1, n1, true, &p)); so.episode_return = (double *)p;
-    TS_CHECK(check_dl(h, out->episode_length, "episode_length", K_I64, 1, n1, true, &p)); so.episode_length = (int64_t *)p;
-    TS_CHECK(check_dl(h, out->contacts, "contacts", K_I32, 1, n1, true, &p)); so.contacts = (int32_t *)p;
-    TS_CHECK(check_dl(h, out->terminated, "terminated", K_U8, 1, n1, true, &p)); so.terminated = (uint8_t *)p;
-    TS_CHECK(check_dl(h, out->truncated, "truncated", K_U8, 1, n1, true, &p)); so.truncated = (uint8_t *)p;
-    TS_CHECK(check_dl(h, out->success, "success", K_U8, 1, n1, true, &p)); so.success = (uint8_t *)p;
-    TS_CHECK(check_dl(h, out->diverged, "diverged", K_U8, 1, n1, true, &p)); so.diverged = (uint8_t *)p;
-    TS_CHECK(check_dl(h, out->clipped, "clipped", K_U8, 1, n1, true, &p)); so.clipped = (uint8_t *)p;
-    TS_CHECK(check_dl(h, out->done_mask, "done_mask", K_U8, 1, n1, true, &p)); so.done_mask = (uint8_t *)p;
+    TS_CHECK(check_dl(h, out->reward, "reward", K_F64, 1, n1, true, &p, nullptr, true)); so.reward = (double *)p;
+    TS_CHECK(check_dl(h, out->distance, "distance", K_F64, 1, n1, true, &p, nullptr, true)); so.distance = (double *)p;
+    TS_CHECK(check_dl(h, out->episode_return, "episode_return", K_F64, 1, n1, true, &p, nullptr, true)); so.episode_return = (double *)p;
+    TS_CHECK(check_dl(h, out->episode_length, "episode_length", K_I64, 1, n1, true, &p, nullptr, true)); so.episode_length = (int64_t *)p;
+    TS_CHECK(check_dl(h, out->contacts, "contacts", K_I32, 1, n1, true, &p, nullptr, true)); so.contacts = (int32_t *)p;
+    TS_CHECK(check_dl(h, out->terminated, "terminated", K_U8, 1, n1, true, &p, nullptr, true)); so.terminated = (uint8_t *)p;
+    TS_CHECK(check_dl(h, out->truncated, "truncated", K_U8, 1, n1, true, &p, nullptr, true)); so.truncated = (uint8_t *)p;
+    TS_CHECK(check_dl(h, out->success, "success", K_U8, 1, n1, true, &p, nullptr, true)); so.success = (uint8_t *)p;
+    TS_CHECK(check_dl(h, out->diverged, "diverged", K_U8, 1, n1, true, &p, nullptr, true)); so.diverged = (uint8_t *)p;
+    TS_CHECK(check_dl(h, out->clipped, "clipped", K_U8, 1, n1, true, &p, nullptr, true)); so.clipped = (uint8_t *)p;
+    TS_CHECK(check_dl(h, out->done_mask, "done_mask", K_U8, 1, n1, true, &p, nullptr, true)); so.done_mask = (uint8_t *)p;
     void *flag = nullptr;
     TS_CHECK(check_dl(h, bad_action_flag, "bad_action_flag", K_I32, 1, one, true, &flag));
     return ts_env_step(h, &s, n, a, a ? !a64 : 0, &so, ovr ? &o : nullptr, (int32_t *)flag, stream);

@@ -870,6 +870,183 @@ int pack_tet_batches(std::vector<Item> &items, const std::vector<int> &o2s, cons
     return residual;
 }
 
+// Owner-gather rounds of fp32 4-byte programs with pinned copies: conflict-free by bipartite edge
+// colouring (lanes x banks).  A pinned neighbour reads the copy on the least-loaded bank, then
+// Koenig's theorem colours each warp's reads with K colours = rounds, K = max(longest list, largest
+// bank load) -- no round has two reads on one bank.  A lane's gaps become -1 (null records).
+// other(p, e): storage position of edge e's endpoint that is not p.
+template <typename Other>
+void colour_gather_rounds(std::vector<std::vector<int>> &lists, std::vector<std::vector<int>> &ecopy, int G, int Vf,
+                          const PinCopies &pc, Other other) {
+    for (int g = 0; g < G; ++g) {
+        const int p0 = 32 * g, p1 = std::min(Vf, 32 * g + 32);
+        if (p1 <= p0) continue;
+        struct Tok { int p, e, copy, bank; };
+        std::vector<Tok> toks;
+        std::vector<int> deg(32, 0), lane_deg(32, 0), pinned_tok;
+        for (int p = p0; p < p1; ++p)
+            for (int e : lists[p]) {
+                const int q = other(p, e);
+                lane_deg[p % 32]++;
+                if (pc.pinned(q)) { pinned_tok.push_back((int)toks.size()); toks.push_back({p, e, 0, -1}); }
+                else { toks.push_back({p, e, 0, q % 32}); deg[q % 32]++; }
+            }
+        for (int ti : pinned_tok) {   // least-loaded copy
+            Tok &t = toks[ti];
+            const int q = other(t.p, t.e);
+            int bc = 0, bb = pc.pos(q, 0) % 32;
+            for (int j = 1; j < pc.n; ++j) {
+                const int b = pc.pos(q, j) % 32;
+                if (deg[b] < deg[bb]) { bb = b; bc = j; }
+            }
+            t.copy = bc; t.bank = bb; deg[bb]++;
+        }
+        const int NC = std::max(*std::max_element(deg.begin(), deg.end()),
+                                *std::max_element(lane_deg.begin(), lane_deg.end()));
+        if (NC == 0) continue;
+        std::vector<int> col(toks.size(), -1), at_l((size_t)32 * NC, -1), at_b((size_t)32 * NC, -1);
+        for (int ti = 0; ti < (int)toks.size(); ++ti) {
+            const int l = toks[ti].p % 32, b = toks[ti].bank;
+            int ca = -1, cb = -1;
+            for (int c = 0; c < NC && ca < 0; ++c) if (at_l[(size_t)l * NC + c] < 0) ca = c;
+            for (int c = 0; c < NC && cb < 0; ++c) if (at_b[(size_t)b * NC + c] < 0) cb = c;
+            if (at_b[(size_t)b * NC + ca] >= 0) {   // flip the (ca, cb) path from bank b
+                std::vector<int> path;
+                int node = b, side = 1, cw = ca;
+                while (true) {
+                    const int e = side ? at_b[(size_t)node * NC + cw] : at_l[(size_t)node * NC + cw];
+                    if (e < 0) break;
+                    path.push_back(e);
+                    node = side ? toks[e].p % 32 : toks[e].bank;
+                    side ^= 1;
+                    cw = cw == ca ? cb : ca;
+                }
+                for (int e : path) { at_l[(size_t)(toks[e].p % 32) * NC + col[e]] = -1; at_b[(size_t)toks[e].bank * NC + col[e]] = -1; }
+                for (int e : path) {
+                    col[e] = col[e] == ca ? cb : ca;
+                    at_l[(size_t)(toks[e].p % 32) * NC + col[e]] = e;
+                    at_b[(size_t)toks[e].bank * NC + col[e]] = e;
+                }
+            }
+            col[ti] = ca;
+            at_l[(size_t)l * NC + ca] = ti;
+            at_b[(size_t)b * NC + ca] = ti;
+        }
+        // rounds -> lists: up to the lane's last coloured round, gaps as nulls (-1)
+        for (int p = p0; p < p1; ++p) {
+            int last = -1;
+            for (int c = 0; c < NC; ++c) if (at_l[(size_t)(p % 32) * NC + c] >= 0) last = c;
+            std::vector<int> nl(last + 1, -1), nc(last + 1, 0);
+            for (int c = 0; c <= last; ++c) {
+                const int ti = at_l[(size_t)(p % 32) * NC + c];
+                if (ti >= 0) { nl[c] = toks[ti].e; nc[c] = toks[ti].copy; }
+            }
+            lists[p] = nl;
+            ecopy[p] = nc;
+        }
+}
+}
+
+// Owner-gather rounds of other fp32 programs: in round k the 32 lanes of a warp read their k-th
+// neighbours; permute each lane's list (and re-pick pinned copies) so one round's neighbours sit in
+// distinct banks as far as possible (deterministic local search, sum over rounds of the largest
+// bank multiplicity).  The order of a vertex's edges is free in fp32 (fp64 keeps edge-index order).
+template <typename Other, typename NbrPos>
+void order_gather_rounds(std::vector<std::vector<int>> &lists, std::vector<std::vector<int>> &ecopy, int G,
+                         const PinCopies &pc, Other other, NbrPos nbr_pos) {
+    uint64_t rs = 0x2545F4914F6CDD1Dull;
+    auto rnd = [&]() { rs ^= rs << 13; rs ^= rs >> 7; rs ^= rs << 17; return rs; };
+    for (int g = 0; g < G; ++g) {
+        int kmax = 0;
+        for (int p = 32 * g; p < 32 * g + 32; ++p) kmax = std::max(kmax, (int)lists[p].size());
+        if (kmax < 1) continue;
+        std::vector<int> cnt((size_t)kmax * 32, 0);
+        auto bank = [&](int p, int k) { return nbr_pos(p, k) % 32; };
+        for (int p = 32 * g; p < 32 * g + 32; ++p)
+            for (int k = 0; k < (int)lists[p].size(); ++k) cnt[(size_t)k * 32 + bank(p, k)]++;
+        auto rmax = [&](int k) { int m = 0; for (int b = 0; b < 32; ++b) m = std::max(m, cnt[(size_t)k * 32 + b]); return m; };
+        const long iters = 6000L * kmax;
+        for (long it = 0; it < iters; ++it) {
+            const int p = 32 * g + (int)(rnd() % 32);
+            const int n = (int)lists[p].size();
+            if (n < 1) continue;
+            if (pc.n > 1 && (rnd() & 1)) {          // another copy of a pinned neighbour
+                const int k = (int)(rnd() % n);
+                if (!pc.pinned(other(p, lists[p][k]))) continue;
+                const int b0 = bank(p, k), c0 = ecopy[p][k];
+                const int before = rmax(k);
+                ecopy[p][k] = (c0 + 1 + (int)(rnd() % (pc.n - 1))) % pc.n;
+                const int b1 = bank(p, k);
+                cnt[(size_t)k * 32 + b0]--; cnt[(size_t)k * 32 + b1]++;
+                if (rmax(k) > before) {
+                    cnt[(size_t)k * 32 + b1]--; cnt[(size_t)k * 32 + b0]++;
+                    ecopy[p][k] = c0;
+                }
+                continue;
+            }
+            if (n < 2) continue;
+            const int ka = (int)(rnd() % n), kb = (int)(rnd() % n);
+            const int ba = bank(p, ka), bb = bank(p, kb);
+            if (ka == kb || ba == bb) continue;
+            const int before = rmax(ka) + rmax(kb);
+            cnt[(size_t)ka * 32 + ba]--; cnt[(size_t)kb * 32 + ba]++;
+            cnt[(size_t)kb * 32 + bb]--; cnt[(size_t)ka * 32 + bb]++;
+            if (rmax(ka) + rmax(kb) <= before) {
+                std::swap(lists[p][ka], lists[p][kb]);
+                std::swap(ecopy[p][ka], ecopy[p][kb]);
+            } else {
+                cnt[(size_t)ka * 32 + ba]++; cnt[(size_t)kb * 32 + ba]--;
+                cnt[(size_t)kb * 32 + bb]++; cnt[(size_t)ka * 32 + bb]--;
+            }
+        }
+}
+}
+
+// Phase-1 work split (the WSPLIT section): each warp takes a contiguous range of 32-item tet batches
+// of the chunk, sized so that its owner edge gather (chunk 0; the longest lane's incidences, CE
+// each) plus its batches (CT each) is about the same for every warp.  int32 [n_chunks][B/32 + 1].
+std::vector<int32_t> warp_split(const std::vector<TsChunk> &chunk_rec, const std::vector<int32_t> &evalence, bool eg,
+                                int B, int VPT, int Vf) {
+    const int NW = B / 32, n_chunks = (int)chunk_rec.size();
+    std::vector<int32_t> wsplit((size_t)n_chunks * (NW + 1), 0);
+    const double CE = 1.0;   // owner-gathered edge incidence vs one tet batch (tuned on B200, tools/sweep_ct.sh)
+    double CT = 4.0;
+    if (const char *env = std::getenv("TS_SPLIT_CT")) CT = std::atof(env);
+    for (int c = 0; c < n_chunks; ++c) {
+        const int nt = chunk_rec[c].tet_count;
+        const int nb = (nt + 31) / 32;
+        std::vector<double> ce(NW, 0.0);
+        if (eg && c == 0)
+            for (int w = 0; w < NW; ++w)
+                for (int lane = 0; lane < 32; ++lane) {
+                    int sum = 0;
+                    for (int r = 0; r < VPT; ++r) {
+                        const int p = r * B + 32 * w + lane;
+                        if (p < Vf) sum += evalence[p];
+                    }
+                    ce[w] = std::max(ce[w], CE * sum);
+                }
+        // smallest level T with sum_w floor((T - ce_w) / CT) >= nb batches (32 items each)
+        double lo = 0.0, hi = 1e9;
+        auto fits = [&](double T) {
+            long tot = 0;
+            for (int w = 0; w < NW; ++w) tot += std::max(0L, (long)std::floor((T - ce[w]) / CT));
+            return tot >= nb;
+        };
+        for (int it = 0; it < 100; ++it) { const double mid = 0.5 * (lo + hi); (fits(mid) ? hi : lo) = mid; }
+        int left = nb, start = 0;
+        for (int w = 0; w < NW; ++w) {
+            int take = std::min(left, std::max(0, (int)std::floor((hi - ce[w]) / CT)));
+            if (w == NW - 1) take = left;
+            wsplit[(size_t)c * (NW + 1) + w] = std::min(start, nt);
+            start += 32 * take;
+            left -= take;
+        }
+        wsplit[(size_t)c * (NW + 1) + NW] = nt;
+    }
+    return wsplit;
+}
+
 }  // namespace
 
 int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector<uint8_t> &blob,
@@ -1475,128 +1652,8 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
             return o2s[a == s2o[p] ? b : a];
         };
         auto nbr_pos = [&](int p, int k) { return pc.pos(other(p, lists[p][k]), ecopy[p][k]); };
-        if (packed && einc_bytes == 4) {
-            // Conflict-free rounds by bipartite edge colouring (lanes x banks): a pinned neighbour
-            // reads the copy on the least-loaded bank, then Koenig's theorem colours the warp's reads
-            // with K colours = rounds, K = max(longest list, largest bank load) -- no round has two
-            // reads on one bank.  A lane's gaps become null records (offset 0xffff): the kernel
-            // loads nothing for them and the degenerate guard zeroes the term (static_cnt adds the
-            // nulls back, like the count of a coincident edge).
-            for (int g = 0; g < G; ++g) {
-                const int p0 = 32 * g, p1 = std::min(Vf, 32 * g + 32);
-                if (p1 <= p0) continue;
-                struct Tok { int p, e, copy, bank; };
-                std::vector<Tok> toks;
-                std::vector<int> deg(32, 0), lane_deg(32, 0), pinned_tok;
-                for (int p = p0; p < p1; ++p)
-                    for (int e : lists[p]) {
-                        const int q = other(p, e);
-                        lane_deg[p % 32]++;
-                        if (pc.pinned(q)) { pinned_tok.push_back((int)toks.size()); toks.push_back({p, e, 0, -1}); }
-                        else { toks.push_back({p, e, 0, q % 32}); deg[q % 32]++; }
-                    }
-                for (int ti : pinned_tok) {   // least-loaded copy
-                    Tok &t = toks[ti];
-                    const int q = other(t.p, t.e);
-                    int bc = 0, bb = pc.pos(q, 0) % 32;
-                    for (int j = 1; j < pc.n; ++j) {
-                        const int b = pc.pos(q, j) % 32;
-                        if (deg[b] < deg[bb]) { bb = b; bc = j; }
-                    }
-                    t.copy = bc; t.bank = bb; deg[bb]++;
-                }
-                const int NC = std::max(*std::max_element(deg.begin(), deg.end()),
-                                        *std::max_element(lane_deg.begin(), lane_deg.end()));
-                if (NC == 0) continue;
-                std::vector<int> col(toks.size(), -1), at_l((size_t)32 * NC, -1), at_b((size_t)32 * NC, -1);
-                for (int ti = 0; ti < (int)toks.size(); ++ti) {
-                    const int l = toks[ti].p % 32, b = toks[ti].bank;
-                    int ca = -1, cb = -1;
-                    for (int c = 0; c < NC && ca < 0; ++c) if (at_l[(size_t)l * NC + c] < 0) ca = c;
-                    for (int c = 0; c < NC && cb < 0; ++c) if (at_b[(size_t)b * NC + c] < 0) cb = c;
-                    if (at_b[(size_t)b * NC + ca] >= 0) {   // flip the (ca, cb) path from bank b
-                        std::vector<int> path;
-                        int node = b, side = 1, cw = ca;
-                        while (true) {
-                            const int e = side ? at_b[(size_t)node * NC + cw] : at_l[(size_t)node * NC + cw];
-                            if (e < 0) break;
-                            path.push_back(e);
-                            node = side ? toks[e].p % 32 : toks[e].bank;
-                            side ^= 1;
-                            cw = cw == ca ? cb : ca;
-                        }
-                        for (int e : path) { at_l[(size_t)(toks[e].p % 32) * NC + col[e]] = -1; at_b[(size_t)toks[e].bank * NC + col[e]] = -1; }
-                        for (int e : path) {
-                            col[e] = col[e] == ca ? cb : ca;
-                            at_l[(size_t)(toks[e].p % 32) * NC + col[e]] = e;
-                            at_b[(size_t)toks[e].bank * NC + col[e]] = e;
-                        }
-                    }
-                    col[ti] = ca;
-                    at_l[(size_t)l * NC + ca] = ti;
-                    at_b[(size_t)b * NC + ca] = ti;
-                }
-                // rounds -> lists: up to the lane's last coloured round, gaps as nulls (-1)
-                for (int p = p0; p < p1; ++p) {
-                    int last = -1;
-                    for (int c = 0; c < NC; ++c) if (at_l[(size_t)(p % 32) * NC + c] >= 0) last = c;
-                    std::vector<int> nl(last + 1, -1), nc(last + 1, 0);
-                    for (int c = 0; c <= last; ++c) {
-                        const int ti = at_l[(size_t)(p % 32) * NC + c];
-                        if (ti >= 0) { nl[c] = toks[ti].e; nc[c] = toks[ti].copy; }
-                    }
-                    lists[p] = nl;
-                    ecopy[p] = nc;
-                }
-            }
-        } else if (R == 4 && o.schedule_banks >= 0) {
-            uint64_t rs = 0x2545F4914F6CDD1Dull;
-            auto rnd = [&]() { rs ^= rs << 13; rs ^= rs >> 7; rs ^= rs << 17; return rs; };
-            for (int g = 0; g < G; ++g) {
-                int kmax = 0;
-                for (int p = 32 * g; p < 32 * g + 32; ++p) kmax = std::max(kmax, (int)lists[p].size());
-                if (kmax < 1) continue;
-                std::vector<int> cnt((size_t)kmax * 32, 0);
-                auto bank = [&](int p, int k) { return nbr_pos(p, k) % 32; };
-                for (int p = 32 * g; p < 32 * g + 32; ++p)
-                    for (int k = 0; k < (int)lists[p].size(); ++k) cnt[(size_t)k * 32 + bank(p, k)]++;
-                auto rmax = [&](int k) { int m = 0; for (int b = 0; b < 32; ++b) m = std::max(m, cnt[(size_t)k * 32 + b]); return m; };
-                const long iters = 6000L * kmax;
-                for (long it = 0; it < iters; ++it) {
-                    const int p = 32 * g + (int)(rnd() % 32);
-                    const int n = (int)lists[p].size();
-                    if (n < 1) continue;
-                    if (pc.n > 1 && (rnd() & 1)) {          // another copy of a pinned neighbour
-                        const int k = (int)(rnd() % n);
-                        if (!pc.pinned(other(p, lists[p][k]))) continue;
-                        const int b0 = bank(p, k), c0 = ecopy[p][k];
-                        const int before = rmax(k);
-                        ecopy[p][k] = (c0 + 1 + (int)(rnd() % (pc.n - 1))) % pc.n;
-                        const int b1 = bank(p, k);
-                        cnt[(size_t)k * 32 + b0]--; cnt[(size_t)k * 32 + b1]++;
-                        if (rmax(k) > before) {
-                            cnt[(size_t)k * 32 + b1]--; cnt[(size_t)k * 32 + b0]++;
-                            ecopy[p][k] = c0;
-                        }
-                        continue;
-                    }
-                    if (n < 2) continue;
-                    const int ka = (int)(rnd() % n), kb = (int)(rnd() % n);
-                    const int ba = bank(p, ka), bb = bank(p, kb);
-                    if (ka == kb || ba == bb) continue;
-                    const int before = rmax(ka) + rmax(kb);
-                    cnt[(size_t)ka * 32 + ba]--; cnt[(size_t)kb * 32 + ba]++;
-                    cnt[(size_t)kb * 32 + bb]--; cnt[(size_t)ka * 32 + bb]++;
-                    if (rmax(ka) + rmax(kb) <= before) {
-                        std::swap(lists[p][ka], lists[p][kb]);
-                        std::swap(ecopy[p][ka], ecopy[p][kb]);
-                    } else {
-                        cnt[(size_t)ka * 32 + ba]++; cnt[(size_t)kb * 32 + ba]--;
-                        cnt[(size_t)kb * 32 + bb]++; cnt[(size_t)ka * 32 + bb]--;
-                    }
-                }
-            }
-        }
+        if (packed && einc_bytes == 4) colour_gather_rounds(lists, ecopy, G, Vf, pc, other);
+        else if (R == 4 && o.schedule_banks >= 0) order_gather_rounds(lists, ecopy, G, pc, other, nbr_pos);
         int base = 0;
         for (int g = 0; g < G; ++g) {
             int kmax = 0;
@@ -1685,45 +1742,7 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
     }
 
     // ---- phase-1 work split across warps -------------------------------------
-    const int NW = B / 32;
-    std::vector<int32_t> wsplit((size_t)n_chunks * (NW + 1), 0);
-    {
-        const double CE = 1.0;   // owner-gathered edge incidence vs one tet item (tuned on B200, tools/tune.py)
-        double CT = 4.0;
-        if (const char *env = std::getenv("TS_SPLIT_CT")) CT = std::atof(env);
-        for (int c = 0; c < n_chunks; ++c) {
-            const int nt = chunk_rec[c].tet_count;
-            const int nb = (nt + 31) / 32;
-            std::vector<double> ce(NW, 0.0);
-            if (eg && c == 0)
-                for (int w = 0; w < NW; ++w)
-                    for (int lane = 0; lane < 32; ++lane) {
-                        int sum = 0;
-                        for (int r = 0; r < VPT; ++r) {
-                            const int p = r * B + 32 * w + lane;
-                            if (p < Vf) sum += evalence[p];
-                        }
-                        ce[w] = std::max(ce[w], CE * sum);
-                    }
-            // smallest level T with sum_w floor((T - ce_w) / CT) >= nb batches (32 items each)
-            double lo = 0.0, hi = 1e9;
-            auto fits = [&](double T) {
-                long tot = 0;
-                for (int w = 0; w < NW; ++w) tot += std::max(0L, (long)std::floor((T - ce[w]) / CT));
-                return tot >= nb;
-            };
-            for (int it = 0; it < 100; ++it) { const double mid = 0.5 * (lo + hi); (fits(mid) ? hi : lo) = mid; }
-            int left = nb, start = 0;
-            for (int w = 0; w < NW; ++w) {
-                int take = std::min(left, std::max(0, (int)std::floor((hi - ce[w]) / CT)));
-                if (w == NW - 1) take = left;
-                wsplit[(size_t)c * (NW + 1) + w] = std::min(start, nt);
-                start += 32 * take;
-                left -= take;
-            }
-            wsplit[(size_t)c * (NW + 1) + NW] = nt;
-        }
-    }
+    const std::vector<int32_t> wsplit = warp_split(chunk_rec, evalence, eg, B, VPT, Vf);
 
     // sizes (bytes) per section
     int64_t sz[TS_SEC_COUNT];

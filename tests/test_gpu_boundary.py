@@ -152,3 +152,25 @@ def test_plugin_entries_typed():
             "ts_run_substeps")
     torch.cuda.synchronize()
     assert not torch.equal(xt, torch.as_tensor(x, device=dev))
+
+
+def test_pinned_host_actions_and_outputs_zero_copy():
+    """ts_env_step_dl reads actions from / writes outputs to page-locked host memory in place (the
+    zero-copy path of step_numpy): same results as device buffers; pageable host memory is rejected."""
+    envs = [_env("fp32", n=4) for _ in range(2)]
+    rng = np.random.default_rng(5)
+    for _ in range(5):
+        a = rng.uniform(-1, 1, (4, 3))
+        outs = []
+        for k, env in enumerate(envs):
+            pin = k == 1
+            act = torch.as_tensor(a).pin_memory() if pin else torch.as_tensor(a, device="cuda:0")
+            mk = (lambda shape, dt: torch.empty(shape, dtype=dt).pin_memory()) if pin else \
+                 (lambda shape, dt: torch.empty(shape, dtype=dt, device="cuda:0"))
+            o = {"obs": mk((4, 6), torch.float64), "reward": mk(4, torch.float64), "done_mask": mk(4, torch.bool)}
+            outs.append(_call_step(env, actions=act, outs=o))
+        for key in ("obs", "reward", "done_mask"):
+            assert torch.equal(outs[0][key].cpu(), outs[1][key].cpu()), key
+        assert torch.equal(envs[0].sim.x, envs[1].sim.x)
+    with pytest.raises(ValidationError, match="reward: expected a CUDA tensor or pinned host memory"):
+        _call_step(envs[0], outs={"reward": torch.empty(4, dtype=torch.float64)})

@@ -13,6 +13,8 @@ from paper_2503_18616_b200 import EnvBatch, load_scene  # noqa: E402
 from paper_2503_18616_b200.mesh import default_scene_path  # noqa: E402
 
 n = 4096
+if len(sys.argv) > 1 and sys.argv[1] == "zero-copy":
+    EnvBatch.numpy_zero_copy = True      # A/B: kernels read / write pinned host memory directly
 env = EnvBatch(load_scene(default_scene_path()), num_envs=n, device="cuda:0")
 env.reset()
 rng = np.random.default_rng(0)
