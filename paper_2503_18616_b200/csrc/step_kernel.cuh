@@ -886,8 +886,9 @@ __device__ __forceinline__ void owner_edges(const TsDevProg &P, const Smem<Real>
                 rc = lds2c(TS_TAB_OFF + 8 * (cur >> 16));
                 lds3c(cur & 0xffffu, qx, qy, qz);
             } else {
-                rc = 2 * P.n_rltab <= TS_TAB_CAP ? reinterpret_cast<const float2 *>(smem_tab(TS_TAB_OFF))[cur >> 16]
-                                                 : __ldg(reinterpret_cast<const float2 *>(P.rltab) + (cur >> 16));
+                // (the pair table through L1: a shared-memory copy behind a runtime test made the
+                // compiler rebuild the shared window per access, profiles/r02m config 2)
+                rc = __ldg(reinterpret_cast<const float2 *>(P.rltab) + (cur >> 16));
                 const float *nq = reinterpret_cast<const float *>(reinterpret_cast<const char *>(m.pos) + (cur & 0xffffu));
                 qx = nq[0]; qy = nq[1]; qz = nq[2];
             }
@@ -1237,8 +1238,7 @@ __device__ __forceinline__ void step_env(const TsDevProg &P, const TsDevProg *pr
         }
     }
     for (int p = t; p < (P.narrow ? P.Vf_pad / 4 : P.Vf_pad); p += B) m.deg[p] = 0;
-    if (FAST || (sizeof(Real) == 4 && P.einc_bytes == 4 && 2 * P.n_rltab <= TS_TAB_CAP)) {
-        // dictionary tables -> shared memory (read by every tet / edge of every substep)
+    if constexpr (FAST) {   // dictionary tables -> shared memory (read by every tet / edge of every substep)
         float *tab = const_cast<float *>(smem_tab(TS_TAB_OFF));
         for (int i = t; i < 2 * TS_TAB_CAP; i += B) {
             const int j = i - TS_TAB_CAP;
