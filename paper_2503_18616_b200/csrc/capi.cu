@@ -257,7 +257,9 @@ static int32_t create_handle(const ts_scene_desc *desc, const ts_layout_opts &o,
     } else {
         decode_part(hb, db, h->prog);
         h->smem = ts_smem_bytes(h->prog, R);
-        if (h->prog.fast && ts_smem_window(device) != TS_SMEM_WINDOW) h->prog.fast = 0;   // generic kernel
+        const bool window_ok = ts_smem_window(device) == TS_SMEM_WINDOW;   // else the generic kernel
+        if (!window_ok) h->prog.fast = 0;
+        h->prog.edges_ok = window_ok ? 1 : 0;
     }
     // L2 prefetch of the program by the command kernel: small programs only -- a multi-MB cluster
     // program's bulk prefetches keep the command kernel alive longer than they save (52,359-tet

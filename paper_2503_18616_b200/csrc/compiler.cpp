@@ -1164,7 +1164,9 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
     // overrides: 1, 2, 4 or 8)
     PinCopies pc;
     pc.Vf_pad = Vf_pad; pc.Vown = Vown; pc.Np_pad = Vown - Vf_pad;
-    if (prec == TS_F32 && !part && eg && o.schedule_banks >= 0 && pc.Np_pad > 0) pc.n = 4;
+    // (not for distance-only programs: the edges kernel is latency-bound and their coloured rounds
+    // measured 8% slower, profiles/r02m config 2)
+    if (prec == TS_F32 && !part && eg && o.schedule_banks >= 0 && pc.Np_pad > 0 && T > 0) pc.n = 4;
     if (const char *env = std::getenv("TS_PIN_COPIES")) {
         const int c = std::atoi(env);
         if (c == 1 || ((c == 2 || c == 4 || c == 8) && prec == TS_F32 && !part && pc.Np_pad > 0)) pc.n = c;

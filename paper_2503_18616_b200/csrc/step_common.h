@@ -74,6 +74,7 @@ struct TsDevProg {
     const uint4 *tet_c;
     int32_t narrow;           // single position buffer + byte degenerate counters (program.h)
     int32_t fast;             // the reach-scene shape: fast_step_kernel (step_kernel.cuh)
+    int32_t edges_ok;         // the shared window matches TS_SMEM_WINDOW: edges_step_kernel allowed
     const void *pf_base;      // the handle's whole device program (all parts): cmd_kernel prefetches
     int64_t pf_bytes;         //   it into L2 so the step kernel's first program reads do not go to HBM
     int32_t edge_gather;      // 1: owner-gathered edges (records below), positions double-buffered
@@ -180,8 +181,9 @@ uint32_t ts_smem_window(int device);
 inline bool ts_use_fast_kernel(const TsDevProg &P, int ablate) {
     return P.fast && P.B <= TS_STEP_MAXT && !(ablate & 256);
 }
-inline bool ts_use_edges_kernel(const TsDevProg &P) {
-    return P.n_chunks == 0 && P.VPT == 1 && P.B <= TS_EDGES_MAXT;
+inline bool ts_use_edges_kernel(const TsDevProg &P) {   // P.edges_ok: the shared window probe matched
+    return P.n_chunks == 0 && P.VPT == 1 && P.B <= TS_EDGES_MAXT && P.edges_ok && P.einc_bytes == 4 &&
+           2 * P.n_rltab <= TS_TAB_CAP;
 }
 template <typename Real>
 cudaError_t ts_launch_step(const TsDevProg &P, const TsParams &S, const TsLaunch &L, int grid,

@@ -848,7 +848,7 @@ __device__ void p1_atts(const TsDevProg &P, const Smem<Real> &m, int begin, int 
 // fp64: -(w_p scale) (x_p - x_q) with the reference's scale expression
 // (ts_lane_edges, _kernels.pyx:121-136) -- bitwise the reference's per-endpoint
 // term, see compiler.cpp; fp32: -coef (1 - rest / dist) (x_p - x_q) with FMAs.
-template <typename Real, bool FAST = false, bool HOIST = FAST>
+template <typename Real, bool FAST = false, bool HOIST = FAST, bool STAB = FAST>
 __device__ __forceinline__ void owner_edges(const TsDevProg &P, const Smem<Real> &m, int p, int lane, Real px,
                                             Real py, Real pz, Real ks, Real &ax, Real &ay, Real &az, int &ndeg,
                                             int ev_h = 0, int rb_h = 0) {
@@ -886,9 +886,10 @@ __device__ __forceinline__ void owner_edges(const TsDevProg &P, const Smem<Real>
                 rc = lds2c(TS_TAB_OFF + 8 * (cur >> 16));
                 lds3c(cur & 0xffffu, qx, qy, qz);
             } else {
-                // (the pair table through L1: a shared-memory copy behind a runtime test made the
-                // compiler rebuild the shared window per access, profiles/r02m config 2)
-                rc = __ldg(reinterpret_cast<const float2 *>(P.rltab) + (cur >> 16));
+                // STAB (the edges kernel): the pair table from its shared copy at a constant address;
+                // otherwise through L1
+                rc = STAB ? lds2c(TS_TAB_OFF + 8 * (cur >> 16))
+                          : __ldg(reinterpret_cast<const float2 *>(P.rltab) + (cur >> 16));
                 const float *nq = reinterpret_cast<const float *>(reinterpret_cast<const char *>(m.pos) + (cur & 0xffffu));
                 qx = nq[0]; qy = nq[1]; qz = nq[2];
             }
@@ -1238,7 +1239,7 @@ __device__ __forceinline__ void step_env(const TsDevProg &P, const TsDevProg *pr
         }
     }
     for (int p = t; p < (P.narrow ? P.Vf_pad / 4 : P.Vf_pad); p += B) m.deg[p] = 0;
-    if constexpr (FAST) {   // dictionary tables -> shared memory (read by every tet / edge of every substep)
+    if constexpr (FAST || EO) {   // dictionary tables -> shared memory (read by every tet / edge of every substep)
         float *tab = const_cast<float *>(smem_tab(TS_TAB_OFF));
         for (int i = t; i < 2 * TS_TAB_CAP; i += B) {
             const int j = i - TS_TAB_CAP;
@@ -1453,8 +1454,8 @@ __device__ __forceinline__ void step_env(const TsDevProg &P, const TsDevProg *pr
                 for (int r = 0; r < VPT; ++r) {
                     const int p = r * B + t;
                     if (P.edge_gather && P.n_chunks == 0 && p < P.Vf)   // distance constraints only
-                        owner_edges<Real>(P, m, p, lane, xr[r], yr[r], zr[r], ks, accx[r], accy[r], accz[r],
-                                          ndeg[r]);
+                        owner_edges<Real, false, false, EO>(P, m, p, lane, xr[r], yr[r], zr[r], ks, accx[r],
+                                                            accy[r], accz[r], ndeg[r]);
                     add_grasp(r);
                 }
             }
@@ -1762,6 +1763,7 @@ __global__ void __launch_bounds__(TS_EDGES_MAXT, TS_EDGES_MINB) edges_step_kerne
                                                             const __grid_constant__ TsLaunch L) {
     pdl_trigger();   // the epilogue may launch early; it waits for this grid before reading
     extern __shared__ __align__(16) unsigned char smem_raw[];
+    if (smem_u32(0) != TS_SMEM_WINDOW) __trap();   // constant shared addresses (lds2c): never silently wrong
     Smem<Real> m = carve<Real>(P, smem_raw);
     if ((L.mode & TS_M_CHECK_ACTIONS) && *L.bad_flag) return;
     for (int64_t env = blockIdx.x; env < L.n_env; env += gridDim.x)
