@@ -1217,6 +1217,43 @@ __device__ __forceinline__ void step_env(const TsDevProg &P, const TsDevProg *pr
     Real *xg = reinterpret_cast<Real *>(L.x) + env * (int64_t)P.V * 3;
     Real *vg = reinterpret_cast<Real *>(L.v) + env * (int64_t)P.V * 3;
 
+    // FAST (one chunk): the per-vertex program words are substep-invariant -> registers, loaded first
+    // so their (after an L2 flush, HBM) latency overlaps the state load and the command kernel
+    int h_base[VPT], h_val[VPT], h_pre[VPT], h_cnt[VPT], h_ev[VPT], h_rb[VPT];
+    int h_tb = 0, h_wb = 0, h_we = 0;   // FAST: the chunk's tet base and this warp's range
+    // cluster parts (a few warps per CTA, latency-bound): the substep-invariant per-vertex words
+    // in registers too -- counts and edge rows always, chunk 0's slot rows when it is the only one
+    constexpr bool HC = CL && sizeof(Real) == 4;   // (the fp64 cluster kernels are out of registers already)
+    const bool hc1 = HC && P.n_chunks == 1;
+    if constexpr (HC) {
+        const TsChunk ch0 = P.chunks[0];
+#pragma unroll
+        for (int r = 0; r < VPT; ++r) {
+            const int p = max(0, min(r * B + t, P.Vf - 1));
+            h_cnt[r] = P.static_cnt[p];
+            h_ev[r] = P.edge_gather ? P.evalence[p] : 0;
+            h_rb[r] = P.edge_gather ? P.eregion[p >> 5] + lane : 0;
+            h_base[r] = hc1 ? P.region[ch0.region_off + (p >> 5)] + lane : 0;
+            h_val[r] = hc1 ? P.valence[ch0.val_off + p] : 0;
+            h_pre[r] = hc1 ? min(h_val[r], P.gsplit[p]) : 0;
+        }
+    }
+    if constexpr (FAST) {
+        const TsChunk ch0 = P.chunks[0];
+        h_tb = ch0.tet_begin;
+        h_wb = P.wsplit[t >> 5];
+        h_we = P.wsplit[(t >> 5) + 1];
+#pragma unroll
+        for (int r = 0; r < VPT; ++r) {
+            const int p = max(0, min(r * B + t, P.Vf - 1));   // rows past Vf are never used
+            h_base[r] = 12 * (P.Vstore + P.region[ch0.region_off + (p >> 5)] + lane);   // bytes from smem_base
+            h_val[r] = P.valence[ch0.val_off + p];
+            h_pre[r] = min(h_val[r], P.gsplit[p]);
+            h_cnt[r] = P.static_cnt[p];
+            h_ev[r] = P.evalence[p];
+            h_rb[r] = P.eregion[p >> 5] + lane;
+        }
+    }
     // ---- A. the state load, then the env's command block (cmd_kernel) ---
     // state -> shared (storage order) / registers: the command kernel does not write x / v, so
     // under programmatic dependent launch this overlaps the command kernel's tail
@@ -1335,42 +1372,6 @@ __device__ __forceinline__ void step_env(const TsDevProg &P, const TsDevProg *pr
         }
         if constexpr (CL) cl::sync();
         else __syncthreads();
-        // FAST (one chunk): the per-vertex program words are substep-invariant -> registers
-        int h_base[VPT], h_val[VPT], h_pre[VPT], h_cnt[VPT], h_ev[VPT], h_rb[VPT];
-        int h_tb = 0, h_wb = 0, h_we = 0;   // FAST: the chunk's tet base and this warp's range
-        // cluster parts (a few warps per CTA, latency-bound): the substep-invariant per-vertex words
-        // in registers too -- counts and edge rows always, chunk 0's slot rows when it is the only one
-        constexpr bool HC = CL && sizeof(Real) == 4;   // (the fp64 cluster kernels are out of registers already)
-        const bool hc1 = HC && P.n_chunks == 1;
-        if constexpr (HC) {
-            const TsChunk ch0 = P.chunks[0];
-#pragma unroll
-            for (int r = 0; r < VPT; ++r) {
-                const int p = max(0, min(r * B + t, P.Vf - 1));
-                h_cnt[r] = P.static_cnt[p];
-                h_ev[r] = P.edge_gather ? P.evalence[p] : 0;
-                h_rb[r] = P.edge_gather ? P.eregion[p >> 5] + lane : 0;
-                h_base[r] = hc1 ? P.region[ch0.region_off + (p >> 5)] + lane : 0;
-                h_val[r] = hc1 ? P.valence[ch0.val_off + p] : 0;
-                h_pre[r] = hc1 ? min(h_val[r], P.gsplit[p]) : 0;
-            }
-        }
-        if constexpr (FAST) {
-            const TsChunk ch0 = P.chunks[0];
-            h_tb = ch0.tet_begin;
-            h_wb = P.wsplit[t >> 5];
-            h_we = P.wsplit[(t >> 5) + 1];
-#pragma unroll
-            for (int r = 0; r < VPT; ++r) {
-                const int p = max(0, min(r * B + t, P.Vf - 1));   // rows past Vf are never used
-                h_base[r] = 12 * (P.Vstore + P.region[ch0.region_off + (p >> 5)] + lane);   // bytes from smem_base
-                h_val[r] = P.valence[ch0.val_off + p];
-                h_pre[r] = min(h_val[r], P.gsplit[p]);
-                h_cnt[r] = P.static_cnt[p];
-                h_ev[r] = P.evalence[p];
-                h_rb[r] = P.eregion[p >> 5] + lane;
-            }
-        }
         const double d0 = sc.drag[0], d1 = sc.drag[1], d2 = sc.drag[2];
         // grasp contribution of owner slot r: after the vertex's edges (_kernels.pyx:283-298)
         auto add_grasp = [&](int r) {
