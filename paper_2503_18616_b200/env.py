@@ -341,18 +341,13 @@ class EnvBatch:
             if not fx["zc"]:
                 fx["host"].copy_(fx["dev_buf"], non_blocking=True)
 
-        with torch.cuda.device(dev):
-            if fx["graph"] is not None and fx["sig"] is self.sim._state:
-                fx["graph"].replay()
-            else:
-                device_side()                       # eager (first call / state tensors replaced) ...
-                fx["done"].record()
-                fx["done"].synchronize()
-                graph = torch.cuda.CUDAGraph()      # ... then record the graph for the next calls
-                with torch.cuda.graph(graph):
-                    device_side()
-                fx["graph"], fx["sig"] = graph, self.sim._state
+        if fx["graph"] is not None and fx["sig"] is self.sim._state and torch.cuda.current_device() == dev.index:
+            fx["graph"].replay()                    # the steady state: one graph launch, no context switch
             fx["done"].record()
+        else:
+            with torch.cuda.device(dev):
+                self._step_numpy_record(fx, device_side)
+                fx["done"].record()
         fx["done"].synchronize()
         self.sim.step_count += 1
         block = fx["raw"].copy()          # one host copy of the packed block; the arrays are views of it
@@ -366,6 +361,20 @@ class EnvBatch:
             "final_observation": out["final_obs"] if done.any() else None,
         }
         return out["obs"], out["reward"], out["terminated"], out["truncated"], info
+
+    def _step_numpy_record(self, fx, device_side):
+        """step_numpy off the steady state: replay on another current device, or -- first call /
+        a state tensor replaced -- one eager step, then the graph of the device side."""
+        if fx["graph"] is not None and fx["sig"] is self.sim._state:
+            fx["graph"].replay()
+            return
+        device_side()
+        fx["done"].record()
+        fx["done"].synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            device_side()
+        fx["graph"], fx["sig"] = graph, self.sim._state
 
     def step(self, actions, validate=True, tool_override=None):
         """env.py:144-197 on the GPU.  Returns (obs, reward, terminated, truncated, info).

@@ -177,7 +177,10 @@ class Simulation:
         keys = (self.x, self.v, self.tool.axis, self.tool.jaw_dir, self.tool.reach,
                 self.tool.clamp_angle, self.grasp_vertex, self.grasped, self._steps, self._l_prev,
                 self._return)
-        sig = tuple((t.data_ptr(), t.dtype, tuple(t.shape), t.stride()) for t in keys)
+        # (tensor object, storage address): a replaced or reallocated tensor rebuilds the views; shape
+        # and stride changes in place are seen through the views (they point at the tensor's own
+        # size / stride arrays) and checked by the library on every call
+        sig = tuple((id(t), t.data_ptr()) for t in keys)
         if self._state is None or self._state[0] != sig:
             self._state = (sig, N.dl_struct(N.EnvTensors, N.ENV_TENSORS, dict(zip(N.ENV_TENSORS, keys))))
         return self._state[1]
