@@ -11,12 +11,15 @@
   reduces phase-1 shared-memory conflicts.
 """
 
+import os
+import sys
+
 import numpy as np
 import pytest
 
 import oracle as O
 import program_interp as PI
-from conftest import build_slab_scene
+from conftest import ROOT, build_slab_scene
 from paper_2503_18616_b200 import scene as S
 
 
@@ -380,3 +383,34 @@ def test_latency_block_policy():
     assert b(294, 1, 148, "fp32") == 384 and b(294, 148, 148, "fp32") == 384
     assert b(294, 149, 148, "fp32") == 0 and b(294, 1, 148, "fp64") == 0
     assert b(500, 1, 148, "fp32") == 0           # 512 cap: no wider than the default 512
+
+
+def test_fast_program_is_bank_conflict_free(reach_scene):
+    """The fp32 production program (pinned copies, packed tet batches, coloured gather rounds,
+    DESIGN.md §2.5): replaying its shared-memory accesses per warp instruction
+    (tools/bank_model.py) every phase-1 / phase-2 access is served in its ideal number of
+    wavefronts -- the compiler's conflict-free construction, checked on the blob the kernel reads."""
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    import bank_model
+    blob, info = S.compile_program(_arrays(reach_scene), precision="fp32")
+    assert info["bank_conflicts_p1"] == 0
+    out = bank_model.model(PI.Program(blob))
+    for cat, (ideal, modelled) in out.items():
+        assert modelled == ideal, (cat, ideal, modelled)
+    # every tet appears exactly once, and the rest volume carries the sign of its (permuted) corner
+    # order: at rest the stored 6 V0 equals the signed 6 V of the corners in program order
+    mesh, rest, _ = reach_scene
+    p = PI.Program(blob)
+    live = (p.tet_slot >= 0).any(axis=1)
+    idx, rv = p.tet_idx[live], p.tet_rv[live]
+    verts = p.s2o[idx]                                      # storage (or pinned-copy) position -> vertex
+    assert sorted(map(tuple, np.sort(verts, axis=1))) == sorted(map(tuple, np.sort(mesh.tets, axis=1)))
+    X = mesh.positions_rest
+    a, b, c, d = (X[verts[:, k]] for k in range(4))
+    six_v = np.einsum("ij,ij->i", np.cross(b - a, c - a), d - a)
+    assert np.allclose(rv, six_v, rtol=1e-5, atol=1e-12)
+    # the kernel reads 6 V0 through the dictionary index in the stream's spare bits
+    tab = p.sec("RVTAB", np.float32, p.h["n_rvtab"]).astype(np.float64)
+    q = p.tet_c[live]
+    ri = ((q[:, 0] >> 14) & 3) | ((q[:, 0] >> 28) & 12) | ((q[:, 1] >> 10) & 48) | ((q[:, 1] >> 24) & 192)
+    assert np.array_equal(tab[ri], rv)
