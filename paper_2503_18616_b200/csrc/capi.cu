@@ -321,9 +321,9 @@ static int launch(ts_handle *h, const TsLaunch &L_in, cudaStream_t s) {
     TsLaunch L = L_in;
     L.cmd = h->cmd;
     int grid = (int)std::min<int64_t>(L.n_env, h->max_grid > 0 ? h->max_grid : (int64_t)1 << 30);
-    cudaError_t e = ts_launch_cmd(h->prog, h->params, L, s);
-    if (e != cudaSuccess) return cuda_fail(e, "command kernel launch");
     const bool timed = 2 * h->tev_used + 1 < (int64_t)h->tev.size();
+    cudaError_t e = ts_launch_cmd(h->prog, h->params, L, s, !(h->params.ablate & 1024));
+    if (e != cudaSuccess) return cuda_fail(e, "command kernel launch");
     // programmatic dependent launch of step and epilogue (each overlaps its predecessor's tail);
     // off while the step kernel is being timed, so its events bracket exactly its own execution
     const bool pdl = !timed && !(h->params.ablate & 1024);
@@ -837,6 +837,7 @@ __global__ void counter_kernel(uint64_t *c) { *c += 1; }
 // small draws: one block reads the device counter, draws, and bumps it itself (one launch)
 __global__ void __launch_bounds__(1024) uniform_bump_kernel(double *out, int64_t n, int64_t first, uint64_t seed,
                                                             uint64_t *dev_counter) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");   // the command kernel may start its prologue
     const uint64_t counter = *dev_counter;
     for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
         const uint64_t r = splitmix64(seed ^ splitmix64(counter * 0x100000001B3ull + (uint64_t)(i + first)));

@@ -192,7 +192,8 @@ cudaError_t ts_launch_step(const TsDevProg &P, const TsParams &S, const TsLaunch
 template <typename Real>
 cudaError_t ts_launch_cluster_step(const TsDevProg *parts, int VPT, int K, int B, const TsParams &S,
                                    const TsLaunch &L, int n_clusters, int smem, cudaStream_t stream);
-cudaError_t ts_launch_cmd(const TsDevProg &P, const TsParams &S, const TsLaunch &L, cudaStream_t stream);
+cudaError_t ts_launch_cmd(const TsDevProg &P, const TsParams &S, const TsLaunch &L, cudaStream_t stream,
+                          bool pdl = false);
 // pdl: programmatic dependent launch -- the kernel may start while the previous kernel of the
 // stream (this library's own command / step kernel) runs, and waits (griddepcontrol.wait) before it
 // reads that kernel's results

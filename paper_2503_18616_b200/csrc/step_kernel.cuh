@@ -1097,8 +1097,6 @@ static __device__ __forceinline__ void env_epilogue(const TsParams &S, const TsL
 static __global__ void __launch_bounds__(128) cmd_kernel(const __grid_constant__ TsDevProg P,
                                                   const __grid_constant__ TsParams S,
                                                   const __grid_constant__ TsLaunch L) {
-    pdl_trigger();   // the step kernel may launch now: it only reads the state before pdl_wait
-    if ((L.mode & TS_M_CHECK_ACTIONS) && *L.bad_flag) return;   // deferred ValidationError
     if (blockIdx.x == 0 && P.pf_base && !(S.ablate & 512)) {
         // the step kernel that follows reads the whole program every substep: start its L2 fill
         // now (bulk prefetch, 16 KB per request, fire and forget) -- after an L2 flush the
@@ -1109,6 +1107,13 @@ static __global__ void __launch_bounds__(128) cmd_kernel(const __grid_constant__
             asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(b + off), "r"(n) : "memory");
         }
     }
+    // launched with programmatic dependent launch: the prefetch above overlaps the stream's previous
+    // kernel (e.g. the action producer); its outputs are read only after this wait
+    pdl_wait();
+    // the step kernel may launch now (it reads the state and the action-check flag before its own
+    // pdl_wait: both are final once this kernel's predecessors are)
+    pdl_trigger();
+    if ((L.mode & TS_M_CHECK_ACTIONS) && *L.bad_flag) return;   // deferred ValidationError
     for (int64_t env = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; env < L.n_env;
          env += (int64_t)gridDim.x * blockDim.x)
         env_command(P, S, L, env, L.cmd[env]);
@@ -1922,8 +1927,11 @@ static int scalar_grid(int64_t n) {
     return (int)(g < 1 ? 1 : (g > 65535 ? 65535 : g));
 }
 
-cudaError_t ts_launch_cmd(const TsDevProg &P, const TsParams &S, const TsLaunch &L, cudaStream_t stream) {
-    tsk::cmd_kernel<<<scalar_grid(L.n_env), 128, 0, stream>>>(P, S, L);
+cudaError_t ts_launch_cmd(const TsDevProg &P, const TsParams &S, const TsLaunch &L, cudaStream_t stream,
+                          bool pdl) {
+    cudaError_t e = ts_launch_pdl(tsk::cmd_kernel, dim3((unsigned)scalar_grid(L.n_env)), dim3(128), 0, stream, pdl,
+                                  P, S, L);
+    if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
 
