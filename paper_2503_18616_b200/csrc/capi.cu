@@ -148,6 +148,7 @@ static void decode_part(const uint8_t *host, const uint8_t *b, TsDevProg &P) {
     P.evalence = reinterpret_cast<const int32_t *>(b + H->off[TS_SEC_EVAL]);
     P.face_gid = reinterpret_cast<const int32_t *>(b + H->off[TS_SEC_FACE_GID]);
     P.Vown = H->Vown; P.cluster_k = H->cluster_k; P.cluster_rank = H->cluster_rank; P.boff = H->boff;
+    P.real_bytes = H->real_bytes;
     P.send_off = reinterpret_cast<const int32_t *>(b + H->off[TS_SEC_SEND_OFF]);
     P.send = reinterpret_cast<const int32_t *>(b + H->off[TS_SEC_SEND]);
     P.face_own = reinterpret_cast<const int32_t *>(b + H->off[TS_SEC_FACE_OWN]);

@@ -75,6 +75,7 @@ struct TsDevProg {
     int32_t narrow;           // single position buffer + byte degenerate counters (program.h)
     int32_t fast;             // the reach-scene shape: fast_step_kernel (step_kernel.cuh)
     int32_t edges_ok;         // the shared window matches TS_SMEM_WINDOW: edges_step_kernel allowed
+    int32_t real_bytes;       // 4 (fp32 state) or 8 (fp64)
     const void *pf_base;      // the handle's whole device program (all parts): cmd_kernel prefetches
     int64_t pf_bytes;         //   it into L2 so the step kernel's first program reads do not go to HBM
     int32_t edge_gather;      // 1: owner-gathered edges (records below), positions double-buffered
