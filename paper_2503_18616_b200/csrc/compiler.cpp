@@ -1293,6 +1293,8 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
 
     // ---- phase-1 schedule (per chunk, per kind) ----------------------------
     const bool sched = o.schedule_banks >= 0;
+    const char *pack_env = std::getenv("TS_PACK_TETS");   // development switch: 0 = round-1 schedule
+    const bool packed = pc.n > 1 && sched && o.schedule_banks != 2 && (!pack_env || std::atoi(pack_env) != 0);
     const int bank_mod = (R == 8) ? 16 : 32;
     std::vector<TsChunk> chunk_rec(n_chunks);
     std::vector<Item> all_items[3];
@@ -1308,8 +1310,10 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
             int conf = 0;
             // tets may get idle lanes (TS_TET_HOLES per 32-item batch) where no conflict-free
             // item is left; every tet still runs exactly once (off by default: slower on B200)
-            std::vector<Item> s = schedule_items(part, bank_mod, 32, sched && kind != TS_CHUNK_ATT, &conf,
-                                                 (kind == TS_CHUNK_TET && o.schedule_banks >= 0) ? g_tet_holes : 0);
+            // (packed programs re-batch their tets from scratch below: no greedy schedule for them)
+            std::vector<Item> s = schedule_items(part, bank_mod, 32,
+                                                 sched && kind != TS_CHUNK_ATT && !(packed && kind == TS_CHUNK_TET),
+                                                 &conf, (kind == TS_CHUNK_TET && o.schedule_banks >= 0) ? g_tet_holes : 0);
             begin[k] = (int)all_items[k].size();
             count[k] = (int)s.size();
             all_items[k].insert(all_items[k].end(), s.begin(), s.end());
@@ -1322,8 +1326,6 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
     }
     // fp32 gather programs with pinned copies: lanes balanced for the owner edge gather, then tets
     // packed into conflict-free batches (balance_lanes, pack_tet_batches)
-    const bool packed = sched && o.schedule_banks != 2 && pc.n > 1 && std::getenv("TS_PACK_TETS") == nullptr
-                        ? true : (std::getenv("TS_PACK_TETS") && std::atoi(std::getenv("TS_PACK_TETS")) && pc.n > 1);
     if (packed) {
         std::vector<std::vector<int>> nbrs(V);
         std::vector<int> tetval(V, 0);
