@@ -54,6 +54,7 @@ static const char *ts_kernel_name_for(const TsDevProg &P, int real_bytes, int cl
         "tsk::cluster_step_kernel<double, 2>", "tsk::cluster_step_kernel<double, 4>"};
     const int d = real_bytes == 8;
     if (cluster_k > 1) return names[10 + 3 * d + (P.VPT <= 1 ? 0 : P.VPT <= 2 ? 1 : 2)];
+    if (d && P.VPT == 1 && P.B <= 320 && !(ablate & 2048)) return "tsk::step2_kernel<double>";
     if (!d && ts_use_fast_kernel(P, ablate)) return names[0];
     if (!d && ts_use_edges_kernel(P)) return names[1];
     const int v = P.VPT <= 1 ? 0 : P.VPT == 2 ? 1 : P.VPT <= 4 ? 2 : 3;   // VPT 3 runs the 4 kernel

@@ -1189,8 +1189,11 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
     // fp32: one thread per free vertex (3 CTAs/SM fit); fp64 runs 1 CTA/SM (shared memory), so it
     // takes 1.5x the threads to widen phase 1 (measured on B200: 3.81 vs 4.30 ms at 4096 envs)
     // cluster parts: 1.5x too -- one env's CTAs run a few warps each and are latency-bound
+    // fp64 programs of at most 320 free positions: one thread per vertex and two CTAs per SM
+    // (step2_kernel) beat 1.5x threads at one CTA per SM
+    const bool wide = (R == 8 && Vf_pad > 320) || part;
     int B = o.block_threads > 0 ? o.block_threads
-                                : std::min(512, std::max(64, (R == 8 || part) ? roundup(Vf_pad * 3 / 2, 32) : Vf_pad));
+                                : std::min(512, std::max(64, wide ? roundup(Vf_pad * 3 / 2, 32) : Vf_pad));
     if (part && part->force_B) B = part->force_B;
     if (B % 32 != 0 || B < 32 || B > 512) { err = "block_threads must be a multiple of 32 in [32, 512]"; return TS_ERR_INVALID; }
     const int VPT = std::max(1, (Vf_pad + B - 1) / B);

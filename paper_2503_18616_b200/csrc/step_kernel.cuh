@@ -1744,6 +1744,20 @@ __global__ void __launch_bounds__(TS_STEP_MAXT, sizeof(Real) == 4 ? TS_STEP_MINB
         step_env<Real, VPT, false>(P, nullptr, S, L, m, env, 0);
 }
 
+// The fp64 validation build of a one-vertex-per-thread program of at most 320 threads: two CTAs per
+// SM (at most 102 registers; two fp64 reach CTAs fit the shared memory) instead of one.
+template <typename Real>
+__global__ void __launch_bounds__(320, 2) step2_kernel(const __grid_constant__ TsDevProg P,
+                                                   const __grid_constant__ TsParams S,
+                                                   const __grid_constant__ TsLaunch L) {
+    pdl_trigger();
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    Smem<Real> m = carve<Real>(P, smem_raw);
+    if ((L.mode & TS_M_CHECK_ACTIONS) && *L.bad_flag) return;
+    for (int64_t env = blockIdx.x; env < L.n_env; env += gridDim.x)
+        step_env<Real, 1, false>(P, nullptr, S, L, m, env, 0);
+}
+
 // The reach-scene shape (fp32, one CTA, one chunk, owner-gathered edges in 4-byte records, byte-offset
 // tet stream with dictionary-coded volumes, no attachments, narrow layout): every layout test resolved
 // at compile time.  ts_fast_program() is the host-side test.
@@ -1863,6 +1877,8 @@ cudaError_t ts_launch_step(const TsDevProg &P, const TsParams &S, const TsLaunch
     if constexpr (sizeof(Real) == 4) {   // shape-specialised fp32 kernels
         if (ts_use_fast_kernel(P, S.ablate)) fn = tsk::fast_step_kernel<Real>;
         else if (ts_use_edges_kernel(P)) fn = tsk::edges_step_kernel<Real>;
+    } else {
+        if (P.VPT == 1 && P.B <= 320 && !(S.ablate & 2048)) fn = tsk::step2_kernel<Real>;
     }
     if (!fn) switch (P.VPT) {
         case 1: fn = tsk::step_kernel<Real, 1>; break;
