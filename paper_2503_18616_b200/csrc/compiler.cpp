@@ -22,6 +22,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <numeric>
 #include <string>
 #include <vector>
@@ -1047,6 +1048,177 @@ std::vector<int32_t> warp_split(const std::vector<TsChunk> &chunk_rec, const std
     return wsplit;
 }
 
+// The owner-gathered distance constraints of a program (EINC / EREGION / EVAL / RLTAB sections).
+struct GatherSpec {
+    const ts_scene_desc *d;
+    const std::vector<char> *edge_live;
+    const std::vector<int> *o2s, *s2o;
+    const PinCopies *pc;
+    std::function<bool(int)> own_free, is_free;
+    int Vf, Vf_pad, G, Vstore, R;
+    bool boff, compact, packed, schedule;
+};
+struct GatherProgram {
+    std::vector<float> pair_tab;              // 4-byte records: {rest length, coefficient} pairs
+    std::vector<int32_t> eregion, evalence;   // [G] base record of each warp group, [Vf_pad] records per vertex
+    std::vector<uint8_t> einc;                // the records, warp-interleaved
+    int einc_bytes = 0, n_einc = 0;           // record size; live (edge, free endpoint) incidences
+};
+
+// Free vertex p walks its live incident edges in edge-index order (the reference's
+// accumulation order, _kernels.pyx:102-139).  Its correction from edge (a, b) is
+//   -(w_p scale) (x_p - x_q),  scale = m ks (dist - rest) / (dist (w_a + w_b) + (1 - m)),
+// bitwise the reference's (-w_a scale) dx for p = a and (w_b scale) dx for p = b, since
+// x_b - x_a = -(x_a - x_b) exactly and the squares / weight sum are symmetric.
+// fp32 byte-offset programs whose rest lengths take few distinct fp32 values (a structured
+// slab has 2) use 4-byte records: {neighbour offset (16) | pair index (16)} with a small table
+// of (rest length, coefficient) pairs -- coefficient = -k_s w_p / (w_p + w_q), i.e. -k_s / 2,
+// or -k_s for a pinned neighbour (uniform free mass) -- half the L1 footprint of the edge
+// stream and one shared load for both operands.  Pair 0 is the null record {0, 0} (a gap of
+// the conflict-free rounds): its term is exactly zero.
+// static_cnt gains one per live incidence (and per null record that reads its own position).
+GatherProgram build_gather(const GatherSpec &gs, std::vector<int32_t> &static_cnt) {
+    const ts_scene_desc &d = *gs.d;
+    const int E = d.n_edge;
+    const double *w = d.inverse_mass;
+    const std::vector<char> &edge_live = *gs.edge_live;
+    const std::vector<int> &o2s = *gs.o2s, &s2o = *gs.s2o;
+    const PinCopies &pc = *gs.pc;
+    const int Vf = gs.Vf, Vf_pad = gs.Vf_pad, G = gs.G, Vstore = gs.Vstore, R = gs.R;
+    const bool boff = gs.boff, compact = gs.compact, packed = gs.packed;
+    const auto &own_free = gs.own_free;
+    const auto &is_free = gs.is_free;
+    GatherProgram out;
+    std::vector<float> rl_tab;
+    std::vector<int> rl_idx(E, -1);
+    if (boff && 12 * Vstore <= 65535) {
+        std::vector<float> vals;
+        for (int e = 0; e < E; ++e) if (edge_live[e]) vals.push_back((float)d.rest_length[e]);
+        std::sort(vals.begin(), vals.end());
+        vals.erase(std::unique(vals.begin(), vals.end()), vals.end());
+        if ((int)vals.size() <= 256) {
+            rl_tab = vals;
+            for (int e = 0; e < E; ++e)
+                if (edge_live[e])
+                    rl_idx[e] = (int)(std::lower_bound(vals.begin(), vals.end(), (float)d.rest_length[e]) - vals.begin());
+        }
+    }
+    out.einc_bytes = !rl_tab.empty() ? 4 : ((R == 4 && compact) ? 8 : 16);
+    const int einc_bytes = out.einc_bytes;
+    std::vector<float> &pair_tab = out.pair_tab;     // RLTAB section of 4-byte programs: {rl, coef} pairs
+    auto pair_index = [&](int e, bool pinned_nbr) {   // 1 + 2 * rest-length index + pinned
+        return 1 + 2 * rl_idx[e] + (pinned_nbr ? 1 : 0);
+    };
+    if (einc_bytes == 4) {
+        pair_tab.assign(2 * (1 + 2 * rl_tab.size()), 0.0f);
+        const float ks_f = (float)d.k_s;
+        for (size_t i = 0; i < rl_tab.size(); ++i)
+            for (int pin = 0; pin < 2; ++pin) {
+                const int k = 1 + 2 * (int)i + pin;
+                pair_tab[2 * k] = rl_tab[i];
+                pair_tab[2 * k + 1] = -(pin ? ks_f : 0.5f * ks_f);
+            }
+    }
+    out.eregion.assign(G, 0);
+    out.evalence.assign(Vf_pad, 0);
+    std::vector<int32_t> &eregion = out.eregion, &evalence = out.evalence;
+    std::vector<uint8_t> &einc = out.einc;
+    int &n_einc = out.n_einc;
+    {
+        std::vector<std::vector<int>> lists(Vf_pad);
+        for (int e = 0; e < E; ++e) {
+            if (!edge_live[e]) continue;
+            const int a = d.edges[2 * e], b = d.edges[2 * e + 1];
+            if (own_free(a)) lists[o2s[a]].push_back(e);
+            if (own_free(b)) lists[o2s[b]].push_back(e);
+        }
+        // fp32: the order of a vertex's edges is free (fp64 keeps edge-index order, the reference's
+        // summation order).  In round k the 32 lanes of a warp read their k-th neighbours: permute
+        // each lane's list so the neighbours of one round sit in distinct banks as far as possible
+        // (deterministic local search, sum over rounds of the largest bank multiplicity)
+        // a pinned neighbour may be read from any of its copies (PinCopies): a second move kind
+        std::vector<std::vector<int>> ecopy(Vf_pad);
+        for (int p = 0; p < Vf_pad; ++p) ecopy[p].assign(lists[p].size(), 0);
+        auto other = [&](int p, int e) {
+            const int a = d.edges[2 * e], b = d.edges[2 * e + 1];
+            return o2s[a == s2o[p] ? b : a];
+        };
+        auto nbr_pos = [&](int p, int k) { return pc.pos(other(p, lists[p][k]), ecopy[p][k]); };
+        if (packed && einc_bytes == 4) colour_gather_rounds(lists, ecopy, G, Vf, pc, other);
+        else if (R == 4 && gs.schedule) order_gather_rounds(lists, ecopy, G, pc, other, nbr_pos);
+        int base = 0;
+        for (int g = 0; g < G; ++g) {
+            int kmax = 0;
+            for (int p = 32 * g; p < 32 * g + 32; ++p) kmax = std::max(kmax, (int)lists[p].size());
+            eregion[g] = base;
+            base += 32 * kmax;
+        }
+        einc.assign(((size_t)base + 32) * einc_bytes, 0);   // + one padding row: unclamped prefetch
+        // null records read a pinned position on a bank their round leaves free (no conflict; a
+        // pinned neighbour is never within 1e-12 of a free vertex, so the null is not degenerate),
+        // or -- when no such position exists -- their own position (dx = 0: degenerate, counted in
+        // static_cnt so the applied count is unchanged)
+        std::vector<int> pin_at_bank(32, -1);
+        for (int q = Vf_pad; q < Vstore; ++q)
+            if (s2o[q] >= 0 && !is_free(s2o[q]) && pin_at_bank[q % 32] < 0) pin_at_bank[q % 32] = q;
+        std::vector<int> null_pos((size_t)G * 64, -2);   // per (warp, round): chosen position (-1: own)
+        auto null_for = [&](int g, int k) {
+            int &np = null_pos[(size_t)g * 64 + std::min(k, 63)];
+            if (np != -2 && k < 64) return np;
+            std::vector<char> used(32, 0);
+            for (int q = 32 * g; q < std::min(Vf, 32 * g + 32); ++q)
+                if (k < (int)lists[q].size() && lists[q][k] >= 0) used[nbr_pos(q, k) % 32] = 1;
+            int pos = -1;
+            for (int b = 0; b < 32 && pos < 0; ++b) if (!used[b] && pin_at_bank[b] >= 0) pos = pin_at_bank[b];
+            if (k < 64) np = pos;
+            return pos;
+        };
+        for (int p = 0; p < Vf; ++p) {
+            const int self = s2o[p];
+            evalence[p] = (int)lists[p].size();
+            for (int k = 0; k < evalence[p]; ++k) {
+                const int e = lists[p][k];
+                if (e < 0) {   // null record (4-byte programs): pair 0, a zero term
+                    uint8_t *rec = einc.data() + (size_t)(eregion[p / 32] + 32 * k + p % 32) * einc_bytes;
+                    const int np = null_for(p / 32, k);
+                    const uint32_t word = (uint32_t)(12 * (np >= 0 ? np : p)) & 0xffffu;
+                    if (np < 0) static_cnt[p] += 1;   // own position: counted degenerate every substep
+                    std::memcpy(rec, &word, 4);
+                    continue;
+                }
+                ++n_einc;
+                static_cnt[p] += 1;
+                const int a = d.edges[2 * e], b = d.edges[2 * e + 1];
+                const int q = a == self ? b : a;
+                const int qpos = nbr_pos(p, k);
+                // bit 31: the neighbour is pinned (w = 0); with uniform free mass that fixes the
+                // weight ratio (compact fp32 records), and halo neighbours of a cluster part are free
+                const int32_t nbr = (boff ? 12 * qpos : qpos) | (is_free(q) ? 0 : (int32_t)0x80000000u);
+                uint8_t *rec = einc.data() + (size_t)(eregion[p / 32] + 32 * k + p % 32) * einc_bytes;
+                const double rl = d.rest_length[e];
+                if (einc_bytes == 4) {
+                    const uint32_t word = (uint32_t)(nbr & 0xffff) | ((uint32_t)pair_index(e, !is_free(q)) << 16);
+                    std::memcpy(rec, &word, 4);
+                    continue;
+                }
+                std::memcpy(rec, &nbr, 4);
+                if (einc_bytes == 8) {
+                    const float f = (float)rl;
+                    std::memcpy(rec + 4, &f, 4);
+                } else if (R == 8) {
+                    std::memcpy(rec + 8, &rl, 8);
+                } else {
+                    const float coef = (float)(d.k_s * w[self] / (w[self] + w[q]));
+                    const float f = (float)rl;
+                    std::memcpy(rec + 4, &coef, 4);
+                    std::memcpy(rec + 8, &f, 4);
+                }
+            }
+        }
+    }
+    return out;
+}
+
 }  // namespace
 
 int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector<uint8_t> &blob,
@@ -1595,142 +1767,18 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
         }
     }
 
-    // ---- owner-gathered edges -------------------------------------------------
-    // Free vertex p walks its live incident edges in edge-index order (the reference's
-    // accumulation order, _kernels.pyx:102-139).  Its correction from edge (a, b) is
-    //   -(w_p scale) (x_p - x_q),  scale = m ks (dist - rest) / (dist (w_a + w_b) + (1 - m)),
-    // bitwise the reference's (-w_a scale) dx for p = a and (w_b scale) dx for p = b, since
-    // x_b - x_a = -(x_a - x_b) exactly and the squares / weight sum are symmetric.
-    // fp32 byte-offset programs whose rest lengths take few distinct fp32 values (a structured
-    // slab has 2) use 4-byte records: {neighbour offset (16) | pair index (16)} with a small table
-    // of (rest length, coefficient) pairs -- coefficient = -k_s w_p / (w_p + w_q), i.e. -k_s / 2,
-    // or -k_s for a pinned neighbour (uniform free mass) -- half the L1 footprint of the edge
-    // stream and one shared load for both operands.  Pair 0 is the null record {0, 0} (a gap of
-    // the conflict-free rounds): its term is exactly zero.
-    std::vector<float> rl_tab;
-    std::vector<int> rl_idx(E, -1);
-    if (eg && boff && 12 * Vstore <= 65535) {
-        std::vector<float> vals;
-        for (int e = 0; e < E; ++e) if (edge_live[e]) vals.push_back((float)d.rest_length[e]);
-        std::sort(vals.begin(), vals.end());
-        vals.erase(std::unique(vals.begin(), vals.end()), vals.end());
-        if ((int)vals.size() <= 256) {
-            rl_tab = vals;
-            for (int e = 0; e < E; ++e)
-                if (edge_live[e])
-                    rl_idx[e] = (int)(std::lower_bound(vals.begin(), vals.end(), (float)d.rest_length[e]) - vals.begin());
-        }
-    }
-    const int einc_bytes = eg ? (!rl_tab.empty() ? 4 : ((R == 4 && compact) ? 8 : 16)) : 0;
-    std::vector<float> pair_tab;                      // RLTAB section of 4-byte programs: {rl, coef} pairs
-    auto pair_index = [&](int e, bool pinned_nbr) {   // 1 + 2 * rest-length index + pinned
-        return 1 + 2 * rl_idx[e] + (pinned_nbr ? 1 : 0);
-    };
-    if (einc_bytes == 4) {
-        pair_tab.assign(2 * (1 + 2 * rl_tab.size()), 0.0f);
-        const float ks_f = (float)d.k_s;
-        for (size_t i = 0; i < rl_tab.size(); ++i)
-            for (int pin = 0; pin < 2; ++pin) {
-                const int k = 1 + 2 * (int)i + pin;
-                pair_tab[2 * k] = rl_tab[i];
-                pair_tab[2 * k + 1] = -(pin ? ks_f : 0.5f * ks_f);
-            }
-    }
-    std::vector<int32_t> eregion(eg ? G : 0, 0), evalence(eg ? Vf_pad : 0, 0);
-    std::vector<uint8_t> einc;
-    int n_einc = 0;
+    // ---- owner-gathered edges (build_gather) -------------------------------------
+    GatherProgram gp;
     if (eg) {
-        std::vector<std::vector<int>> lists(Vf_pad);
-        for (int e = 0; e < E; ++e) {
-            if (!edge_live[e]) continue;
-            const int a = d.edges[2 * e], b = d.edges[2 * e + 1];
-            if (own_free(a)) lists[o2s[a]].push_back(e);
-            if (own_free(b)) lists[o2s[b]].push_back(e);
-        }
-        // fp32: the order of a vertex's edges is free (fp64 keeps edge-index order, the reference's
-        // summation order).  In round k the 32 lanes of a warp read their k-th neighbours: permute
-        // each lane's list so the neighbours of one round sit in distinct banks as far as possible
-        // (deterministic local search, sum over rounds of the largest bank multiplicity)
-        // a pinned neighbour may be read from any of its copies (PinCopies): a second move kind
-        std::vector<std::vector<int>> ecopy(Vf_pad);
-        for (int p = 0; p < Vf_pad; ++p) ecopy[p].assign(lists[p].size(), 0);
-        auto other = [&](int p, int e) {
-            const int a = d.edges[2 * e], b = d.edges[2 * e + 1];
-            return o2s[a == s2o[p] ? b : a];
-        };
-        auto nbr_pos = [&](int p, int k) { return pc.pos(other(p, lists[p][k]), ecopy[p][k]); };
-        if (packed && einc_bytes == 4) colour_gather_rounds(lists, ecopy, G, Vf, pc, other);
-        else if (R == 4 && o.schedule_banks >= 0) order_gather_rounds(lists, ecopy, G, pc, other, nbr_pos);
-        int base = 0;
-        for (int g = 0; g < G; ++g) {
-            int kmax = 0;
-            for (int p = 32 * g; p < 32 * g + 32; ++p) kmax = std::max(kmax, (int)lists[p].size());
-            eregion[g] = base;
-            base += 32 * kmax;
-        }
-        einc.assign(((size_t)base + 32) * einc_bytes, 0);   // + one padding row: unclamped prefetch
-        // null records read a pinned position on a bank their round leaves free (no conflict; a
-        // pinned neighbour is never within 1e-12 of a free vertex, so the null is not degenerate),
-        // or -- when no such position exists -- their own position (dx = 0: degenerate, counted in
-        // static_cnt so the applied count is unchanged)
-        std::vector<int> pin_at_bank(32, -1);
-        for (int q = Vf_pad; q < Vstore; ++q)
-            if (s2o[q] >= 0 && !is_free(s2o[q]) && pin_at_bank[q % 32] < 0) pin_at_bank[q % 32] = q;
-        std::vector<int> null_pos((size_t)G * 64, -2);   // per (warp, round): chosen position (-1: own)
-        auto null_for = [&](int g, int k) {
-            int &np = null_pos[(size_t)g * 64 + std::min(k, 63)];
-            if (np != -2 && k < 64) return np;
-            std::vector<char> used(32, 0);
-            for (int q = 32 * g; q < std::min(Vf, 32 * g + 32); ++q)
-                if (k < (int)lists[q].size() && lists[q][k] >= 0) used[nbr_pos(q, k) % 32] = 1;
-            int pos = -1;
-            for (int b = 0; b < 32 && pos < 0; ++b) if (!used[b] && pin_at_bank[b] >= 0) pos = pin_at_bank[b];
-            if (k < 64) np = pos;
-            return pos;
-        };
-        for (int p = 0; p < Vf; ++p) {
-            const int self = s2o[p];
-            evalence[p] = (int)lists[p].size();
-            for (int k = 0; k < evalence[p]; ++k) {
-                const int e = lists[p][k];
-                if (e < 0) {   // null record (4-byte programs): pair 0, a zero term
-                    uint8_t *rec = einc.data() + (size_t)(eregion[p / 32] + 32 * k + p % 32) * einc_bytes;
-                    const int np = null_for(p / 32, k);
-                    const uint32_t word = (uint32_t)(12 * (np >= 0 ? np : p)) & 0xffffu;
-                    if (np < 0) static_cnt[p] += 1;   // own position: counted degenerate every substep
-                    std::memcpy(rec, &word, 4);
-                    continue;
-                }
-                ++n_einc;
-                static_cnt[p] += 1;
-                const int a = d.edges[2 * e], b = d.edges[2 * e + 1];
-                const int q = a == self ? b : a;
-                const int qpos = nbr_pos(p, k);
-                // bit 31: the neighbour is pinned (w = 0); with uniform free mass that fixes the
-                // weight ratio (compact fp32 records), and halo neighbours of a cluster part are free
-                const int32_t nbr = (boff ? 12 * qpos : qpos) | (is_free(q) ? 0 : (int32_t)0x80000000u);
-                uint8_t *rec = einc.data() + (size_t)(eregion[p / 32] + 32 * k + p % 32) * einc_bytes;
-                const double rl = d.rest_length[e];
-                if (einc_bytes == 4) {
-                    const uint32_t word = (uint32_t)(nbr & 0xffff) | ((uint32_t)pair_index(e, !is_free(q)) << 16);
-                    std::memcpy(rec, &word, 4);
-                    continue;
-                }
-                std::memcpy(rec, &nbr, 4);
-                if (einc_bytes == 8) {
-                    const float f = (float)rl;
-                    std::memcpy(rec + 4, &f, 4);
-                } else if (R == 8) {
-                    std::memcpy(rec + 8, &rl, 8);
-                } else {
-                    const float coef = (float)(d.k_s * w[self] / (w[self] + w[q]));
-                    const float f = (float)rl;
-                    std::memcpy(rec + 4, &coef, 4);
-                    std::memcpy(rec + 8, &f, 4);
-                }
-            }
-        }
+        GatherSpec gs{&d, &edge_live, &o2s, &s2o, &pc, own_free, is_free, Vf, Vf_pad, G, Vstore, R,
+                      boff, compact, packed, o.schedule_banks >= 0};
+        gp = build_gather(gs, static_cnt);
     }
+    const int einc_bytes = gp.einc_bytes;
+    const std::vector<float> &pair_tab = gp.pair_tab;
+    const std::vector<int32_t> &eregion = gp.eregion, &evalence = gp.evalence;
+    const std::vector<uint8_t> &einc = gp.einc;
+    const int n_einc = gp.n_einc;
 
     // ---- cluster part: halo sends and face-vertex owners ----------------------
     std::vector<int32_t> send_off, send, face_own;
