@@ -1228,7 +1228,9 @@ __device__ __forceinline__ void step_env(const TsDevProg &P, const TsDevProg *pr
     int h_tb = 0, h_wb = 0, h_we = 0;   // FAST: the chunk's tet base and this warp's range
     // cluster parts (a few warps per CTA, latency-bound): the substep-invariant per-vertex words
     // in registers too -- counts and edge rows always, chunk 0's slot rows when it is the only one
-    constexpr bool HC = CL && sizeof(Real) == 4;   // (the fp64 cluster kernels are out of registers already)
+    // (also the fp64 one-vertex-per-thread kernels: one CTA at 1-2 per SM, latency-bound; not the fp64
+    // cluster kernels, out of registers already)
+    constexpr bool HC = (CL && sizeof(Real) == 4) || (!CL && !FAST && !EO && sizeof(Real) == 8 && VPT == 1);
     const bool hc1 = HC && P.n_chunks == 1;
     if constexpr (HC) {
         const TsChunk ch0 = P.chunks[0];
