@@ -209,7 +209,8 @@ def _program_key(arrays: SceneArrays, o) -> str:
     return h.hexdigest()
 
 
-_COMPILER_ENV = ("TS_SA_FOCUS", "TS_REFINE_ITERS", "TS_TET_HOLES", "TS_SPLIT_CT", "TS_NARROW")
+_COMPILER_ENV = ("TS_SA_FOCUS", "TS_REFINE_ITERS", "TS_TET_HOLES", "TS_SPLIT_CT", "TS_NARROW", "TS_PIN_COPIES",
+                 "TS_PIN_SHIFT", "TS_PACK_TETS", "TS_PACK_ITERS", "TS_TET_EXTRA_BATCHES")
 
 
 def compile_program(arrays: SceneArrays, **layout):
