@@ -1071,7 +1071,7 @@ struct GatherProgram {
 // bitwise the reference's (-w_a scale) dx for p = a and (w_b scale) dx for p = b, since
 // x_b - x_a = -(x_a - x_b) exactly and the squares / weight sum are symmetric.
 // fp32 byte-offset programs whose rest lengths take few distinct fp32 values (a structured
-// slab has 2) use 4-byte records: {neighbour offset (16) | pair index (16)} with a small table
+// slab has 2) use 4-byte records: {neighbour offset (16) | 8 x pair index (16)} with a small table
 // of (rest length, coefficient) pairs -- coefficient = -k_s w_p / (w_p + w_q), i.e. -k_s / 2,
 // or -k_s for a pinned neighbour (uniform free mass) -- half the L1 footprint of the edge
 // stream and one shared load for both operands.  Pair 0 is the null record {0, 0} (a gap of
@@ -1153,7 +1153,7 @@ GatherProgram build_gather(const GatherSpec &gs, std::vector<int32_t> &static_cn
             eregion[g] = base;
             base += 32 * kmax;
         }
-        einc.assign(((size_t)base + 32) * einc_bytes, 0);   // + one padding row: unclamped prefetch
+        einc.assign(((size_t)base + 64) * einc_bytes, 0);   // + two padding rows: unclamped prefetches
         // null records read a pinned position on a bank their round leaves free (no conflict; a
         // pinned neighbour is never within 1e-12 of a free vertex, so the null is not degenerate),
         // or -- when no such position exists -- their own position (dx = 0: degenerate, counted in
@@ -1197,7 +1197,8 @@ GatherProgram build_gather(const GatherSpec &gs, std::vector<int32_t> &static_cn
                 uint8_t *rec = einc.data() + (size_t)(eregion[p / 32] + 32 * k + p % 32) * einc_bytes;
                 const double rl = d.rest_length[e];
                 if (einc_bytes == 4) {
-                    const uint32_t word = (uint32_t)(nbr & 0xffff) | ((uint32_t)pair_index(e, !is_free(q)) << 16);
+                    // upper half: the pair's byte offset in the table (8 B per pair): one shift to decode
+                    const uint32_t word = (uint32_t)(nbr & 0xffff) | ((uint32_t)(8 * pair_index(e, !is_free(q))) << 16);
                     std::memcpy(rec, &word, 4);
                     continue;
                 }

@@ -26,6 +26,8 @@
 #include <math.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 #include "step_common.h"
 
 namespace tsk {
@@ -569,16 +571,22 @@ __device__ __forceinline__ void tet_item_b(const char *pb, char *sb, int *deg, i
     // 0xffff: a pinned corner has no slot -- a predicated store (no branch, no shared "trash" slot,
     // so every shared word has one writer per phase)
     const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(sb);
-    auto st3 = [&](unsigned o, float gx, float gy, float gz) {
-        asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %0, 65535;\n\t"
-                     "@p st.shared.f32 [%1], %2;\n\t@p st.shared.f32 [%1+4], %3;\n\t"
-                     "@p st.shared.f32 [%1+8], %4;\n\t}"
-                     ::"r"(o), "r"(sbase + o), "f"(sc * gx), "f"(sc * gy), "f"(sc * gz) : "memory");
-    };
-    st3(q.z & 0xffffu, Gax, Gay, Gaz);
-    st3(q.z >> 16, Gbx, Gby, Gbz);
-    st3(q.w & 0xffffu, Gcx, Gcy, Gcz);
-    st3(q.w >> 16, Gdx, Gdy, Gdz);
+    // the four corners' stores in one block, interleaved (as tet_item_fast: stays predicated)
+    const unsigned sa = q.z & 0xffffu, sb_ = q.z >> 16, sc_ = q.w & 0xffffu, sd = q.w >> 16;
+    asm volatile("{\n\t.reg .pred pa, pb, pc, pd;\n\t"
+                 "setp.ne.u32 pa, %0, 65535;\n\tsetp.ne.u32 pb, %1, 65535;\n\t"
+                 "setp.ne.u32 pc, %2, 65535;\n\tsetp.ne.u32 pd, %3, 65535;\n\t"
+                 "@pa st.shared.f32 [%4], %8;\n\t@pb st.shared.f32 [%5], %11;\n\t"
+                 "@pc st.shared.f32 [%6], %14;\n\t@pd st.shared.f32 [%7], %17;\n\t"
+                 "@pa st.shared.f32 [%4+4], %9;\n\t@pb st.shared.f32 [%5+4], %12;\n\t"
+                 "@pc st.shared.f32 [%6+4], %15;\n\t@pd st.shared.f32 [%7+4], %18;\n\t"
+                 "@pa st.shared.f32 [%4+8], %10;\n\t@pb st.shared.f32 [%5+8], %13;\n\t"
+                 "@pc st.shared.f32 [%6+8], %16;\n\t@pd st.shared.f32 [%7+8], %19;\n\t}"
+                 ::"r"(sa), "r"(sb_), "r"(sc_), "r"(sd), "r"(sbase + sa), "r"(sbase + sb_), "r"(sbase + sc_),
+                 "r"(sbase + sd), "f"(sc * Gax), "f"(sc * Gay), "f"(sc * Gaz), "f"(sc * Gbx), "f"(sc * Gby),
+                 "f"(sc * Gbz), "f"(sc * Gcx), "f"(sc * Gcy), "f"(sc * Gcz), "f"(sc * Gdx), "f"(sc * Gdy),
+                 "f"(sc * Gdz)
+                 : "memory");
     if (degenerate) {
         if (oa < vfp_b) deg_add(narrow, deg, oa / 12);
         if (ob < vfp_b) deg_add(narrow, deg, ob / 12);
@@ -589,8 +597,14 @@ __device__ __forceinline__ void tet_item_b(const char *pb, char *sb, int *deg, i
 
 // The fast kernel's tet item: byte offsets from the 32-bit shared base sb (positions and slots share
 // it: narrow layout), rest volume 6 V0 given; same arithmetic as tet_item_b.
+// RV4: only bits 14-15 of the first field carry the 6 V0 index, so the other three position
+// fields need at most one operation each
+template <bool RV4>
 __device__ __forceinline__ void tet_item_fast(int *deg, uint4 q, float rvi, float kv, unsigned vfp_b) {
-    const unsigned oa = q.x & 0x3fffu, ob = (q.x >> 16) & 0x3fffu, oc = q.y & 0x3fffu, od = (q.y >> 16) & 0x3fffu;
+    const unsigned oa = q.x & 0x3fffu;
+    const unsigned ob = RV4 ? q.x >> 16 : (q.x >> 16) & 0x3fffu;
+    const unsigned oc = RV4 ? q.y & 0xffffu : q.y & 0x3fffu;
+    const unsigned od = RV4 ? q.y >> 16 : (q.y >> 16) & 0x3fffu;
     float ax, ay, az, bx, by, bz, cx, cy, cz, dx, dy, dz;
     lds3c(oa, ax, ay, az);
     lds3c(ob, bx, by, bz);
@@ -615,17 +629,23 @@ __device__ __forceinline__ void tet_item_fast(int *deg, uint4 q, float rvi, floa
     const float den = tet_den(Gax, Gay, Gaz, Gbx, Gby, Gbz, Gcx, Gcy, Gcz, Gdx, Gdy, Gdz);
     const bool degenerate = !(den > 3.6e-17f);                  // sum|grad|^2 <= 1e-18
     const float sc = degenerate ? 0.0f : (-kv * c6) * rcp_ftz(den);
-    auto st3 = [&](unsigned o, float gx, float gy, float gz) {   // 0xffff: pinned corner, store predicated off
-        asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %0, 65535;\n\t"
-                     "@p st.shared.f32 [%0+%4], %1;\n\t@p st.shared.f32 [%0+%5], %2;\n\t"
-                     "@p st.shared.f32 [%0+%6], %3;\n\t}"
-                     ::"r"(o), "f"(sc * gx), "f"(sc * gy), "f"(sc * gz), "n"(TS_SB), "n"(TS_SB + 4), "n"(TS_SB + 8)
-                     : "memory");
-    };
-    st3(q.z & 0xffffu, Gax, Gay, Gaz);
-    st3(q.z >> 16, Gbx, Gby, Gbz);
-    st3(q.w & 0xffffu, Gcx, Gcy, Gcz);
-    st3(q.w >> 16, Gdx, Gdy, Gdz);
+    // 0xffff: pinned corner, its stores predicated off.  One asm block with the four corners'
+    // stores interleaved: ptxas keeps them predicated (per-corner blocks were turned into
+    // BSSY / BRA / BSYNC regions, 3 extra instructions per corner)
+    asm volatile("{\n\t.reg .pred pa, pb, pc, pd;\n\t"
+                 "setp.ne.u32 pa, %0, 65535;\n\tsetp.ne.u32 pb, %1, 65535;\n\t"
+                 "setp.ne.u32 pc, %2, 65535;\n\tsetp.ne.u32 pd, %3, 65535;\n\t"
+                 "@pa st.shared.f32 [%0+%16], %4;\n\t@pb st.shared.f32 [%1+%16], %7;\n\t"
+                 "@pc st.shared.f32 [%2+%16], %10;\n\t@pd st.shared.f32 [%3+%16], %13;\n\t"
+                 "@pa st.shared.f32 [%0+%17], %5;\n\t@pb st.shared.f32 [%1+%17], %8;\n\t"
+                 "@pc st.shared.f32 [%2+%17], %11;\n\t@pd st.shared.f32 [%3+%17], %14;\n\t"
+                 "@pa st.shared.f32 [%0+%18], %6;\n\t@pb st.shared.f32 [%1+%18], %9;\n\t"
+                 "@pc st.shared.f32 [%2+%18], %12;\n\t@pd st.shared.f32 [%3+%18], %15;\n\t}"
+                 ::"r"(q.z & 0xffffu), "r"(q.z >> 16), "r"(q.w & 0xffffu), "r"(q.w >> 16),
+                 "f"(sc * Gax), "f"(sc * Gay), "f"(sc * Gaz), "f"(sc * Gbx), "f"(sc * Gby), "f"(sc * Gbz),
+                 "f"(sc * Gcx), "f"(sc * Gcy), "f"(sc * Gcz), "f"(sc * Gdx), "f"(sc * Gdy), "f"(sc * Gdz),
+                 "n"(TS_SB), "n"(TS_SB + 4), "n"(TS_SB + 8)
+                 : "memory");
     if (degenerate) {
         if (oa < vfp_b) deg_add(1, deg, oa / 12);
         if (ob < vfp_b) deg_add(1, deg, ob / 12);
@@ -650,7 +670,7 @@ __device__ __forceinline__ void p1_tets_fast(const TsDevProg &P, int *deg, int b
         nq = __ldg(ip);
         const unsigned ri = RV4 ? ((q.x >> 14) & 3u)
                                 : (((q.x >> 14) & 3u) | ((q.x >> 28) & 12u) | ((q.y >> 10) & 48u) | ((q.y >> 24) & 192u));
-        tet_item_fast(deg, q, lds1c(TS_TAB_OFF + 4 * TS_TAB_CAP + 4 * ri), kv, vfp_b);
+        tet_item_fast<RV4>(deg, q, lds1c(TS_TAB_OFF + 4 * TS_TAB_CAP + 4 * ri), kv, vfp_b);
     }
 }
 
@@ -872,34 +892,79 @@ __device__ __forceinline__ void owner_edges(const TsDevProg &P, const Smem<Real>
             ndeg += mm == 0.0;
         }
     } else if (FAST || P.einc_bytes == 4) {
-        // 4-byte records: {neighbour byte offset | pair index << 16}, pair = {rest length, -k_s w_p /
+        // 4-byte records: {neighbour byte offset | pair byte offset << 16}, pair = {rest length, -k_s w_p /
         // (w_p + w_q)} (pair 0 = {0, 0}: a null record of the compiler's conflict-free rounds, whose
         // term is exactly zero)
         const unsigned *rec = reinterpret_cast<const unsigned *>(P.einc) + rb;
-        unsigned q = __ldg(rec);
-        for (int k = 0; k < ev; ++k) {
-            const unsigned cur = q;
-            q = __ldg(rec + 32 * (k + 1));
-            float qx, qy, qz;
-            float2 rc;
+        // FAST: the loop runs without the degenerate-edge select / count (|d| <= 1e-12 never happens in
+        // a live simulation); it tracks the smallest |d|^2 instead and, when an edge was degenerate,
+        // this vertex's edges are summed again with the exact rule below -- same result either way
+        // (a NaN |d|^2 leaves NaN sums on both paths).  The edges are summed from zero and added at
+        // the end: the edges come first in every vertex's sum, so the accumulators are +0 here and
+        // the result is bitwise the in-place sum (no saved copies live across the loop)
+        float ex = 0.0f, ey = 0.0f, ez = 0.0f;
+        float d2min = 3.0e38f;
+        // neighbour position and {rest, coefficient} pair of a record (FAST: constant shared
+        // addresses; STAB, the edges kernel: the pair table's shared copy; else through L1)
+        auto fetch = [&](unsigned r, float &qx, float &qy, float &qz, float2 &rc) {
             if constexpr (FAST) {
-                rc = lds2c(TS_TAB_OFF + 8 * (cur >> 16));
-                lds3c(cur & 0xffffu, qx, qy, qz);
+                rc = lds2c(TS_TAB_OFF + (r >> 16));
+                lds3c(r & 0xffffu, qx, qy, qz);
             } else {
-                // STAB (the edges kernel): the pair table from its shared copy at a constant address;
-                // otherwise through L1
-                rc = STAB ? lds2c(TS_TAB_OFF + 8 * (cur >> 16))
-                          : __ldg(reinterpret_cast<const float2 *>(P.rltab) + (cur >> 16));
-                const float *nq = reinterpret_cast<const float *>(reinterpret_cast<const char *>(m.pos) + (cur & 0xffffu));
+                rc = STAB ? lds2c(TS_TAB_OFF + (r >> 16))
+                          : __ldg(reinterpret_cast<const float2 *>(reinterpret_cast<const char *>(P.rltab) +
+                                                                    (r >> 16)));
+                const float *nq = reinterpret_cast<const float *>(reinterpret_cast<const char *>(m.pos) + (r & 0xffffu));
                 qx = nq[0]; qy = nq[1]; qz = nq[2];
             }
-            const float dx = px - qx, dy = py - qy, dz = pz - qz;
-            const float d2 = __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, dx * dx));
-            const bool degenerate = !(d2 >= 1e-24f);
-            const float f = degenerate ? 0.0f : __fmaf_rn(-rc.x, rsqrt_ftz(d2), 1.0f);
-            const float c = rc.y * f;
-            ax = __fmaf_rn(c, dx, ax); ay = __fmaf_rn(c, dy, ay); az = __fmaf_rn(c, dz, az);
-            ndeg += degenerate;
+        };
+        if constexpr (FAST) {
+            // software-pipelined: record k + 2 and the shared operands of record k + 1 are in flight
+            // while record k's term is computed (the shared loads no longer wait behind the previous
+            // term's arithmetic).  Loads past a lane's last record read a neighbouring lane's record
+            // row or a zero padding row -- in-bounds offsets, results unused.
+            unsigned qn = __ldg(rec + 32);
+            float nx, ny, nz;
+            float2 nrc;
+            fetch(__ldg(rec), nx, ny, nz, nrc);
+            for (int k = 0; k < ev; ++k) {
+                const float qx = nx, qy = ny, qz = nz;
+                const float2 rc = nrc;
+                fetch(qn, nx, ny, nz, nrc);
+                qn = __ldg(rec + 32 * (k + 2));
+                const float dx = px - qx, dy = py - qy, dz = pz - qz;
+                const float d2 = __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, dx * dx));
+                const float c = rc.y * __fmaf_rn(-rc.x, rsqrt_ftz(d2), 1.0f);
+                d2min = fminf(d2min, d2);
+                ex = __fmaf_rn(c, dx, ex); ey = __fmaf_rn(c, dy, ey); ez = __fmaf_rn(c, dz, ez);
+            }
+        }
+        // the exact rule: every edge of the other kernels (measured faster there than the pipelined
+        // loop -- the edges kernel is latency-bound), and a FAST vertex with a degenerate edge
+        auto exact = [&](float &sx, float &sy, float &sz) {
+            unsigned q = __ldg(rec);
+            for (int k = 0; k < ev; ++k) {
+                const unsigned cur = q;
+                q = __ldg(rec + 32 * (k + 1));
+                float qx, qy, qz;
+                float2 rc;
+                fetch(cur, qx, qy, qz, rc);
+                const float dx = px - qx, dy = py - qy, dz = pz - qz;
+                const float d2 = __fmaf_rn(dz, dz, __fmaf_rn(dy, dy, dx * dx));
+                const bool degenerate = !(d2 >= 1e-24f);
+                const float c = rc.y * (degenerate ? 0.0f : __fmaf_rn(-rc.x, rsqrt_ftz(d2), 1.0f));
+                sx = __fmaf_rn(c, dx, sx); sy = __fmaf_rn(c, dy, sy); sz = __fmaf_rn(c, dz, sz);
+                ndeg += degenerate;
+            }
+        };
+        if constexpr (FAST) {
+            if (d2min < 1e-24f) {
+                ex = ey = ez = 0.0f;
+                exact(ex, ey, ez);
+            }
+            ax += ex; ay += ey; az += ez;
+        } else {
+            exact(ax, ay, az);
         }
     } else if (P.einc_bytes == 8 && P.boff) {
         // byte-offset records, padded by one row: the prefetch of record k + 1 needs no clamp
@@ -1230,7 +1295,8 @@ __device__ __forceinline__ void step_env(const TsDevProg &P, const TsDevProg *pr
     // in registers too -- counts and edge rows always, chunk 0's slot rows when it is the only one
     // (also the fp64 one-vertex-per-thread kernels: one CTA at 1-2 per SM, latency-bound; not the fp64
     // cluster kernels, out of registers already)
-    constexpr bool HC = (CL && sizeof(Real) == 4) || (!CL && !FAST && !EO && sizeof(Real) == 8 && VPT == 1);
+    constexpr bool HC = (CL && sizeof(Real) == 4) || (!CL && !FAST && sizeof(Real) == 8 && VPT == 1 && !EO) ||
+                       (EO && sizeof(Real) == 4);   // the edges kernel: counts and edge rows
     const bool hc1 = HC && P.n_chunks == 1;
     if constexpr (HC) {
         const TsChunk ch0 = P.chunks[0];
@@ -1462,8 +1528,8 @@ __device__ __forceinline__ void step_env(const TsDevProg &P, const TsDevProg *pr
                 for (int r = 0; r < VPT; ++r) {
                     const int p = r * B + t;
                     if (P.edge_gather && P.n_chunks == 0 && p < P.Vf)   // distance constraints only
-                        owner_edges<Real, false, false, EO>(P, m, p, lane, xr[r], yr[r], zr[r], ks, accx[r],
-                                                            accy[r], accz[r], ndeg[r]);
+                        owner_edges<Real, false, HC, EO>(P, m, p, lane, xr[r], yr[r], zr[r], ks, accx[r],
+                                                         accy[r], accz[r], ndeg[r], h_ev[r], h_rb[r]);
                     add_grasp(r);
                 }
             }

@@ -70,9 +70,9 @@ class Program:
             raw = self.sec("EINC", np.uint8, max(n, 1) * eb).reshape(-1, eb)
             word = raw[:, 0:4].copy().view(np.uint32)[:, 0]
             self.e_null = np.zeros(len(word), bool)
-            if eb == 4:           # {offset | pair index << 16}; pairs {rest, -k_s w_p / (w_p + w_q)}
+            if eb == 4:           # {offset | 8 pair index << 16}; pairs {rest, -k_s w_p / (w_p + w_q)}
                 tab = self.sec("RLTAB", np.float32, 2 * H["n_rltab"]).reshape(-1, 2).astype(np.float64)
-                idx = word >> 16
+                idx = (word >> 16) >> 3      # the pair's byte offset in the table, 8 B per pair
                 self.e_rest = tab[idx, 0]
                 self.e_pair_coef = tab[idx, 1]
                 self.e_coef = None

@@ -82,7 +82,7 @@ def model(prog: Program):
             nb = (rec & 0xFFFF).astype(np.int64)
             for c in range(3):
                 acc("edge_load", HEAD + nb + 4 * c)
-            acc("edge_rl", TAB + 8 * (rec >> 16).astype(np.int64))     # {rest, coef} pair (one 64-bit load)
+            acc("edge_rl", TAB + (rec >> 16).astype(np.int64))     # {rest, coef} pair (one 64-bit load)
         pitch = H.get("slot_pitch", 32) or 32
         for k in range(int(max(val[p] for p in ps))):
             act = np.asarray([p for p in ps if k < val[p]])
