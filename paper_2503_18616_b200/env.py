@@ -87,12 +87,13 @@ class StepInfo(dict):
 
 
 # output buffer layout of one step: (name, dtype, trailing shape)
+# final_obs last: step_numpy copies the block without it and fetches it only when a row is done
 _OUTS = [("reward", torch.float64, ()), ("distance", torch.float64, ()),
          ("episode_return", torch.float64, ()), ("episode_length", torch.int64, ()),
-         ("obs", None, (OBSERVATION_SIZE,)), ("final_obs", None, (OBSERVATION_SIZE,)),
+         ("obs", None, (OBSERVATION_SIZE,)),
          ("contacts", torch.int32, ()), ("terminated", torch.bool, ()), ("truncated", torch.bool, ()),
          ("success", torch.bool, ()), ("diverged", torch.bool, ()), ("clipped", torch.bool, ()),
-         ("done_mask", torch.bool, ())]
+         ("done_mask", torch.bool, ()), ("final_obs", None, (OBSERVATION_SIZE,))]
 
 
 class EnvBatch:
@@ -135,7 +136,10 @@ class EnvBatch:
         self._dev_actions = None
         self._layout = self._out_layout()
         self._numpy_layout = self._out_layout(torch.float64)
-        self.numpy_block_bytes = self._numpy_layout[1]   # D2H bytes per step_numpy call
+        # D2H bytes of a step_numpy call: the block without final_obs, + final_obs when a row is done
+        self.numpy_block_bytes = self._numpy_layout[0][-1][3]
+        self.numpy_final_obs_bytes = self._numpy_layout[0][-1][4]
+        self.numpy_d2h_bytes = 0   # running total over step_numpy calls
 
     # -- reference-named state (views of the device state) ------------------
     @property
@@ -298,10 +302,12 @@ class EnvBatch:
         The first call runs eagerly and then records the device side of a step as a CUDA graph;
         later calls validate the actions on the host, fill the pinned action buffer, replay the
         graph and wait for it.  The graph holds the H2D copy of the actions from a pinned buffer,
-        the three step kernels and ONE D2H copy of the packed output block into pinned memory
-        (``numpy_zero_copy = True`` instead lets the kernels read the actions and write the block
-        in pinned host memory directly -- measured slower, off by default).  The graph is re-recorded if a state tensor was
-        replaced.  The returned arrays are views of one fresh host copy of the block (never
+        the three step kernels and ONE D2H copy of the packed output block into pinned memory --
+        all of it but final_obs, which is fetched after the wait only when a row is done (with
+        max_episode_steps = 100 that is one step in a hundred).  (``numpy_zero_copy = True``
+        instead lets the kernels read the actions and write the block in pinned host memory
+        directly -- measured slower, off by default.)  The graph is re-recorded if a state tensor
+        was replaced.  The returned arrays are views of one fresh host copy of the block (never
         aliased with the next step's output).
         """
         if not self._ready:
@@ -320,9 +326,11 @@ class EnvBatch:
             # float64 observations, as the reference returns: the obs views are float64 (_numpy_layout)
             so = N.dl_struct(N.StepOutTensors, N.STEP_OUTS, views)
             hv = [(name, torch.empty(0, dtype=dt).numpy().dtype, shape, off, nb) for name, dt, shape, off, nb in layout]
+            fo_off = self.numpy_block_bytes   # final_obs: the block's tail
             pin_a = torch.empty((n, ACTION_SIZE), dtype=torch.float64, pin_memory=True)
             dev_a = pin_a if zc else torch.empty((n, ACTION_SIZE), dtype=torch.float64, device=self.device)
-            fx = self._np_fast = {"dev_buf": dev_buf, "so": so, "host": host, "raw": host.numpy(), "hv": hv,
+            fx = self._np_fast = {"dev_buf": dev_buf, "so": so, "host": host, "raw": host.numpy()[:fo_off],
+                                  "hv": hv[:-1], "fo": hv[-1], "fo_host": host[fo_off:], "fo_dev": dev_buf[fo_off:],
                                   "pin_a": pin_a, "pin_np": pin_a.numpy(), "dev_a": dev_a, "dl_a": N.dl(dev_a),
                                   "done": torch.cuda.Event(), "graph": None, "sig": None, "zc": zc}
         pin = fx["pin_np"]
@@ -331,6 +339,7 @@ class EnvBatch:
             raise ValidationError("actions must be finite")
         st = self.sim.state_struct()
         dev = self.device
+        fo_len = self.numpy_block_bytes
 
         def device_side():
             if not fx["zc"]:
@@ -339,7 +348,7 @@ class EnvBatch:
                                                       ctypes.byref(fx["so"]), None, None, self.sim.stream_ptr()),
                     "ts_env_step")
             if not fx["zc"]:
-                fx["host"].copy_(fx["dev_buf"], non_blocking=True)
+                fx["host"][:fo_len].copy_(fx["dev_buf"][:fo_len], non_blocking=True)
 
         if fx["graph"] is not None and fx["sig"] is self.sim._state and torch.cuda.current_device() == dev.index:
             fx["graph"].replay()                    # the steady state: one graph launch, no context switch
@@ -351,14 +360,23 @@ class EnvBatch:
         fx["done"].synchronize()
         self.sim.step_count += 1
         block = fx["raw"].copy()          # one host copy of the packed block; the arrays are views of it
-        out = {name: block[off:off + nb].view(dt).reshape(shape) for name, dt, shape, off, nb in fx["hv"]}
+        out = {name: np.ndarray(shape, dt, block, off) for name, dt, shape, off, nb in fx["hv"]}
         done = out["done_mask"]
+        d2h = fo_len
+        final = None
+        if done.any():                    # final_obs only now (its rows are zero where not done)
+            if not fx["zc"]:
+                fx["fo_host"].copy_(fx["fo_dev"])
+                d2h += self.numpy_final_obs_bytes
+            _, dt, shape, off, nb = fx["fo"]
+            final = np.ndarray(shape, dt, fx["host"].numpy()[off:off + nb].copy())
+        self.numpy_d2h_bytes += d2h
         info = {
             "distance": out["distance"], "success": out["success"], "diverged": out["diverged"],
             "clipped": out["clipped"], "contacts": int(out["contacts"].sum()),
             "contacts_per_env": out["contacts"], "episode_return": out["episode_return"],
             "episode_length": out["episode_length"], "done_mask": done,
-            "final_observation": out["final_obs"] if done.any() else None,
+            "final_observation": final,
         }
         return out["obs"], out["reward"], out["terminated"], out["truncated"], info
 
