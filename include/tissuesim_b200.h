@@ -355,6 +355,11 @@ int32_t ts_kernel_time(ts_handle *h, double *total_ms, int64_t *launches);
  * program selects), as ncu prints it -- for profiles and the bench's roofline line. */
 const char *ts_step_kernel_name(ts_handle *h);
 
+/* Launch an instantiated CUDA graph (cudaGraphExec_t) on `stream` and wait for it: the steady
+ * state of the host-buffer step (EnvBatch.step_numpy: the recorded H2D action copy, the step's
+ * kernels and the D2H output copy) in one call. */
+int32_t ts_graph_launch_sync(void *graph_exec, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -532,6 +532,15 @@ int32_t ts_uniform_actions_dev(double *actions, int64_t num_envs, int64_t first_
     return TS_OK;
 }
 
+int32_t ts_graph_launch_sync(void *graph_exec, void *stream) {
+    if (!graph_exec) return fail(TS_ERR_INVALID, "null graph");
+    const cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    cudaError_t e = cudaGraphLaunch(reinterpret_cast<cudaGraphExec_t>(graph_exec), s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return cuda_fail(e, "graph launch");
+    return TS_OK;
+}
+
 int32_t ts_set_max_grid(ts_handle *h, int32_t max_grid) {
     if (!h) return fail(TS_ERR_INVALID, "null argument");
     h->max_grid = max_grid;

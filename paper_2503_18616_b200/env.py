@@ -351,13 +351,14 @@ class EnvBatch:
                 fx["host"][:fo_len].copy_(fx["dev_buf"][:fo_len], non_blocking=True)
 
         if fx["graph"] is not None and fx["sig"] is self.sim._state and torch.cuda.current_device() == dev.index:
-            fx["graph"].replay()                    # the steady state: one graph launch, no context switch
-            fx["done"].record()
+            # the steady state: launch the recorded graph on the current stream and wait, one call
+            N.check(self.sim.scene.lib.ts_graph_launch_sync(fx["exec"], torch._C._cuda_getCurrentRawStream(dev.index)),
+                    "step_numpy")
         else:
             with torch.cuda.device(dev):
                 self._step_numpy_record(fx, device_side)
                 fx["done"].record()
-        fx["done"].synchronize()
+            fx["done"].synchronize()
         self.sim.step_count += 1
         block = fx["raw"].copy()          # one host copy of the packed block; the arrays are views of it
         out = {name: np.ndarray(shape, dt, block, off) for name, dt, shape, off, nb in fx["hv"]}
@@ -392,7 +393,8 @@ class EnvBatch:
         graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(graph):
             device_side()
-        fx["graph"], fx["sig"] = graph, self.sim._state
+        ex = graph.raw_cuda_graph_exec()                 # cudaGraphExec_t (an address)
+        fx["graph"], fx["sig"], fx["exec"] = graph, self.sim._state, ex if isinstance(ex, int) else int(ex)
 
     def step(self, actions, validate=True, tool_override=None):
         """env.py:144-197 on the GPU.  Returns (obs, reward, terminated, truncated, info).
