@@ -392,6 +392,9 @@ def measure(ctx, wl, n, steps, warmup, precision="fp32", cluster=0, e2e=True, fl
     ctx.barrier()
     torch.cuda.synchronize(dev)
     with ClockSampler(ctx.local) as clocks:
+        # ~5 ms of GPU work ahead of the timed launches (untimed: the first event follows it), so a
+        # host stall (the clock sampler thread, the GIL) never leaves the GPU idle inside a bracket
+        torch.cuda._sleep(10_000_000)
         for i in range(steps):
             if flush_l2:
                 flush.fill_(i & 0xFF)                   # evict the state from L2 (untimed)
@@ -401,6 +404,7 @@ def measure(ctx, wl, n, steps, warmup, precision="fp32", cluster=0, e2e=True, fl
         torch.cuda.synchronize(dev)
         # ---- the fused step kernel alone (roofline denominator): plain launches, library events
         N.check(lib.ts_kernel_timing(handle, 1, steps), "ts_kernel_timing")
+        torch.cuda._sleep(10_000_000)   # see above: the host queues ahead of the GPU
         for i in range(steps):
             if flush_l2:
                 flush.fill_(i & 0xFF)

@@ -868,7 +868,7 @@ __device__ void p1_atts(const TsDevProg &P, const Smem<Real> &m, int begin, int 
 // fp64: -(w_p scale) (x_p - x_q) with the reference's scale expression
 // (ts_lane_edges, _kernels.pyx:121-136) -- bitwise the reference's per-endpoint
 // term, see compiler.cpp; fp32: -coef (1 - rest / dist) (x_p - x_q) with FMAs.
-template <typename Real, bool FAST = false, bool HOIST = FAST, bool STAB = FAST>
+template <typename Real, bool FAST = false, bool HOIST = FAST, bool STAB = FAST, bool PIPE = FAST>
 __device__ __forceinline__ void owner_edges(const TsDevProg &P, const Smem<Real> &m, int p, int lane, Real px,
                                             Real py, Real pz, Real ks, Real &ax, Real &ay, Real &az, int &ndeg,
                                             int ev_h = 0, int rb_h = 0) {
@@ -896,7 +896,7 @@ __device__ __forceinline__ void owner_edges(const TsDevProg &P, const Smem<Real>
         // (w_p + w_q)} (pair 0 = {0, 0}: a null record of the compiler's conflict-free rounds, whose
         // term is exactly zero)
         const unsigned *rec = reinterpret_cast<const unsigned *>(P.einc) + rb;
-        // FAST: the loop runs without the degenerate-edge select / count (|d| <= 1e-12 never happens in
+        // PIPE (the fast kernel): the loop runs without the degenerate-edge select / count (|d| <= 1e-12 never happens in
         // a live simulation); it tracks the smallest |d|^2 instead and, when an edge was degenerate,
         // this vertex's edges are summed again with the exact rule below -- same result either way
         // (a NaN |d|^2 leaves NaN sums on both paths).  The edges are summed from zero and added at
@@ -918,7 +918,7 @@ __device__ __forceinline__ void owner_edges(const TsDevProg &P, const Smem<Real>
                 qx = nq[0]; qy = nq[1]; qz = nq[2];
             }
         };
-        if constexpr (FAST) {
+        if constexpr (PIPE) {
             // software-pipelined: record k + 2 and the shared operands of record k + 1 are in flight
             // while record k's term is computed (the shared loads no longer wait behind the previous
             // term's arithmetic).  Loads past a lane's last record read a neighbouring lane's record
@@ -957,7 +957,7 @@ __device__ __forceinline__ void owner_edges(const TsDevProg &P, const Smem<Real>
                 ndeg += degenerate;
             }
         };
-        if constexpr (FAST) {
+        if constexpr (PIPE) {
             if (d2min < 1e-24f) {
                 ex = ey = ez = 0.0f;
                 exact(ex, ey, ez);
