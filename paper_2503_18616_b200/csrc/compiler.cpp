@@ -1220,205 +1220,267 @@ GatherProgram build_gather(const GatherSpec &gs, std::vector<int32_t> &static_cn
     return out;
 }
 
-}  // namespace
+// ---------------------------------------------------------------------------
+// compile_program: one CTA's program for a scene (or one part of a cluster program), in stages.
+// Each stage reads the members the earlier ones set; every stage that can reject the input
+// returns a status (err holds the message).
+// ---------------------------------------------------------------------------
+class ProgramCompiler {
+public:
+    ProgramCompiler(const ts_scene_desc &d_, const ts_layout_opts &o_, const PartSpec *part_, std::string &err_)
+        : d(d_), o(o_), part(part_), err(err_) {}
 
-int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector<uint8_t> &blob,
-                    ts_layout_info &info, std::string &err, const PartSpec *part) {
-    if (part && (int)part->own.size() != d.n_vert) { err = "part ownership mask size"; return TS_ERR_INVALID; }
-    g_search_effort = part ? 0.1 : 1.0;
-    g_tet_holes = 0;   // measured: 2-8 idle lanes per batch cut conflicts but cost more issue (slower)
-    if (const char *env = std::getenv("TS_TET_HOLES")) g_tet_holes = std::atoi(env);
-    const int V = d.n_vert, E = d.n_edge, T = d.n_tet, F = d.n_face, A = d.n_att;
-    const int prec = o.precision;
-    if (prec != TS_F32 && prec != TS_F64) { err = "precision must be TS_F32 or TS_F64"; return TS_ERR_INVALID; }
-    const int R = prec == TS_F64 ? 8 : 4;
-    if (V < 0 || E < 0 || T < 0 || F < 0 || A < 0) { err = "negative counts"; return TS_ERR_INVALID; }
-    if (V > 0 && (!d.positions_rest || !d.inverse_mass)) { err = "missing vertex arrays"; return TS_ERR_INVALID; }
-    auto bad_vid = [&](int v) { return v < 0 || v >= V; };
-    for (int i = 0; i < 2 * E; ++i) if (bad_vid(d.edges[i])) { err = "edge vertex index out of range"; return TS_ERR_INVALID; }
-    for (int i = 0; i < 4 * T; ++i) if (bad_vid(d.tets[i])) { err = "tet vertex index out of range"; return TS_ERR_INVALID; }
-    for (int i = 0; i < 3 * F; ++i) if (bad_vid(d.faces[i])) { err = "face vertex index out of range"; return TS_ERR_INVALID; }
-    for (int i = 0; i < A; ++i) {
-        if (bad_vid(d.att_vertex[i])) { err = "attachment vertex out of range"; return TS_ERR_INVALID; }
-        if (d.att_is_face[i])
-            for (int k = 0; k < 3; ++k) if (bad_vid(d.att_faces[3 * i + k])) { err = "attachment face vertex out of range"; return TS_ERR_INVALID; }
+    int run(std::vector<uint8_t> &blob, ts_layout_info &info) {
+        int st;
+        if ((st = validate()) != TS_OK) return st;
+        live_constraints();
+        local_set();
+        if ((st = storage_order()) != TS_OK) return st;
+        collect_items();
+        if ((st = chunking()) != TS_OK) return st;
+        schedule();
+        if ((st = assign_slots()) != TS_OK) return st;
+        emit_tables();
+        compact_streams();
+        if (eg) {   // owner-gathered edges (build_gather)
+            GatherSpec gs{&d, &edge_live, &o2s, &s2o, &pc, [this](int v) { return own_free(v); },
+                          [this](int v) { return is_free(v); }, Vf, Vf_pad, G, Vstore, R,
+                          boff, compact, packed, o.schedule_banks >= 0};
+            gp = build_gather(gs, static_cnt);
+        }
+        cluster_tables();
+        wsplit = warp_split(chunk_rec, gp.evalence, eg, B, VPT, Vf);
+        assemble(blob, info);
+        return TS_OK;
     }
-    const double *w = d.inverse_mass;
-    auto is_free = [&](int v) { return w[v] > 0.0; };
+
+private:
+    const ts_scene_desc &d;
+    const ts_layout_opts &o;
+    const PartSpec *part;
+    std::string &err;
+
+    int fail(int status, const char *msg) { err = msg; return status; }
+
+    // ---- inputs -------------------------------------------------------------
+    int V = 0, E = 0, T = 0, F = 0, A = 0, prec = 0, R = 4;
+    const double *w = nullptr;
+    bool eg = false;
+    bool is_free(int v) const { return w[v] > 0.0; }
     // cluster part: this CTA of the env's cluster owns (updates, writes back) part->own vertices
     // and reads a halo of other parts' vertices, refreshed over DSMEM every substep
-    auto own = [&](int v) { return !part || part->own[v] != 0; };
-    auto own_free = [&](int v) { return is_free(v) && own(v); };
+    bool own(int v) const { return !part || part->own[v] != 0; }
+    bool own_free(int v) const { return is_free(v) && own(v); }
 
-    // edge_gather: distance constraints are gathered by the owner thread of each free vertex
-    // (no phase-1 items, no slots); only attachments and tets go through slots
-    // (the default; measured on B200, 4096 envs, reach_1170, with the gather done next to the
-    // phase-1 tets: fp32 0.677 vs 0.949 ms/step, fp64 3.58 vs 3.64 ms/step)
-    const bool eg = part || o.edge_gather >= 0;
+    int validate() {
+        V = d.n_vert; E = d.n_edge; T = d.n_tet; F = d.n_face; A = d.n_att;
+        prec = o.precision;
+        if (prec != TS_F32 && prec != TS_F64) return fail(TS_ERR_INVALID, "precision must be TS_F32 or TS_F64");
+        R = prec == TS_F64 ? 8 : 4;
+        if (V < 0 || E < 0 || T < 0 || F < 0 || A < 0) return fail(TS_ERR_INVALID, "negative counts");
+        if (V > 0 && (!d.positions_rest || !d.inverse_mass)) return fail(TS_ERR_INVALID, "missing vertex arrays");
+        auto bad_vid = [&](int v) { return v < 0 || v >= V; };
+        for (int i = 0; i < 2 * E; ++i) if (bad_vid(d.edges[i])) return fail(TS_ERR_INVALID, "edge vertex index out of range");
+        for (int i = 0; i < 4 * T; ++i) if (bad_vid(d.tets[i])) return fail(TS_ERR_INVALID, "tet vertex index out of range");
+        for (int i = 0; i < 3 * F; ++i) if (bad_vid(d.faces[i])) return fail(TS_ERR_INVALID, "face vertex index out of range");
+        for (int i = 0; i < A; ++i) {
+            if (bad_vid(d.att_vertex[i])) return fail(TS_ERR_INVALID, "attachment vertex out of range");
+            if (d.att_is_face[i])
+                for (int k = 0; k < 3; ++k)
+                    if (bad_vid(d.att_faces[3 * i + k])) return fail(TS_ERR_INVALID, "attachment face vertex out of range");
+        }
+        w = d.inverse_mass;
+        // edge_gather: distance constraints are gathered by the owner thread of each free vertex
+        // (no phase-1 items, no slots); only attachments and tets go through slots
+        // (the default; measured on B200, 4096 envs, reach_1170, with the gather done next to the
+        // phase-1 tets: fp32 0.677 vs 0.949 ms/step, fp64 3.58 vs 3.64 ms/step)
+        eg = part || o.edge_gather >= 0;
+        return TS_OK;
+    }
 
     // ---- live constraints and per-vertex incidence counts ---------------
-    std::vector<int> inc(V, 0), inc_e(V, 0);
-    std::vector<char> edge_live(E), att_live(A), tet_live(T);
-    for (int e = 0; e < E; ++e) {
-        int a = d.edges[2 * e], b = d.edges[2 * e + 1];
-        edge_live[e] = (w[a] + w[b]) > 0.0;  // _kernels.pyx:111 skips wsum <= 0
-        if (edge_live[e]) { inc[a] += is_free(a); inc[b] += is_free(b); inc_e[a] += is_free(a); inc_e[b] += is_free(b); }
-    }
-    std::vector<double> att_wv(A), att_wc(A);
-    for (int i = 0; i < A; ++i) {
-        int v = d.att_vertex[i];
-        const int *f = d.att_faces + 3 * i;
-        att_wv[i] = w[v];
-        att_wc[i] = d.att_is_face[i] ? (w[f[0]] + w[f[1]] + w[f[2]]) / 3.0 : 0.0;
-        att_live[i] = (att_wv[i] + att_wc[i]) > 0.0;  // _kernels.pyx:309
-        if (!att_live[i]) continue;
-        inc[v] += is_free(v);
-        if (d.att_is_face[i]) for (int k = 0; k < 3; ++k) inc[f[k]] += is_free(f[k]);
-    }
-    for (int t = 0; t < T; ++t) {
-        const int *q = d.tets + 4 * t;
-        bool any = false;
-        for (int k = 0; k < 4; ++k) any |= is_free(q[k]);
-        tet_live[t] = any;  // all-pinned tets only touch pinned accumulators
-        if (any) for (int k = 0; k < 4; ++k) inc[q[k]] += is_free(q[k]);
+    std::vector<int> inc, inc_e;
+    std::vector<char> edge_live, att_live, tet_live;
+    std::vector<double> att_wv, att_wc;
+
+    void live_constraints() {
+        inc.assign(V, 0); inc_e.assign(V, 0);
+        edge_live.assign(E, 0); att_live.assign(A, 0); tet_live.assign(T, 0);
+        for (int e = 0; e < E; ++e) {
+            int a = d.edges[2 * e], b = d.edges[2 * e + 1];
+            edge_live[e] = (w[a] + w[b]) > 0.0;  // _kernels.pyx:111 skips wsum <= 0
+            if (edge_live[e]) { inc[a] += is_free(a); inc[b] += is_free(b); inc_e[a] += is_free(a); inc_e[b] += is_free(b); }
+        }
+        att_wv.assign(A, 0.0); att_wc.assign(A, 0.0);
+        for (int i = 0; i < A; ++i) {
+            int v = d.att_vertex[i];
+            const int *f = d.att_faces + 3 * i;
+            att_wv[i] = w[v];
+            att_wc[i] = d.att_is_face[i] ? (w[f[0]] + w[f[1]] + w[f[2]]) / 3.0 : 0.0;
+            att_live[i] = (att_wv[i] + att_wc[i]) > 0.0;  // _kernels.pyx:309
+            if (!att_live[i]) continue;
+            inc[v] += is_free(v);
+            if (d.att_is_face[i]) for (int k = 0; k < 3; ++k) inc[f[k]] += is_free(f[k]);
+        }
+        for (int t = 0; t < T; ++t) {
+            const int *q = d.tets + 4 * t;
+            bool any = false;
+            for (int k = 0; k < 4; ++k) any |= is_free(q[k]);
+            tet_live[t] = any;  // all-pinned tets only touch pinned accumulators
+            if (any) for (int k = 0; k < 4; ++k) inc[q[k]] += is_free(q[k]);
+        }
     }
 
     // ---- local vertex set (parts: owned + halo) ---------------------------
-    std::vector<char> local(V, part ? 0 : 1);
-    auto local_tet = [&](int t) {
+    std::vector<char> local;
+    std::vector<int> faces_local;
+    int Floc = 0;
+    bool local_tet(int t) const {
         if (!tet_live[t]) return false;
         if (!part) return true;
         for (int k = 0; k < 4; ++k) if (own_free(d.tets[4 * t + k])) return true;
         return false;
-    };
-    auto local_edge = [&](int e) {
+    }
+    bool local_edge(int e) const {
         return edge_live[e] && (!part || own_free(d.edges[2 * e]) || own_free(d.edges[2 * e + 1]));
-    };
-    auto local_att = [&](int i) {
+    }
+    bool local_att(int i) const {
         if (!att_live[i]) return false;
         if (!part || own_free(d.att_vertex[i])) return true;
         if (d.att_is_face[i]) for (int k = 0; k < 3; ++k) if (own_free(d.att_faces[3 * i + k])) return true;
         return false;
-    };
-    std::vector<int> faces_local;
-    if (part) {
-        for (int v = 0; v < V; ++v) if (own(v)) local[v] = 1;
-        for (int e = 0; e < E; ++e) if (local_edge(e)) local[d.edges[2 * e]] = local[d.edges[2 * e + 1]] = 1;
-        for (int t = 0; t < T; ++t) if (local_tet(t)) for (int k = 0; k < 4; ++k) local[d.tets[4 * t + k]] = 1;
-        for (int i = 0; i < A; ++i) if (local_att(i)) {
-            local[d.att_vertex[i]] = 1;
-            if (d.att_is_face[i]) for (int k = 0; k < 3; ++k) local[d.att_faces[3 * i + k]] = 1;
-        }
-        faces_local = part->faces;
-        for (int f : faces_local) for (int k = 0; k < 3; ++k) local[d.faces[3 * f + k]] = 1;
-    } else {
-        faces_local.resize(F);
-        std::iota(faces_local.begin(), faces_local.end(), 0);
     }
-    const int Floc = (int)faces_local.size();
+
+    void local_set() {
+        local.assign(V, part ? 0 : 1);
+        if (part) {
+            for (int v = 0; v < V; ++v) if (own(v)) local[v] = 1;
+            for (int e = 0; e < E; ++e) if (local_edge(e)) local[d.edges[2 * e]] = local[d.edges[2 * e + 1]] = 1;
+            for (int t = 0; t < T; ++t) if (local_tet(t)) for (int k = 0; k < 4; ++k) local[d.tets[4 * t + k]] = 1;
+            for (int i = 0; i < A; ++i) if (local_att(i)) {
+                local[d.att_vertex[i]] = 1;
+                if (d.att_is_face[i]) for (int k = 0; k < 3; ++k) local[d.att_faces[3 * i + k]] = 1;
+            }
+            faces_local = part->faces;
+            for (int f : faces_local) for (int k = 0; k < 3; ++k) local[d.faces[3 * f + k]] = 1;
+        } else {
+            faces_local.resize(F);
+            std::iota(faces_local.begin(), faces_local.end(), 0);
+        }
+        Floc = (int)faces_local.size();
+    }
 
     // ---- storage order -------------------------------------------------
-    // [owned free (cost-sorted) | pad | owned pinned | pad | halo (other parts' vertices) | pad]
-    std::vector<int> free_v, pinned_v, halo_v;
-    for (int v = 0; v < V; ++v) {
-        if (!local[v]) continue;
-        if (!own(v)) halo_v.push_back(v);
-        else (is_free(v) ? free_v : pinned_v).push_back(v);
-    }
-    // warps own vertices of similar per-substep gather cost: an owner-gathered edge costs about
-    // three slot reads (it recomputes the correction), a slot one
-    std::vector<int> cost(V);
-    for (int v = 0; v < V; ++v) cost[v] = eg ? inc[v] + 2 * inc_e[v] : inc[v];
-    std::stable_sort(free_v.begin(), free_v.end(), [&](int a, int b) { return cost[a] > cost[b]; });
-    const int Vf = (int)free_v.size();
-    const int Vf_pad = roundup(Vf, 32);
-    const int Vown = Vf_pad + roundup((int)pinned_v.size(), 32);
-    // pinned copies (PinCopies): fp32 single-CTA gather programs with a bank schedule (TS_PIN_COPIES
-    // overrides: 1, 2, 4 or 8)
+    int Vf = 0, Vf_pad = 0, Vown = 0, Vstore = 0, B = 0, VPT = 1, G = 0;
     PinCopies pc;
-    pc.Vf_pad = Vf_pad; pc.Vown = Vown; pc.Np_pad = Vown - Vf_pad;
-    // (not for distance-only programs: the edges kernel is latency-bound and their coloured rounds
-    // measured 8% slower, profiles/r02m config 2)
-    if (prec == TS_F32 && !part && eg && o.schedule_banks >= 0 && pc.Np_pad > 0 && T > 0) pc.n = 4;
-    if (const char *env = std::getenv("TS_PIN_COPIES")) {
-        const int c = std::atoi(env);
-        if (c == 1 || ((c == 2 || c == 4 || c == 8) && prec == TS_F32 && !part && pc.Np_pad > 0)) pc.n = c;
-    }
-    int Vstore = Vown + roundup((int)halo_v.size(), 32) + (pc.n - 1) * pc.Np_pad;
-    if (part && part->force_Vstore) {
-        if (part->force_Vstore < Vstore) { err = "forced Vstore too small"; return TS_ERR_INVALID; }
-        Vstore = part->force_Vstore;
-    }
-    std::vector<int> s2o(Vstore, -1), o2s(V, -1);
-    for (int i = 0; i < Vf; ++i) { s2o[i] = free_v[i]; o2s[free_v[i]] = i; }
-    for (size_t i = 0; i < pinned_v.size(); ++i) { s2o[Vf_pad + i] = pinned_v[i]; o2s[pinned_v[i]] = Vf_pad + (int)i; }
-    for (size_t i = 0; i < halo_v.size(); ++i) { s2o[Vown + i] = halo_v[i]; o2s[halo_v[i]] = Vown + (int)i; }
-    auto place_copies = [&]() {   // s2o of the pinned copies from the primaries' (final) positions
+    std::vector<int> s2o, o2s;
+    void place_copies() {   // s2o of the pinned copies from the primaries' (final) positions
         for (int p = Vf_pad; p < Vown; ++p)
             for (int j = 1; j < pc.n; ++j) s2o[pc.pos(p, j)] = s2o[p];
-    };
-    place_copies();
+    }
 
-    // fp32: one thread per free vertex (3 CTAs/SM fit); fp64 runs 1 CTA/SM (shared memory), so it
-    // takes 1.5x the threads to widen phase 1 (measured on B200: 3.81 vs 4.30 ms at 4096 envs)
-    // cluster parts: 1.5x too -- one env's CTAs run a few warps each and are latency-bound
-    // fp64 programs of at most 320 free positions: one thread per vertex and two CTAs per SM
-    // (step2_kernel) beat 1.5x threads at one CTA per SM
-    const bool wide = (R == 8 && Vf_pad > 320) || part;
-    int B = o.block_threads > 0 ? o.block_threads
+    int storage_order() {
+        // [owned free (cost-sorted) | pad | owned pinned | pad | halo (other parts' vertices) | pad]
+        std::vector<int> free_v, pinned_v, halo_v;
+        for (int v = 0; v < V; ++v) {
+            if (!local[v]) continue;
+            if (!own(v)) halo_v.push_back(v);
+            else (is_free(v) ? free_v : pinned_v).push_back(v);
+        }
+        // warps own vertices of similar per-substep gather cost: an owner-gathered edge costs about
+        // three slot reads (it recomputes the correction), a slot one
+        std::vector<int> cost(V);
+        for (int v = 0; v < V; ++v) cost[v] = eg ? inc[v] + 2 * inc_e[v] : inc[v];
+        std::stable_sort(free_v.begin(), free_v.end(), [&](int a, int b) { return cost[a] > cost[b]; });
+        Vf = (int)free_v.size();
+        Vf_pad = roundup(Vf, 32);
+        Vown = Vf_pad + roundup((int)pinned_v.size(), 32);
+        // pinned copies (PinCopies): fp32 single-CTA gather programs with a bank schedule (TS_PIN_COPIES
+        // overrides: 1, 2, 4 or 8)
+        pc.Vf_pad = Vf_pad; pc.Vown = Vown; pc.Np_pad = Vown - Vf_pad;
+        // (not for distance-only programs: the edges kernel is latency-bound and their coloured rounds
+        // measured 8% slower, profiles/r02m config 2)
+        if (prec == TS_F32 && !part && eg && o.schedule_banks >= 0 && pc.Np_pad > 0 && T > 0) pc.n = 4;
+        if (const char *env = std::getenv("TS_PIN_COPIES")) {
+            const int c = std::atoi(env);
+            if (c == 1 || ((c == 2 || c == 4 || c == 8) && prec == TS_F32 && !part && pc.Np_pad > 0)) pc.n = c;
+        }
+        Vstore = Vown + roundup((int)halo_v.size(), 32) + (pc.n - 1) * pc.Np_pad;
+        if (part && part->force_Vstore) {
+            if (part->force_Vstore < Vstore) return fail(TS_ERR_INVALID, "forced Vstore too small");
+            Vstore = part->force_Vstore;
+        }
+        s2o.assign(Vstore, -1); o2s.assign(V, -1);
+        for (int i = 0; i < Vf; ++i) { s2o[i] = free_v[i]; o2s[free_v[i]] = i; }
+        for (size_t i = 0; i < pinned_v.size(); ++i) { s2o[Vf_pad + i] = pinned_v[i]; o2s[pinned_v[i]] = Vf_pad + (int)i; }
+        for (size_t i = 0; i < halo_v.size(); ++i) { s2o[Vown + i] = halo_v[i]; o2s[halo_v[i]] = Vown + (int)i; }
+        place_copies();
+
+        // fp32: one thread per free vertex (3 CTAs/SM fit); fp64 runs 1 CTA/SM (shared memory), so it
+        // takes 1.5x the threads to widen phase 1 (measured on B200: 3.81 vs 4.30 ms at 4096 envs)
+        // cluster parts: 1.5x too -- one env's CTAs run a few warps each and are latency-bound
+        // fp64 programs of at most 320 free positions: one thread per vertex and two CTAs per SM
+        // (step2_kernel) beat 1.5x threads at one CTA per SM
+        const bool wide = (R == 8 && Vf_pad > 320) || part;
+        B = o.block_threads > 0 ? o.block_threads
                                 : std::min(512, std::max(64, wide ? roundup(Vf_pad * 3 / 2, 32) : Vf_pad));
-    if (part && part->force_B) B = part->force_B;
-    if (B % 32 != 0 || B < 32 || B > 512) { err = "block_threads must be a multiple of 32 in [32, 512]"; return TS_ERR_INVALID; }
-    const int VPT = std::max(1, (Vf_pad + B - 1) / B);
-    if (VPT > 8) { err = "mesh too large for one CTA per environment (more than 8 vertices per thread)"; return TS_ERR_UNSUPPORTED; }
-    const int G = Vf_pad / 32;
+        if (part && part->force_B) B = part->force_B;
+        if (B % 32 != 0 || B < 32 || B > 512) return fail(TS_ERR_INVALID, "block_threads must be a multiple of 32 in [32, 512]");
+        VPT = std::max(1, (Vf_pad + B - 1) / B);
+        if (VPT > 8) return fail(TS_ERR_UNSUPPORTED, "mesh too large for one CTA per environment (more than 8 vertices per thread)");
+        G = Vf_pad / 32;
+        return TS_OK;
+    }
 
     // ---- items per kind (constraint index order) -----------------------
-    auto P = [&](int v) { return o2s[v]; };
     std::vector<Item> kinds[3];
-    for (int e = 0; e < E; ++e) if (local_edge(e)) {
-        Item it{}; it.kind = TS_CHUNK_EDGE; it.index = e; it.nroles = 2;
-        it.vid[0] = d.edges[2 * e]; it.vid[1] = d.edges[2 * e + 1];
-        it.pos[0] = P(it.vid[0]); it.pos[1] = P(it.vid[1]);
-        kinds[0].push_back(it);
-    }
-    for (int i = 0; i < A; ++i) if (local_att(i)) {
-        Item it{}; it.kind = TS_CHUNK_ATT; it.index = i;
-        it.vid[0] = d.att_vertex[i];
-        it.pos[0] = P(it.vid[0]);
-        if (d.att_is_face[i]) {
-            it.nroles = 4;
-            for (int k = 0; k < 3; ++k) { it.vid[1 + k] = d.att_faces[3 * i + k]; it.pos[1 + k] = P(it.vid[1 + k]); }
-        } else it.nroles = 1;
-        kinds[1].push_back(it);
-    }
-    for (int t = 0; t < T; ++t) if (local_tet(t)) {
-        Item it{}; it.kind = TS_CHUNK_TET; it.index = t; it.nroles = 4;
-        for (int k = 0; k < 4; ++k) { it.vid[k] = d.tets[4 * t + k]; it.pos[k] = P(it.vid[k]); }
-        kinds[2].push_back(it);
+
+    void collect_items() {
+        auto P = [&](int v) { return o2s[v]; };
+        for (int e = 0; e < E; ++e) if (local_edge(e)) {
+            Item it{}; it.kind = TS_CHUNK_EDGE; it.index = e; it.nroles = 2;
+            it.vid[0] = d.edges[2 * e]; it.vid[1] = d.edges[2 * e + 1];
+            it.pos[0] = P(it.vid[0]); it.pos[1] = P(it.vid[1]);
+            kinds[0].push_back(it);
+        }
+        for (int i = 0; i < A; ++i) if (local_att(i)) {
+            Item it{}; it.kind = TS_CHUNK_ATT; it.index = i;
+            it.vid[0] = d.att_vertex[i];
+            it.pos[0] = P(it.vid[0]);
+            if (d.att_is_face[i]) {
+                it.nroles = 4;
+                for (int k = 0; k < 3; ++k) { it.vid[1 + k] = d.att_faces[3 * i + k]; it.pos[1 + k] = P(it.vid[1 + k]); }
+            } else it.nroles = 1;
+            kinds[1].push_back(it);
+        }
+        for (int t = 0; t < T; ++t) if (local_tet(t)) {
+            Item it{}; it.kind = TS_CHUNK_TET; it.index = t; it.nroles = 4;
+            for (int k = 0; k < 4; ++k) { it.vid[k] = d.tets[4 * t + k]; it.pos[k] = P(it.vid[k]); }
+            kinds[2].push_back(it);
+        }
     }
 
     // ---- chunking by slot budget ---------------------------------------
-    // The reference's per-vertex accumulation order is the constraint sequence
-    // [live edges..., grasp, live attachments..., live tets...].  Chunks are
-    // contiguous ranges of that sequence (kinds may mix); the grasp is spliced
-    // into the chunk where the edges end, after each vertex's edge slots.
-    std::vector<Item> seq;
-    for (int k = eg ? 1 : 0; k < 3; ++k) seq.insert(seq.end(), kinds[k].begin(), kinds[k].end());
-    // slot budget per chunk: explicit, or what the CTA's shared memory leaves next to the positions
-    int budget = o.max_chunk_slots > 0 ? o.max_chunk_slots : (1 << 30);
-    if (o.max_chunk_slots <= 0) {
-        const int fixed = ts_smem_layout_bytes(Vstore, 0, Vf_pad, Floc, R, eg ? 1 : 0);
-        const int avail = (TS_SMEM_LIMIT - fixed) / (3 * R) - 32;    // minus a margin of 32 slots
-        if (avail < 7 * Floc || avail < 64) {
-            err = "mesh too large for one CTA per environment (shared memory); use a cluster program";
-            return TS_ERR_UNSUPPORTED;
-        }
-        budget = avail;
-    }
     struct ChunkBuild { std::vector<Item> items; std::vector<int> val; std::vector<int> kmax; int padded; };
     std::vector<ChunkBuild> chunks;
-    {
+    int budget = 0, n_chunks = 0, grasp_chunk = 0;
+
+    int chunking() {
+        // The reference's per-vertex accumulation order is the constraint sequence
+        // [live edges..., grasp, live attachments..., live tets...].  Chunks are
+        // contiguous ranges of that sequence (kinds may mix); the grasp is spliced
+        // into the chunk where the edges end, after each vertex's edge slots.
+        std::vector<Item> seq;
+        for (int k = eg ? 1 : 0; k < 3; ++k) seq.insert(seq.end(), kinds[k].begin(), kinds[k].end());
+        // slot budget per chunk: explicit, or what the CTA's shared memory leaves next to the positions
+        budget = o.max_chunk_slots > 0 ? o.max_chunk_slots : (1 << 30);
+        if (o.max_chunk_slots <= 0) {
+            const int fixed = ts_smem_layout_bytes(Vstore, 0, Vf_pad, Floc, R, eg ? 1 : 0);
+            const int avail = (TS_SMEM_LIMIT - fixed) / (3 * R) - 32;    // minus a margin of 32 slots
+            if (avail < 7 * Floc || avail < 64)
+                return fail(TS_ERR_UNSUPPORTED, "mesh too large for one CTA per environment (shared memory); use a cluster program");
+            budget = avail;
+        }
         size_t i = 0;
         while (i < seq.size()) {
             ChunkBuild c;
@@ -1451,58 +1513,80 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
             }
             chunks.push_back(std::move(c));
         }
-    }
-    const int n_chunks = (int)chunks.size();
-    // grasp chunk: the chunk holding the first non-edge item (n_chunks if there is none)
-    int grasp_chunk = n_chunks;
-    if (eg) grasp_chunk = 0;   // after the owner's edges, before any slot (gsplit = 0)
-    else {
-        const size_t n_edges = kinds[0].size();
-        if (n_edges < seq.size()) {
-            size_t pos = 0;
-            for (int c = 0; c < n_chunks; ++c) {
-                if (n_edges < pos + chunks[c].items.size()) { grasp_chunk = c; break; }
-                pos += chunks[c].items.size();
+        n_chunks = (int)chunks.size();
+        // grasp chunk: the chunk holding the first non-edge item (n_chunks if there is none)
+        grasp_chunk = n_chunks;
+        if (eg) grasp_chunk = 0;   // after the owner's edges, before any slot (gsplit = 0)
+        else {
+            const size_t n_edges = kinds[0].size();
+            if (n_edges < seq.size()) {
+                size_t pos = 0;
+                for (int c = 0; c < n_chunks; ++c) {
+                    if (n_edges < pos + chunks[c].items.size()) { grasp_chunk = c; break; }
+                    pos += chunks[c].items.size();
+                }
             }
         }
+        return TS_OK;
     }
 
     // ---- phase-1 schedule (per chunk, per kind) ----------------------------
-    const bool sched = o.schedule_banks >= 0;
-    const char *pack_env = std::getenv("TS_PACK_TETS");   // development switch: 0 = round-1 schedule
-    const bool packed = pc.n > 1 && sched && o.schedule_banks != 2 && (!pack_env || std::atoi(pack_env) != 0);
-    const int bank_mod = (R == 8) ? 16 : 32;
-    std::vector<TsChunk> chunk_rec(n_chunks);
+    bool packed = false;
+    int bank_mod = 32, total_conf = 0;
+    std::vector<TsChunk> chunk_rec;
     std::vector<Item> all_items[3];
-    for (int c = 0; c < n_chunks; ++c) {
-        ChunkBuild &cb = chunks[c];
-        TsChunk &r = chunk_rec[c];
-        std::memset(&r, 0, sizeof(r));
-        int begin[3], count[3];
-        for (int k = 0; k < 3; ++k) {
-            const int kind = k == 0 ? TS_CHUNK_EDGE : (k == 1 ? TS_CHUNK_ATT : TS_CHUNK_TET);
-            std::vector<Item> part;
-            for (const Item &it : cb.items) if (it.kind == kind) { part.push_back(it); part.back().chunk = c; }
-            int conf = 0;
-            // tets may get idle lanes (TS_TET_HOLES per 32-item batch) where no conflict-free
-            // item is left; every tet still runs exactly once (off by default: slower on B200)
-            // (packed programs re-batch their tets from scratch below: no greedy schedule for them)
-            std::vector<Item> s = schedule_items(part, bank_mod, 32,
-                                                 sched && kind != TS_CHUNK_ATT && !(packed && kind == TS_CHUNK_TET),
-                                                 &conf, (kind == TS_CHUNK_TET && o.schedule_banks >= 0) ? g_tet_holes : 0);
-            begin[k] = (int)all_items[k].size();
-            count[k] = (int)s.size();
-            all_items[k].insert(all_items[k].end(), s.begin(), s.end());
+
+    void schedule() {
+        const bool sched = o.schedule_banks >= 0;
+        const char *pack_env = std::getenv("TS_PACK_TETS");   // development switch: 0 = round-1 schedule
+        packed = pc.n > 1 && sched && o.schedule_banks != 2 && (!pack_env || std::atoi(pack_env) != 0);
+        bank_mod = (R == 8) ? 16 : 32;
+        chunk_rec.assign(n_chunks, TsChunk{});
+        for (int c = 0; c < n_chunks; ++c) {
+            ChunkBuild &cb = chunks[c];
+            TsChunk &r = chunk_rec[c];
+            std::memset(&r, 0, sizeof(r));
+            int begin[3], count[3];
+            for (int k = 0; k < 3; ++k) {
+                const int kind = k == 0 ? TS_CHUNK_EDGE : (k == 1 ? TS_CHUNK_ATT : TS_CHUNK_TET);
+                std::vector<Item> part_items;
+                for (const Item &it : cb.items) if (it.kind == kind) { part_items.push_back(it); part_items.back().chunk = c; }
+                int conf = 0;
+                // tets may get idle lanes (TS_TET_HOLES per 32-item batch) where no conflict-free
+                // item is left; every tet still runs exactly once (off by default: slower on B200)
+                // (packed programs re-batch their tets from scratch below: no greedy schedule for them)
+                std::vector<Item> s = schedule_items(part_items, bank_mod, 32,
+                                                     sched && kind != TS_CHUNK_ATT && !(packed && kind == TS_CHUNK_TET),
+                                                     &conf, (kind == TS_CHUNK_TET && o.schedule_banks >= 0) ? g_tet_holes : 0);
+                begin[k] = (int)all_items[k].size();
+                count[k] = (int)s.size();
+                all_items[k].insert(all_items[k].end(), s.begin(), s.end());
+            }
+            r.edge_begin = begin[0]; r.edge_count = count[0];
+            r.att_begin = begin[1]; r.att_count = count[1];
+            r.tet_begin = begin[2]; r.tet_count = count[2];
+            r.region_off = c * G;
+            r.val_off = c * Vf_pad;
         }
-        r.edge_begin = begin[0]; r.edge_count = count[0];
-        r.att_begin = begin[1]; r.att_count = count[1];
-        r.tet_begin = begin[2]; r.tet_count = count[2];
-        r.region_off = c * G;
-        r.val_off = c * Vf_pad;
+        if (packed) pack();
+        // joint refinement: item order, vertex lanes inside each warp, role order (see bank_refine)
+        if (sched && o.schedule_banks != 2 && !packed) refine();
+        // final positions of every role (pinned corners: the copy they read)
+        for (int k = 0; k < 3; ++k)
+            for (Item &it : all_items[k])
+                for (int r = 0; r < it.nroles; ++r) it.pos[r] = pc.pos(o2s[it.vid[r]], it.copy[r]);
+        total_conf = 0;
+        for (int c = 0; c < n_chunks; ++c) {
+            TsChunk &r = chunk_rec[c];
+            r.conflicts = batch_conflicts(all_items[0], r.edge_begin, r.edge_count, bank_mod) +
+                          batch_conflicts(all_items[2], r.tet_begin, r.tet_count, bank_mod);
+            total_conf += r.conflicts;
+        }
     }
+
     // fp32 gather programs with pinned copies: lanes balanced for the owner edge gather, then tets
     // packed into conflict-free batches (balance_lanes, pack_tet_batches)
-    if (packed) {
+    void pack() {
         std::vector<std::vector<int>> nbrs(V);
         std::vector<int> tetval(V, 0);
         for (int e = 0; e < E; ++e) {
@@ -1519,23 +1603,29 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
         std::vector<Item> tets_out;
         int resid = 0;
         for (int c = 0; c < n_chunks; ++c) {
-            std::vector<Item> part;
+            std::vector<Item> part_items;
             for (int i = 0; i < chunk_rec[c].tet_count; ++i) {
                 const Item &it = all_items[2][chunk_rec[c].tet_begin + i];
-                if (it.index >= 0) { part.push_back(it); part.back().sign = 1; for (int r = 0; r < 4; ++r) part.back().copy[r] = 0; }
+                if (it.index >= 0) {
+                    part_items.push_back(it);
+                    part_items.back().sign = 1;
+                    for (int r = 0; r < 4; ++r) part_items.back().copy[r] = 0;
+                }
             }
-            std::sort(part.begin(), part.end(), [](const Item &x, const Item &y) { return x.index < y.index; });
-            for (Item &it : part) for (int r = 0; r < 4; ++r) it.vid[r] = d.tets[4 * it.index + r];   // reference corner order
-            resid += pack_tet_batches(part, o2s, s2o, pc, Vstore);
+            std::sort(part_items.begin(), part_items.end(), [](const Item &x, const Item &y) { return x.index < y.index; });
+            for (Item &it : part_items) for (int r = 0; r < 4; ++r) it.vid[r] = d.tets[4 * it.index + r];   // reference corner order
+            resid += pack_tet_batches(part_items, o2s, s2o, pc, Vstore);
             chunk_rec[c].tet_begin = (int)tets_out.size();
-            chunk_rec[c].tet_count = (int)part.size();
-            tets_out.insert(tets_out.end(), part.begin(), part.end());
+            chunk_rec[c].tet_count = (int)part_items.size();
+            tets_out.insert(tets_out.end(), part_items.begin(), part_items.end());
         }
         all_items[2].swap(tets_out);
         if (std::getenv("TS_DEBUG_REFINE")) std::fprintf(stderr, "pack_tet_batches: residual %d\n", resid);
     }
-    // joint refinement: item order, vertex lanes inside each warp, role order (see bank_refine)
-    if (sched && o.schedule_banks != 2 && !packed) {
+
+    // the round-1 schedule: simulated-annealing refinement of item order, lanes and roles, then edges
+    // by bipartite edge colouring
+    void refine() {
         std::vector<ListRef> lists;
         for (int c = 0; c < n_chunks; ++c) {
             if (chunk_rec[c].edge_count) lists.push_back({&all_items[0], chunk_rec[c].edge_begin, chunk_rec[c].edge_count});
@@ -1546,199 +1636,207 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
         // edges: exact conflict-free batches by bipartite edge colouring (with the final positions)
         std::vector<Item> edges_out;
         for (int c = 0; c < n_chunks; ++c) {
-            std::vector<Item> part(all_items[0].begin() + chunk_rec[c].edge_begin,
-                                   all_items[0].begin() + chunk_rec[c].edge_begin + chunk_rec[c].edge_count);
-            for (Item &it : part) for (int r = 0; r < it.nroles; ++r) it.pos[r] = o2s[it.vid[r]];
-            std::vector<Item> colored = part;
+            std::vector<Item> part_items(all_items[0].begin() + chunk_rec[c].edge_begin,
+                                         all_items[0].begin() + chunk_rec[c].edge_begin + chunk_rec[c].edge_count);
+            for (Item &it : part_items) for (int r = 0; r < it.nroles; ++r) it.pos[r] = o2s[it.vid[r]];
+            std::vector<Item> colored = part_items;
             if (edge_coloring_schedule(colored, o2s, s2o, Vf_pad, bank_mod)) {
                 for (Item &it : colored) for (int r = 0; r < it.nroles; ++r) it.pos[r] = o2s[it.vid[r]];
                 if (batch_conflicts(colored, 0, (int)colored.size(), bank_mod) <
-                    batch_conflicts(part, 0, (int)part.size(), bank_mod))
-                    part.swap(colored);
+                    batch_conflicts(part_items, 0, (int)part_items.size(), bank_mod))
+                    part_items.swap(colored);
             }
             chunk_rec[c].edge_begin = (int)edges_out.size();
-            chunk_rec[c].edge_count = (int)part.size();
-            edges_out.insert(edges_out.end(), part.begin(), part.end());
+            chunk_rec[c].edge_count = (int)part_items.size();
+            edges_out.insert(edges_out.end(), part_items.begin(), part_items.end());
         }
         all_items[0].swap(edges_out);
     }
-    // final positions of every role (pinned corners: the copy they read)
-    for (int k = 0; k < 3; ++k)
-        for (Item &it : all_items[k])
-            for (int r = 0; r < it.nroles; ++r) it.pos[r] = pc.pos(o2s[it.vid[r]], it.copy[r]);
-    int total_conf = 0;
-    for (int c = 0; c < n_chunks; ++c) {
-        TsChunk &r = chunk_rec[c];
-        r.conflicts = batch_conflicts(all_items[0], r.edge_begin, r.edge_count, bank_mod) +
-                      batch_conflicts(all_items[2], r.tet_begin, r.tet_count, bank_mod);
-        total_conf += r.conflicts;
-    }
 
     // ---- slot assignment (reference per-vertex order, final positions) --------
-    // Slots are numbered per vertex in the constraint sequence order (edges,
-    // attachments, tets, each by index) whatever the phase-1 schedule is.
-    std::vector<int32_t> region((size_t)n_chunks * G), valence((size_t)n_chunks * Vf_pad), static_cnt(Vf_pad, 0);
-    std::vector<int32_t> gsplit(Vf_pad, 0);
+    std::vector<int32_t> region, valence, static_cnt, gsplit;
     int slot_cap = 0, n_slots_total = 0;
-    for (int c = 0; c < n_chunks; ++c) {
-        TsChunk &rec = chunk_rec[c];
-        // items of this chunk in sequence order
-        std::vector<Item *> seqc;
-        for (int k = 0; k < 3; ++k) {
-            const int b0 = k == 0 ? rec.edge_begin : (k == 1 ? rec.att_begin : rec.tet_begin);
-            const int n0 = k == 0 ? rec.edge_count : (k == 1 ? rec.att_count : rec.tet_count);
-            std::vector<Item *> part;
-            for (int i = 0; i < n0; ++i) part.push_back(&all_items[k][b0 + i]);
-            std::sort(part.begin(), part.end(), [](const Item *x, const Item *y) { return x->index < y->index; });
-            seqc.insert(seqc.end(), part.begin(), part.end());
-        }
-        std::vector<int> kmax(G, 0), val(Vf_pad, 0);
-        for (Item *it : seqc)
-            for (int r = 0; r < it->nroles; ++r)
-                if (it->pos[r] < Vf_pad) { const int p = it->pos[r]; kmax[p / 32] = std::max(kmax[p / 32], ++val[p]); }
-        int base = 0;
-        for (int g = 0; g < G; ++g) { region[(size_t)c * G + g] = base; base += 32 * kmax[g]; }
-        rec.slot_count = base;
-        // pinned endpoints get no slot (-1: the kernel predicates that store off; every store then
-        // has exactly one writer, so the step is clean under compute-sanitizer racecheck)
-        slot_cap = std::max(slot_cap, base);
-        std::vector<int> k_next(Vf_pad, 0);
-        for (Item *it : seqc) {
-            for (int r = 0; r < it->nroles; ++r) {
-                const int p = it->pos[r];
-                if (p >= Vf_pad) { it->slot[r] = -1; continue; }
-                it->slot[r] = region[(size_t)c * G + p / 32] + 32 * k_next[p] + (p % 32);
-                k_next[p]++;
-                if (c == grasp_chunk && it->kind == TS_CHUNK_EDGE) gsplit[p] = k_next[p];
+
+    int assign_slots() {
+        // Slots are numbered per vertex in the constraint sequence order (edges,
+        // attachments, tets, each by index) whatever the phase-1 schedule is.
+        region.assign((size_t)n_chunks * G, 0); valence.assign((size_t)n_chunks * Vf_pad, 0);
+        static_cnt.assign(Vf_pad, 0); gsplit.assign(Vf_pad, 0);
+        slot_cap = 0; n_slots_total = 0;
+        for (int c = 0; c < n_chunks; ++c) {
+            TsChunk &rec = chunk_rec[c];
+            // items of this chunk in sequence order
+            std::vector<Item *> seqc;
+            for (int k = 0; k < 3; ++k) {
+                const int b0 = k == 0 ? rec.edge_begin : (k == 1 ? rec.att_begin : rec.tet_begin);
+                const int n0 = k == 0 ? rec.edge_count : (k == 1 ? rec.att_count : rec.tet_count);
+                std::vector<Item *> part_items;
+                for (int i = 0; i < n0; ++i) part_items.push_back(&all_items[k][b0 + i]);
+                std::sort(part_items.begin(), part_items.end(), [](const Item *x, const Item *y) { return x->index < y->index; });
+                seqc.insert(seqc.end(), part_items.begin(), part_items.end());
+            }
+            std::vector<int> kmax(G, 0), val(Vf_pad, 0);
+            for (Item *it : seqc)
+                for (int r = 0; r < it->nroles; ++r)
+                    if (it->pos[r] < Vf_pad) { const int p = it->pos[r]; kmax[p / 32] = std::max(kmax[p / 32], ++val[p]); }
+            int base = 0;
+            for (int g = 0; g < G; ++g) { region[(size_t)c * G + g] = base; base += 32 * kmax[g]; }
+            rec.slot_count = base;
+            // pinned endpoints get no slot (-1: the kernel predicates that store off; every store then
+            // has exactly one writer, so the step is clean under compute-sanitizer racecheck)
+            slot_cap = std::max(slot_cap, base);
+            std::vector<int> k_next(Vf_pad, 0);
+            for (Item *it : seqc) {
+                for (int r = 0; r < it->nroles; ++r) {
+                    const int p = it->pos[r];
+                    if (p >= Vf_pad) { it->slot[r] = -1; continue; }
+                    it->slot[r] = region[(size_t)c * G + p / 32] + 32 * k_next[p] + (p % 32);
+                    k_next[p]++;
+                    if (c == grasp_chunk && it->kind == TS_CHUNK_EDGE) gsplit[p] = k_next[p];
+                }
+            }
+            for (int p = 0; p < Vf_pad; ++p) {
+                valence[(size_t)c * Vf_pad + p] = k_next[p];
+                static_cnt[p] += k_next[p];
+                n_slots_total += k_next[p];
             }
         }
-        for (int p = 0; p < Vf_pad; ++p) {
-            valence[(size_t)c * Vf_pad + p] = k_next[p];
-            static_cnt[p] += k_next[p];
-            n_slots_total += k_next[p];
+        // contact records reuse the slot buffer: 3F records x 7 reals <= 3 arrays x S reals
+        slot_cap = std::max(slot_cap, 7 * Floc);
+        slot_cap = roundup(std::max(slot_cap, 32), 32);
+        if (part && part->force_slot_cap) {
+            if (part->force_slot_cap < slot_cap) return fail(TS_ERR_INVALID, "forced slot capacity too small");
+            slot_cap = part->force_slot_cap;
         }
-    }
-    // contact records reuse the slot buffer: 3F records x 7 reals <= 3 arrays x S reals
-    slot_cap = std::max(slot_cap, 7 * Floc);
-    slot_cap = roundup(std::max(slot_cap, 32), 32);
-    if (part && part->force_slot_cap) {
-        if (part->force_slot_cap < slot_cap) { err = "forced slot capacity too small"; return TS_ERR_INVALID; }
-        slot_cap = part->force_slot_cap;
+        return TS_OK;
     }
 
-    // ---- emit --------------------------------------------------------------
-    const int nE = (int)all_items[0].size(), nA = (int)all_items[1].size(), nT = (int)all_items[2].size();
-    std::vector<int32_t> edge_idx(4 * (size_t)nE), tet_idx(4 * (size_t)nT), tet_slot(4 * (size_t)nT);
-    std::vector<int32_t> att_idx(4 * (size_t)nA), att_slot(4 * (size_t)nA);
-    std::vector<double> edge_par(4 * (size_t)nE), tet_rv(nT), att_par(4 * (size_t)nA), att_anc(4 * (size_t)nA);
-    for (int i = 0; i < nE; ++i) {
-        const Item &it = all_items[0][i];
-        const int a = it.vid[0], b = it.vid[1];   // roles may be swapped by the bank refinement
-        edge_idx[4 * i + 0] = it.pos[0]; edge_idx[4 * i + 1] = it.pos[1];
-        edge_idx[4 * i + 2] = it.slot[0]; edge_idx[4 * i + 3] = it.slot[1];
-        if (it.index < 0) {   // padding lane of a colour class: pinned endpoints, no slot
-            edge_par[4 * i + 0] = 0.0; edge_par[4 * i + 1] = 0.0; edge_par[4 * i + 2] = 0.0;
-            edge_par[4 * i + 3] = 1.0;
-            continue;
+    // ---- emit: the full (uncompressed) tables ----------------------------------
+    int nE = 0, nA = 0, nT = 0;
+    std::vector<int32_t> edge_idx, tet_idx, tet_slot, att_idx, att_slot;
+    std::vector<double> edge_par, tet_rv, att_par, att_anc, wst, rest;
+    std::vector<int32_t> faces_s, faces_o, face_gid;
+
+    void emit_tables() {
+        nE = (int)all_items[0].size(); nA = (int)all_items[1].size(); nT = (int)all_items[2].size();
+        edge_idx.assign(4 * (size_t)nE, 0); tet_idx.assign(4 * (size_t)nT, 0); tet_slot.assign(4 * (size_t)nT, 0);
+        att_idx.assign(4 * (size_t)nA, 0); att_slot.assign(4 * (size_t)nA, 0);
+        edge_par.assign(4 * (size_t)nE, 0.0); tet_rv.assign(nT, 0.0);
+        att_par.assign(4 * (size_t)nA, 0.0); att_anc.assign(4 * (size_t)nA, 0.0);
+        for (int i = 0; i < nE; ++i) {
+            const Item &it = all_items[0][i];
+            const int a = it.vid[0], b = it.vid[1];   // roles may be swapped by the bank refinement
+            edge_idx[4 * i + 0] = it.pos[0]; edge_idx[4 * i + 1] = it.pos[1];
+            edge_idx[4 * i + 2] = it.slot[0]; edge_idx[4 * i + 3] = it.slot[1];
+            if (it.index < 0) {   // padding lane of a colour class: pinned endpoints, no slot
+                edge_par[4 * i + 0] = 0.0; edge_par[4 * i + 1] = 0.0; edge_par[4 * i + 2] = 0.0;
+                edge_par[4 * i + 3] = 1.0;
+                continue;
+            }
+            edge_par[4 * i + 0] = d.rest_length[it.index];
+            if (R == 8) {   // exact build: the reference's operands
+                edge_par[4 * i + 1] = w[a]; edge_par[4 * i + 2] = w[b]; edge_par[4 * i + 3] = w[a] + w[b];
+            } else {        // fp32 build: ca = -(ks wa / wsum)(1 - rl/dist), cb = (ks wb / wsum)(1 - rl/dist)
+                const double wsum = w[a] + w[b];
+                edge_par[4 * i + 1] = d.k_s * w[a] / wsum; edge_par[4 * i + 2] = d.k_s * w[b] / wsum;
+                edge_par[4 * i + 3] = 0.0;
+            }
         }
-        edge_par[4 * i + 0] = d.rest_length[it.index];
-        if (R == 8) {   // exact build: the reference's operands
-            edge_par[4 * i + 1] = w[a]; edge_par[4 * i + 2] = w[b]; edge_par[4 * i + 3] = w[a] + w[b];
-        } else {        // fp32 build: ca = -(ks wa / wsum)(1 - rl/dist), cb = (ks wb / wsum)(1 - rl/dist)
-            const double wsum = w[a] + w[b];
-            edge_par[4 * i + 1] = d.k_s * w[a] / wsum; edge_par[4 * i + 2] = d.k_s * w[b] / wsum;
-            edge_par[4 * i + 3] = 0.0;
+        for (int i = 0; i < nT; ++i) {
+            const Item &it = all_items[2][i];
+            if (it.index < 0) {   // idle lane of a batch: slot -1 (compact: 0xffff) tells the kernel to skip it
+                for (int k = 0; k < 4; ++k) { tet_idx[4 * i + k] = 0; tet_slot[4 * i + k] = -1; }
+                tet_rv[i] = 0.0;
+                continue;
+            }
+            for (int k = 0; k < 4; ++k) { tet_idx[4 * i + k] = it.pos[k]; tet_slot[4 * i + k] = it.slot[k]; }
+            // fp32 build works with unscaled cross products G = 6 grad: it needs 6 V0
+            tet_rv[i] = R == 8 ? d.rest_volume[it.index] : it.sign * 6.0 * d.rest_volume[it.index];
         }
-    }
-    for (int i = 0; i < nT; ++i) {
-        const Item &it = all_items[2][i];
-        if (it.index < 0) {   // idle lane of a batch: slot -1 (compact: 0xffff) tells the kernel to skip it
-            for (int k = 0; k < 4; ++k) { tet_idx[4 * i + k] = 0; tet_slot[4 * i + k] = -1; }
-            tet_rv[i] = 0.0;
-            continue;
+        for (int i = 0; i < nA; ++i) {
+            const Item &it = all_items[1][i];
+            int t = it.index;
+            att_idx[4 * i + 0] = it.pos[0];
+            att_slot[4 * i + 0] = it.slot[0];
+            for (int k = 1; k < 4; ++k) {
+                att_idx[4 * i + k] = it.nroles == 4 ? it.pos[k] : it.pos[0];
+                att_slot[4 * i + k] = it.nroles == 4 ? it.slot[k] : -1;
+            }
+            att_par[4 * i + 0] = d.att_rest[t]; att_par[4 * i + 1] = d.att_k[t];
+            att_par[4 * i + 2] = att_wv[t]; att_par[4 * i + 3] = att_wc[t];
+            const double *an = d.att_anchor + 3 * t;
+            att_anc[4 * i + 0] = d.att_is_face[t] ? 0.0 : an[0];
+            att_anc[4 * i + 1] = d.att_is_face[t] ? 0.0 : an[1];
+            att_anc[4 * i + 2] = d.att_is_face[t] ? 0.0 : an[2];
+            att_anc[4 * i + 3] = d.att_is_face[t] ? 1.0 : 0.0;
         }
-        for (int k = 0; k < 4; ++k) { tet_idx[4 * i + k] = it.pos[k]; tet_slot[4 * i + k] = it.slot[k]; }
-        // fp32 build works with unscaled cross products G = 6 grad: it needs 6 V0
-        tet_rv[i] = R == 8 ? d.rest_volume[it.index] : it.sign * 6.0 * d.rest_volume[it.index];
-    }
-    for (int i = 0; i < nA; ++i) {
-        const Item &it = all_items[1][i];
-        int t = it.index;
-        att_idx[4 * i + 0] = it.pos[0];
-        att_slot[4 * i + 0] = it.slot[0];
-        for (int k = 1; k < 4; ++k) {
-            att_idx[4 * i + k] = it.nroles == 4 ? it.pos[k] : it.pos[0];
-            att_slot[4 * i + k] = it.nroles == 4 ? it.slot[k] : -1;
+        wst.assign(Vstore, 0.0);
+        for (int p = 0; p < Vstore; ++p) if (s2o[p] >= 0) wst[p] = w[s2o[p]];
+        faces_s.assign(3 * (size_t)Floc, 0); faces_o.assign(3 * (size_t)Floc, 0); face_gid.assign(Floc, 0);
+        for (int i = 0; i < Floc; ++i) {
+            const int f = faces_local[i];
+            face_gid[i] = f;
+            for (int k = 0; k < 3; ++k) { faces_o[3 * i + k] = d.faces[3 * f + k]; faces_s[3 * i + k] = o2s[d.faces[3 * f + k]]; }
         }
-        att_par[4 * i + 0] = d.att_rest[t]; att_par[4 * i + 1] = d.att_k[t];
-        att_par[4 * i + 2] = att_wv[t]; att_par[4 * i + 3] = att_wc[t];
-        const double *an = d.att_anchor + 3 * t;
-        att_anc[4 * i + 0] = d.att_is_face[t] ? 0.0 : an[0];
-        att_anc[4 * i + 1] = d.att_is_face[t] ? 0.0 : an[1];
-        att_anc[4 * i + 2] = d.att_is_face[t] ? 0.0 : an[2];
-        att_anc[4 * i + 3] = d.att_is_face[t] ? 1.0 : 0.0;
+        rest.assign(3 * (size_t)V, 0.0);
+        for (int i = 0; i < 3 * V; ++i) rest[i] = d.positions_rest[i];
     }
-    std::vector<double> wst(Vstore, 0.0);
-    for (int p = 0; p < Vstore; ++p) if (s2o[p] >= 0) wst[p] = w[s2o[p]];
-    std::vector<int32_t> faces_s(3 * (size_t)Floc), faces_o(3 * (size_t)Floc), face_gid(Floc);
-    for (int i = 0; i < Floc; ++i) {
-        const int f = faces_local[i];
-        face_gid[i] = f;
-        for (int k = 0; k < 3; ++k) { faces_o[3 * i + k] = d.faces[3 * f + k]; faces_s[3 * i + k] = o2s[d.faces[3 * f + k]]; }
-    }
-    std::vector<double> rest(3 * (size_t)V);
-    for (int i = 0; i < 3 * V; ++i) rest[i] = d.positions_rest[i];
 
     // ---- compact 16-bit item streams ---------------------------------------
-    // Every mesh built by load_scene has one inverse mass for all free vertices
-    // (mesh.py:217: uniform mass), so an edge needs only its rest length: the
-    // per-endpoint weights follow from which endpoints are pinned.
     double w_free = 0.0;
-    bool uniform = true;
-    for (int v = 0; v < V; ++v)
-        if (is_free(v)) {
-            if (w_free == 0.0) w_free = w[v];
-            else if (w[v] != w_free) uniform = false;
-        }
-    const bool compact = o.compact >= 0 && uniform && Vstore <= 65535 && slot_cap <= 65535;
-    // fp32 gather programs: the compact tet stream and the edge records carry BYTE offsets
-    // (12 x position / slot index) so the kernel addresses shared memory without multiplies;
-    // the streams are padded by one CTA's worth of zero items so prefetches need no clamp
-    const bool boff = compact && eg && R == 4 && 12 * Vstore <= 65535 && 12 * slot_cap <= 65535;
-    const int scale_b = boff ? 12 : 1;
-    // narrow layout (program.h): legal when nothing reads neighbour positions in phase 2 (the
-    // distance-only program gathers edges there) and no cluster peer reads the ping-pong copy.
-    // Narrow programs put the positions first, so byte-offset streams address positions and
-    // slots from ONE base (slot offsets carry + 12 Vstore) -- which must fit the 16-bit fields
-    bool narrow = false;
-    {
-        int maxval = 0;
-        for (int v : valence) maxval = std::max(maxval, v);
-        const char *nv = std::getenv("TS_NARROW");
-        // (distance-only gather programs stay wide: a narrow one needs a second barrier between the
-        // gather and the in-place apply, measured slower even at 4 CTAs / SM, profiles/r02j)
-        narrow = !part && (n_chunks >= 1 || !eg) && maxval <= 255 && !(nv && nv[0] == '0') &&
-                 (!boff || 12 * (Vstore + slot_cap) < 65535);
-    }
-    const int slot_b0 = (narrow && boff) ? 12 * Vstore : 0;
-    // rest volumes as a dictionary index in the spare top bits of the four 16-bit position
-    // offsets (2 bits each; needs 12 Vstore < 16384) when few distinct 6 V0 values exist
+    bool compact = false, boff = false, narrow = false;
     std::vector<float> rv_tab;
-    std::vector<int> rv_idx(nT, 0);
-    if (boff && 12 * Vstore < 16384) {
-        std::vector<float> vals;
-        for (int i = 0; i < nT; ++i) if (all_items[2][i].index >= 0) vals.push_back((float)tet_rv[i]);
-        std::sort(vals.begin(), vals.end());
-        vals.erase(std::unique(vals.begin(), vals.end()), vals.end());
-        if (!vals.empty() && (int)vals.size() <= 256) {
-            rv_tab = vals;
-            for (int i = 0; i < nT; ++i)
-                if (all_items[2][i].index >= 0)
-                    rv_idx[i] = (int)(std::lower_bound(vals.begin(), vals.end(), (float)tet_rv[i]) - vals.begin());
+    std::vector<uint32_t> edge_c, tet_c;
+
+    void compact_streams() {
+        // Every mesh built by load_scene has one inverse mass for all free vertices
+        // (mesh.py:217: uniform mass), so an edge needs only its rest length: the
+        // per-endpoint weights follow from which endpoints are pinned.
+        bool uniform = true;
+        w_free = 0.0;
+        for (int v = 0; v < V; ++v)
+            if (is_free(v)) {
+                if (w_free == 0.0) w_free = w[v];
+                else if (w[v] != w_free) uniform = false;
+            }
+        compact = o.compact >= 0 && uniform && Vstore <= 65535 && slot_cap <= 65535;
+        // fp32 gather programs: the compact tet stream and the edge records carry BYTE offsets
+        // (12 x position / slot index) so the kernel addresses shared memory without multiplies;
+        // the streams are padded by one CTA's worth of zero items so prefetches need no clamp
+        boff = compact && eg && R == 4 && 12 * Vstore <= 65535 && 12 * slot_cap <= 65535;
+        const int scale_b = boff ? 12 : 1;
+        // narrow layout (program.h): legal when nothing reads neighbour positions in phase 2 (the
+        // distance-only program gathers edges there) and no cluster peer reads the ping-pong copy.
+        // Narrow programs put the positions first, so byte-offset streams address positions and
+        // slots from ONE base (slot offsets carry + 12 Vstore) -- which must fit the 16-bit fields
+        {
+            int maxval = 0;
+            for (int v : valence) maxval = std::max(maxval, v);
+            const char *nv = std::getenv("TS_NARROW");
+            // (distance-only gather programs stay wide: a narrow one needs a second barrier between the
+            // gather and the in-place apply, measured slower even at 4 CTAs / SM, profiles/r02j)
+            narrow = !part && (n_chunks >= 1 || !eg) && maxval <= 255 && !(nv && nv[0] == '0') &&
+                     (!boff || 12 * (Vstore + slot_cap) < 65535);
         }
-    }
-    std::vector<uint32_t> edge_c(compact ? 4 * (size_t)nE : 0), tet_c(compact ? 4 * ((size_t)nT + B) : 0);
-    if (compact) {
+        const int slot_b0 = (narrow && boff) ? 12 * Vstore : 0;
+        // rest volumes as a dictionary index in the spare top bits of the four 16-bit position
+        // offsets (2 bits each; needs 12 Vstore < 16384) when few distinct 6 V0 values exist
+        std::vector<int> rv_idx(nT, 0);
+        if (boff && 12 * Vstore < 16384) {
+            std::vector<float> vals;
+            for (int i = 0; i < nT; ++i) if (all_items[2][i].index >= 0) vals.push_back((float)tet_rv[i]);
+            std::sort(vals.begin(), vals.end());
+            vals.erase(std::unique(vals.begin(), vals.end()), vals.end());
+            if (!vals.empty() && (int)vals.size() <= 256) {
+                rv_tab = vals;
+                for (int i = 0; i < nT; ++i)
+                    if (all_items[2][i].index >= 0)
+                        rv_idx[i] = (int)(std::lower_bound(vals.begin(), vals.end(), (float)tet_rv[i]) - vals.begin());
+            }
+        }
+        edge_c.assign(compact ? 4 * (size_t)nE : 0, 0);
+        tet_c.assign(compact ? 4 * ((size_t)nT + B) : 0, 0);
+        if (!compact) return;
         auto pk = [](int lo, int hi) { return (uint32_t)(lo & 0xffff) | ((uint32_t)(hi & 0xffff) << 16); };
         for (int i = 0; i < nE; ++i) {
             edge_c[4 * i + 0] = pk(edge_idx[4 * i + 0], edge_idx[4 * i + 1]);
@@ -1768,22 +1866,13 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
         }
     }
 
-    // ---- owner-gathered edges (build_gather) -------------------------------------
+    // ---- owner-gathered edges, cluster tables, warp split ------------------------
     GatherProgram gp;
-    if (eg) {
-        GatherSpec gs{&d, &edge_live, &o2s, &s2o, &pc, own_free, is_free, Vf, Vf_pad, G, Vstore, R,
-                      boff, compact, packed, o.schedule_banks >= 0};
-        gp = build_gather(gs, static_cnt);
-    }
-    const int einc_bytes = gp.einc_bytes;
-    const std::vector<float> &pair_tab = gp.pair_tab;
-    const std::vector<int32_t> &eregion = gp.eregion, &evalence = gp.evalence;
-    const std::vector<uint8_t> &einc = gp.einc;
-    const int n_einc = gp.n_einc;
+    std::vector<int32_t> send_off, send, face_own, wsplit;
 
-    // ---- cluster part: halo sends and face-vertex owners ----------------------
-    std::vector<int32_t> send_off, send, face_own;
-    if (part && part->halo_of) {
+    // cluster part: halo sends and face-vertex owners
+    void cluster_tables() {
+        if (!(part && part->halo_of)) return;
         send_off.assign(Vf_pad + 1, 0);
         for (int p = 0; p < Vf_pad; ++p) {
             if (p < Vf)
@@ -1797,108 +1886,119 @@ int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector
         }
     }
 
-    // ---- phase-1 work split across warps -------------------------------------
-    const std::vector<int32_t> wsplit = warp_split(chunk_rec, evalence, eg, B, VPT, Vf);
+    // ---- the blob: header + 256-byte aligned sections ------------------------------
+    void assemble(std::vector<uint8_t> &blob, ts_layout_info &info) {
+        const std::vector<float> &pair_tab = gp.pair_tab;
+        int64_t sz[TS_SEC_COUNT];
+        sz[TS_SEC_CHUNK] = (int64_t)n_chunks * sizeof(TsChunk);
+        sz[TS_SEC_EDGE_IDX] = 16LL * nE;
+        sz[TS_SEC_EDGE_PAR] = 4LL * R * nE;
+        sz[TS_SEC_TET_IDX] = 16LL * nT;
+        sz[TS_SEC_TET_SLOT] = 16LL * nT;
+        sz[TS_SEC_TET_RV] = (int64_t)R * (nT + B);   // padded like the compact stream
+        sz[TS_SEC_ATT_IDX] = 16LL * nA;
+        sz[TS_SEC_ATT_SLOT] = 16LL * nA;
+        sz[TS_SEC_ATT_PAR] = 4LL * R * nA;
+        sz[TS_SEC_ATT_ANCHOR] = 4LL * R * nA;
+        sz[TS_SEC_REGION] = 4LL * region.size();
+        sz[TS_SEC_VALENCE] = 4LL * valence.size();
+        sz[TS_SEC_STATIC_CNT] = 4LL * Vf_pad;
+        sz[TS_SEC_S2O] = 4LL * Vstore;
+        sz[TS_SEC_O2S] = 4LL * V;
+        sz[TS_SEC_W] = (int64_t)R * Vstore;
+        sz[TS_SEC_FACES] = 12LL * Floc;
+        sz[TS_SEC_FACES_ORIG] = 12LL * Floc;
+        sz[TS_SEC_REST] = 3LL * R * V;
+        sz[TS_SEC_GSPLIT] = 4LL * Vf_pad;
+        sz[TS_SEC_EDGE_C] = 4LL * edge_c.size();
+        sz[TS_SEC_TET_C] = 4LL * tet_c.size();
+        sz[TS_SEC_EINC] = (int64_t)gp.einc.size();
+        sz[TS_SEC_EREGION] = 4LL * gp.eregion.size();
+        sz[TS_SEC_EVAL] = 4LL * gp.evalence.size();
+        sz[TS_SEC_FACE_GID] = 4LL * face_gid.size();
+        sz[TS_SEC_SEND_OFF] = 4LL * send_off.size();
+        sz[TS_SEC_SEND] = 4LL * send.size();
+        sz[TS_SEC_FACE_OWN] = 4LL * face_own.size();
+        sz[TS_SEC_WSPLIT] = 4LL * wsplit.size();
+        sz[TS_SEC_RLTAB] = 4LL * pair_tab.size();
+        sz[TS_SEC_RVTAB] = 4LL * rv_tab.size();
+        TsProgHeader hdr{};
+        hdr.compact = compact ? 1 : 0;
+        hdr.w_free = w_free;
+        hdr.magic = TS_PROG_MAGIC; hdr.version = TS_PROG_VERSION; hdr.real_bytes = R; hdr.n_sections = TS_SEC_COUNT;
+        hdr.V = V; hdr.Vf = Vf; hdr.Vf_pad = Vf_pad; hdr.Vstore = Vstore;
+        hdr.F = Floc; hdr.B = B; hdr.VPT = VPT; hdr.G = G;
+        hdr.Vown = Vown; hdr.cluster_k = part ? part->K : 1; hdr.cluster_rank = part ? part->rank : 0;
+        hdr.boff = boff ? 1 : 0;
+        hdr.rvdict = rv_tab.empty() ? 0 : 1;
+        hdr.n_rltab = (int)pair_tab.size() / 2; hdr.n_rvtab = (int)rv_tab.size();
+        hdr.n_chunks = n_chunks; hdr.grasp_chunk = grasp_chunk; hdr.slot_capacity = slot_cap; hdr.n_att = nA;
+        hdr.n_edge_items = nE; hdr.n_tet_items = nT; hdr.n_att_items = nA; hdr.bank_conflicts = total_conf;
+        hdr.n_slots_total = n_slots_total;
+        hdr.edge_gather = eg ? 1 : 0; hdr.einc_bytes = gp.einc_bytes;
+        hdr.narrow = narrow ? 1 : 0;
+        int64_t off = roundup((int)sizeof(TsProgHeader), 256);
+        for (int s = 0; s < TS_SEC_COUNT; ++s) { hdr.off[s] = off; off += ((sz[s] + 255) / 256) * 256; }
+        hdr.total_bytes = off;
+        blob.assign((size_t)off, 0);
+        std::memcpy(blob.data(), &hdr, sizeof(hdr));
+        put(blob, hdr.off[TS_SEC_CHUNK], chunk_rec);
+        put(blob, hdr.off[TS_SEC_EDGE_IDX], edge_idx);
+        put(blob, hdr.off[TS_SEC_TET_IDX], tet_idx);
+        put(blob, hdr.off[TS_SEC_TET_SLOT], tet_slot);
+        put(blob, hdr.off[TS_SEC_ATT_IDX], att_idx);
+        put(blob, hdr.off[TS_SEC_ATT_SLOT], att_slot);
+        put(blob, hdr.off[TS_SEC_REGION], region);
+        put(blob, hdr.off[TS_SEC_VALENCE], valence);
+        put(blob, hdr.off[TS_SEC_STATIC_CNT], static_cnt);
+        put(blob, hdr.off[TS_SEC_S2O], s2o);
+        put(blob, hdr.off[TS_SEC_O2S], o2s);
+        put(blob, hdr.off[TS_SEC_FACES], faces_s);
+        put(blob, hdr.off[TS_SEC_FACES_ORIG], faces_o);
+        put(blob, hdr.off[TS_SEC_GSPLIT], gsplit);
+        put(blob, hdr.off[TS_SEC_EDGE_C], edge_c);
+        put(blob, hdr.off[TS_SEC_TET_C], tet_c);
+        put(blob, hdr.off[TS_SEC_EINC], gp.einc);
+        put(blob, hdr.off[TS_SEC_EREGION], gp.eregion);
+        put(blob, hdr.off[TS_SEC_EVAL], gp.evalence);
+        put(blob, hdr.off[TS_SEC_FACE_GID], face_gid);
+        put(blob, hdr.off[TS_SEC_SEND_OFF], send_off);
+        put(blob, hdr.off[TS_SEC_SEND], send);
+        put(blob, hdr.off[TS_SEC_FACE_OWN], face_own);
+        put(blob, hdr.off[TS_SEC_WSPLIT], wsplit);
+        put(blob, hdr.off[TS_SEC_RLTAB], pair_tab);
+        put(blob, hdr.off[TS_SEC_RVTAB], rv_tab);
+        auto put_real = [&](int sec, const std::vector<double> &v) {
+            if (R == 8) put(blob, hdr.off[sec], v);
+            else { std::vector<float> f(v.begin(), v.end()); put(blob, hdr.off[sec], f); }
+        };
+        put_real(TS_SEC_EDGE_PAR, edge_par);
+        put_real(TS_SEC_TET_RV, tet_rv);
+        put_real(TS_SEC_ATT_PAR, att_par);
+        put_real(TS_SEC_ATT_ANCHOR, att_anc);
+        put_real(TS_SEC_W, wst);
+        put_real(TS_SEC_REST, rest);
 
-    // sizes (bytes) per section
-    int64_t sz[TS_SEC_COUNT];
-    sz[TS_SEC_CHUNK] = (int64_t)n_chunks * sizeof(TsChunk);
-    sz[TS_SEC_EDGE_IDX] = 16LL * nE;
-    sz[TS_SEC_EDGE_PAR] = 4LL * R * nE;
-    sz[TS_SEC_TET_IDX] = 16LL * nT;
-    sz[TS_SEC_TET_SLOT] = 16LL * nT;
-    sz[TS_SEC_TET_RV] = (int64_t)R * (nT + B);   // padded like the compact stream
-    sz[TS_SEC_ATT_IDX] = 16LL * nA;
-    sz[TS_SEC_ATT_SLOT] = 16LL * nA;
-    sz[TS_SEC_ATT_PAR] = 4LL * R * nA;
-    sz[TS_SEC_ATT_ANCHOR] = 4LL * R * nA;
-    sz[TS_SEC_REGION] = 4LL * region.size();
-    sz[TS_SEC_VALENCE] = 4LL * valence.size();
-    sz[TS_SEC_STATIC_CNT] = 4LL * Vf_pad;
-    sz[TS_SEC_S2O] = 4LL * Vstore;
-    sz[TS_SEC_O2S] = 4LL * V;
-    sz[TS_SEC_W] = (int64_t)R * Vstore;
-    sz[TS_SEC_FACES] = 12LL * Floc;
-    sz[TS_SEC_FACES_ORIG] = 12LL * Floc;
-    sz[TS_SEC_REST] = 3LL * R * V;
-    sz[TS_SEC_GSPLIT] = 4LL * Vf_pad;
-    sz[TS_SEC_EDGE_C] = 4LL * edge_c.size();
-    sz[TS_SEC_TET_C] = 4LL * tet_c.size();
-    sz[TS_SEC_EINC] = (int64_t)einc.size();
-    sz[TS_SEC_EREGION] = 4LL * eregion.size();
-    sz[TS_SEC_EVAL] = 4LL * evalence.size();
-    sz[TS_SEC_FACE_GID] = 4LL * face_gid.size();
-    sz[TS_SEC_SEND_OFF] = 4LL * send_off.size();
-    sz[TS_SEC_SEND] = 4LL * send.size();
-    sz[TS_SEC_FACE_OWN] = 4LL * face_own.size();
-    sz[TS_SEC_WSPLIT] = 4LL * wsplit.size();
-    sz[TS_SEC_RLTAB] = 4LL * pair_tab.size();
-    sz[TS_SEC_RVTAB] = 4LL * rv_tab.size();
-    TsProgHeader hdr{};
-    hdr.compact = compact ? 1 : 0;
-    hdr.w_free = w_free;
-    hdr.magic = TS_PROG_MAGIC; hdr.version = TS_PROG_VERSION; hdr.real_bytes = R; hdr.n_sections = TS_SEC_COUNT;
-    hdr.V = V; hdr.Vf = Vf; hdr.Vf_pad = Vf_pad; hdr.Vstore = Vstore;
-    hdr.F = Floc; hdr.B = B; hdr.VPT = VPT; hdr.G = G;
-    hdr.Vown = Vown; hdr.cluster_k = part ? part->K : 1; hdr.cluster_rank = part ? part->rank : 0;
-    hdr.boff = boff ? 1 : 0;
-    hdr.rvdict = rv_tab.empty() ? 0 : 1;
-    hdr.n_rltab = (int)pair_tab.size() / 2; hdr.n_rvtab = (int)rv_tab.size();
-    hdr.n_chunks = n_chunks; hdr.grasp_chunk = grasp_chunk; hdr.slot_capacity = slot_cap; hdr.n_att = nA;
-    hdr.n_edge_items = nE; hdr.n_tet_items = nT; hdr.n_att_items = nA; hdr.bank_conflicts = total_conf;
-    hdr.n_slots_total = n_slots_total;
-    hdr.edge_gather = eg ? 1 : 0; hdr.einc_bytes = einc_bytes;
-    hdr.narrow = narrow ? 1 : 0;
-    int64_t off = roundup((int)sizeof(TsProgHeader), 256);
-    for (int s = 0; s < TS_SEC_COUNT; ++s) { hdr.off[s] = off; off += ((sz[s] + 255) / 256) * 256; }
-    hdr.total_bytes = off;
-    blob.assign((size_t)off, 0);
-    std::memcpy(blob.data(), &hdr, sizeof(hdr));
-    put(blob, hdr.off[TS_SEC_CHUNK], chunk_rec);
-    put(blob, hdr.off[TS_SEC_EDGE_IDX], edge_idx);
-    put(blob, hdr.off[TS_SEC_TET_IDX], tet_idx);
-    put(blob, hdr.off[TS_SEC_TET_SLOT], tet_slot);
-    put(blob, hdr.off[TS_SEC_ATT_IDX], att_idx);
-    put(blob, hdr.off[TS_SEC_ATT_SLOT], att_slot);
-    put(blob, hdr.off[TS_SEC_REGION], region);
-    put(blob, hdr.off[TS_SEC_VALENCE], valence);
-    put(blob, hdr.off[TS_SEC_STATIC_CNT], static_cnt);
-    put(blob, hdr.off[TS_SEC_S2O], s2o);
-    put(blob, hdr.off[TS_SEC_O2S], o2s);
-    put(blob, hdr.off[TS_SEC_FACES], faces_s);
-    put(blob, hdr.off[TS_SEC_FACES_ORIG], faces_o);
-    put(blob, hdr.off[TS_SEC_GSPLIT], gsplit);
-    put(blob, hdr.off[TS_SEC_EDGE_C], edge_c);
-    put(blob, hdr.off[TS_SEC_TET_C], tet_c);
-    put(blob, hdr.off[TS_SEC_EINC], einc);
-    put(blob, hdr.off[TS_SEC_EREGION], eregion);
-    put(blob, hdr.off[TS_SEC_EVAL], evalence);
-    put(blob, hdr.off[TS_SEC_FACE_GID], face_gid);
-    put(blob, hdr.off[TS_SEC_SEND_OFF], send_off);
-    put(blob, hdr.off[TS_SEC_SEND], send);
-    put(blob, hdr.off[TS_SEC_FACE_OWN], face_own);
-    put(blob, hdr.off[TS_SEC_WSPLIT], wsplit);
-    put(blob, hdr.off[TS_SEC_RLTAB], pair_tab);
-    put(blob, hdr.off[TS_SEC_RVTAB], rv_tab);
-    auto put_real = [&](int sec, const std::vector<double> &v) {
-        if (R == 8) put(blob, hdr.off[sec], v);
-        else { std::vector<float> f(v.begin(), v.end()); put(blob, hdr.off[sec], f); }
-    };
-    put_real(TS_SEC_EDGE_PAR, edge_par);
-    put_real(TS_SEC_TET_RV, tet_rv);
-    put_real(TS_SEC_ATT_PAR, att_par);
-    put_real(TS_SEC_ATT_ANCHOR, att_anc);
-    put_real(TS_SEC_W, wst);
-    put_real(TS_SEC_REST, rest);
+        std::memset(&info, 0, sizeof(info));
+        info.precision = prec; info.block_threads = B; info.vertices_per_thread = VPT; info.n_chunks = n_chunks;
+        info.n_free = Vf; info.n_store = Vstore; info.slot_capacity = slot_cap;
+        info.n_edge_items = nE; info.n_tet_items = nT; info.n_att_items = nA; info.n_slots_total = n_slots_total;
+        info.bank_conflicts_p1 = total_conf; info.program_bytes = off; info.compact = compact ? 1 : 0;
+        info.edge_gather = eg ? 1 : 0; info.n_edge_incidences = gp.n_einc;
+        info.slot_budget = budget; info.cluster_size = part ? part->K : 1;
+    }
+};
 
-    std::memset(&info, 0, sizeof(info));
-    info.precision = prec; info.block_threads = B; info.vertices_per_thread = VPT; info.n_chunks = n_chunks;
-    info.n_free = Vf; info.n_store = Vstore; info.slot_capacity = slot_cap;
-    info.n_edge_items = nE; info.n_tet_items = nT; info.n_att_items = nA; info.n_slots_total = n_slots_total;
-    info.bank_conflicts_p1 = total_conf; info.program_bytes = off; info.compact = compact ? 1 : 0;
-    info.edge_gather = eg ? 1 : 0; info.n_edge_incidences = n_einc;
-    info.slot_budget = budget; info.cluster_size = part ? part->K : 1;
-    return TS_OK;
+}  // namespace
+
+int compile_program(const ts_scene_desc &d, const ts_layout_opts &o, std::vector<uint8_t> &blob,
+                    ts_layout_info &info, std::string &err, const PartSpec *part) {
+    if (part && (int)part->own.size() != d.n_vert) { err = "part ownership mask size"; return TS_ERR_INVALID; }
+    g_search_effort = part ? 0.1 : 1.0;
+    g_tet_holes = 0;   // measured: 2-8 idle lanes per batch cut conflicts but cost more issue (slower)
+    if (const char *env = std::getenv("TS_TET_HOLES")) g_tet_holes = std::atoi(env);
+    ProgramCompiler pc(d, o, part, err);
+    return pc.run(blob, info);
 }
 
 
