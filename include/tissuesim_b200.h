@@ -360,6 +360,11 @@ const char *ts_step_kernel_name(ts_handle *h);
  * kernels and the D2H output copy) in one call. */
 int32_t ts_graph_launch_sync(void *graph_exec, void *stream);
 
+/* The same in two halves: launch (asynchronous) and wait for the stream -- the caller does host
+ * work (the next output block's allocation) while the graph runs. */
+int32_t ts_graph_launch(void *graph_exec, void *stream);
+int32_t ts_stream_sync(void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -168,6 +168,8 @@ _SIGNATURES = {
     "ts_kernel_time": ([_P, _P, _P], _I32),
     "ts_step_kernel_name": ([_P], ctypes.c_char_p),
     "ts_graph_launch_sync": ([_P, _P], _I32),
+    "ts_graph_launch": ([_P, _P], _I32),
+    "ts_stream_sync": ([_P], _I32),
     "ts_env_step_dl": ([_P, _P, _P, _P, _P, _P, _P], _I32),
     "ts_env_reset_dl": ([_P, _P, _P, _P, _P], _I32),
     "ts_env_observe_dl": ([_P, _P, _P, _P], _I32),

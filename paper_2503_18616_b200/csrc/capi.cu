@@ -541,6 +541,20 @@ int32_t ts_graph_launch_sync(void *graph_exec, void *stream) {
     return TS_OK;
 }
 
+int32_t ts_graph_launch(void *graph_exec, void *stream) {
+    if (!graph_exec) return fail(TS_ERR_INVALID, "null graph");
+    const cudaError_t e = cudaGraphLaunch(reinterpret_cast<cudaGraphExec_t>(graph_exec),
+                                          reinterpret_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "graph launch");
+    return TS_OK;
+}
+
+int32_t ts_stream_sync(void *stream) {
+    const cudaError_t e = cudaStreamSynchronize(reinterpret_cast<cudaStream_t>(stream));
+    if (e != cudaSuccess) return cuda_fail(e, "stream synchronize");
+    return TS_OK;
+}
+
 int32_t ts_set_max_grid(ts_handle *h, int32_t max_grid) {
     if (!h) return fail(TS_ERR_INVALID, "null argument");
     h->max_grid = max_grid;

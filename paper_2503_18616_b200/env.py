@@ -351,16 +351,22 @@ class EnvBatch:
                 fx["host"][:fo_len].copy_(fx["dev_buf"][:fo_len], non_blocking=True)
 
         if fx["graph"] is not None and fx["sig"] is self.sim._state and torch.cuda.current_device() == dev.index:
-            # the steady state: launch the recorded graph on the current stream and wait, one call
-            N.check(self.sim.scene.lib.ts_graph_launch_sync(fx["exec"], torch._C._cuda_getCurrentRawStream(dev.index)),
-                    "step_numpy")
+            # the steady state: launch the recorded graph on the current stream; while it runs, take
+            # (and page in) the fresh host block this step's outputs are copied to; then wait
+            lib = self.sim.scene.lib
+            stream = torch._C._cuda_getCurrentRawStream(dev.index)
+            N.check(lib.ts_graph_launch(fx["exec"], stream), "step_numpy")
+            block = np.empty(fx["raw"].shape, np.uint8)
+            block.fill(0)
+            N.check(lib.ts_stream_sync(stream), "step_numpy")
         else:
             with torch.cuda.device(dev):
                 self._step_numpy_record(fx, device_side)
                 fx["done"].record()
             fx["done"].synchronize()
+            block = np.empty(fx["raw"].shape, np.uint8)
         self.sim.step_count += 1
-        block = fx["raw"].copy()          # one host copy of the packed block; the arrays are views of it
+        np.copyto(block, fx["raw"])       # one host copy of the packed block; the arrays are views of it
         out = {name: np.ndarray(shape, dt, block, off) for name, dt, shape, off, nb in fx["hv"]}
         done = out["done_mask"]
         d2h = fo_len
