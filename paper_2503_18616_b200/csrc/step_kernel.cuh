@@ -240,7 +240,7 @@ __device__ __forceinline__ void bary_pt(const Real *b, const Real *pa, const Rea
 // Narrow phase of one (face, capsule) pair that passed the AABB test.
 // Returns sd; fills depth/dir/bary when sd < 0.
 template <typename Real>
-__device__ __noinline__ Real witness(const Cap<Real> &C, const Real *pa_, const Real *pb_, const Real *pc_, int iters,
+__device__ __forceinline__ Real witness(const Cap<Real> &C, const Real *pa_, const Real *pb_, const Real *pc_, int iters,
                         Real *dir, Real *bary_out) {
     // register copies: the outputs live on the caller's stack and could alias the inputs
     const Real pa[3] = {pa_[0], pa_[1], pa_[2]}, pb[3] = {pb_[0], pb_[1], pb_[2]}, pc[3] = {pc_[0], pc_[1], pc_[2]};
