@@ -240,8 +240,8 @@ __device__ __forceinline__ void bary_pt(const Real *b, const Real *pa, const Rea
 // Narrow phase of one (face, capsule) pair that passed the AABB test.
 // Returns sd; fills depth/dir/bary when sd < 0.
 template <typename Real>
-__device__ __forceinline__ Real witness(const Cap<Real> &C, const Real *pa_, const Real *pb_, const Real *pc_, int iters,
-                        Real *dir, Real *bary_out) {
+__device__ __forceinline__ Real witness_body(const Cap<Real> &C, const Real *pa_, const Real *pb_, const Real *pc_,
+                                             int iters, Real *dir, Real *bary_out) {
     // register copies: the outputs live on the caller's stack and could alias the inputs
     const Real pa[3] = {pa_[0], pa_[1], pa_[2]}, pb[3] = {pb_[0], pb_[1], pb_[2]}, pc[3] = {pc_[0], pc_[1], pc_[2]};
     Real bary[3];
@@ -284,6 +284,19 @@ __device__ __forceinline__ Real witness(const Cap<Real> &C, const Real *pa_, con
     dir[0] = g[0]; dir[1] = g[1]; dir[2] = g[2];
     bary_out[0] = bary[0]; bary_out[1] = bary[1]; bary_out[2] = bary[2];
     return sd;
+}
+// fp32 kernels inline the narrow phase (no call frame: 0.522 -> 0.514 ms per 4096-env step); the
+// fp64 kernels keep it a call (inlined they spill more: 2.966 -> 2.998 ms)
+static __device__ __noinline__ double witness_f64(const Cap<double> &C, const double *pa, const double *pb, const double *pc,
+                                           int iters, double *dir, double *bary) {
+    return witness_body<double>(C, pa, pb, pc, iters, dir, bary);
+}
+
+template <typename Real>
+__device__ __forceinline__ Real witness(const Cap<Real> &C, const Real *pa, const Real *pb, const Real *pc, int iters,
+                                        Real *dir, Real *bary) {
+    if constexpr (sizeof(Real) == 8) return witness_f64(C, pa, pb, pc, iters, dir, bary);
+    else return witness_body<Real>(C, pa, pb, pc, iters, dir, bary);
 }
 
 template <typename Real> __device__ __forceinline__ Real fused_sq3(Real a, Real b, Real c);
