@@ -98,7 +98,7 @@ static __device__ void rodrigues(const double *vec, const double *k, double c, d
 }
 
 // ToolBatch.apply_commands for one row, tool.py:307-345
-static __device__ __noinline__ void apply_command(const TsParams &S, Pose &p, const double *tgt, double angle,
+static __device__ __forceinline__ void apply_command(const TsParams &S, Pose &p, const double *tgt, double angle,
                               bool &clipped, bool &rejected) {
     double b[3];
     clipped = false;
@@ -151,7 +151,7 @@ static __device__ __noinline__ void apply_command(const TsParams &S, Pose &p, co
 }
 
 // ToolBatch.capsule_rows for one row, tool.py:347-370
-static __device__ __noinline__ void capsule_rows(const TsParams &S, const Pose &p, double rows[3][7]) {
+static __device__ __forceinline__ void capsule_rows(const TsParams &S, const Pose &p, double rows[3][7]) {
     double piv[3];
     for (int c = 0; c < 3; ++c) piv[c] = S.rcm[c] + (p.reach - S.clamp_len) * p.ax[c];
     double ca, sa;
