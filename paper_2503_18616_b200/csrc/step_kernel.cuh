@@ -30,6 +30,18 @@
 
 #include "step_common.h"
 
+// loop unroll factors of the fast kernel's hot loops (development overrides: -DTS_TET_UNROLL=...)
+#ifndef TS_TET_UNROLL
+#define TS_TET_UNROLL 2
+#endif
+#ifndef TS_SLOT_UNROLL
+#define TS_SLOT_UNROLL 4
+#endif
+#ifndef TS_EDGE_UNROLL
+#define TS_EDGE_UNROLL 4
+#endif
+constexpr int kTetUnroll = TS_TET_UNROLL, kSlotUnroll = TS_SLOT_UNROLL, kEdgeUnroll = TS_EDGE_UNROLL;
+
 namespace tsk {
 
 template <typename Real> struct R4;
@@ -676,7 +688,7 @@ __device__ __forceinline__ void p1_tets_fast(const TsDevProg &P, int *deg, int b
     const unsigned vfp_b = 12u * (unsigned)P.Vf_pad;
     const uint4 *ip = P.tet_c + begin + wb + lane;
     uint4 nq = __ldg(ip);
-#pragma unroll 2
+#pragma unroll kTetUnroll
     for (int i = wb + lane; i < we; i += 32) {
         const uint4 q = nq;
         ip += 32;
@@ -940,6 +952,7 @@ __device__ __forceinline__ void owner_edges(const TsDevProg &P, const Smem<Real>
             float nx, ny, nz;
             float2 nrc;
             fetch(__ldg(rec), nx, ny, nz, nrc);
+#pragma unroll kEdgeUnroll
             for (int k = 0; k < ev; ++k) {
                 const float qx = nx, qy = ny, qz = nz;
                 const float2 rc = nrc;
@@ -1522,7 +1535,7 @@ __device__ __forceinline__ void step_env(const TsDevProg &P, const TsDevProg *pr
                                 ax += m.SX(sidx); ay += m.SY(sidx); az += m.SZ(sidx);
                             }
                         };
-#pragma unroll 4
+#pragma unroll kSlotUnroll
                         for (int k = 0; k < pre; ++k) add_slot(k);
                         if (gchunk) {
                             accx[r] = ax; accy[r] = ay; accz[r] = az;
