@@ -45,6 +45,14 @@ def test_abi_version_and_errors():
     assert b"null" in lib.ts_last_error()
 
 
+def test_graph_launch_rejects_null_graph():
+    """The step_numpy launch helpers validate before touching CUDA (safe on a CPU-only host)."""
+    lib = N.load()
+    for fn in (lib.ts_graph_launch, lib.ts_graph_launch_sync):
+        assert fn(None, None) == N.TS_ERR_INVALID
+        assert b"null graph" in lib.ts_last_error()
+
+
 def test_library_is_sm100a():
     out = os.popen(f"cuobjdump --list-elf {N.LIB_PATH}").read()
     assert "sm_100a" in out
