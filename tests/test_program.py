@@ -414,3 +414,14 @@ def test_fast_program_is_bank_conflict_free(reach_scene):
     q = p.tet_c[live]
     ri = ((q[:, 0] >> 14) & 3) | ((q[:, 0] >> 28) & 12) | ((q[:, 1] >> 10) & 48) | ((q[:, 1] >> 24) & 192)
     assert np.array_equal(tab[ri], rv)
+
+
+@pytest.mark.parametrize("layout", [{}, {"precision": "fp64"}, {"cluster_size": 2}])
+def test_compiler_is_deterministic(layout):
+    """The same scene and options compile to the same bytes every time (the searches use fixed
+    seeds) -- the program cache and every parity claim on a cached program rely on it."""
+    arrays = _arrays(build_slab_scene(nx=5, ny=3, nz=2))
+    o = S.layout_opts(**layout)
+    b1, i1 = S._compile_raw(arrays, o)
+    b2, i2 = S._compile_raw(arrays, o)
+    assert np.array_equal(b1, b2) and bytes(i1) == bytes(i2)
